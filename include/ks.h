@@ -1,0 +1,164 @@
+/*
+ * ks.h -- C ABI of the B200-native Odd-Even parallel-in-time Kalman smoother
+ * (Gargir & Toledo, "Parallel-in-Time Kalman Smoothing Using Orthogonal
+ * Transformations", arXiv 2502.11686; P:n = line n of the paper text).
+ *
+ * All arithmetic is fp64 and runs in sm_100a kernels on the caller's CUDA
+ * stream.  No function allocates device memory: the caller (PyTorch) owns the
+ * workspace and all buffers.  Blocks are row-major.
+ *
+ * Problem (Eq. (1)-(6)), with the paper's evolution matrix
+ * H_i = I (the *observation* matrix, paper G_i, is called H here
+ * as in BASELINE.json):
+ *     x_i = F_i x_{i-1} + c_i + eps_i,  cov(eps_i) = K_i      (i >= 1)
+ *     o_i = H_i x_i + delta_i,          cov(delta_i) = L_i    (m_i >= 0 rows)
+ *     x_hat = argmin sum_i |V_i(x_i - F_i x_{i-1} - c_i)|^2 + |W_i(o_i - H_i x_i)|^2
+ * with V_i^T V_i = K_i^{-1}, W_i^T W_i = L_i^{-1}.  The outputs are
+ * the smoothed states x_hat_i and their covariances cov(x_hat_i), the diagonal
+ * blocks of (R^T R)^{-1}.  There is no prior on x_0:
+ * the stacked matrix UA must have full column rank.
+ *
+ * Call order (each returns KS_ERR_ORDER when called out of order):
+ *     ks_create -> ks_whiten -> ks_factor -> ks_solve [-> ks_selinv] -> ks_get
+ * ks_selinv is optional (the paper's "NC" variant).  All calls only
+ * ENQUEUE work on the stream given to ks_create; only ks_sync_status and
+ * ks_get with host destination buffers synchronise.
+ */
+#ifndef KS_H
+#define KS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ks_ctx ks_ctx;
+
+/* Status codes.  Argument/launch errors are returned synchronously; numerical
+ * failures (NOT_SPD, RANK) are recorded on the device and reported by
+ * ks_sync_status (after which outputs are undefined). */
+enum {
+    KS_OK = 0,
+    KS_ERR_ARG = 1,       /* bad argument (null pointer, size, stride, flags)   */
+    KS_ERR_ORDER = 2,     /* call out of order                                  */
+    KS_ERR_CUDA = 3,      /* a CUDA launch/runtime call failed                  */
+    KS_ERR_NCCL = 4,      /* NCCL missing or an NCCL call failed (multi-GPU)    */
+    KS_ERR_NOT_SPD = 5,   /* K_i or L_i not SPD: Cholesky pivot <= 0     */
+    KS_ERR_RANK = 6,      /* UA rank deficient: |R_jj[d][d]| <= 1e-13*|stack|_F */
+    KS_ERR_WORKSPACE = 7  /* workspace too small or misaligned                  */
+};
+
+/* ks_problem.flags */
+enum {
+    KS_HOST_INPUTS = 1u,  /* F,H,c,o,K,L,m are HOST pointers (pinned recommended);
+                             ks_whiten copies them into the workspace first      */
+    KS_OUTPUTS_BOUND = 2u /* the caller binds states_out (and cov_out, unless it
+                             never calls ks_selinv) in ks_create, so the
+                             workspace holds no output buffers                   */
+};
+
+/* One problem (or, multi-GPU, one rank's contiguous shard of steps).
+ * Per-step arrays have their own stride in doubles; stride 0 = the same block
+ * at every step (a constant model).  Rows of H, o, L beyond m_i are ignored.
+ * F, K, c of the first GLOBAL step are ignored (x_0 has no evolution equation,
+ * P:153-154); on a shard that does not start at global step 0, the first local
+ * step's F, K, c couple it to the previous shard's last step (no halo). */
+typedef struct ks_problem {
+    int64_t nsteps;          /* N >= 1 states in this context (paper k+1)          */
+    int32_t n;               /* state dimension, 1 <= n <= KS_MAX_N                */
+    int32_t m_max;           /* max observation dimension, 0 <= m_max <= KS_MAX_M  */
+    const int32_t *m;        /* [N] observation dims in [0, m_max]; NULL = all m_max */
+    const double *F;         /* [N][n][n]      evolution F_i                        */
+    const double *H;         /* [N][m_max][n]  observation H_i (paper G_i)          */
+    const double *c;         /* [N][n]         forcing c_i; NULL = 0                */
+    const double *o;         /* [N][m_max]     observations o_i                     */
+    const double *K;         /* [N][n][n]      evolution-noise covariance (SPD)     */
+    const double *L;         /* [N][m_max][m_max] observation-noise covariance (SPD) */
+    int64_t sF, sH, sc, so, sK, sL;   /* per-step strides in doubles, 0 = constant */
+    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND                  */
+} ks_problem;
+
+#define KS_MAX_N 64
+#define KS_MAX_M 64
+
+/* Multi-GPU time sharding.  NULL = one GPU owns all steps.
+ * Every rank passes nsteps = N_global / nranks, which must be a power of two;
+ * rank r owns global steps [r*nsteps, (r+1)*nsteps).  The boundary exchange
+ * is one allgather of each rank's reduced boundary column, done by ks_factor
+ * through the NCCL communicator given here (an ncclComm_t cast to void*), or,
+ * with comm == NULL, through the caller: see ks_boundary_buffers. */
+typedef struct ks_shard {
+    int32_t rank;
+    int32_t nranks;
+    void *nccl_comm;         /* ncclComm_t or NULL (caller-driven exchange)        */
+} ks_shard;
+
+/* Bytes of device workspace a context needs (0 on bad arguments). */
+size_t ks_workspace_bytes(const ks_problem *p, const ks_shard *shard);
+
+/* Create a context.  `workspace` is a device buffer of >= ks_workspace_bytes
+ * bytes, 256-byte aligned, borrowed for the context's lifetime.  `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Input arrays are borrowed until
+ * the work enqueued by ks_whiten has completed.  `states_out` ([N][n]) and
+ * `cov_out` ([N][n][n]) are optional DEVICE buffers that ks_solve / ks_selinv
+ * write directly (zero-copy); when NULL, results live in the workspace and
+ * ks_get copies them out.  The shard struct is copied. */
+int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_bytes,
+              void *stream, const ks_shard *shard, double *states_out, double *cov_out);
+
+/* Phase 1: Cholesky K_i = Lam Lam^T, L_i = M M^T and
+ * triangular solves: C_i = M^{-1}H_i, y_i = M^{-1}o_i, -B_i = -Lam^{-1}F_i,
+ * D_i = Lam^{-1}, e_i = Lam^{-1}c_i.  A non-SPD K_i/L_i is recorded. */
+int ks_whiten(ks_ctx *ctx);
+
+/* Phase 2: recursive odd-even block QR of U A P with
+ * Q^T U b, level by level; each level is one launch over all (even, odd)
+ * column pairs.  Stores per eliminated column T = R_jj^{-1}[R_{j,l} R_{j,r}],
+ * w = R_jj^{-1} z_j and P = R_jj^{-1} R_jj^{-T} for the backward phases.
+ * Multi-GPU: local levels, boundary allgather, replicated boundary levels. */
+int ks_factor(ks_ctx *ctx);
+
+/* Phase 3: block back-substitution over the levels in reverse:
+ * x_j = w_j - T_l x_l - T_r x_r. */
+int ks_solve(ks_ctx *ctx);
+
+/* Phase 4 (Alg. 2): odd-even block SelInv over the levels in
+ * reverse: S_{j,I} = -T S_{I,I}, S_jj = P - S_{j,I} T^T, symmetrised. */
+int ks_selinv(ks_ctx *ctx);
+
+/* Copy results into caller buffers (device or host; NULL = skip).  A pointer
+ * equal to the bound output buffer is a no-op.  Host destinations synchronise
+ * the stream.  cov requires a prior ks_selinv. */
+int ks_get(ks_ctx *ctx, double *states, double *cov);
+
+/* Synchronise the stream and report the first numerical failure:
+ * KS_OK, KS_ERR_NOT_SPD (bad_kind 1 = K, 2 = L) or KS_ERR_RANK; bad_step is
+ * the local step index (or -1).  Also surfaces asynchronous CUDA errors. */
+int ks_sync_status(ks_ctx *ctx, int64_t *bad_step, int *bad_kind);
+
+/* Multi-GPU with nccl_comm == NULL: after ks_factor returns KS_OK on every
+ * rank, the caller allgathers `send` (bytes each) from every rank into
+ * `recv` (nranks * bytes, rank order) on the context's stream, then calls
+ * ks_factor_boundary.  Device pointers inside the workspace. */
+int ks_boundary_buffers(ks_ctx *ctx, void **send, void **recv, size_t *bytes);
+int ks_factor_boundary(ks_ctx *ctx);
+
+/* Per-kernel-family device timing with CUDA events recorded around every
+ * launch (0 = off).  Families: 0 whiten, 1 factor levels, 2 backward levels,
+ * 3 boundary/other.  ms[f] = summed event time, launches[f] = count. */
+int ks_set_timing(ks_ctx *ctx, int on);
+int ks_get_timing(ks_ctx *ctx, double ms[4], int64_t launches[4]);
+
+/* Number of factor levels (ceil(log2 N) + 1 on one GPU) and kernel launches
+ * enqueued by the last whiten..selinv sequence. */
+int ks_info(ks_ctx *ctx, int64_t *levels, int64_t *launches);
+
+const char *ks_strerror(int code);
+void ks_destroy(ks_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_H */

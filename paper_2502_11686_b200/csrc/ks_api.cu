@@ -1,0 +1,584 @@
+// Host side of the C ABI declared in include/ks.h: argument checks, the
+// workspace carve, the level plan (trailing-ones rule), the
+// per-level launch loops, the multi-GPU boundary exchange and the status word.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/ks.h"
+#include "ks_internal.cuh"
+
+using namespace ks;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct Carve {
+  char *base;
+  size_t off = 0;
+  template <class T>
+  T *take(size_t count) {
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off = align_up(off + count * sizeof(T));
+    return p;
+  }
+};
+
+// ---- NCCL (dlopen'ed: the library has no link-time NCCL dependency) ----
+typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int /*ncclDataType_t*/, void *,
+                                 cudaStream_t);
+
+struct Nccl {
+  void *h = nullptr;
+  nccl_allgather_fn allgather = nullptr;
+  bool load() {
+    if (h) return allgather != nullptr;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
+    return allgather != nullptr;
+  }
+};
+Nccl g_nccl;
+
+}  // namespace
+
+struct ks_ctx {
+  ks_problem p{};
+  int64_t N = 0;
+  int n = 0, mx = 0;
+  cudaStream_t stream = nullptr;
+  bool host_inputs = false;
+  // sharding
+  bool sharded = false;
+  int rank = 0, nranks = 1, q = 0;
+  void *comm = nullptr;
+  // device views of the inputs
+  const int32_t *m = nullptr;
+  const double *F = nullptr, *H = nullptr, *c = nullptr, *o = nullptr, *K = nullptr, *L = nullptr;
+  // staging for host inputs
+  int32_t *st_m = nullptr;
+  double *st_F = nullptr, *st_H = nullptr, *st_c = nullptr, *st_o = nullptr, *st_K = nullptr,
+         *st_L = nullptr;
+  size_t nF = 0, nH = 0, nc = 0, no = 0, nK = 0, nL = 0;  // staged doubles
+  // level 0 (whitened)
+  unsigned long long *status = nullptr;
+  double *C0 = nullptr, *y0 = nullptr, *El0 = nullptr, *Er0 = nullptr, *e0 = nullptr,
+         *Mchol = nullptr;
+  int64_t cntE = 1, cntC = 1;
+  // local levels 0..nlev-1 (sharded: 0..q-1)
+  std::vector<int64_t> K_;
+  std::vector<double *> ent, rrec, X;
+  // boundary levels (sharded)
+  std::vector<int64_t> Kb;
+  std::vector<double *> entb, rrecb, Xb;
+  double *send = nullptr, *recv = nullptr, *bx = nullptr, *bS = nullptr, *hx = nullptr,
+         *hS = nullptr, *Xq_local = nullptr;
+  // outputs
+  double *xout = nullptr, *Sout = nullptr;
+  int stage = 0;  // 0 created, 1 whitened, 2 local-factored (sharded), 3 factored
+  bool solved = false, covd = false;
+  int64_t launches = 0;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_family;
+  double t_ms[4] = {0, 0, 0, 0};
+  int64_t t_cnt[4] = {0, 0, 0, 0};
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e) {
+  if (e == cudaSuccess) return KS_OK;
+  fprintf(stderr, "[ks] CUDA error: %s\n", cudaGetErrorString(e));
+  return KS_ERR_CUDA;
+}
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+int validate(const ks_problem *p, const ks_shard *sh) {
+  if (!p) return KS_ERR_ARG;
+  if (p->nsteps < 1 || p->n < 1 || p->n > KS_MAX_N || p->m_max < 0 || p->m_max > KS_MAX_M)
+    return KS_ERR_ARG;
+  if (!p->F || !p->K || (p->m_max > 0 && (!p->H || !p->o || !p->L))) return KS_ERR_ARG;
+  if (p->sF < 0 || p->sH < 0 || p->sc < 0 || p->so < 0 || p->sK < 0 || p->sL < 0) return KS_ERR_ARG;
+  const int64_t n = p->n, mx = p->m_max;
+  if ((p->sF && p->sF < n * n) || (p->sK && p->sK < n * n) || (p->sH && p->sH < mx * n) ||
+      (p->sL && p->sL < mx * mx) || (p->sc && p->sc < n) || (p->so && p->so < mx))
+    return KS_ERR_ARG;
+  if (p->flags & ~(uint32_t)(KS_HOST_INPUTS | KS_OUTPUTS_BOUND)) return KS_ERR_ARG;
+  if (factor_smem_bytes(p->n, p->m_max > p->n ? p->m_max : p->n) > 227 * 1024) return KS_ERR_ARG;
+  if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
+  if (sh) {
+    if (sh->nranks < 1 || sh->rank < 0 || sh->rank >= sh->nranks) return KS_ERR_ARG;
+    if (sh->nranks > 1 && (!is_pow2(p->nsteps) || p->nsteps < 2)) return KS_ERR_ARG;
+  }
+  return KS_OK;
+}
+
+// Lay out (or just size, when base == nullptr) the workspace.
+size_t carve(ks_ctx *c, char *base) {
+  Carve w{base};
+  const ks_problem &p = c->p;
+  const int64_t N = c->N;
+  const int n = c->n, mx = c->mx;
+  const int64_t nn = (int64_t)n * n, E = entry_doubles(n), Rr = rrec_doubles(n);
+  c->status = w.take<unsigned long long>(2);
+  if (c->host_inputs) {
+    auto cnt = [&](int64_t s, int64_t blk) { return (size_t)(s ? (N - 1) * s + blk : blk); };
+    c->nF = cnt(p.sF, nn);
+    c->nK = cnt(p.sK, nn);
+    c->nH = mx ? cnt(p.sH, (int64_t)mx * n) : 0;
+    c->nL = mx ? cnt(p.sL, (int64_t)mx * mx) : 0;
+    c->no = mx ? cnt(p.so, mx) : 0;
+    c->nc = p.c ? cnt(p.sc, n) : 0;
+    c->st_m = p.m ? w.take<int32_t>(N) : nullptr;
+    c->st_F = w.take<double>(c->nF);
+    c->st_K = w.take<double>(c->nK);
+    c->st_H = w.take<double>(c->nH);
+    c->st_L = w.take<double>(c->nL);
+    c->st_o = w.take<double>(c->no);
+    c->st_c = p.c ? w.take<double>(c->nc) : nullptr;
+  }
+  c->cntE = (p.sF == 0 && p.sK == 0 && (p.c == nullptr || p.sc == 0)) ? 1 : N;
+  c->cntC = (p.sH == 0 && p.sL == 0 && p.m == nullptr) ? 1 : N;
+  c->El0 = w.take<double>(c->cntE * nn);
+  c->Er0 = w.take<double>(c->cntE * nn);
+  c->e0 = w.take<double>(c->cntE * n);
+  c->C0 = w.take<double>(c->cntC * mx * n + 1);
+  c->y0 = w.take<double>(N * mx + 1);
+  c->Mchol = w.take<double>((size_t)mx * mx + 1);
+  // local levels
+  c->K_.clear(); c->ent.clear(); c->rrec.clear(); c->X.clear();
+  int64_t K = N;
+  for (int L = 0;; ++L) {
+    if (c->sharded && L == c->q) break;
+    c->K_.push_back(K);
+    c->ent.push_back(L == 0 ? nullptr : w.take<double>(K * E));
+    c->rrec.push_back(w.take<double>(((K + 1) / 2) * Rr));
+    c->X.push_back(L == 0 ? nullptr : w.take<double>((K + 1) * nn));
+    if (K == 1) break;
+    K /= 2;
+  }
+  if (c->sharded) {
+    const int P = c->nranks;
+    c->send = w.take<double>(E);
+    c->recv = w.take<double>((int64_t)P * E);
+    c->Xq_local = w.take<double>(2 * nn);
+    c->hx = w.take<double>(n);
+    c->hS = w.take<double>(nn);
+    c->bx = w.take<double>((int64_t)P * n);
+    c->bS = w.take<double>((int64_t)P * nn);
+    c->Kb.clear(); c->entb.clear(); c->rrecb.clear(); c->Xb.clear();
+    int64_t Kb = P;
+    for (int L = 0;; ++L) {
+      c->Kb.push_back(Kb);
+      c->entb.push_back(L == 0 ? c->recv : w.take<double>(Kb * E));
+      c->rrecb.push_back(w.take<double>(((Kb + 1) / 2) * Rr));
+      c->Xb.push_back(w.take<double>((Kb + 1) * nn));
+      if (Kb == 1) break;
+      Kb /= 2;
+    }
+  }
+  if (!(p.flags & KS_OUTPUTS_BOUND)) {
+    c->xout = c->xout ? c->xout : w.take<double>(N * n);
+    c->Sout = c->Sout ? c->Sout : w.take<double>(N * nn);
+  }
+  return w.off;
+}
+
+struct Launch {
+  ks_ctx *c;
+  int fam;
+  cudaEvent_t e1 = nullptr;
+  Launch(ks_ctx *c_, int f) : c(c_), fam(f) {
+    if (c->timing) {
+      if (c->ev_used + 2 > c->ev_pool.size()) {
+        for (int i = 0; i < 64; ++i) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          c->ev_pool.push_back(e);
+        }
+      }
+      cudaEvent_t e0 = c->ev_pool[c->ev_used++];
+      e1 = c->ev_pool[c->ev_used++];
+      c->ev_family.push_back(f);
+      cudaEventRecord(e0, c->stream);
+    }
+    c->launches++;
+  }
+  ~Launch() {
+    if (e1) cudaEventRecord(e1, c->stream);
+  }
+};
+
+EntryView level0_view(const ks_ctx *c) {
+  EntryView v;
+  const int n = c->n, mx = c->mx;
+  const int64_t nn = (int64_t)n * n;
+  v.C = c->C0; v.sC = c->cntC == 1 ? 0 : (int64_t)mx * n;
+  v.y = c->y0; v.sy = mx;
+  v.El = c->El0; v.sEl = c->cntE == 1 ? 0 : nn;
+  v.Er = c->Er0; v.sEr = c->cntE == 1 ? 0 : nn;
+  v.e = c->e0; v.se = c->cntE == 1 ? 0 : n;
+  v.RC = mx;
+  return v;
+}
+
+EntryView aos_view(const double *ent, int n) {
+  EntryView v;
+  const int64_t E = entry_doubles(n), nn = (int64_t)n * n;
+  v.C = ent; v.y = ent + nn; v.El = ent + nn + n; v.Er = ent + 2 * nn + n; v.e = ent + 3 * nn + n;
+  v.sC = v.sy = v.sEl = v.sEr = v.se = E;
+  v.RC = n;
+  return v;
+}
+
+int run_factor_levels(ks_ctx *c, bool boundary) {
+  const int n = c->n;
+  const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
+  const int Lb = boundary ? c->q : 0;
+  for (size_t i = 0; i < Ks.size(); ++i) {
+    FactorLevelArgs a;
+    const int L = Lb + (int)i;
+    if (!boundary && i == 0) {
+      a.in = level0_view(c);
+    } else {
+      a.in = aos_view(boundary ? c->entb[i] : c->ent[i], n);
+    }
+    a.K = Ks[i];
+    a.n = n;
+    a.level = L;
+    a.lbase = boundary ? c->q : 0;
+    a.status = c->status;
+    if (boundary) {
+      a.t0 = 0;
+      a.step0 = 0;  // reported as boundary-domain index
+      a.next = (i + 1 < Ks.size()) ? c->entb[i + 1] : nullptr;
+      a.rrec = c->rrecb[i];
+    } else {
+      a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+      a.step0 = 0;
+      if (i + 1 < Ks.size()) a.next = c->ent[i + 1];
+      else a.next = c->sharded ? c->send : nullptr;
+      a.rrec = c->rrec[i];
+    }
+    Launch l(c, boundary ? 3 : 1);
+    cudaError_t e = launch_factor_level(a, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return KS_OK;
+}
+
+int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
+  const int n = c->n;
+  const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
+  for (int i = (int)Ks.size() - 1; i >= 0; --i) {
+    BackwardLevelArgs a;
+    a.K = Ks[i];
+    a.n = n;
+    a.shift = i;
+    a.do_state = do_state;
+    a.do_cov = do_cov;
+    if (boundary) {
+      a.rrec = c->rrecb[i];
+      a.t0 = 0;
+      a.x = c->bx;
+      a.S = c->bS;
+      a.xhalo = nullptr;
+      a.Shalo = nullptr;
+      a.Xup = (i + 1 < (int)Ks.size()) ? c->Xb[i + 1] : nullptr;
+      a.Xcur = c->Xb[i];
+    } else {
+      a.rrec = c->rrec[i];
+      a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+      a.x = c->xout;
+      a.S = c->Sout;
+      a.xhalo = c->hx;
+      a.Shalo = c->hS;
+      if (i + 1 < (int)Ks.size()) a.Xup = c->X[i + 1];
+      else a.Xup = c->sharded ? c->Xq_local : nullptr;
+      a.Xcur = (i >= 1) ? c->X[i] : nullptr;
+    }
+    Launch l(c, boundary ? 3 : 2);
+    cudaError_t e = launch_backward_level(a, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return KS_OK;
+}
+
+// Boundary results -> this rank's local domain (SURVEY §8(e) back phase).
+int scatter_boundary(ks_ctx *c, bool states, bool cov) {
+  const int n = c->n, r = c->rank;
+  const int64_t nn = (int64_t)n * n, M = c->N;
+  cudaError_t e = cudaSuccess;
+  if (states) {
+    e = cudaMemcpyAsync(c->xout + (M - 1) * n, c->bx + (int64_t)r * n, n * 8, cudaMemcpyDeviceToDevice, c->stream);
+    if (r > 0 && e == cudaSuccess)
+      e = cudaMemcpyAsync(c->hx, c->bx + (int64_t)(r - 1) * n, n * 8, cudaMemcpyDeviceToDevice, c->stream);
+  }
+  if (cov && e == cudaSuccess) {
+    e = cudaMemcpyAsync(c->Sout + (M - 1) * nn, c->bS + r * nn, nn * 8, cudaMemcpyDeviceToDevice, c->stream);
+    if (r > 0 && e == cudaSuccess) {
+      e = cudaMemcpyAsync(c->hS, c->bS + (r - 1) * nn, nn * 8, cudaMemcpyDeviceToDevice, c->stream);
+      // slot -1 of the local level-q cross array: S_{b_{r-1}, b_r} = boundary X_q slot r-1
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->Xq_local, c->Xb[0] + (int64_t)r * nn, nn * 8, cudaMemcpyDeviceToDevice,
+                            c->stream);
+    }
+  }
+  return cuda_fail(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ks_workspace_bytes(const ks_problem *p, const ks_shard *sh) {
+  if (validate(p, sh) != KS_OK) return 0;
+  ks_ctx c;
+  c.p = *p;
+  c.N = p->nsteps; c.n = p->n; c.mx = p->m_max;
+  c.host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
+  if (sh && sh->nranks > 1) {
+    c.sharded = true; c.rank = sh->rank; c.nranks = sh->nranks;
+    int q = 0;
+    while ((1ll << q) < p->nsteps) ++q;
+    c.q = q;
+  }
+  return carve(&c, nullptr) + kAlign;
+}
+
+int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_bytes, void *stream,
+              const ks_shard *sh, double *states_out, double *cov_out) {
+  if (!out) return KS_ERR_ARG;
+  *out = nullptr;
+  int v = validate(p, sh);
+  if (v) return v;
+  if (!workspace || ((uintptr_t)workspace % kAlign) != 0) return KS_ERR_WORKSPACE;
+  size_t need = ks_workspace_bytes(p, sh);
+  if (ws_bytes + kAlign < need) return KS_ERR_WORKSPACE;
+  ks_ctx *c = new (std::nothrow) ks_ctx;
+  if (!c) return KS_ERR_ARG;
+  c->p = *p;
+  c->N = p->nsteps; c->n = p->n; c->mx = p->m_max;
+  c->stream = (cudaStream_t)stream;
+  c->host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
+  if (sh && sh->nranks > 1) {
+    c->sharded = true; c->rank = sh->rank; c->nranks = sh->nranks; c->comm = sh->nccl_comm;
+    int q = 0;
+    while ((1ll << q) < p->nsteps) ++q;
+    c->q = q;
+    if (c->comm && !g_nccl.load()) { delete c; return KS_ERR_NCCL; }
+  }
+  c->xout = states_out;
+  c->Sout = cov_out;
+  if ((p->flags & KS_OUTPUTS_BOUND) && !states_out) { delete c; return KS_ERR_ARG; }
+  carve(c, (char *)workspace);
+  if (c->host_inputs) {
+    c->m = c->st_m; c->F = c->st_F; c->K = c->st_K; c->H = c->st_H; c->L = c->st_L;
+    c->o = c->st_o; c->c = c->st_c;
+  } else {
+    c->m = p->m; c->F = p->F; c->K = p->K; c->H = p->H; c->L = p->L; c->o = p->o; c->c = p->c;
+  }
+  *out = c;
+  return KS_OK;
+}
+
+int ks_whiten(ks_ctx *c) {
+  if (!c) return KS_ERR_ARG;
+  cudaError_t e = cudaMemsetAsync(c->status, 0xff, 16, c->stream);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (c->host_inputs) {
+    const ks_problem &p = c->p;
+    struct { void *d; const void *h; size_t bytes; } cp[] = {
+        {c->st_m, p.m, p.m ? (size_t)c->N * 4 : 0}, {c->st_F, p.F, c->nF * 8}, {c->st_K, p.K, c->nK * 8},
+        {c->st_H, p.H, c->nH * 8}, {c->st_L, p.L, c->nL * 8}, {c->st_o, p.o, c->no * 8},
+        {c->st_c, p.c, c->nc * 8}};
+    for (auto &x : cp)
+      if (x.bytes) {
+        e = cudaMemcpyAsync(x.d, x.h, x.bytes, cudaMemcpyHostToDevice, c->stream);
+        if (e != cudaSuccess) return cuda_fail(e);
+      }
+  }
+  WhitenArgs a;
+  a.N = c->N; a.n = c->n; a.m_max = c->mx; a.m = c->m;
+  a.F = c->F; a.H = c->H; a.c = c->c; a.o = c->o; a.K = c->K; a.L = c->L;
+  a.sF = c->p.sF; a.sH = c->p.sH; a.sc = c->p.sc; a.so = c->p.so; a.sK = c->p.sK; a.sL = c->p.sL;
+  a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
+  a.C = c->C0; a.y = c->y0; a.El = c->El0; a.Er = c->Er0; a.e = c->e0;
+  a.cntE = c->cntE; a.cntC = c->cntC; a.Mchol = c->Mchol; a.status = c->status;
+  {
+    Launch l(c, 0);
+    e = launch_whiten(a, c->stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(e);
+  c->stage = 1;
+  c->solved = c->covd = false;
+  return KS_OK;
+}
+
+int ks_factor(ks_ctx *c) {
+  if (!c) return KS_ERR_ARG;
+  if (c->stage < 1) return KS_ERR_ORDER;
+  int r = run_factor_levels(c, false);
+  if (r) return r;
+  if (!c->sharded) {
+    c->stage = 3;
+    return KS_OK;
+  }
+  c->stage = 2;
+  if (!c->comm) return KS_OK;  // caller-driven exchange: ks_boundary_buffers + ks_factor_boundary
+  const size_t E = (size_t)entry_doubles(c->n);
+  int rc = g_nccl.allgather(c->send, c->recv, E, /*ncclFloat64*/ 8, c->comm, c->stream);
+  if (rc != 0) return KS_ERR_NCCL;
+  return ks_factor_boundary(c);
+}
+
+int ks_boundary_buffers(ks_ctx *c, void **send, void **recv, size_t *bytes) {
+  if (!c || !c->sharded) return KS_ERR_ARG;
+  if (send) *send = c->send;
+  if (recv) *recv = c->recv;
+  if (bytes) *bytes = (size_t)entry_doubles(c->n) * 8;
+  return KS_OK;
+}
+
+int ks_factor_boundary(ks_ctx *c) {
+  if (!c || !c->sharded) return KS_ERR_ARG;
+  if (c->stage != 2) return KS_ERR_ORDER;
+  int r = run_factor_levels(c, true);
+  if (r) return r;
+  c->stage = 3;
+  return KS_OK;
+}
+
+int ks_solve(ks_ctx *c) {
+  if (!c) return KS_ERR_ARG;
+  if (c->stage < 3) return KS_ERR_ORDER;
+  int r;
+  if (c->sharded) {
+    if ((r = run_backward_levels(c, true, 1, 0))) return r;
+    if ((r = scatter_boundary(c, true, false))) return r;
+  }
+  if ((r = run_backward_levels(c, false, 1, 0))) return r;
+  c->solved = true;
+  return KS_OK;
+}
+
+int ks_selinv(ks_ctx *c) {
+  if (!c || !c->Sout) return KS_ERR_ARG;
+  if (c->stage < 3) return KS_ERR_ORDER;
+  int r;
+  if (c->sharded) {
+    if ((r = run_backward_levels(c, true, 0, 1))) return r;
+    if ((r = scatter_boundary(c, false, true))) return r;
+  }
+  if ((r = run_backward_levels(c, false, 0, 1))) return r;
+  c->covd = true;
+  return KS_OK;
+}
+
+int ks_get(ks_ctx *c, double *states, double *cov) {
+  if (!c) return KS_ERR_ARG;
+  if ((states && !c->solved) || (cov && !c->covd)) return KS_ERR_ORDER;
+  bool host = false;
+  cudaError_t e = cudaSuccess;
+  auto copy = [&](double *dst, const double *src, size_t bytes) {
+    if (!dst || dst == src || e != cudaSuccess) return;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, dst) != cudaSuccess) { cudaGetLastError(); at.type = cudaMemoryTypeUnregistered; }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) host = true;
+    e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
+  };
+  copy(states, c->xout, (size_t)c->N * c->n * 8);
+  copy(cov, c->Sout, (size_t)c->N * c->n * c->n * 8);
+  if (e == cudaSuccess && host) e = cudaStreamSynchronize(c->stream);
+  return cuda_fail(e);
+}
+
+int ks_sync_status(ks_ctx *c, int64_t *bad_step, int *bad_kind) {
+  if (!c) return KS_ERR_ARG;
+  if (bad_step) *bad_step = -1;
+  if (bad_kind) *bad_kind = 0;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(e);
+  unsigned long long st = 0;
+  e = cudaMemcpy(&st, c->status, 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (st == kStatusOk) return KS_OK;
+  const int kind = (int)(st & 0xff);
+  if (bad_step) *bad_step = (int64_t)(st >> 8) - 1;
+  if (kind == kBadRank) return KS_ERR_RANK;
+  if (bad_kind) *bad_kind = kind;
+  return KS_ERR_NOT_SPD;
+}
+
+int ks_set_timing(ks_ctx *c, int on) {
+  if (!c) return KS_ERR_ARG;
+  c->timing = on != 0;
+  c->ev_used = 0;
+  c->ev_family.clear();
+  for (int f = 0; f < 4; ++f) { c->t_ms[f] = 0; c->t_cnt[f] = 0; }
+  return KS_OK;
+}
+
+int ks_get_timing(ks_ctx *c, double ms[4], int64_t launches[4]) {
+  if (!c) return KS_ERR_ARG;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (size_t i = 0; i < c->ev_family.size(); ++i) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]);
+    c->t_ms[c->ev_family[i]] += t;
+    c->t_cnt[c->ev_family[i]] += 1;
+  }
+  c->ev_used = 0;
+  c->ev_family.clear();
+  for (int f = 0; f < 4; ++f) {
+    if (ms) ms[f] = c->t_ms[f];
+    if (launches) launches[f] = c->t_cnt[f];
+  }
+  return KS_OK;
+}
+
+int ks_info(ks_ctx *c, int64_t *levels, int64_t *launches) {
+  if (!c) return KS_ERR_ARG;
+  if (levels) *levels = (int64_t)c->K_.size() + (int64_t)c->Kb.size();
+  if (launches) *launches = c->launches;
+  return KS_OK;
+}
+
+const char *ks_strerror(int code) {
+  switch (code) {
+    case KS_OK: return "ok";
+    case KS_ERR_ARG: return "bad argument";
+    case KS_ERR_ORDER: return "call out of order";
+    case KS_ERR_CUDA: return "CUDA error";
+    case KS_ERR_NCCL: return "NCCL unavailable or failed";
+    case KS_ERR_NOT_SPD: return "noise covariance not SPD";
+    case KS_ERR_RANK: return "least-squares matrix rank deficient";
+    case KS_ERR_WORKSPACE: return "workspace too small or misaligned";
+    default: return "unknown";
+  }
+}
+
+void ks_destroy(ks_ctx *c) {
+  if (!c) return;
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Internal declarations shared by the ks kernels and the host ABI.
+// (Not shared with oracle/ -- the oracle has its own, independent C code.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ks {
+
+// Status word: min over (step+1) << 8 | kind, written with atomicMin.
+enum BadKind : int { kBadK = 1, kBadL = 2, kBadRank = 3 };
+constexpr unsigned long long kStatusOk = ~0ull;
+
+// Relative rank tolerance (header: |R_jj[d][d]| <= 1e-13 |stacked column|_F).
+constexpr double kRankTol = 1e-13;
+
+// A level's reduced system: column t owns a C-like block
+// C_t [RC x n] with RHS y_t [RC], and (if it has a left neighbour) the
+// coupling row [El_t | Er_t] (n x n each, acting on columns t-1 and t) with
+// RHS e_t.  Level 0: C = W G, El = -V F, Er = V, e = V c.
+struct EntryView {
+  const double *C, *y, *El, *Er, *e;
+  int64_t sC, sy, sEl, sEr, se;  // per-column strides in doubles (0 = constant)
+  int RC;                        // row capacity of C (zero padded)
+};
+
+// AoS layout of a level >= 1 entry: [C (n x n) | y (n) | El (n x n) | Er (n x n) | e (n)]
+__host__ __device__ inline int64_t entry_doubles(int n) { return 3ll * n * n + 2ll * n; }
+// R record of an eliminated column: [Tl (n x n) | Tr (n x n) | P (n x n) | w (n)]
+__host__ __device__ inline int64_t rrec_doubles(int n) { return 3ll * n * n + n; }
+
+struct FactorLevelArgs {
+  EntryView in;
+  double *next;          // level L+1 entries, AoS, entry_doubles(n) each
+  double *rrec;          // R records, rrec_doubles(n) each, index t/2
+  int64_t K;             // columns at this level
+  int64_t t0;            // global offset of column 0 (has_left(t) = t + t0 > 0)
+  int n;
+  int level;             // L: column t <-> step ((t + 1) << (level - lbase)) - 1 + step0
+  int lbase;
+  int64_t step0;         // for status reporting only
+  unsigned long long *status;
+};
+
+struct BackwardLevelArgs {
+  const double *rrec;
+  int64_t K, t0;
+  int n;
+  int shift;             // level - lbase: column t <-> domain index ((t + 1) << shift) - 1
+  double *x;             // domain states   [*, n]
+  double *S;             // domain covariances [*, n, n]
+  const double *xhalo;   // domain index -1 (multi-GPU left neighbour), may be null
+  const double *Shalo;
+  const double *Xup;     // cross blocks of level L+1 (slot q at Xup + (q + 1) n^2), may be null
+  double *Xcur;          // cross blocks of level L to write (null at level 0 / when not needed)
+  int do_state, do_cov;
+};
+
+struct WhitenArgs {
+  int64_t N;             // steps
+  int n, m_max;
+  const int32_t *m;      // [N] or null
+  const double *F, *H, *c, *o, *K, *L;
+  int64_t sF, sH, sc, so, sK, sL;
+  int64_t first_global;  // global index of local step 0 (step 0 has no evolution row)
+  // outputs
+  double *C, *y, *El, *Er, *e;
+  int64_t cntE, cntC;    // number of distinct evolution / observation blocks (1 or N)
+  double *Mchol;         // [m_max x m_max] scratch when cntC == 1
+  unsigned long long *status;
+};
+
+// kernel launchers (ks_kernels.cu); return cudaGetLastError()
+cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s);
+cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s);
+cudaError_t launch_backward_level(const BackwardLevelArgs &a, cudaStream_t s);
+size_t factor_smem_bytes(int n, int RC);
+size_t backward_smem_bytes(int n);
+
+}  // namespace ks

@@ -1,0 +1,257 @@
+"""Thin ctypes binding of libks.so (include/ks.h) -- argument marshalling only.
+
+Every step of the smoother runs in the sm_100a kernels of ``csrc/``; this
+module only turns torch tensors into pointers, strides and a CUDA stream.
+There is no CPU fallback: if the extension is missing, importing
+``lib()`` raises.
+
+Names follow the ABI: ``ks_create``, ``ks_whiten``, ``ks_factor``,
+``ks_solve``, ``ks_selinv``, ``ks_get``.  ``Smoother`` bundles one context.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libks.so")
+
+KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
+    KS_ERR_WORKSPACE = range(8)
+KS_HOST_INPUTS, KS_OUTPUTS_BOUND = 1, 2
+FAMILIES = ("whiten", "factor", "backward", "boundary")
+
+EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
+           "ks_get", "ks_sync_status", "ks_boundary_buffers", "ks_factor_boundary",
+           "ks_set_timing", "ks_get_timing", "ks_info", "ks_strerror", "ks_destroy")
+
+
+class KsError(RuntimeError):
+    def __init__(self, code: int, what: str = "", step: int = -1, kind: int = 0):
+        msg = f"{what}: {strerror(code)} (code {code})"
+        if step >= 0:
+            msg += f" at step {step}" + (f" (kind {kind})" if kind else "")
+        super().__init__(msg)
+        self.code, self.step, self.kind = code, step, kind
+
+
+class ks_problem(C.Structure):
+    _fields_ = [("nsteps", C.c_int64), ("n", C.c_int32), ("m_max", C.c_int32),
+                ("m", C.c_void_p), ("F", C.c_void_p), ("H", C.c_void_p), ("c", C.c_void_p),
+                ("o", C.c_void_p), ("K", C.c_void_p), ("L", C.c_void_p),
+                ("sF", C.c_int64), ("sH", C.c_int64), ("sc", C.c_int64), ("so", C.c_int64),
+                ("sK", C.c_int64), ("sL", C.c_int64), ("flags", C.c_uint32)]
+
+
+class ks_shard(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_comm", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree libks.so; fail loudly if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, sz = C.c_void_p, C.c_int64, C.c_int, C.c_size_t
+        L.ks_workspace_bytes.argtypes = [C.POINTER(ks_problem), C.POINTER(ks_shard)]
+        L.ks_workspace_bytes.restype = sz
+        L.ks_create.argtypes = [C.POINTER(vp), C.POINTER(ks_problem), vp, sz, vp,
+                                C.POINTER(ks_shard), vp, vp]
+        for f in ("ks_whiten", "ks_factor", "ks_solve", "ks_selinv", "ks_factor_boundary"):
+            getattr(L, f).argtypes = [vp]
+        L.ks_get.argtypes = [vp, vp, vp]
+        L.ks_sync_status.argtypes = [vp, C.POINTER(i64), C.POINTER(i32)]
+        L.ks_boundary_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(sz)]
+        L.ks_set_timing.argtypes = [vp, i32]
+        L.ks_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64)]
+        L.ks_info.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.ks_strerror.argtypes = [i32]
+        L.ks_strerror.restype = C.c_char_p
+        L.ks_destroy.argtypes = [vp]
+        L.ks_destroy.restype = None
+        for f in EXPORTS:
+            if f not in ("ks_workspace_bytes", "ks_strerror", "ks_destroy"):
+                getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def strerror(code: int) -> str:
+    try:
+        return lib().ks_strerror(code).decode()
+    except ImportError:
+        return str(code)
+
+
+def _check(code: int, what: str):
+    if code != KS_OK:
+        raise KsError(code, what)
+
+
+def _stride(a: Optional[torch.Tensor]) -> int:
+    if a is None or a.shape[0] == 1:
+        return 0
+    return int(np.prod(a.shape[1:]))
+
+
+def _as_tensor(a, device, pin=False):
+    if a is None:
+        return None
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    if device is not None:
+        t = t.to(device)
+    elif pin and not t.is_pinned():
+        t = t.pin_memory()
+    return t.contiguous()
+
+
+class Smoother:
+    """One ks_ctx over a problem whose arrays are torch tensors (or numpy).
+
+    ``problem`` is any object with N, n, m_max, m, F, H, K, L, o, c attributes
+    (e.g. ``generators.Problem``).  ``host_inputs=True`` keeps the inputs in
+    pinned host memory and lets ks_whiten copy them (end-to-end path).
+    ``shard=(rank, nranks, nccl_comm_or_None)`` for time-sharded multi-GPU.
+    """
+
+    def __init__(self, problem, device="cuda", stream: Optional[torch.cuda.Stream] = None,
+                 host_inputs: bool = False, bind_outputs: bool = True, cov: bool = True,
+                 shard=None, inputs=None):
+        self.L = lib()
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        p = problem
+        self.N, self.n, self.m_max = int(p.N), int(p.n), int(p.m_max)
+        tgt = None if host_inputs else self.device
+        if inputs is None:
+            inputs = {k: _as_tensor(getattr(p, k), tgt, pin=host_inputs)
+                      for k in ("F", "H", "K", "L", "o", "c")}
+            inputs["m"] = _as_tensor(np.ascontiguousarray(p.m, np.int32), tgt, pin=host_inputs)
+        self.inputs = inputs  # keep alive (borrowed by the library)
+        for k in ("F", "H", "K", "L", "o", "c"):
+            t = inputs[k]
+            assert t is None or t.dtype == torch.float64
+        pr = ks_problem()
+        pr.nsteps, pr.n, pr.m_max = self.N, self.n, self.m_max
+        ptr = lambda t: None if t is None else t.data_ptr()
+        pr.m = ptr(inputs["m"])
+        pr.F, pr.H, pr.c, pr.o, pr.K, pr.L = (ptr(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
+        pr.sF, pr.sH, pr.sc, pr.so, pr.sK, pr.sL = (_stride(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
+        pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0)
+        self.problem = pr
+        self.shard = None
+        if shard is not None:
+            sh = ks_shard()
+            sh.rank, sh.nranks = int(shard[0]), int(shard[1])
+            sh.nccl_comm = shard[2] if len(shard) > 2 else None
+            self.shard = sh
+        shp = C.byref(self.shard) if self.shard is not None else None
+        nbytes = self.L.ks_workspace_bytes(C.byref(pr), shp)
+        if nbytes == 0:
+            raise KsError(KS_ERR_ARG, "ks_workspace_bytes")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.states = self.cov = None
+        if bind_outputs:
+            self.states = torch.empty((self.N, self.n), dtype=torch.float64, device=self.device)
+            if cov:
+                self.cov = torch.empty((self.N, self.n, self.n), dtype=torch.float64, device=self.device)
+        ctx = C.c_void_p()
+        _check(self.L.ks_create(C.byref(ctx), C.byref(pr), self.workspace.data_ptr(), nbytes,
+                                self.stream.cuda_stream, shp,
+                                None if self.states is None else self.states.data_ptr(),
+                                None if self.cov is None else self.cov.data_ptr()), "ks_create")
+        self.ctx = ctx
+
+    # --- the ABI calls -------------------------------------------------------
+    def whiten(self):
+        _check(self.L.ks_whiten(self.ctx), "ks_whiten")
+
+    def factor(self):
+        _check(self.L.ks_factor(self.ctx), "ks_factor")
+
+    def factor_boundary(self):
+        _check(self.L.ks_factor_boundary(self.ctx), "ks_factor_boundary")
+
+    def boundary_buffers(self):
+        s, r, b = C.c_void_p(), C.c_void_p(), C.c_size_t()
+        _check(self.L.ks_boundary_buffers(self.ctx, C.byref(s), C.byref(r), C.byref(b)),
+               "ks_boundary_buffers")
+        return s.value, r.value, b.value
+
+    def boundary_tensors(self):
+        """(send, recv) as uint8 views of the workspace: the caller-driven
+        boundary allgather is dist.all_gather_into_tensor(recv, send)."""
+        s, r, nb = self.boundary_buffers()
+        base = self.workspace.data_ptr()
+        P = self.shard.nranks
+        return (self.workspace[s - base:s - base + nb], self.workspace[r - base:r - base + P * nb])
+
+    def solve(self):
+        _check(self.L.ks_solve(self.ctx), "ks_solve")
+
+    def selinv(self):
+        _check(self.L.ks_selinv(self.ctx), "ks_selinv")
+
+    def get(self, states=None, cov=None):
+        """Copy results into torch tensors (device or host)."""
+        sp = None if states is None else states.data_ptr()
+        cp = None if cov is None else cov.data_ptr()
+        _check(self.L.ks_get(self.ctx, sp, cp), "ks_get")
+        return states, cov
+
+    def sync_status(self):
+        st, kd = C.c_int64(-1), C.c_int(0)
+        rc = self.L.ks_sync_status(self.ctx, C.byref(st), C.byref(kd))
+        return rc, st.value, kd.value
+
+    def check(self):
+        rc, st, kd = self.sync_status()
+        if rc != KS_OK:
+            raise KsError(rc, "ks_sync_status", st, kd)
+
+    def set_timing(self, on=True):
+        _check(self.L.ks_set_timing(self.ctx, 1 if on else 0), "ks_set_timing")
+
+    def timing(self):
+        ms = (C.c_double * 4)()
+        cnt = (C.c_int64 * 4)()
+        _check(self.L.ks_get_timing(self.ctx, ms, cnt), "ks_get_timing")
+        return {f: (ms[i], cnt[i]) for i, f in enumerate(FAMILIES)}
+
+    def info(self):
+        lv, la = C.c_int64(), C.c_int64()
+        _check(self.L.ks_info(self.ctx, C.byref(lv), C.byref(la)), "ks_info")
+        return {"levels": lv.value, "launches": la.value}
+
+    def run(self, cov: bool = True):
+        """whiten -> factor -> solve [-> selinv] (enqueue only)."""
+        self.whiten()
+        self.factor()
+        self.solve()
+        if cov:
+            self.selinv()
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                self.L.ks_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+
+def smooth(problem, cov: bool = True, device="cuda"):
+    """Convenience: full pipeline, returns (states, cov) as device tensors."""
+    s = Smoother(problem, device=device, cov=cov)
+    s.run(cov=cov)
+    s.check()
+    return s.states, s.cov

@@ -1,0 +1,206 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle.
+
+Metric: per-step normwise relative error,
+e_state = max_i |x_i - x_i^ora|_inf / |x_i^ora|_inf <= 1e-9 and
+e_cov   = max_i |S_ii - S_ii^ora|_max / |S_ii^ora|_max <= 1e-8 (BASELINE.json).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2502_11686_b200 import generators as gen
+from tests.dense import rel_cov_err, rel_state_err
+
+pytestmark = pytest.mark.gpu
+
+TOL_X, TOL_S = 1e-9, 1e-8
+
+
+def ks():
+    from paper_2502_11686_b200 import ks as _ks
+    return _ks
+
+
+def gpu_smooth(p, cov=True, **kw):
+    s = ks().Smoother(p, cov=cov, **kw)
+    s.run(cov=cov)
+    s.check()
+    x = s.states.cpu().numpy()
+    S = s.cov.cpu().numpy() if cov else None
+    return x, S, s
+
+
+def assert_parity(p, cov=True, **kw):
+    x, S, s = gpu_smooth(p, cov=cov, **kw)
+    xo, So = oracle.smooth(p)
+    ex = rel_state_err(x, xo)
+    assert ex <= TOL_X, f"{p.name} N={p.N}: state err {ex:.3e}"
+    if cov:
+        es = rel_cov_err(S, So)
+        assert es <= TOL_S, f"{p.name} N={p.N}: cov err {es:.3e}"
+        assert np.array_equal(S, np.swapaxes(S, 1, 2))
+    return s
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7, 8, 9, 15, 16, 17, 31, 33, 64, 100, 127, 257])
+@pytest.mark.parametrize("n", [1, 2, 3, 6])
+def test_random_small_all_parities(N, n):
+    rng = np.random.default_rng(N * 100 + n)
+    m = None if N > 1 else n
+    p = gen.random_problem(rng, N, n, m=m)
+    if N > 1:
+        p.m[-1] = max(p.m[-1], 1)
+    assert_parity(p)
+
+
+@pytest.mark.parametrize("const", [False, True])
+@pytest.mark.parametrize("n,mmax", [(4, 9), (8, 3), (12, 12), (24, 5), (48, 48)])
+def test_random_dims(n, mmax, const):
+    rng = np.random.default_rng(n * 7 + mmax)
+    N = 45
+    m = np.full(N, mmax, np.int32) if const else rng.integers(0, mmax + 1, N).astype(np.int32)
+    m[0] = max(m[0], n) if mmax >= n else m[0]
+    if mmax < n:
+        m[:] = mmax
+    p = gen.random_problem(rng, N, n, m=m, m_max=mmax, const=const)
+    assert_parity(p)
+
+
+@pytest.mark.parametrize("cfg,N", [("c1", None), ("c2", 2000), ("c3", 2001), ("c4", 301),
+                                   ("c5", 1 << 16), ("c5", 12345)])
+def test_configs_reduced(cfg, N):
+    assert_parity(gen.make(cfg, N=N))
+
+
+@pytest.mark.parametrize("n", [6, 48])
+def test_paper_benchmark_class(n):
+    """The paper's own problem class."""
+    assert_parity(gen.paper_problem(1000 if n == 6 else 200, n, seed=n))
+
+
+def test_nc_variant_states_only():
+    p = gen.make("c2", N=999)
+    x, _, s = gpu_smooth(p, cov=False)
+    assert rel_state_err(x, oracle.smooth(p, cov=False)) <= TOL_X
+
+
+def test_noise_free_recovery():
+    p = gen.make("c2", N=3000, noise_free=True)
+    x, _, _ = gpu_smooth(p, cov=False)
+    assert rel_state_err(x, p.x_true) <= 1e-9
+
+
+def test_determinism_bitwise():
+    p = gen.make("c3", N=5000)
+    x1, S1, _ = gpu_smooth(p)
+    x2, S2, _ = gpu_smooth(p)
+    assert np.array_equal(x1, x2) and np.array_equal(S1, S2)
+
+
+def test_host_inputs_and_get():
+    """KS_HOST_INPUTS (pinned host inputs, H2D inside ks_whiten) and ks_get
+    into host and device buffers give the same bits as device inputs."""
+    p = gen.make("c2", N=1500)
+    x1, S1, _ = gpu_smooth(p)
+    s = ks().Smoother(p, host_inputs=True, bind_outputs=False)
+    s.run()
+    xs = torch.empty((p.N, p.n), dtype=torch.float64).pin_memory()
+    Ss = torch.empty((p.N, p.n, p.n), dtype=torch.float64).pin_memory()
+    s.get(xs, Ss)
+    s.check()
+    assert np.array_equal(xs.numpy(), x1) and np.array_equal(Ss.numpy(), S1)
+    xd = torch.empty((p.N, p.n), dtype=torch.float64, device="cuda")
+    s.get(xd, None)
+    assert np.array_equal(xd.cpu().numpy(), x1)
+
+
+def test_level_count():
+    for N in (1, 2, 3, 7, 8, 9, 1000, 4096):
+        s = ks().Smoother(gen.make("c1", N=max(N, 2)) if N > 1 else gen.random_problem(
+            np.random.default_rng(0), 1, 2, m=2))
+        assert s.info()["levels"] == int(np.floor(np.log2(s.N))) + 1
+
+
+def test_error_not_spd():
+    rng = np.random.default_rng(9)
+    p = gen.random_problem(rng, 20, 3, m=3)
+    p.K[7] = -np.eye(3)
+    s = ks().Smoother(p)
+    s.run()
+    rc, step, kind = s.sync_status()
+    assert rc == ks().KS_ERR_NOT_SPD and step == 7 and kind == 1
+    p = gen.random_problem(rng, 20, 3, m=3)
+    p.L[11] = np.diag([1.0, 1.0, -2.0])
+    s = ks().Smoother(p)
+    s.run()
+    rc, step, kind = s.sync_status()
+    assert rc == ks().KS_ERR_NOT_SPD and step == 11 and kind == 2
+
+
+def test_error_rank():
+    rng = np.random.default_rng(10)
+    p = gen.random_problem(rng, 16, 2, m=0)
+    s = ks().Smoother(p)
+    s.run()
+    rc, _, _ = s.sync_status()
+    assert rc == ks().KS_ERR_RANK
+
+
+def test_error_order_and_args():
+    p = gen.make("c1", N=64)
+    s = ks().Smoother(p)
+    with pytest.raises(ks().KsError) as ei:
+        s.factor()
+    assert ei.value.code == ks().KS_ERR_ORDER
+    s.whiten()
+    with pytest.raises(ks().KsError):
+        s.solve()
+    with pytest.raises(ks().KsError):
+        s.get(torch.empty((64, 2), dtype=torch.float64, device="cuda"))
+
+
+def _virtual_shards(p, P, cov=True):
+    """The time-sharded multi-GPU algorithm with P ranks emulated on one GPU:
+    each rank's local levels run in its own context; the allgather is a
+    device copy into every rank's receive buffer (no rank waits on another)."""
+    M = p.N // P
+    parts = [ks().Smoother(p.slice(r * M, (r + 1) * M), shard=(r, P, None)) for r in range(P)]
+    for s in parts:
+        s.whiten()
+        s.factor()
+    views = [s.boundary_tensors() for s in parts]
+    gathered = torch.cat([snd for snd, _ in views])
+    for s, (_, rcv) in zip(parts, views):
+        rcv.copy_(gathered)
+        s.factor_boundary()
+        s.solve()
+        if cov:
+            s.selinv()
+    for s in parts:
+        s.check()
+    x = np.concatenate([s.states.cpu().numpy() for s in parts])
+    S = np.concatenate([s.cov.cpu().numpy() for s in parts]) if cov else None
+    return x, S
+
+
+@pytest.mark.parametrize("cfg,N,P", [("c5", 1 << 12, 2), ("c5", 1 << 12, 4), ("c5", 1 << 12, 8),
+                                     ("c2", 1 << 11, 2), ("c3", 1 << 11, 8), ("c1", 1 << 10, 4),
+                                     ("c2", 3 * 256, 3), ("c4", 64, 2)])
+def test_virtual_shards_match_oracle(cfg, N, P):
+    p = gen.make(cfg, N=N)
+    x, S = _virtual_shards(p, P)
+    xo, So = oracle.smooth(p)
+    assert rel_state_err(x, xo) <= TOL_X
+    assert rel_cov_err(S, So) <= TOL_S
+    x1, S1, _ = gpu_smooth(p)
+    if (N // P) & (N // P - 1) == 0 and P & (P - 1) == 0:
+        # power-of-two shards: same elimination order as one GPU
+        assert rel_state_err(x, x1) <= 1e-12 and rel_cov_err(S, S1) <= 1e-12
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+def test_configs_full_size(cfg):
+    """BASELINE.json configs at full size, every output compared."""
+    assert_parity(gen.make(cfg))
