@@ -151,8 +151,14 @@ int ks_factor_boundary(ks_ctx *ctx);
 int ks_set_timing(ks_ctx *ctx, int on);
 int ks_get_timing(ks_ctx *ctx, double ms[4], int64_t launches[4]);
 
-/* Number of factor levels (ceil(log2 N) + 1 on one GPU) and kernel launches
- * enqueued by the last whiten..selinv sequence. */
+/* The individual timed launches since ks_set_timing (synchronises): returns
+ * their count (negative = -error code) and fills up to `cap` entries of
+ * family[], level[] (recursion level L) and ms[]. */
+int64_t ks_get_launch_times(ks_ctx *ctx, int64_t cap, int32_t *family, int32_t *level, float *ms);
+
+/* Number of factor levels (floor(log2 N) + 1 on one GPU, plus the boundary
+ * levels when sharded) and the number of kernels launched by this context so
+ * far (cumulative). */
 int ks_info(ks_ctx *ctx, int64_t *levels, int64_t *launches);
 
 const char *ks_strerror(int code);

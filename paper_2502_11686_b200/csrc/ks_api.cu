@@ -94,7 +94,9 @@ struct ks_ctx {
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<int> ev_family;
+  std::vector<int> ev_family, ev_level;
+  std::vector<int32_t> rec_family, rec_level;
+  std::vector<float> rec_ms;
   double t_ms[4] = {0, 0, 0, 0};
   int64_t t_cnt[4] = {0, 0, 0, 0};
 };
@@ -204,7 +206,7 @@ struct Launch {
   ks_ctx *c;
   int fam;
   cudaEvent_t e1 = nullptr;
-  Launch(ks_ctx *c_, int f) : c(c_), fam(f) {
+  Launch(ks_ctx *c_, int f, int level, int nkernels = 1) : c(c_), fam(f) {
     if (c->timing) {
       if (c->ev_used + 2 > c->ev_pool.size()) {
         for (int i = 0; i < 64; ++i) {
@@ -216,9 +218,10 @@ struct Launch {
       cudaEvent_t e0 = c->ev_pool[c->ev_used++];
       e1 = c->ev_pool[c->ev_used++];
       c->ev_family.push_back(f);
+      c->ev_level.push_back(level);
       cudaEventRecord(e0, c->stream);
     }
-    c->launches++;
+    c->launches += nkernels;
   }
   ~Launch() {
     if (e1) cudaEventRecord(e1, c->stream);
@@ -234,6 +237,7 @@ EntryView level0_view(const ks_ctx *c) {
   v.El = c->El0; v.sEl = c->cntE == 1 ? 0 : nn;
   v.Er = c->Er0; v.sEr = c->cntE == 1 ? 0 : nn;
   v.e = c->e0; v.se = c->cntE == 1 ? 0 : n;
+  v.nrm = nullptr; v.snrm = 0;
   v.RC = mx;
   return v;
 }
@@ -242,7 +246,8 @@ EntryView aos_view(const double *ent, int n) {
   EntryView v;
   const int64_t E = entry_doubles(n), nn = (int64_t)n * n;
   v.C = ent; v.y = ent + nn; v.El = ent + nn + n; v.Er = ent + 2 * nn + n; v.e = ent + 3 * nn + n;
-  v.sC = v.sy = v.sEl = v.sEr = v.se = E;
+  v.nrm = ent + 3 * nn + 2 * n;
+  v.sC = v.sy = v.sEl = v.sEr = v.se = v.snrm = E;
   v.RC = n;
   return v;
 }
@@ -276,7 +281,7 @@ int run_factor_levels(ks_ctx *c, bool boundary) {
       else a.next = c->sharded ? c->send : nullptr;
       a.rrec = c->rrec[i];
     }
-    Launch l(c, boundary ? 3 : 1);
+    Launch l(c, boundary ? 3 : 1, L);
     cudaError_t e = launch_factor_level(a, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
@@ -313,7 +318,7 @@ int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
       else a.Xup = c->sharded ? c->Xq_local : nullptr;
       a.Xcur = (i >= 1) ? c->X[i] : nullptr;
     }
-    Launch l(c, boundary ? 3 : 2);
+    Launch l(c, boundary ? 3 : 2, (boundary ? c->q : 0) + i);
     cudaError_t e = launch_backward_level(a, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
@@ -422,7 +427,7 @@ int ks_whiten(ks_ctx *c) {
   a.C = c->C0; a.y = c->y0; a.El = c->El0; a.Er = c->Er0; a.e = c->e0;
   a.cntE = c->cntE; a.cntC = c->cntC; a.Mchol = c->Mchol; a.status = c->status;
   {
-    Launch l(c, 0);
+    Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->cntC == 1));
     e = launch_whiten(a, c->stream);
   }
   if (e != cudaSuccess) return cuda_fail(e);
@@ -528,15 +533,21 @@ int ks_sync_status(ks_ctx *c, int64_t *bad_step, int *bad_kind) {
 
 int ks_set_timing(ks_ctx *c, int on) {
   if (!c) return KS_ERR_ARG;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(e);
   c->timing = on != 0;
   c->ev_used = 0;
   c->ev_family.clear();
+  c->ev_level.clear();
+  c->rec_family.clear();
+  c->rec_level.clear();
+  c->rec_ms.clear();
   for (int f = 0; f < 4; ++f) { c->t_ms[f] = 0; c->t_cnt[f] = 0; }
   return KS_OK;
 }
 
-int ks_get_timing(ks_ctx *c, double ms[4], int64_t launches[4]) {
-  if (!c) return KS_ERR_ARG;
+namespace {
+int drain_events(ks_ctx *c) {
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_fail(e);
   for (size_t i = 0; i < c->ev_family.size(); ++i) {
@@ -544,14 +555,39 @@ int ks_get_timing(ks_ctx *c, double ms[4], int64_t launches[4]) {
     cudaEventElapsedTime(&t, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]);
     c->t_ms[c->ev_family[i]] += t;
     c->t_cnt[c->ev_family[i]] += 1;
+    c->rec_family.push_back(c->ev_family[i]);
+    c->rec_level.push_back(c->ev_level[i]);
+    c->rec_ms.push_back(t);
   }
   c->ev_used = 0;
   c->ev_family.clear();
+  c->ev_level.clear();
+  return KS_OK;
+}
+}  // namespace
+
+int ks_get_timing(ks_ctx *c, double ms[4], int64_t launches[4]) {
+  if (!c) return KS_ERR_ARG;
+  int r = drain_events(c);
+  if (r) return r;
   for (int f = 0; f < 4; ++f) {
     if (ms) ms[f] = c->t_ms[f];
     if (launches) launches[f] = c->t_cnt[f];
   }
   return KS_OK;
+}
+
+int64_t ks_get_launch_times(ks_ctx *c, int64_t cap, int32_t *family, int32_t *level, float *ms) {
+  if (!c) return -KS_ERR_ARG;
+  int r = drain_events(c);
+  if (r) return -r;
+  const int64_t cnt = (int64_t)c->rec_ms.size();
+  for (int64_t i = 0; i < cnt && i < cap; ++i) {
+    if (family) family[i] = c->rec_family[i];
+    if (level) level[i] = c->rec_level[i];
+    if (ms) ms[i] = c->rec_ms[i];
+  }
+  return cnt;
 }
 
 int ks_info(ks_ctx *c, int64_t *levels, int64_t *launches) {

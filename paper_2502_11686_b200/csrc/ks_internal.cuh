@@ -10,7 +10,9 @@ namespace ks {
 enum BadKind : int { kBadK = 1, kBadL = 2, kBadRank = 3 };
 constexpr unsigned long long kStatusOk = ~0ull;
 
-// Relative rank tolerance (header: |R_jj[d][d]| <= 1e-13 |stacked column|_F).
+// Relative rank tolerance: |R_jj[d][d]| <= 1e-13 * |block column j of UA|_F
+// (the Frobenius norm of the original whitened block column, which Q^T
+// preserves; reading R9).
 constexpr double kRankTol = 1e-13;
 
 // A level's reduced system: column t owns a C-like block
@@ -20,11 +22,14 @@ constexpr double kRankTol = 1e-13;
 struct EntryView {
   const double *C, *y, *El, *Er, *e;
   int64_t sC, sy, sEl, sEr, se;  // per-column strides in doubles (0 = constant)
+  const double *nrm;             // |UA block column|_F of the column (null at level 0:
+  int64_t snrm;                  //  computed from the whitened blocks)
   int RC;                        // row capacity of C (zero padded)
 };
 
-// AoS layout of a level >= 1 entry: [C (n x n) | y (n) | El (n x n) | Er (n x n) | e (n)]
-__host__ __device__ inline int64_t entry_doubles(int n) { return 3ll * n * n + 2ll * n; }
+// AoS layout of a level >= 1 entry:
+//   [C (n x n) | y (n) | El (n x n) | Er (n x n) | e (n) | nrm (1)]
+__host__ __device__ inline int64_t entry_doubles(int n) { return 3ll * n * n + 2ll * n + 1; }
 // R record of an eliminated column: [Tl (n x n) | Tr (n x n) | P (n x n) | w (n)]
 __host__ __device__ inline int64_t rrec_doubles(int n) { return 3ll * n * n + n; }
 

@@ -112,6 +112,29 @@ __device__ void cta_house(double *A, int lda, int rows, int npiv, int ncols, dou
   }
 }
 
+// Sum of squares of `count` contiguous doubles, reduced by warp 0 and
+// returned to every thread through sh[2].
+__device__ double cta_sumsq(const double *g, int count, double *sh) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < count; i += 32) s = fma(g[i], g[i], s);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (threadIdx.x == 0) sh[2] = s;
+  }
+  __syncthreads();
+  return sh[2];
+}
+
+// |UA block column of level-0 column t|_F^2 = |C_t|^2 + |Er_t|^2 + |El_{t+1}|^2.
+__device__ double col_norm2_l0(const EntryView &in, int n, int64_t t, bool hl, bool hr, double *sh) {
+  double s = cta_sumsq(in.C + t * in.sC, in.RC * n, sh);
+  if (hl) s += cta_sumsq(in.Er + t * in.sEr, n * n, sh);
+  if (hr) s += cta_sumsq(in.El + (t + 1) * in.sEl, n * n, sh);
+  return s;
+}
+
 struct FactorSmem {
   int lda1, lda2, lda3, szB;
   double *S1, *B, *Zs, *scr, *sh;
@@ -151,6 +174,16 @@ __device__ void eliminate(const FactorLevelArgs &a, FactorSmem &f, int64_t t, bo
   const int lda1 = f.lda1, lda2 = f.lda2, lda3 = f.lda3;
   double *S1 = f.S1, *B = f.B;
 
+  // reference norms for the rank test (column t) and for the survivor t+1
+  double nrm_t, nrm_u = 0.0;
+  if (in.nrm) {
+    nrm_t = in.nrm[t * in.snrm];
+    if (has_right) nrm_u = in.nrm[(t + 1) * in.snrm];
+  } else {
+    nrm_t = sqrt(col_norm2_l0(in, n, t, has_left, has_right, f.sh));
+    if (has_right) nrm_u = sqrt(col_norm2_l0(in, n, t + 1, true, t + 2 < a.K, f.sh));
+  }
+
   // ---- stage 1 ----
   ld_blk(S1, lda1, 0, 0, in.C + t * in.sC, n, RC, n, RC, 1.0);
   zero_blk(S1, lda1, 0, n, RC, n);
@@ -184,6 +217,7 @@ __device__ void eliminate(const FactorLevelArgs &a, FactorSmem &f, int64_t t, bo
     const int valid = rows3 < n ? rows3 : n;
     st_blk(ent, n, B, lda3, 0, 0, n, n, valid);             // C'
     st_blk(ent + n * n, 1, B, lda3, 0, n, n, 1, valid);     // y'
+    if (tid == 0) ent[3 * n * n + 2 * n] = nrm_u;
     __syncthreads();
   }
 
@@ -222,10 +256,7 @@ __device__ void eliminate(const FactorLevelArgs &a, FactorSmem &f, int64_t t, bo
 
   // ---- R record: rank check, T = R^{-1}[R_l R_r], w = R^{-1} z, P = R^{-1} R^{-T} ----
   if (tid == 0) {
-    double fro2 = 0.0;
-    for (int j = 0; j < n; ++j)
-      for (int i = 0; i <= j; ++i) fro2 = fma(B[i + j * lda2], B[i + j * lda2], fro2);
-    const double thr = kRankTol * sqrt(fro2);
+    const double thr = kRankTol * nrm_t;
     bool bad = false;
     for (int d = 0; d < n; ++d) bad |= !(fabs(B[d + d * lda2]) > thr);
     if (bad) {

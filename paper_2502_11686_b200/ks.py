@@ -27,7 +27,8 @@ FAMILIES = ("whiten", "factor", "backward", "boundary")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
            "ks_get", "ks_sync_status", "ks_boundary_buffers", "ks_factor_boundary",
-           "ks_set_timing", "ks_get_timing", "ks_info", "ks_strerror", "ks_destroy")
+           "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info", "ks_strerror",
+           "ks_destroy")
 
 
 class KsError(RuntimeError):
@@ -74,12 +75,15 @@ def lib():
         L.ks_set_timing.argtypes = [vp, i32]
         L.ks_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64)]
         L.ks_info.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
+        L.ks_get_launch_times.argtypes = [vp, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_float)]
+        L.ks_get_launch_times.restype = i64
         L.ks_strerror.argtypes = [i32]
         L.ks_strerror.restype = C.c_char_p
         L.ks_destroy.argtypes = [vp]
         L.ks_destroy.restype = None
         for f in EXPORTS:
-            if f not in ("ks_workspace_bytes", "ks_strerror", "ks_destroy"):
+            if f not in ("ks_workspace_bytes", "ks_strerror", "ks_destroy", "ks_get_launch_times"):
                 getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -226,6 +230,15 @@ class Smoother:
         cnt = (C.c_int64 * 4)()
         _check(self.L.ks_get_timing(self.ctx, ms, cnt), "ks_get_timing")
         return {f: (ms[i], cnt[i]) for i, f in enumerate(FAMILIES)}
+
+    def launch_times(self):
+        """[(family, level, ms)] of every timed launch since set_timing()."""
+        n = self.L.ks_get_launch_times(self.ctx, 0, None, None, None)
+        if n < 0:
+            raise KsError(-n, "ks_get_launch_times")
+        fam = (C.c_int32 * max(n, 1))(); lev = (C.c_int32 * max(n, 1))(); ms = (C.c_float * max(n, 1))()
+        self.L.ks_get_launch_times(self.ctx, n, fam, lev, ms)
+        return [(FAMILIES[fam[i]], lev[i], ms[i]) for i in range(n)]
 
     def info(self):
         lv, la = C.c_int64(), C.c_int64()
