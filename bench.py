@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: smoothed steps/s of the Odd-Even Kalman smoother (states +
+covariances, fp64) on BASELINE.json config 5 (k = 2^22 steps, n = 6, m = 3,
+constant-velocity model), time-sharded over N GPUs (strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ks|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = ks_whiten + ks_factor (+ boundary allgather + ks_factor_boundary
+on N > 1) + ks_solve + ks_selinv with inputs resident in HBM (outputs bound
+to caller buffers, so ks_get is free).  The working set (~11 GB) is far
+larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle
+(the reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+METRIC = "smoothed steps/s (states+covariances, fp64)"
+UNIT = "steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ks", choices=["ks", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--N", type=int, default=None, help="override the config's step count")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 21,
+                    help="steps of the workload the oracle cpu_baseline runs (~10 s)")
+    ap.add_argument("--ref-sample", type=int, default=1 << 18,
+                    help="steps per --impl reference step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="profiling runs: no e2e / cpu baseline")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload_desc(cfg, N):
+    d = {"c1": "k=1000, n=2, m=2 rotation model", "c2": "k=1e5, n=m=6 random SPD noise",
+         "c3": "k=1e5, n=6, m_i in {0,2,6}", "c4": "k=2e4, n=m=48",
+         "c5": "k=2^22, n=6, m=3 constant-velocity 3-D model"}[cfg]
+    return f"BASELINE.json config {cfg[1]} ({d}), N={N}"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.count(",") >= 8]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def roofline(launches, N, n, m, strides, p64_tf):
+    """Dominant launch (largest total time in the timed region) vs its roofline."""
+    from paper_2502_11686_b200 import model
+    groups = {}
+    for fam, lev, ms in launches:
+        groups.setdefault((fam, lev), []).append(ms)
+    (fam, lev), mss = max(groups.items(), key=lambda kv: sum(kv[1]))
+    avg_s = sum(mss) / len(mss) / 1e3
+    by, fl, units = model.launch_cost(fam, lev, N, n, m, strides)
+    bw, bw_src = peaks()
+    t_hbm, t_fp = by / (bw * 1e9), fl / (p64_tf * 1e12)
+    total = sum(sum(v) for v in groups.values())
+    share = sum(mss) / total
+    if t_hbm >= t_fp:
+        ach = by / avg_s / 1e9
+        r = {"bound": "hbm", "achieved": ach, "peak": bw, "unit": "GB/s", "frac": ach / bw,
+             "peak_source": bw_src}
+    else:
+        ach = fl / avg_s / 1e12
+        r = {"bound": "alu", "achieved": ach, "peak": p64_tf, "unit": "TFLOP/s", "frac": ach / p64_tf,
+             "peak_source": "measured fp64 DFMA peak (ks_peak_fp64_tflops, this run)"}
+    r.update({"traffic": None, "kernel": f"{fam}_level_kernel L={lev}", "launch_ms": avg_s * 1e3,
+              "share_of_step": share, "algorithmic_bytes": by, "algorithmic_flops": fl,
+              "units": units,
+              "other_roof_frac": (fl / avg_s / 1e12 / p64_tf) if r["bound"] == "hbm"
+              else (by / avg_s / 1e9 / bw)})
+    return r
+
+
+def run_reference(a, world, rank):
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2502_11686_b200 import generators as gen
+    N = a.N or gen.CONFIGS[a.config]["N"]
+    S = min(a.ref_sample, N)
+    p = gen.make(a.config, N=S)
+    oracle.build()
+    for _ in range(a.warmup):
+        oracle.smooth(p)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        oracle.smooth(p)
+    dt = (time.perf_counter() - t0) / a.steps
+    v = S / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(a.config, N), "parallelism": "1 host core"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"first {S} steps of the workload per step (plain-C "
+                                       f"sequential Paige-Saunders + Alg. 1, oracle/)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    a = parse()
+    world, rank, local = dist_env()
+    if a.impl == "reference":
+        return run_reference(a, world, rank)
+    from paper_2502_11686_b200 import generators as gen
+    from paper_2502_11686_b200 import ks, model
+    assert torch.cuda.is_available(), "bench needs a GPU (there is no CPU fallback)"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = world
+    p = gen.make(a.config, N=a.N)
+    N = p.N
+    assert N % P == 0, "steps must split evenly over ranks"
+    M = N // P
+    local_p = p.slice(rank * M, (rank + 1) * M) if P > 1 else p
+    strides = {"C": int(local_p.H.shape[0] > 1 or local_p.L.shape[0] > 1),
+               "E": int(local_p.F.shape[0] > 1 or local_p.K.shape[0] > 1 or local_p.c is not None)}
+    stream = torch.cuda.current_stream(dev)
+    p64 = ks.peak_fp64_tflops(stream)
+
+    sm = ks.Smoother(local_p, device=dev, shard=(rank, P, None) if P > 1 else None)
+    views = sm.boundary_tensors() if P > 1 else None
+
+    def step(s, v, get=None):
+        s.whiten()
+        s.factor()
+        if P > 1:
+            dist.all_gather_into_tensor(v[1], v[0])
+            s.factor_boundary()
+        s.solve()
+        s.selinv()
+        if get is not None:
+            s.get(*get)
+
+    for _ in range(max(a.warmup, 1)):
+        step(sm, views)
+    sm.check()
+    torch.cuda.synchronize()
+    if P > 1:
+        dist.barrier()
+    sm.set_timing(True)
+    l0 = sm.info()["launches"]
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if P > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step(sm, views)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if P > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    if P > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = sm.launch_times()
+    n_launch = (sm.info()["launches"] - l0) // a.steps
+    fam_ms = {}
+    for fam, lev, t in launches:
+        fam_ms[fam] = fam_ms.get(fam, 0.0) + t / a.steps
+    sm.set_timing(False)
+    sm.check()
+    value = N / (ms / 1e3)
+    rl = roofline(launches, M, p.n, p.m_max, strides, p64)
+    sb, sf = model.step_totals(M, p.n, p.m_max, strides)
+    bw = peaks()[0]
+    step_rl = {"algorithmic_bytes": sb, "algorithmic_flops": sf,
+               "hbm_frac": sb / (ms / 1e3) / 1e9 / bw, "fp64_frac": sf / (ms / 1e3) / 1e12 / p64}
+
+    e2e = None
+    if not (a.no_e2e or a.quick):
+        del sm
+        torch.cuda.empty_cache()
+        s2 = ks.Smoother(local_p, device=dev, host_inputs=True, bind_outputs=False,
+                         shard=(rank, P, None) if P > 1 else None)
+        v2 = s2.boundary_tensors() if P > 1 else None
+        xh = torch.empty((M, p.n), dtype=torch.float64).pin_memory()
+        Sh = torch.empty((M, p.n, p.n), dtype=torch.float64).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in s2.inputs.values() if t is not None)
+        d2h = xh.numel() * 8 + Sh.numel() * 8
+        ke = max(1, min(a.steps, 5))
+        for _ in range(max(a.warmup, 1)):
+            step(s2, v2, (xh, Sh))
+        s2.check()
+        if P > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(ke):
+            step(s2, v2, (xh, Sh))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        mse = e0.elapsed_time(e1) / ke
+        if P > 1:
+            t = torch.tensor([mse], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            mse = float(t.item())
+        e2e = {"value": N / (mse / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * P),
+               "d2h_bytes_per_step": int(d2h * P), "ms_per_step": mse, "steps": ke,
+               "path": "ks_create(KS_HOST_INPUTS) pinned host inputs -> whiten(H2D) .. selinv -> "
+                       "ks_get(pinned host states, cov)"}
+
+    cpu = None
+    if rank == 0 and P == 1 and not (a.no_cpu_baseline or a.quick):
+        import oracle
+        S = min(a.cpu_sample, N)
+        q = p.slice(0, S) if S < N else p
+        oracle.build()
+        t0 = time.perf_counter()
+        oracle.smooth(q)
+        dt = time.perf_counter() - t0
+        cpu = {"value": S / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {S} of the {N} steps, one pass of the plain-C sequential "
+                         f"Paige-Saunders + Alg. 1 oracle ({dt:.1f} s, 1 thread)",
+               "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": f"synthetic: generators.make('{a.config}') (seeded, BASELINE.json recipe)",
+                "config": {"workload": workload_desc(a.config, N), "N": N, "n": p.n, "m": p.m_max,
+                           "parallelism": f"time-shard x{P}" if P > 1 else "1 GPU",
+                           "l2": "working set (~11 GB at c5) >> 126 MB L2; no flush"},
+                "roofline": rl, "step_roofline": step_rl, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(n_launch), "clocks": clocks,
+                "phases_ms": fam_ms, "fp64_peak_tflops": p64}
+        print(json.dumps(line), flush=True)
+    if P > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

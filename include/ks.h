@@ -146,10 +146,12 @@ int ks_boundary_buffers(ks_ctx *ctx, void **send, void **recv, size_t *bytes);
 int ks_factor_boundary(ks_ctx *ctx);
 
 /* Per-kernel-family device timing with CUDA events recorded around every
- * launch (0 = off).  Families: 0 whiten, 1 factor levels, 2 backward levels,
- * 3 boundary/other.  ms[f] = summed event time, launches[f] = count. */
+ * launch on the context's stream (0 = off; ks_set_timing synchronises and
+ * resets).  Families: 0 whiten, 1 factor levels, 2 solve levels, 3 selinv
+ * levels, 4 multi-GPU boundary system.  ms[f] = summed event time,
+ * launches[f] = timed launches (synchronises). */
 int ks_set_timing(ks_ctx *ctx, int on);
-int ks_get_timing(ks_ctx *ctx, double ms[4], int64_t launches[4]);
+int ks_get_timing(ks_ctx *ctx, double ms[5], int64_t launches[5]);
 
 /* The individual timed launches since ks_set_timing (synchronises): returns
  * their count (negative = -error code) and fills up to `cap` entries of
@@ -160,6 +162,11 @@ int64_t ks_get_launch_times(ks_ctx *ctx, int64_t cap, int32_t *family, int32_t *
  * levels when sharded) and the number of kernels launched by this context so
  * far (cumulative). */
 int ks_info(ks_ctx *ctx, int64_t *levels, int64_t *launches);
+
+/* Diagnostics: measured fp64 FMA throughput of the current device in
+ * TFLOP/s (a DFMA-chain kernel over all SMs, best of 3, on `stream`), the
+ * FP64 roofline denominator (MEASURED_PEAKS.json has none).  <= 0 on error. */
+double ks_peak_fp64_tflops(void *stream);
 
 const char *ks_strerror(int code);
 void ks_destroy(ks_ctx *ctx);

@@ -97,8 +97,8 @@ struct ks_ctx {
   std::vector<int> ev_family, ev_level;
   std::vector<int32_t> rec_family, rec_level;
   std::vector<float> rec_ms;
-  double t_ms[4] = {0, 0, 0, 0};
-  int64_t t_cnt[4] = {0, 0, 0, 0};
+  double t_ms[5] = {0, 0, 0, 0, 0};
+  int64_t t_cnt[5] = {0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -281,13 +281,15 @@ int run_factor_levels(ks_ctx *c, bool boundary) {
       else a.next = c->sharded ? c->send : nullptr;
       a.rrec = c->rrec[i];
     }
-    Launch l(c, boundary ? 3 : 1, L);
+    Launch l(c, boundary ? 4 : 1, L);
     cudaError_t e = launch_factor_level(a, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
   return KS_OK;
 }
 
+// Timing families: 0 whiten, 1 factor levels, 2 solve levels, 3 selinv levels,
+// 4 boundary system (multi-GPU).
 int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
   const int n = c->n;
   const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
@@ -318,7 +320,7 @@ int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
       else a.Xup = c->sharded ? c->Xq_local : nullptr;
       a.Xcur = (i >= 1) ? c->X[i] : nullptr;
     }
-    Launch l(c, boundary ? 3 : 2, (boundary ? c->q : 0) + i);
+    Launch l(c, boundary ? 4 : (do_cov ? 3 : 2), (boundary ? c->q : 0) + i);
     cudaError_t e = launch_backward_level(a, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
@@ -542,7 +544,7 @@ int ks_set_timing(ks_ctx *c, int on) {
   c->rec_family.clear();
   c->rec_level.clear();
   c->rec_ms.clear();
-  for (int f = 0; f < 4; ++f) { c->t_ms[f] = 0; c->t_cnt[f] = 0; }
+  for (int f = 0; f < 5; ++f) { c->t_ms[f] = 0; c->t_cnt[f] = 0; }
   return KS_OK;
 }
 
@@ -566,11 +568,11 @@ int drain_events(ks_ctx *c) {
 }
 }  // namespace
 
-int ks_get_timing(ks_ctx *c, double ms[4], int64_t launches[4]) {
+int ks_get_timing(ks_ctx *c, double ms[5], int64_t launches[5]) {
   if (!c) return KS_ERR_ARG;
   int r = drain_events(c);
   if (r) return r;
-  for (int f = 0; f < 4; ++f) {
+  for (int f = 0; f < 5; ++f) {
     if (ms) ms[f] = c->t_ms[f];
     if (launches) launches[f] = c->t_cnt[f];
   }

@@ -23,12 +23,12 @@ LIB_PATH = os.path.join(_HERE, "libks.so")
 KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
     KS_ERR_WORKSPACE = range(8)
 KS_HOST_INPUTS, KS_OUTPUTS_BOUND = 1, 2
-FAMILIES = ("whiten", "factor", "backward", "boundary")
+FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
            "ks_get", "ks_sync_status", "ks_boundary_buffers", "ks_factor_boundary",
-           "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info", "ks_strerror",
-           "ks_destroy")
+           "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info",
+           "ks_peak_fp64_tflops", "ks_strerror", "ks_destroy")
 
 
 class KsError(RuntimeError):
@@ -78,12 +78,15 @@ def lib():
         L.ks_get_launch_times.argtypes = [vp, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                           C.POINTER(C.c_float)]
         L.ks_get_launch_times.restype = i64
+        L.ks_peak_fp64_tflops.argtypes = [vp]
+        L.ks_peak_fp64_tflops.restype = C.c_double
         L.ks_strerror.argtypes = [i32]
         L.ks_strerror.restype = C.c_char_p
         L.ks_destroy.argtypes = [vp]
         L.ks_destroy.restype = None
         for f in EXPORTS:
-            if f not in ("ks_workspace_bytes", "ks_strerror", "ks_destroy", "ks_get_launch_times"):
+            if f not in ("ks_workspace_bytes", "ks_strerror", "ks_destroy", "ks_get_launch_times",
+                         "ks_peak_fp64_tflops"):
                 getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -226,8 +229,8 @@ class Smoother:
         _check(self.L.ks_set_timing(self.ctx, 1 if on else 0), "ks_set_timing")
 
     def timing(self):
-        ms = (C.c_double * 4)()
-        cnt = (C.c_int64 * 4)()
+        ms = (C.c_double * 5)()
+        cnt = (C.c_int64 * 5)()
         _check(self.L.ks_get_timing(self.ctx, ms, cnt), "ks_get_timing")
         return {f: (ms[i], cnt[i]) for i, f in enumerate(FAMILIES)}
 
@@ -260,6 +263,12 @@ class Smoother:
                 self.ctx = None
         except Exception:
             pass
+
+
+def peak_fp64_tflops(stream=None) -> float:
+    """Measured DFMA throughput (TFLOP/s) of the current device."""
+    st = stream if stream is not None else torch.cuda.current_stream()
+    return float(lib().ks_peak_fp64_tflops(st.cuda_stream))
 
 
 def smooth(problem, cov: bool = True, device="cuda"):
