@@ -54,9 +54,12 @@ enum {
 enum {
     KS_HOST_INPUTS = 1u,  /* F,H,c,o,K,L,m are HOST pointers (pinned recommended);
                              ks_whiten copies them into the workspace first      */
-    KS_OUTPUTS_BOUND = 2u /* the caller binds states_out (and cov_out, unless it
+    KS_OUTPUTS_BOUND = 2u,/* the caller binds states_out (and cov_out, unless it
                              never calls ks_selinv) in ks_create, so the
                              workspace holds no output buffers                   */
+    KS_GENERIC_PATH = 4u  /* force the CTA-per-pair shared-memory kernels even
+                             when n, m_max <= 8 (default there: one thread per
+                             pair, registers + Givens; used to cross-check)     */
 };
 
 /* One problem (or, multi-GPU, one rank's contiguous shard of steps).
@@ -77,7 +80,7 @@ typedef struct ks_problem {
     const double *K;         /* [N][n][n]      evolution-noise covariance (SPD)     */
     const double *L;         /* [N][m_max][m_max] observation-noise covariance (SPD) */
     int64_t sF, sH, sc, so, sK, sL;   /* per-step strides in doubles, 0 = constant */
-    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND                  */
+    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH */
 } ks_problem;
 
 #define KS_MAX_N 64

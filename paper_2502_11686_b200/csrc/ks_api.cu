@@ -85,6 +85,11 @@ struct ks_ctx {
   std::vector<double *> entb, rrecb, Xb;
   double *send = nullptr, *recv = nullptr, *bx = nullptr, *bS = nullptr, *hx = nullptr,
          *hS = nullptr, *Xq_local = nullptr;
+  // small-n path (ks_small.cu): element-major level arrays
+  bool small = false;
+  int64_t ldN = 0;
+  std::vector<int64_t> ent_ld, rec_ld, X_ld, entb_ld, recb_ld, Xb_ld;
+  double *nC0 = nullptr, *nEr0 = nullptr, *nEl0 = nullptr, *zscratch = nullptr;
   // outputs
   double *xout = nullptr, *Sout = nullptr;
   int stage = 0;  // 0 created, 1 whitened, 2 local-factored (sharded), 3 factored
@@ -111,6 +116,12 @@ int cuda_fail(cudaError_t e) {
 
 bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 
+bool use_small(const ks_problem *p) {
+  return p->n <= kSmallMaxN && p->m_max <= kSmallMaxM && !(p->flags & KS_GENERIC_PATH);
+}
+
+int64_t round32(int64_t x) { return (x + 31) & ~int64_t(31); }
+
 int validate(const ks_problem *p, const ks_shard *sh) {
   if (!p) return KS_ERR_ARG;
   if (p->nsteps < 1 || p->n < 1 || p->n > KS_MAX_N || p->m_max < 0 || p->m_max > KS_MAX_M)
@@ -121,9 +132,11 @@ int validate(const ks_problem *p, const ks_shard *sh) {
   if ((p->sF && p->sF < n * n) || (p->sK && p->sK < n * n) || (p->sH && p->sH < mx * n) ||
       (p->sL && p->sL < mx * mx) || (p->sc && p->sc < n) || (p->so && p->so < mx))
     return KS_ERR_ARG;
-  if (p->flags & ~(uint32_t)(KS_HOST_INPUTS | KS_OUTPUTS_BOUND)) return KS_ERR_ARG;
-  if (factor_smem_bytes(p->n, p->m_max > p->n ? p->m_max : p->n) > 227 * 1024) return KS_ERR_ARG;
-  if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
+  if (p->flags & ~(uint32_t)(KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH)) return KS_ERR_ARG;
+  if (!use_small(p)) {
+    if (factor_smem_bytes(p->n, p->m_max > p->n ? p->m_max : p->n) > 227 * 1024) return KS_ERR_ARG;
+    if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
+  }
   if (sh) {
     if (sh->nranks < 1 || sh->rank < 0 || sh->rank >= sh->nranks) return KS_ERR_ARG;
     if (sh->nranks > 1 && (!is_pow2(p->nsteps) || p->nsteps < 2)) return KS_ERR_ARG;
@@ -157,21 +170,43 @@ size_t carve(ks_ctx *c, char *base) {
   }
   c->cntE = (p.sF == 0 && p.sK == 0 && (p.c == nullptr || p.sc == 0)) ? 1 : N;
   c->cntC = (p.sH == 0 && p.sL == 0 && p.m == nullptr) ? 1 : N;
-  c->El0 = w.take<double>(c->cntE * nn);
-  c->Er0 = w.take<double>(c->cntE * nn);
-  c->e0 = w.take<double>(c->cntE * n);
-  c->C0 = w.take<double>(c->cntC * mx * n + 1);
-  c->y0 = w.take<double>(N * mx + 1);
+  const bool sm = c->small;
+  const int64_t Rs = small_rrec_doubles(n);
+  if (sm) {
+    c->ldN = round32(N);
+    const int64_t colsE = c->cntE == 1 ? 1 : c->ldN, colsC = c->cntC == 1 ? 1 : c->ldN;
+    c->El0 = w.take<double>(nn * colsE);
+    c->Er0 = w.take<double>(nn * colsE);
+    c->e0 = w.take<double>(n * colsE);
+    c->nEr0 = w.take<double>(colsE);
+    c->nEl0 = w.take<double>(colsE);
+    c->C0 = w.take<double>(mx * n * colsC + 1);
+    c->nC0 = w.take<double>(colsC);
+    c->y0 = w.take<double>(mx * c->ldN + 1);
+    c->zscratch = w.take<double>(nn + n);
+  } else {
+    c->El0 = w.take<double>(c->cntE * nn);
+    c->Er0 = w.take<double>(c->cntE * nn);
+    c->e0 = w.take<double>(c->cntE * n);
+    c->C0 = w.take<double>(c->cntC * mx * n + 1);
+    c->y0 = w.take<double>(N * mx + 1);
+  }
   c->Mchol = w.take<double>((size_t)mx * mx + 1);
   // local levels
   c->K_.clear(); c->ent.clear(); c->rrec.clear(); c->X.clear();
+  c->ent_ld.clear(); c->rec_ld.clear(); c->X_ld.clear();
   int64_t K = N;
   for (int L = 0;; ++L) {
     if (c->sharded && L == c->q) break;
     c->K_.push_back(K);
-    c->ent.push_back(L == 0 ? nullptr : w.take<double>(K * E));
-    c->rrec.push_back(w.take<double>(((K + 1) / 2) * Rr));
-    c->X.push_back(L == 0 ? nullptr : w.take<double>((K + 1) * nn));
+    const int64_t le = sm ? round32(K) : K, lr = sm ? round32((K + 1) / 2) : (K + 1) / 2,
+                  lx = sm ? round32(K + 1) : K + 1;
+    c->ent_ld.push_back(le);
+    c->rec_ld.push_back(lr);
+    c->X_ld.push_back(lx);
+    c->ent.push_back(L == 0 ? nullptr : w.take<double>(le * E));
+    c->rrec.push_back(w.take<double>(lr * (sm ? Rs : Rr)));
+    c->X.push_back(L == 0 ? nullptr : w.take<double>(lx * nn));
     if (K == 1) break;
     K /= 2;
   }
@@ -185,12 +220,18 @@ size_t carve(ks_ctx *c, char *base) {
     c->bx = w.take<double>((int64_t)P * n);
     c->bS = w.take<double>((int64_t)P * nn);
     c->Kb.clear(); c->entb.clear(); c->rrecb.clear(); c->Xb.clear();
+    c->entb_ld.clear(); c->recb_ld.clear(); c->Xb_ld.clear();
     int64_t Kb = P;
     for (int L = 0;; ++L) {
       c->Kb.push_back(Kb);
-      c->entb.push_back(L == 0 ? c->recv : w.take<double>(Kb * E));
-      c->rrecb.push_back(w.take<double>(((Kb + 1) / 2) * Rr));
-      c->Xb.push_back(w.take<double>((Kb + 1) * nn));
+      const int64_t le = sm ? round32(Kb) : Kb, lr = sm ? round32((Kb + 1) / 2) : (Kb + 1) / 2,
+                    lx = sm ? round32(Kb + 1) : Kb + 1;
+      c->entb_ld.push_back(L == 0 ? -1 : le);      // level q entries: the AoS recv buffer
+      c->recb_ld.push_back(lr);
+      c->Xb_ld.push_back(lx);
+      c->entb.push_back(L == 0 ? c->recv : w.take<double>(le * E));
+      c->rrecb.push_back(w.take<double>(lr * (sm ? Rs : Rr)));
+      c->Xb.push_back(w.take<double>(lx * nn));
       if (Kb == 1) break;
       Kb /= 2;
     }
@@ -252,7 +293,139 @@ EntryView aos_view(const double *ent, int n) {
   return v;
 }
 
+// ---- small-path views (element e of column t at p[e*es + t*cs]) ----
+CArr carr(const double *p, int64_t es, int64_t cs) { return CArr{p, es, cs}; }
+Arr arr(double *p, int64_t es, int64_t cs) { return Arr{p, es, cs}; }
+
+// entry field offsets (elements): C, y, El, Er, e, nrm
+void entry_offsets(int n, int64_t off[6]) {
+  const int64_t nn = (int64_t)n * n;
+  off[0] = 0; off[1] = nn; off[2] = nn + n; off[3] = 2 * nn + n; off[4] = 3 * nn + n; off[5] = 3 * nn + 2 * n;
+}
+
+// ld > 0: element-major with leading dimension ld; ld < 0: AoS records.
+SmallIn small_in(const double *base, int64_t ld, int n) {
+  int64_t o[6];
+  entry_offsets(n, o);
+  const int64_t E = entry_doubles(n);
+  const int64_t es = ld > 0 ? ld : 1, cs = ld > 0 ? 1 : E;
+  SmallIn v;
+  v.C = carr(base + o[0] * es, es, cs); v.y = carr(base + o[1] * es, es, cs);
+  v.El = carr(base + o[2] * es, es, cs); v.Er = carr(base + o[3] * es, es, cs);
+  v.e = carr(base + o[4] * es, es, cs); v.nrm = carr(base + o[5] * es, es, cs);
+  v.nC = v.nEr = v.nEl = carr(nullptr, 0, 0);
+  v.RC = n; v.tri = 1;
+  return v;
+}
+
+SmallOut small_out(double *base, int64_t ld, int n) {
+  SmallOut v;
+  if (!base) { v.C = v.y = v.El = v.Er = v.e = v.nrm = arr(nullptr, 0, 0); return v; }
+  int64_t o[6];
+  entry_offsets(n, o);
+  const int64_t E = entry_doubles(n);
+  const int64_t es = ld > 0 ? ld : 1, cs = ld > 0 ? 1 : E;
+  v.C = arr(base + o[0] * es, es, cs); v.y = arr(base + o[1] * es, es, cs);
+  v.El = arr(base + o[2] * es, es, cs); v.Er = arr(base + o[3] * es, es, cs);
+  v.e = arr(base + o[4] * es, es, cs); v.nrm = arr(base + o[5] * es, es, cs);
+  return v;
+}
+
+SmallIn small_level0(const ks_ctx *c) {
+  const bool cE = c->cntE == 1, cC = c->cntC == 1;
+  const int64_t esE = cE ? 1 : c->ldN, csE = cE ? 0 : 1, esC = cC ? 1 : c->ldN, csC = cC ? 0 : 1;
+  SmallIn v;
+  v.C = carr(c->C0, esC, csC);
+  v.y = carr(c->y0, c->ldN, 1);
+  v.El = carr(c->El0, esE, csE);
+  v.Er = carr(c->Er0, esE, csE);
+  v.e = carr(c->e0, esE, csE);
+  v.nrm = carr(nullptr, 0, 0);
+  v.nC = carr(c->nC0, 1, csC);
+  v.nEr = carr(c->nEr0, 1, csE);
+  v.nEl = carr(c->nEl0, 1, csE);
+  v.RC = c->mx; v.tri = 0;
+  return v;
+}
+
+SmallRec small_rec(double *base, int64_t ld, int n) {
+  const int64_t nn = (int64_t)n * n;
+  SmallRec r;
+  r.Tl = arr(base, ld, 1);
+  r.Tr = arr(base + nn * ld, ld, 1);
+  r.w = arr(base + 2 * nn * ld, ld, 1);
+  r.P = arr(base + (2 * nn + n) * ld, ld, 1);
+  return r;
+}
+
+int run_small_factor_levels(ks_ctx *c, bool boundary) {
+  const int n = c->n;
+  const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
+  const int Lb = boundary ? c->q : 0;
+  for (size_t i = 0; i < Ks.size(); ++i) {
+    SmallFactorArgs a;
+    const int L = Lb + (int)i;
+    const bool last = i + 1 == Ks.size();
+    if (!boundary) {
+      a.in = (i == 0) ? small_level0(c) : small_in(c->ent[i], c->ent_ld[i], n);
+      if (!last) a.out = small_out(c->ent[i + 1], c->ent_ld[i + 1], n);
+      else a.out = small_out(c->sharded ? c->send : nullptr, -1, n);
+      a.rec = small_rec(c->rrec[i], c->rec_ld[i], n);
+      a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+    } else {
+      a.in = small_in(c->entb[i], c->entb_ld[i], n);
+      a.out = small_out(last ? nullptr : c->entb[i + 1], last ? -1 : c->entb_ld[i + 1], n);
+      a.rec = small_rec(c->rrecb[i], c->recb_ld[i], n);
+      a.t0 = 0;
+    }
+    a.K = Ks[i];
+    a.level = L;
+    a.lbase = boundary ? c->q : 0;
+    a.step0 = 0;
+    a.status = c->status;
+    a.zscratch = c->zscratch;
+    Launch l(c, boundary ? 4 : 1, L);
+    cudaError_t e = launch_small_factor(a, n, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return KS_OK;
+}
+
+int run_small_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
+  const int n = c->n;
+  const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
+  for (int i = (int)Ks.size() - 1; i >= 0; --i) {
+    SmallBackwardArgs a;
+    const SmallRec r = small_rec(boundary ? c->rrecb[i] : c->rrec[i], boundary ? c->recb_ld[i] : c->rec_ld[i], n);
+    a.Tl = carr(r.Tl.p, r.Tl.es, 1); a.Tr = carr(r.Tr.p, r.Tr.es, 1);
+    a.w = carr(r.w.p, r.w.es, 1); a.P = carr(r.P.p, r.P.es, 1);
+    a.K = Ks[i];
+    a.shift = i;
+    a.do_state = do_state;
+    a.do_cov = do_cov;
+    const bool top = i + 1 == (int)Ks.size();
+    if (boundary) {
+      a.t0 = 0;
+      a.x = c->bx; a.S = c->bS; a.xhalo = nullptr; a.Shalo = nullptr;
+      a.Xup = top ? carr(nullptr, 0, 0) : carr(c->Xb[i + 1], c->Xb_ld[i + 1], 1);
+      a.Xcur = arr(c->Xb[i], c->Xb_ld[i], 1);
+    } else {
+      a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+      a.x = c->xout; a.S = c->Sout; a.xhalo = c->hx; a.Shalo = c->hS;
+      if (!top) a.Xup = carr(c->X[i + 1], c->X_ld[i + 1], 1);
+      else a.Xup = c->sharded ? carr(c->Xq_local, 2, 1) : carr(nullptr, 0, 0);
+      a.Xcur = (i >= 1) ? arr(c->X[i], c->X_ld[i], 1) : arr(nullptr, 0, 0);
+    }
+    if (!do_cov) a.Xcur = arr(nullptr, 0, 0);
+    Launch l(c, boundary ? 4 : (do_cov ? 3 : 2), (boundary ? c->q : 0) + i);
+    cudaError_t e = launch_small_backward(a, n, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return KS_OK;
+}
+
 int run_factor_levels(ks_ctx *c, bool boundary) {
+  if (c->small) return run_small_factor_levels(c, boundary);
   const int n = c->n;
   const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
   const int Lb = boundary ? c->q : 0;
@@ -291,6 +464,7 @@ int run_factor_levels(ks_ctx *c, bool boundary) {
 // Timing families: 0 whiten, 1 factor levels, 2 solve levels, 3 selinv levels,
 // 4 boundary system (multi-GPU).
 int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
+  if (c->small) return run_small_backward_levels(c, boundary, do_state, do_cov);
   const int n = c->n;
   const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
   for (int i = (int)Ks.size() - 1; i >= 0; --i) {
@@ -342,9 +516,14 @@ int scatter_boundary(ks_ctx *c, bool states, bool cov) {
     if (r > 0 && e == cudaSuccess) {
       e = cudaMemcpyAsync(c->hS, c->bS + (r - 1) * nn, nn * 8, cudaMemcpyDeviceToDevice, c->stream);
       // slot -1 of the local level-q cross array: S_{b_{r-1}, b_r} = boundary X_q slot r-1
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(c->Xq_local, c->Xb[0] + (int64_t)r * nn, nn * 8, cudaMemcpyDeviceToDevice,
-                            c->stream);
+      if (e == cudaSuccess) {
+        if (c->small)   // element-major: slot r-1 is column r of Xb[0]; Xq_local has ld 2
+          e = cudaMemcpy2DAsync(c->Xq_local, 2 * 8, c->Xb[0] + r, c->Xb_ld[0] * 8, 8, nn,
+                                cudaMemcpyDeviceToDevice, c->stream);
+        else
+          e = cudaMemcpyAsync(c->Xq_local, c->Xb[0] + (int64_t)r * nn, nn * 8, cudaMemcpyDeviceToDevice,
+                              c->stream);
+      }
     }
   }
   return cuda_fail(e);
@@ -360,6 +539,7 @@ size_t ks_workspace_bytes(const ks_problem *p, const ks_shard *sh) {
   c.p = *p;
   c.N = p->nsteps; c.n = p->n; c.mx = p->m_max;
   c.host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
+  c.small = use_small(p);
   if (sh && sh->nranks > 1) {
     c.sharded = true; c.rank = sh->rank; c.nranks = sh->nranks;
     int q = 0;
@@ -384,6 +564,7 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
   c->N = p->nsteps; c->n = p->n; c->mx = p->m_max;
   c->stream = (cudaStream_t)stream;
   c->host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
+  c->small = use_small(p);
   if (sh && sh->nranks > 1) {
     c->sharded = true; c->rank = sh->rank; c->nranks = sh->nranks; c->comm = sh->nccl_comm;
     int q = 0;
@@ -420,6 +601,29 @@ int ks_whiten(ks_ctx *c) {
         e = cudaMemcpyAsync(x.d, x.h, x.bytes, cudaMemcpyHostToDevice, c->stream);
         if (e != cudaSuccess) return cuda_fail(e);
       }
+  }
+  if (c->small) {
+    SmallWhitenArgs a;
+    a.N = c->N; a.n = c->n; a.m_max = c->mx; a.m = c->m;
+    a.F = c->F; a.H = c->H; a.c = c->c; a.o = c->o; a.K = c->K; a.L = c->L;
+    a.sF = c->p.sF; a.sH = c->p.sH; a.sc = c->p.sc; a.so = c->p.so; a.sK = c->p.sK; a.sL = c->p.sL;
+    a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
+    a.cntE = c->cntE; a.cntC = c->cntC;
+    const bool cE = c->cntE == 1, cC = c->cntC == 1;
+    const int64_t esE = cE ? 1 : c->ldN, csE = cE ? 0 : 1, esC = cC ? 1 : c->ldN, csC = cC ? 0 : 1;
+    a.C = arr(c->C0, esC, csC); a.y = arr(c->y0, c->ldN, 1);
+    a.El = arr(c->El0, esE, csE); a.Er = arr(c->Er0, esE, csE); a.e = arr(c->e0, esE, csE);
+    a.nC = arr(c->nC0, 1, csC); a.nEr = arr(c->nEr0, 1, csE); a.nEl = arr(c->nEl0, 1, csE);
+    a.Mchol = c->Mchol; a.status = c->status;
+    int nl = 0;
+    {
+      Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->cntC == 1));
+      e = launch_small_whiten(a, c->stream, &nl);
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    c->stage = 1;
+    c->solved = c->covd = false;
+    return KS_OK;
   }
   WhitenArgs a;
   a.N = c->N; a.n = c->n; a.m_max = c->mx; a.m = c->m;

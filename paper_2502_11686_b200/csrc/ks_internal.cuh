@@ -74,6 +74,74 @@ struct WhitenArgs {
   unsigned long long *status;
 };
 
+// ---------------------------------------------------------------------------
+// Small-n path (n <= 8, m_max <= 8; ks_small.cu): one thread per column pair,
+// blocks in registers, Givens row streaming, element-major (SoA) level arrays.
+// ---------------------------------------------------------------------------
+constexpr int kSmallMaxN = 8;
+constexpr int kSmallMaxM = 8;
+
+// Strided view: element e of column t lives at p[e * es + t * cs]
+// (SoA: es = leading dimension, cs = 1; AoS: es = 1, cs = record size;
+//  constant: es = 1, cs = 0).
+struct Arr {
+  double *p;
+  int64_t es, cs;
+};
+struct CArr {
+  const double *p;
+  int64_t es, cs;
+};
+
+struct SmallIn {               // level-L columns
+  CArr C, y, El, Er, e, nrm;   // C: RC x n row-major (upper triangular when tri)
+  CArr nC, nEr, nEl;           // level 0 only: |C_j|^2, |Er_j|^2, |El_j|^2 (rank reference)
+  int RC, tri;
+};
+struct SmallOut {              // level-(L+1) survivor columns (tri C)
+  Arr C, y, El, Er, e, nrm;
+};
+struct SmallRec {              // R record: T_l, T_r (n x n), w (n), P (packed upper n(n+1)/2)
+  Arr Tl, Tr, w, P;
+};
+struct SmallFactorArgs {
+  SmallIn in;
+  SmallOut out;
+  SmallRec rec;
+  int64_t K, t0;
+  int level, lbase;
+  int64_t step0;
+  unsigned long long *status;
+  double *zscratch;            // n (n + 1) doubles: the odd level's last-column leftover Z
+};
+struct SmallBackwardArgs {
+  CArr Tl, Tr, w, P;
+  int64_t K, t0;
+  int shift;
+  double *x, *S;               // domain outputs, row-major [*, n] / [*, n, n]
+  const double *xhalo, *Shalo;
+  CArr Xup;                    // S_{q,q+1} of level L+1 at column q+1 (p null: none)
+  Arr Xcur;                    // level-L cross blocks to write (p null: skip)
+  int do_state, do_cov;
+};
+struct SmallWhitenArgs {
+  int64_t N;
+  int n, m_max;
+  const int32_t *m;
+  const double *F, *H, *c, *o, *K, *L;
+  int64_t sF, sH, sc, so, sK, sL;
+  int64_t first_global;
+  int64_t cntE, cntC;
+  Arr C, y, El, Er, e, nC, nEr, nEl;
+  double *Mchol;               // m_max^2 scratch (constant observation model)
+  unsigned long long *status;
+};
+size_t small_entry_doubles(int n);                  // = entry_doubles(n)
+int64_t small_rrec_doubles(int n);                  // 2 n^2 + n + n(n+1)/2
+cudaError_t launch_small_whiten(const SmallWhitenArgs &a, cudaStream_t s, int *nlaunch);
+cudaError_t launch_small_factor(const SmallFactorArgs &a, int n, cudaStream_t s);
+cudaError_t launch_small_backward(const SmallBackwardArgs &a, int n, cudaStream_t s);
+
 // kernel launchers (ks_kernels.cu); return cudaGetLastError()
 cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s);
 cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s);

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "libks.so")
 
 KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
     KS_ERR_WORKSPACE = range(8)
-KS_HOST_INPUTS, KS_OUTPUTS_BOUND = 1, 2
+KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH = 1, 2, 4
 FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
@@ -132,7 +132,7 @@ class Smoother:
 
     def __init__(self, problem, device="cuda", stream: Optional[torch.cuda.Stream] = None,
                  host_inputs: bool = False, bind_outputs: bool = True, cov: bool = True,
-                 shard=None, inputs=None):
+                 shard=None, inputs=None, generic: bool = False):
         self.L = lib()
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -142,7 +142,10 @@ class Smoother:
         if inputs is None:
             inputs = {k: _as_tensor(getattr(p, k), tgt, pin=host_inputs)
                       for k in ("F", "H", "K", "L", "o", "c")}
-            inputs["m"] = _as_tensor(np.ascontiguousarray(p.m, np.int32), tgt, pin=host_inputs)
+            m = np.ascontiguousarray(p.m, np.int32)
+            # all m_i == m_max: pass m = NULL (lets a constant observation model
+            # be whitened once, stride 0)
+            inputs["m"] = None if bool(np.all(m == p.m_max)) else _as_tensor(m, tgt, pin=host_inputs)
         self.inputs = inputs  # keep alive (borrowed by the library)
         for k in ("F", "H", "K", "L", "o", "c"):
             t = inputs[k]
@@ -153,7 +156,8 @@ class Smoother:
         pr.m = ptr(inputs["m"])
         pr.F, pr.H, pr.c, pr.o, pr.K, pr.L = (ptr(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
         pr.sF, pr.sH, pr.sc, pr.so, pr.sK, pr.sL = (_stride(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
-        pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0)
+        pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0) | \
+            (KS_GENERIC_PATH if generic else 0)
         self.problem = pr
         self.shard = None
         if shard is not None:

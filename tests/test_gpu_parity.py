@@ -43,15 +43,20 @@ def assert_parity(p, cov=True, **kw):
     return s
 
 
+@pytest.mark.parametrize("generic", [False, True])
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7, 8, 9, 15, 16, 17, 31, 33, 64, 100, 127, 257])
-@pytest.mark.parametrize("n", [1, 2, 3, 6])
-def test_random_small_all_parities(N, n):
+@pytest.mark.parametrize("n", [1, 2, 3, 6, 8])
+def test_random_small_all_parities(N, n, generic):
+    """Both kernel families: the small-n register path (default for n, m <= 8)
+    and the CTA shared-memory path (KS_GENERIC_PATH)."""
     rng = np.random.default_rng(N * 100 + n)
     m = None if N > 1 else n
-    p = gen.random_problem(rng, N, n, m=m)
+    p = gen.random_problem(rng, N, n, m=m, m_max=n + 1 if n < 8 else 8)
+    if n == 8:
+        p.m = np.minimum(p.m, 8)
     if N > 1:
         p.m[-1] = max(p.m[-1], 1)
-    assert_parity(p)
+    assert_parity(p, generic=generic)
 
 
 @pytest.mark.parametrize("const", [False, True])
@@ -67,10 +72,11 @@ def test_random_dims(n, mmax, const):
     assert_parity(p)
 
 
+@pytest.mark.parametrize("generic", [False, True])
 @pytest.mark.parametrize("cfg,N", [("c1", None), ("c2", 2000), ("c3", 2001), ("c4", 301),
                                    ("c5", 1 << 16), ("c5", 12345)])
-def test_configs_reduced(cfg, N):
-    assert_parity(gen.make(cfg, N=N))
+def test_configs_reduced(cfg, N, generic):
+    assert_parity(gen.make(cfg, N=N), generic=generic)
 
 
 @pytest.mark.parametrize("n", [6, 48])
@@ -91,11 +97,19 @@ def test_noise_free_recovery():
     assert rel_state_err(x, p.x_true) <= 1e-9
 
 
-def test_determinism_bitwise():
+@pytest.mark.parametrize("generic", [False, True])
+def test_determinism_bitwise(generic):
     p = gen.make("c3", N=5000)
-    x1, S1, _ = gpu_smooth(p)
-    x2, S2, _ = gpu_smooth(p)
+    x1, S1, _ = gpu_smooth(p, generic=generic)
+    x2, S2, _ = gpu_smooth(p, generic=generic)
     assert np.array_equal(x1, x2) and np.array_equal(S1, S2)
+
+
+def test_small_and_generic_paths_agree():
+    p = gen.make("c2", N=4097)
+    x1, S1, _ = gpu_smooth(p)
+    x2, S2, _ = gpu_smooth(p, generic=True)
+    assert rel_state_err(x1, x2) <= 1e-12 and rel_cov_err(S1, S2) <= 1e-12
 
 
 def test_host_inputs_and_get():
@@ -160,12 +174,13 @@ def test_error_order_and_args():
         s.get(torch.empty((64, 2), dtype=torch.float64, device="cuda"))
 
 
-def _virtual_shards(p, P, cov=True):
+def _virtual_shards(p, P, cov=True, generic=False):
     """The time-sharded multi-GPU algorithm with P ranks emulated on one GPU:
     each rank's local levels run in its own context; the allgather is a
     device copy into every rank's receive buffer (no rank waits on another)."""
     M = p.N // P
-    parts = [ks().Smoother(p.slice(r * M, (r + 1) * M), shard=(r, P, None)) for r in range(P)]
+    parts = [ks().Smoother(p.slice(r * M, (r + 1) * M), shard=(r, P, None), generic=generic)
+             for r in range(P)]
     for s in parts:
         s.whiten()
         s.factor()
@@ -184,16 +199,17 @@ def _virtual_shards(p, P, cov=True):
     return x, S
 
 
+@pytest.mark.parametrize("generic", [False, True])
 @pytest.mark.parametrize("cfg,N,P", [("c5", 1 << 12, 2), ("c5", 1 << 12, 4), ("c5", 1 << 12, 8),
                                      ("c2", 1 << 11, 2), ("c3", 1 << 11, 8), ("c1", 1 << 10, 4),
                                      ("c2", 3 * 256, 3), ("c4", 64, 2)])
-def test_virtual_shards_match_oracle(cfg, N, P):
+def test_virtual_shards_match_oracle(cfg, N, P, generic):
     p = gen.make(cfg, N=N)
-    x, S = _virtual_shards(p, P)
+    x, S = _virtual_shards(p, P, generic=generic)
     xo, So = oracle.smooth(p)
     assert rel_state_err(x, xo) <= TOL_X
     assert rel_cov_err(S, So) <= TOL_S
-    x1, S1, _ = gpu_smooth(p)
+    x1, S1, _ = gpu_smooth(p, generic=generic)
     if (N // P) & (N // P - 1) == 0 and P & (P - 1) == 0:
         # power-of-two shards: same elimination order as one GPU
         assert rel_state_err(x, x1) <= 1e-12 and rel_cov_err(S, S1) <= 1e-12
