@@ -609,6 +609,7 @@ int ks_whiten(ks_ctx *c) {
     a.sF = c->p.sF; a.sH = c->p.sH; a.sc = c->p.sc; a.so = c->p.so; a.sK = c->p.sK; a.sL = c->p.sL;
     a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
     a.cntE = c->cntE; a.cntC = c->cntC;
+    a.constC = (c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr);
     const bool cE = c->cntE == 1, cC = c->cntC == 1;
     const int64_t esE = cE ? 1 : c->ldN, csE = cE ? 0 : 1, esC = cC ? 1 : c->ldN, csC = cC ? 0 : 1;
     a.C = arr(c->C0, esC, csC); a.y = arr(c->y0, c->ldN, 1);
@@ -617,7 +618,7 @@ int ks_whiten(ks_ctx *c) {
     a.Mchol = c->Mchol; a.status = c->status;
     int nl = 0;
     {
-      Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->cntC == 1));
+      Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
       e = launch_small_whiten(a, c->stream, &nl);
     }
     if (e != cudaSuccess) return cuda_fail(e);
@@ -632,8 +633,9 @@ int ks_whiten(ks_ctx *c) {
   a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
   a.C = c->C0; a.y = c->y0; a.El = c->El0; a.Er = c->Er0; a.e = c->e0;
   a.cntE = c->cntE; a.cntC = c->cntC; a.Mchol = c->Mchol; a.status = c->status;
+  a.constC = (c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr);
   {
-    Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->cntC == 1));
+    Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
     e = launch_whiten(a, c->stream);
   }
   if (e != cudaSuccess) return cuda_fail(e);

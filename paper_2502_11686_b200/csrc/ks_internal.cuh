@@ -70,7 +70,8 @@ struct WhitenArgs {
   // outputs
   double *C, *y, *El, *Er, *e;
   int64_t cntE, cntC;    // number of distinct evolution / observation blocks (1 or N)
-  double *Mchol;         // [m_max x m_max] scratch when cntC == 1
+  int constC;            // constant observation model (H, L stride 0, m = NULL): y by a separate kernel
+  double *Mchol;         // [m_max x m_max] scratch when constC
   unsigned long long *status;
 };
 
@@ -132,6 +133,7 @@ struct SmallWhitenArgs {
   int64_t sF, sH, sc, so, sK, sL;
   int64_t first_global;
   int64_t cntE, cntC;
+  int constC;                  // constant observation model: y_i = M^{-1} o_i by small_whiten_y
   Arr C, y, El, Er, e, nC, nEr, nEl;
   double *Mchol;               // m_max^2 scratch (constant observation model)
   unsigned long long *status;

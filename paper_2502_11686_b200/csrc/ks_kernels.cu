@@ -510,7 +510,7 @@ __global__ void whiten_obs_kernel(WhitenArgs a) {
     const int r = k / n, cc = k - r * n;
     C[k] = (r < mi) ? X[r + cc * mi] : 0.0;
   }
-  if (a.cntC != 1) {
+  if (!a.constC) {
     for (int r = tid; r < mx; r += NT) a.y[i * mx + r] = (r < mi) ? X[r + n * mi] : 0.0;
   } else {
     for (int k = tid; k < mi * mi; k += NT) {
@@ -581,7 +581,7 @@ cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s) {
   if (mx > 0) {
     const size_t so = 8 * ((size_t)mx * mx + (size_t)mx * (n + 1) + 8);
     whiten_obs_kernel<<<(unsigned)a.cntC, threads_for(n > mx ? n : mx), so, s>>>(a);
-    if (a.cntC == 1) {
+    if (a.constC) {
       const int T = 256;
       whiten_y_kernel<<<(unsigned)((a.N + T - 1) / T), T, 8 * (size_t)mx * mx, s>>>(a);
     }

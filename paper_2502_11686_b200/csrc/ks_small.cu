@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(128) small_whiten_obs(SmallWhitenArgs a) {
 #pragma unroll
   for (int c = 0; c <= N; ++c) {          // N columns of H, then o
     const bool is_o = (c == N);
-    if (is_o && a.cntC == 1) break;
+    if (is_o && a.constC) break;
     double x[MM];
 #pragma unroll
     for (int r = 0; r < MM; ++r) {
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(128) small_whiten_obs(SmallWhitenArgs a) {
     }
   }
   stv(a.nC, 0, i, nc);
-  if (a.cntC == 1) {
+  if (a.constC) {
 #pragma unroll
     for (int r = 0; r < MM; ++r)
 #pragma unroll
@@ -676,7 +676,7 @@ cudaError_t whiten_n(const SmallWhitenArgs &a, cudaStream_t s, int *nl) {
   if (a.m_max > 0) {
     small_whiten_obs<N><<<(unsigned)((a.cntC + T - 1) / T), T, 0, s>>>(a);
     *nl += 1;
-    if (a.cntC == 1) {
+    if (a.constC) {
       small_whiten_y<<<(unsigned)((a.N + 255) / 256), 256, 0, s>>>(a);
       *nl += 1;
     }
