@@ -186,6 +186,7 @@ def main():
         return run_reference(a, world, rank)
     from paper_2502_11686_b200 import generators as gen
     from paper_2502_11686_b200 import ks, model
+    from paper_2502_11686_b200 import dist as kdist
     assert torch.cuda.is_available(), "bench needs a GPU (there is no CPU fallback)"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -194,9 +195,9 @@ def main():
     P = world
     p = gen.make(a.config, N=a.N)
     N = p.N
-    assert N % P == 0, "steps must split evenly over ranks"
-    M = N // P
-    local_p = p.slice(rank * M, (rank + 1) * M) if P > 1 else p
+    lo, hi = kdist.shard_range(N, rank, P)
+    M = hi - lo
+    local_p = p.slice(lo, hi) if P > 1 else p
     strides = {"C": int(local_p.H.shape[0] > 1 or local_p.L.shape[0] > 1),
                "E": int(local_p.F.shape[0] > 1 or local_p.K.shape[0] > 1 or local_p.c is not None)}
     stream = torch.cuda.current_stream(dev)
@@ -209,7 +210,7 @@ def main():
         s.whiten()
         s.factor()
         if P > 1:
-            dist.all_gather_into_tensor(v[1], v[0])
+            kdist.exchange_boundary(v[0], v[1])
             s.factor_boundary()
         s.solve()
         s.selinv()
@@ -241,9 +242,7 @@ def main():
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / a.steps
     if P > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = kdist.max_over_ranks(ms, dev)
     launches = sm.launch_times()
     n_launch = (sm.info()["launches"] - l0) // a.steps
     fam_ms = {}
@@ -283,9 +282,7 @@ def main():
         torch.cuda.synchronize()
         mse = e0.elapsed_time(e1) / ke
         if P > 1:
-            t = torch.tensor([mse], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            mse = float(t.item())
+            mse = kdist.max_over_ranks(mse, dev)
         e2e = {"value": N / (mse / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * P),
                "d2h_bytes_per_step": int(d2h * P), "ms_per_step": mse, "steps": ke,
                "path": "ks_create(KS_HOST_INPUTS) pinned host inputs -> whiten(H2D) .. selinv -> "

@@ -87,8 +87,6 @@ struct ks_ctx {
          *hS = nullptr, *Xq_local = nullptr;
   // small-n path (ks_small.cu): element-major level arrays
   bool small = false;
-  int64_t ldN = 0;
-  std::vector<int64_t> ent_ld, rec_ld, X_ld, entb_ld, recb_ld, Xb_ld;
   double *nC0 = nullptr, *nEr0 = nullptr, *nEl0 = nullptr, *zscratch = nullptr;
   // outputs
   double *xout = nullptr, *Sout = nullptr;
@@ -120,7 +118,6 @@ bool use_small(const ks_problem *p) {
   return p->n <= kSmallMaxN && p->m_max <= kSmallMaxM && !(p->flags & KS_GENERIC_PATH);
 }
 
-int64_t round32(int64_t x) { return (x + 31) & ~int64_t(31); }
 
 int validate(const ks_problem *p, const ks_shard *sh) {
   if (!p) return KS_ERR_ARG;
@@ -173,16 +170,16 @@ size_t carve(ks_ctx *c, char *base) {
   const bool sm = c->small;
   const int64_t Rs = small_rrec_doubles(n);
   if (sm) {
-    c->ldN = round32(N);
-    const int64_t colsE = c->cntE == 1 ? 1 : c->ldN, colsC = c->cntC == 1 ? 1 : c->ldN;
-    c->El0 = w.take<double>(nn * colsE);
-    c->Er0 = w.take<double>(nn * colsE);
-    c->e0 = w.take<double>(n * colsE);
-    c->nEr0 = w.take<double>(colsE);
-    c->nEl0 = w.take<double>(colsE);
-    c->C0 = w.take<double>(mx * n * colsC + 1);
-    c->nC0 = w.take<double>(colsC);
-    c->y0 = w.take<double>(mx * c->ldN + 1);
+    const bool cE = c->cntE == 1, cC = c->cntC == 1;
+    auto sz = [&](bool cst, int64_t E) { return cst ? E : tiled_doubles(N, E); };
+    c->El0 = w.take<double>(sz(cE, nn));
+    c->Er0 = w.take<double>(sz(cE, nn));
+    c->e0 = w.take<double>(sz(cE, n));
+    c->nEr0 = w.take<double>(sz(cE, 1));
+    c->nEl0 = w.take<double>(sz(cE, 1));
+    c->C0 = w.take<double>(sz(cC, (int64_t)mx * n) + 1);
+    c->nC0 = w.take<double>(sz(cC, 1));
+    c->y0 = w.take<double>(tiled_doubles(N, mx) + 1);
     c->zscratch = w.take<double>(nn + n);
   } else {
     c->El0 = w.take<double>(c->cntE * nn);
@@ -194,19 +191,16 @@ size_t carve(ks_ctx *c, char *base) {
   c->Mchol = w.take<double>((size_t)mx * mx + 1);
   // local levels
   c->K_.clear(); c->ent.clear(); c->rrec.clear(); c->X.clear();
-  c->ent_ld.clear(); c->rec_ld.clear(); c->X_ld.clear();
   int64_t K = N;
   for (int L = 0;; ++L) {
     if (c->sharded && L == c->q) break;
     c->K_.push_back(K);
-    const int64_t le = sm ? round32(K) : K, lr = sm ? round32((K + 1) / 2) : (K + 1) / 2,
-                  lx = sm ? round32(K + 1) : K + 1;
-    c->ent_ld.push_back(le);
-    c->rec_ld.push_back(lr);
-    c->X_ld.push_back(lx);
-    c->ent.push_back(L == 0 ? nullptr : w.take<double>(le * E));
-    c->rrec.push_back(w.take<double>(lr * (sm ? Rs : Rr)));
-    c->X.push_back(L == 0 ? nullptr : w.take<double>(lx * nn));
+    const int64_t ne = sm ? tiled_doubles(K, E) : K * E;
+    const int64_t nr = sm ? tiled_doubles((K + 1) / 2, Rs) : ((K + 1) / 2) * Rr;
+    const int64_t nx = sm ? tiled_doubles(K + 1, nn) : (K + 1) * nn;
+    c->ent.push_back(L == 0 ? nullptr : w.take<double>(ne));
+    c->rrec.push_back(w.take<double>(nr));
+    c->X.push_back(L == 0 ? nullptr : w.take<double>(nx));
     if (K == 1) break;
     K /= 2;
   }
@@ -214,24 +208,19 @@ size_t carve(ks_ctx *c, char *base) {
     const int P = c->nranks;
     c->send = w.take<double>(E);
     c->recv = w.take<double>((int64_t)P * E);
-    c->Xq_local = w.take<double>(2 * nn);
+    c->Xq_local = w.take<double>(sm ? tiled_doubles(2, nn) : 2 * nn);
     c->hx = w.take<double>(n);
     c->hS = w.take<double>(nn);
     c->bx = w.take<double>((int64_t)P * n);
     c->bS = w.take<double>((int64_t)P * nn);
     c->Kb.clear(); c->entb.clear(); c->rrecb.clear(); c->Xb.clear();
-    c->entb_ld.clear(); c->recb_ld.clear(); c->Xb_ld.clear();
     int64_t Kb = P;
     for (int L = 0;; ++L) {
       c->Kb.push_back(Kb);
-      const int64_t le = sm ? round32(Kb) : Kb, lr = sm ? round32((Kb + 1) / 2) : (Kb + 1) / 2,
-                    lx = sm ? round32(Kb + 1) : Kb + 1;
-      c->entb_ld.push_back(L == 0 ? -1 : le);      // level q entries: the AoS recv buffer
-      c->recb_ld.push_back(lr);
-      c->Xb_ld.push_back(lx);
-      c->entb.push_back(L == 0 ? c->recv : w.take<double>(le * E));
-      c->rrecb.push_back(w.take<double>(lr * (sm ? Rs : Rr)));
-      c->Xb.push_back(w.take<double>(lx * nn));
+      // the boundary system (P columns) always runs on the generic AoS kernels
+      c->entb.push_back(L == 0 ? c->recv : w.take<double>(Kb * E));
+      c->rrecb.push_back(w.take<double>(((Kb + 1) / 2) * Rr));
+      c->Xb.push_back(w.take<double>((Kb + 1) * nn));
       if (Kb == 1) break;
       Kb /= 2;
     }
@@ -293,131 +282,79 @@ EntryView aos_view(const double *ent, int n) {
   return v;
 }
 
-// ---- small-path views (element e of column t at p[e*es + t*cs]) ----
-CArr carr(const double *p, int64_t es, int64_t cs) { return CArr{p, es, cs}; }
-Arr arr(double *p, int64_t es, int64_t cs) { return Arr{p, es, cs}; }
-
-// entry field offsets (elements): C, y, El, Er, e, nrm
-void entry_offsets(int n, int64_t off[6]) {
-  const int64_t nn = (int64_t)n * n;
-  off[0] = 0; off[1] = nn; off[2] = nn + n; off[3] = 2 * nn + n; off[4] = 3 * nn + n; off[5] = 3 * nn + 2 * n;
-}
-
-// ld > 0: element-major with leading dimension ld; ld < 0: AoS records.
-SmallIn small_in(const double *base, int64_t ld, int n) {
-  int64_t o[6];
-  entry_offsets(n, o);
-  const int64_t E = entry_doubles(n);
-  const int64_t es = ld > 0 ? ld : 1, cs = ld > 0 ? 1 : E;
-  SmallIn v;
-  v.C = carr(base + o[0] * es, es, cs); v.y = carr(base + o[1] * es, es, cs);
-  v.El = carr(base + o[2] * es, es, cs); v.Er = carr(base + o[3] * es, es, cs);
-  v.e = carr(base + o[4] * es, es, cs); v.nrm = carr(base + o[5] * es, es, cs);
-  v.nC = v.nEr = v.nEl = carr(nullptr, 0, 0);
-  v.RC = n; v.tri = 1;
-  return v;
-}
-
-SmallOut small_out(double *base, int64_t ld, int n) {
-  SmallOut v;
-  if (!base) { v.C = v.y = v.El = v.Er = v.e = v.nrm = arr(nullptr, 0, 0); return v; }
-  int64_t o[6];
-  entry_offsets(n, o);
-  const int64_t E = entry_doubles(n);
-  const int64_t es = ld > 0 ? ld : 1, cs = ld > 0 ? 1 : E;
-  v.C = arr(base + o[0] * es, es, cs); v.y = arr(base + o[1] * es, es, cs);
-  v.El = arr(base + o[2] * es, es, cs); v.Er = arr(base + o[3] * es, es, cs);
-  v.e = arr(base + o[4] * es, es, cs); v.nrm = arr(base + o[5] * es, es, cs);
-  return v;
-}
+// ---- small-path views (tiled, 32 columns per tile; see TView) ----
+TView tv(const double *p, int64_t ts) { return TView{const_cast<double *>(p), ts}; }
 
 SmallIn small_level0(const ks_ctx *c) {
+  const int n = c->n, mx = c->mx;
+  const int64_t nn = (int64_t)n * n;
   const bool cE = c->cntE == 1, cC = c->cntC == 1;
-  const int64_t esE = cE ? 1 : c->ldN, csE = cE ? 0 : 1, esC = cC ? 1 : c->ldN, csC = cC ? 0 : 1;
   SmallIn v;
-  v.C = carr(c->C0, esC, csC);
-  v.y = carr(c->y0, c->ldN, 1);
-  v.El = carr(c->El0, esE, csE);
-  v.Er = carr(c->Er0, esE, csE);
-  v.e = carr(c->e0, esE, csE);
-  v.nrm = carr(nullptr, 0, 0);
-  v.nC = carr(c->nC0, 1, csC);
-  v.nEr = carr(c->nEr0, 1, csE);
-  v.nEl = carr(c->nEl0, 1, csE);
-  v.RC = c->mx; v.tri = 0;
+  v.C = tv(c->C0, cC ? 0 : 32 * (int64_t)mx * n);
+  v.y = tv(c->y0, 32 * (int64_t)mx);
+  v.El = tv(c->El0, cE ? 0 : 32 * nn);
+  v.Er = tv(c->Er0, cE ? 0 : 32 * nn);
+  v.e = tv(c->e0, cE ? 0 : 32 * (int64_t)n);
+  v.nC = tv(c->nC0, cC ? 0 : 32);
+  v.nEr = tv(c->nEr0, cE ? 0 : 32);
+  v.nEl = tv(c->nEl0, cE ? 0 : 32);
+  v.RC = mx;
+  v.ent = tv(nullptr, 0);
   return v;
 }
 
-SmallRec small_rec(double *base, int64_t ld, int n) {
-  const int64_t nn = (int64_t)n * n;
-  SmallRec r;
-  r.Tl = arr(base, ld, 1);
-  r.Tr = arr(base + nn * ld, ld, 1);
-  r.w = arr(base + 2 * nn * ld, ld, 1);
-  r.P = arr(base + (2 * nn + n) * ld, ld, 1);
-  return r;
-}
-
-int run_small_factor_levels(ks_ctx *c, bool boundary) {
+int run_small_factor_levels(ks_ctx *c) {
   const int n = c->n;
-  const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
-  const int Lb = boundary ? c->q : 0;
+  const int64_t E = entry_doubles(n), Rs = small_rrec_doubles(n);
+  const std::vector<int64_t> &Ks = c->K_;
   for (size_t i = 0; i < Ks.size(); ++i) {
     SmallFactorArgs a;
-    const int L = Lb + (int)i;
     const bool last = i + 1 == Ks.size();
-    if (!boundary) {
-      a.in = (i == 0) ? small_level0(c) : small_in(c->ent[i], c->ent_ld[i], n);
-      if (!last) a.out = small_out(c->ent[i + 1], c->ent_ld[i + 1], n);
-      else a.out = small_out(c->sharded ? c->send : nullptr, -1, n);
-      a.rec = small_rec(c->rrec[i], c->rec_ld[i], n);
-      a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+    if (i == 0) {
+      a.in = small_level0(c);
     } else {
-      a.in = small_in(c->entb[i], c->entb_ld[i], n);
-      a.out = small_out(last ? nullptr : c->entb[i + 1], last ? -1 : c->entb_ld[i + 1], n);
-      a.rec = small_rec(c->rrecb[i], c->recb_ld[i], n);
-      a.t0 = 0;
+      a.in = small_level0(c);
+      a.in.ent = tv(c->ent[i], 32 * E);
     }
+    a.outAoS = 0;
+    if (!last) a.out = tv(c->ent[i + 1], 32 * E);
+    else if (c->sharded) { a.out = tv(c->send, E); a.outAoS = 1; }
+    else a.out = tv(nullptr, 0);
+    a.rec = tv(c->rrec[i], 32 * Rs);
+    a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
     a.K = Ks[i];
-    a.level = L;
-    a.lbase = boundary ? c->q : 0;
+    a.level = (int)i;
+    a.lbase = 0;
     a.step0 = 0;
     a.status = c->status;
     a.zscratch = c->zscratch;
-    Launch l(c, boundary ? 4 : 1, L);
+    a.cE = c->cntE == 1;
+    a.cC = c->cntC == 1;
+    Launch l(c, 1, (int)i);
     cudaError_t e = launch_small_factor(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
   return KS_OK;
 }
 
-int run_small_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
+int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
   const int n = c->n;
-  const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
+  const int64_t nn = (int64_t)n * n, Rs = small_rrec_doubles(n);
+  const std::vector<int64_t> &Ks = c->K_;
   for (int i = (int)Ks.size() - 1; i >= 0; --i) {
     SmallBackwardArgs a;
-    const SmallRec r = small_rec(boundary ? c->rrecb[i] : c->rrec[i], boundary ? c->recb_ld[i] : c->rec_ld[i], n);
-    a.Tl = carr(r.Tl.p, r.Tl.es, 1); a.Tr = carr(r.Tr.p, r.Tr.es, 1);
-    a.w = carr(r.w.p, r.w.es, 1); a.P = carr(r.P.p, r.P.es, 1);
+    a.rec = tv(c->rrec[i], 32 * Rs);
     a.K = Ks[i];
     a.shift = i;
     a.do_state = do_state;
     a.do_cov = do_cov;
     const bool top = i + 1 == (int)Ks.size();
-    if (boundary) {
-      a.t0 = 0;
-      a.x = c->bx; a.S = c->bS; a.xhalo = nullptr; a.Shalo = nullptr;
-      a.Xup = top ? carr(nullptr, 0, 0) : carr(c->Xb[i + 1], c->Xb_ld[i + 1], 1);
-      a.Xcur = arr(c->Xb[i], c->Xb_ld[i], 1);
-    } else {
-      a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
-      a.x = c->xout; a.S = c->Sout; a.xhalo = c->hx; a.Shalo = c->hS;
-      if (!top) a.Xup = carr(c->X[i + 1], c->X_ld[i + 1], 1);
-      else a.Xup = c->sharded ? carr(c->Xq_local, 2, 1) : carr(nullptr, 0, 0);
-      a.Xcur = (i >= 1) ? arr(c->X[i], c->X_ld[i], 1) : arr(nullptr, 0, 0);
-    }
-    if (!do_cov) a.Xcur = arr(nullptr, 0, 0);
-    Launch l(c, boundary ? 4 : (do_cov ? 3 : 2), (boundary ? c->q : 0) + i);
+    a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+    a.x = c->xout; a.S = c->Sout; a.xhalo = c->hx; a.Shalo = c->hS;
+    if (!top) a.Xup = tv(c->X[i + 1], 32 * nn);
+    else a.Xup = c->sharded ? tv(c->Xq_local, 32 * nn) : tv(nullptr, 0);
+    a.Xcur = (i >= 1 && do_cov) ? tv(c->X[i], 32 * nn) : tv(nullptr, 0);
+    Launch l(c, do_cov ? 3 : 2, i);
     cudaError_t e = launch_small_backward(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
@@ -425,7 +362,7 @@ int run_small_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov
 }
 
 int run_factor_levels(ks_ctx *c, bool boundary) {
-  if (c->small) return run_small_factor_levels(c, boundary);
+  if (c->small && !boundary) return run_small_factor_levels(c);
   const int n = c->n;
   const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
   const int Lb = boundary ? c->q : 0;
@@ -464,7 +401,7 @@ int run_factor_levels(ks_ctx *c, bool boundary) {
 // Timing families: 0 whiten, 1 factor levels, 2 solve levels, 3 selinv levels,
 // 4 boundary system (multi-GPU).
 int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
-  if (c->small) return run_small_backward_levels(c, boundary, do_state, do_cov);
+  if (c->small && !boundary) return run_small_backward_levels(c, do_state, do_cov);
   const int n = c->n;
   const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
   for (int i = (int)Ks.size() - 1; i >= 0; --i) {
@@ -517,8 +454,8 @@ int scatter_boundary(ks_ctx *c, bool states, bool cov) {
       e = cudaMemcpyAsync(c->hS, c->bS + (r - 1) * nn, nn * 8, cudaMemcpyDeviceToDevice, c->stream);
       // slot -1 of the local level-q cross array: S_{b_{r-1}, b_r} = boundary X_q slot r-1
       if (e == cudaSuccess) {
-        if (c->small)   // element-major: slot r-1 is column r of Xb[0]; Xq_local has ld 2
-          e = cudaMemcpy2DAsync(c->Xq_local, 2 * 8, c->Xb[0] + r, c->Xb_ld[0] * 8, 8, nn,
+        if (c->small)   // tiled local layout: element e of column 0 (slot -1) at 32 e
+          e = cudaMemcpy2DAsync(c->Xq_local, 32 * 8, c->Xb[0] + (int64_t)r * nn, 8, 8, nn,
                                 cudaMemcpyDeviceToDevice, c->stream);
         else
           e = cudaMemcpyAsync(c->Xq_local, c->Xb[0] + (int64_t)r * nn, nn * 8, cudaMemcpyDeviceToDevice,
@@ -610,11 +547,10 @@ int ks_whiten(ks_ctx *c) {
     a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
     a.cntE = c->cntE; a.cntC = c->cntC;
     a.constC = (c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr);
-    const bool cE = c->cntE == 1, cC = c->cntC == 1;
-    const int64_t esE = cE ? 1 : c->ldN, csE = cE ? 0 : 1, esC = cC ? 1 : c->ldN, csC = cC ? 0 : 1;
-    a.C = arr(c->C0, esC, csC); a.y = arr(c->y0, c->ldN, 1);
-    a.El = arr(c->El0, esE, csE); a.Er = arr(c->Er0, esE, csE); a.e = arr(c->e0, esE, csE);
-    a.nC = arr(c->nC0, 1, csC); a.nEr = arr(c->nEr0, 1, csE); a.nEl = arr(c->nEl0, 1, csE);
+    const SmallIn v = small_level0(c);
+    a.C = v.C; a.y = v.y; a.El = v.El; a.Er = v.Er; a.e = v.e; a.nC = v.nC; a.nEr = v.nEr; a.nEl = v.nEl;
+    a.cE = c->cntE == 1;
+    a.cC = c->cntC == 1;
     a.Mchol = c->Mchol; a.status = c->status;
     int nl = 0;
     {

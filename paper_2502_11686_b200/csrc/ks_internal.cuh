@@ -82,47 +82,46 @@ struct WhitenArgs {
 constexpr int kSmallMaxN = 8;
 constexpr int kSmallMaxM = 8;
 
-// Strided view: element e of column t lives at p[e * es + t * cs]
-// (SoA: es = leading dimension, cs = 1; AoS: es = 1, cs = record size;
-//  constant: es = 1, cs = 0).
-struct Arr {
+// Tiled ("AoSoA") view, 32 columns per tile: element e of column t lives at
+//   p[(t >> 5) * ts + 32 e + (t & 31)]          (element stride ES = 32)
+// so that a warp reading element e of 32 consecutive columns issues one
+// coalesced 256-byte access and every element offset inside a column is a
+// compile-time immediate; AoS records and constant blocks use
+//   p[t * ts + e]                               (ES = 1; ts = 0: constant)
+struct TView {
   double *p;
-  int64_t es, cs;
+  int64_t ts;
 };
-struct CArr {
-  const double *p;
-  int64_t es, cs;
-};
+__host__ __device__ inline int64_t tiled_doubles(int64_t cols, int64_t E) { return ((cols + 31) / 32) * 32 * E; }
 
 struct SmallIn {               // level-L columns
-  CArr C, y, El, Er, e, nrm;   // C: RC x n row-major (upper triangular when tri)
-  CArr nC, nEr, nEl;           // level 0 only: |C_j|^2, |Er_j|^2, |El_j|^2 (rank reference)
-  int RC, tri;
-};
-struct SmallOut {              // level-(L+1) survivor columns (tri C)
-  Arr C, y, El, Er, e, nrm;
-};
-struct SmallRec {              // R record: T_l, T_r (n x n), w (n), P (packed upper n(n+1)/2)
-  Arr Tl, Tr, w, P;
+  // level 0 (whitened inputs), one view per field (constant model: ES = 1,
+  // ts = 0); C: RC x n row-major
+  TView C, y, El, Er, e;
+  TView nC, nEr, nEl;          // |C_j|^2, |Er_j|^2, |El_j|^2 (rank reference)
+  int RC;
+  // level >= 1: tiled entry records [C (n x n, upper tri) | y | El | Er | e | nrm]
+  TView ent;
 };
 struct SmallFactorArgs {
   SmallIn in;
-  SmallOut out;
-  SmallRec rec;
+  TView out;                   // level-(L+1) survivor entries: tiled, or AoS (outAoS)
+  TView rec;                   // tiled R records [Tl (n x n) | Tr (n x n) | w (n) | P (n(n+1)/2)]
   int64_t K, t0;
   int level, lbase;
   int64_t step0;
   unsigned long long *status;
   double *zscratch;            // n (n + 1) doubles: the odd level's last-column leftover Z
+  int cE, cC, outAoS;          // level 0: constant evolution / observation blocks
 };
 struct SmallBackwardArgs {
-  CArr Tl, Tr, w, P;
+  TView rec;                   // tiled R records
   int64_t K, t0;
   int shift;
   double *x, *S;               // domain outputs, row-major [*, n] / [*, n, n]
   const double *xhalo, *Shalo;
-  CArr Xup;                    // S_{q,q+1} of level L+1 at column q+1 (p null: none)
-  Arr Xcur;                    // level-L cross blocks to write (p null: skip)
+  TView Xup;                   // tiled S_{q,q+1} of level L+1 at column q+1 (p null: none)
+  TView Xcur;                  // tiled level-L cross blocks to write (p null: skip)
   int do_state, do_cov;
 };
 struct SmallWhitenArgs {
@@ -134,7 +133,8 @@ struct SmallWhitenArgs {
   int64_t first_global;
   int64_t cntE, cntC;
   int constC;                  // constant observation model: y_i = M^{-1} o_i by small_whiten_y
-  Arr C, y, El, Er, e, nC, nEr, nEl;
+  TView C, y, El, Er, e, nC, nEr, nEl;   // tiled per step, or ES = 1 / ts = 0 when constant
+  int cE, cC;                  // layout flags of the above (1 = constant block)
   double *Mchol;               // m_max^2 scratch (constant observation model)
   unsigned long long *status;
 };

@@ -1,0 +1,902 @@
+// Small-n path implementation (templates); instantiated per n by ks_small_n<n>.cu
+// so that the eight state dimensions compile in parallel.
+#pragma once
+// Small-n path (n <= 8, m_max <= 8) of the Odd-Even Kalman smoother.
+//
+// One THREAD per (even, odd) column pair / per eliminated column, every block
+// held in registers (the state dimension N is a template parameter, so all
+// loops unroll and all block indices are compile-time), and every block QR
+// done by Givens row streaming into a packed upper-triangular R: a stacked
+// QR [R; rows] is computed by rotating one row at a time into R.  Givens and
+// Householder produce the same R up to row signs (both are Q R of the same
+// stack), and the row-streaming form needs only one streamed row
+// in registers at a time instead of the whole (2n+m) x (3n+1) stack, which is
+// what lets a whole pair fit in one thread's registers.  Level arrays are
+// element-major (SoA), so the 32 threads of a warp load element e of 32
+// consecutive columns with one coalesced 256-byte access.
+//
+// P:n = line n of the paper text.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ks_internal.cuh"
+
+#ifndef KS_F6_BLOCKS
+#define KS_F6_BLOCKS 4
+#endif
+
+namespace ks {
+namespace smalld {
+
+template <int N>
+struct Tri {
+  static constexpr int size = N * (N + 1) / 2;
+  static constexpr __host__ __device__ int at(int i, int j) { return i * N - (i * (i - 1)) / 2 + (j - i); }
+};
+
+// Column base of a tiled (ES = 32) or AoS / constant (ES = 1) view; element e
+// of the column is then at base[ES * e], a compile-time immediate offset.
+template <int ES>
+__device__ __forceinline__ double *cb(const TView &v, int64_t t) {
+  return ES == 32 ? v.p + (t >> 5) * v.ts + (t & 31) : v.p + t * v.ts;
+}
+template <int ES>
+__device__ __forceinline__ double ldv(const TView &v, int64_t t, int e) {
+  return __ldg(cb<ES>(v, t) + ES * e);
+}
+template <int ES>
+__device__ __forceinline__ void stv(const TView &v, int64_t t, int e, double x) {
+  cb<ES>(v, t)[ES * e] = x;
+}
+// L1 prefetch of element e of column t (no registers): the row loops fetch
+// the next streamed row while rotating the current one.
+template <int ES>
+__device__ __forceinline__ void pfv(const TView &v, int64_t t, int e) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(cb<ES>(v, t) + ES * e));
+}
+
+__device__ __forceinline__ void report(unsigned long long *st, int64_t step, int kind) {
+  if (st) atomicMin(st, ((unsigned long long)(step + 1) << 8) | (unsigned long long)kind);
+}
+
+// 1/sqrt(h) for h > 0: the MUFU approximation refined by two Newton steps
+// (each doubles the correct bits: ~2^-22 -> ~2^-44 -> full double).  No
+// special-case branches (h is a sum of squares with b != 0 where it is used).
+__device__ __forceinline__ double rsqrt_nr(double h) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h));
+  double hy = h * y;
+  y = fma(0.5 * y, fma(-hy, y, 1.0), y);
+  hy = h * y;
+  y = fma(0.5 * y, fma(-hy, y, 1.0), y);
+  return y;
+}
+
+// Givens rotation zeroing b against the pivot a: (a, b) <- (r, 0).
+// b == 0 selects the identity (c = 1, s = 0), so zero (padding) rows are exact
+// no-ops; branch-free (selects) so that ragged rows do not diverge.
+__device__ __forceinline__ void make_rot(double &a, double &b, double &c, double &s) {
+  const bool id = (b == 0.0);
+  const double h = fma(a, a, b * b);
+  const double ih = rsqrt_nr(id ? 1.0 : h);
+  c = id ? 1.0 : a * ih;
+  s = id ? 0.0 : b * ih;
+  a = id ? a : h * ih;
+  b = 0.0;
+}
+
+__device__ __forceinline__ void rot(double &x, double &y, double c, double s) {
+  const double nx = fma(c, x, s * y);
+  const double ny = fma(c, y, -(s * x));
+  x = nx;
+  y = ny;
+}
+
+// ---------------------------------------------------------------- factor ---
+
+// Eliminate column t of the level in one thread.
+//   stage 1: rotate the rows of [El_{t+1} | Er_{t+1} | e_{t+1}] into
+//            R = C_t (level 0: the rows of C_t into R = 0 first), giving R~_t,
+//            X_t, z~_t; each leftover row [0 | d | y~] (a row of D~_{t+1})
+//   stage 3: is rotated at once into R3 = C_{t+1}, giving the survivor's
+//            C'_{t+1} (plus the leftover Z rows of an odd level's last column)
+//   stage 2: rotate the rows of [Er_t | El_t | 0 | e_t] into [R~_t | 0 | X_t | z~_t]
+//            giving R_tt, R_{t,t-1}, R_{t,t+1}, z_t; the leftover rows are the
+//            survivor's new coupling row [Z_t | X~_t | z^_t].  No left
+//            neighbour: "nothing to do".
+//   post:    T_l = R^{-1} R_{t,t-1}, T_r = R^{-1} R_{t,t+1}, w = R^{-1} z_t,
+//            P = R^{-1} R^{-T} (packed) -> R record.
+// Entry element offsets (entry_doubles layout).
+template <int N>
+struct Ent {
+  static constexpr int C = 0, y = N * N, El = N * N + N, Er = 2 * N * N + N, e = 3 * N * N + N,
+                       nrm = 3 * N * N + 2 * N;
+};
+// R record element offsets.
+template <int N>
+struct Rr {
+  static constexpr int Tl = 0, Tr = N * N, w = 2 * N * N, P = 2 * N * N + N;
+};
+
+template <int N, bool L0, bool CE, bool CC, bool OAOS>
+__device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_t t, bool hr, bool hl,
+                                                int64_t pnext, bool zs_in, bool zs_out) {
+  using TR = Tri<N>;
+  using EN = Ent<N>;
+  using RR = Rr<N>;
+  const SmallIn &in = a.in;
+  // field loads: level 0 per-field views (constant blocks: ES = 1, ts = 0),
+  // level >= 1 one tiled entry record view
+  constexpr int ESE = CE ? 1 : 32, ESC = CC ? 1 : 32, ESO = OAOS ? 1 : 32;
+  auto ldC = [&](int e, int64_t c) { return L0 ? ldv<ESC>(in.C, c, e) : ldv<32>(in.ent, c, EN::C + e); };
+  auto ldY = [&](int e, int64_t c) { return L0 ? ldv<32>(in.y, c, e) : ldv<32>(in.ent, c, EN::y + e); };
+  auto ldEl = [&](int e, int64_t c) { return L0 ? ldv<ESE>(in.El, c, e) : ldv<32>(in.ent, c, EN::El + e); };
+  auto ldEr = [&](int e, int64_t c) { return L0 ? ldv<ESE>(in.Er, c, e) : ldv<32>(in.ent, c, EN::Er + e); };
+  auto ldE = [&](int e, int64_t c) { return L0 ? ldv<ESE>(in.e, c, e) : ldv<32>(in.ent, c, EN::e + e); };
+  auto sto = [&](int e, double v) { stv<ESO>(a.out, pnext, e, v); };
+  // prefetch row i of a block field (n elements per row) of column c
+  auto pfEl = [&](int i, int64_t c) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (L0) pfv<ESE>(in.El, c, i * N + j); else pfv<32>(in.ent, c, EN::El + i * N + j);
+    }
+  };
+  auto pfEr = [&](int i, int64_t c) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (L0) pfv<ESE>(in.Er, c, i * N + j); else pfv<32>(in.ent, c, EN::Er + i * N + j);
+    }
+  };
+  const int64_t rcol = t >> 1;
+  auto str = [&](int e, double v) { stv<32>(a.rec, rcol, e, v); };
+  double R[TR::size];
+  double X[N][N];
+  double z[N];
+
+  // rank reference: |block column of UA|_F (reading R9)
+  double ref2, ref2u = 0.0;
+  if (!L0) {
+    const double v = ldv<32>(in.ent, t, EN::nrm);
+    ref2 = v * v;
+    if (hr) {
+      const double u = ldv<32>(in.ent, t + 1, EN::nrm);
+      ref2u = u * u;
+    }
+  } else {
+    ref2 = ldv<ESC>(in.nC, t, 0) + (hl ? ldv<ESE>(in.nEr, t, 0) : 0.0) +
+           (hr ? ldv<ESE>(in.nEl, t + 1, 0) : 0.0);
+    if (hr)
+      ref2u = ldv<ESC>(in.nC, t + 1, 0) + ldv<ESE>(in.nEr, t + 1, 0) +
+              (t + 2 < a.K ? ldv<ESE>(in.nEl, t + 2, 0) : 0.0);
+  }
+
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    z[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) X[i][j] = 0.0;
+  }
+  // Per-thread shared-memory parking (element-major: element e of this
+  // thread at sp[e * blockDim.x]): the stage-1 leftover rows (N x (N+1)) and
+  // a copy of R~_t (packed), so that at most ~76 doubles are live in
+  // registers at any point (stage 1 -> stage 2 pass B -> stage 3 -> pass A).
+  extern __shared__ double smem_park[];
+  double *sp = smem_park + threadIdx.x;
+  const int bs = blockDim.x;
+  auto park = [&](int e, double v) { sp[e * bs] = v; };
+  auto unpark = [&](int e) { return sp[e * bs]; };
+  constexpr int kLeft = 0, kRt = N * (N + 1);
+
+  // ---- stage 1 base: R = C_t ----
+  if (hr) {
+    pfEl(0, t + 1);
+    pfEr(0, t + 1);
+  } else if (hl) {
+    pfEr(0, t);
+  }
+  if (!L0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i; j < N; ++j) R[TR::at(i, j)] = ldC(i * N + j, t);
+      z[i] = ldY(i, t);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < TR::size; ++k) R[k] = 0.0;
+#pragma unroll 1
+    for (int r = 0; r < in.RC; ++r) {
+      double row[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) row[j] = ldC(r * N + j, t);
+      double yr = ldY(r, t);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double c, s;
+        make_rot(R[TR::at(k, k)], row[k], c, s);
+#pragma unroll
+        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], row[j], c, s);
+        rot(z[k], yr, c, s);
+      }
+    }
+  }
+
+  // ---- stage 1: rows of [El_{t+1} | Er_{t+1} | e_{t+1}] into [R | X | z] ----
+  // leftover rows [0 | d | y~] (rows of D~_{t+1}) are parked for stage 3.
+  if (hr) {
+    const int64_t u = t + 1;
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+      double el[N], er[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        el[j] = ldEl(i * N + j, u);
+        er[j] = ldEr(i * N + j, u);
+      }
+      double ee = ldE(i, u);
+      if (i + 1 < N) {
+        pfEl(i + 1, u);
+        pfEr(i + 1, u);
+      } else if (hl) {
+        pfEr(0, t);
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double c, s;
+        make_rot(R[TR::at(k, k)], el[k], c, s);
+#pragma unroll
+        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], el[j], c, s);
+#pragma unroll
+        for (int j = 0; j < N; ++j) rot(X[k][j], er[j], c, s);
+        rot(z[k], ee, c, s);
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) park(kLeft + i * (N + 1) + j, er[j]);
+      park(kLeft + i * (N + 1) + N, ee);
+    }
+  }
+
+  // ---- stage 2, pass B: rows of [Er_t | 0] into [R~_t | X_t] -> R_tt, R_{t,t+1}, X~_t ----
+  // (pass A below recomputes the same rotations -- bitwise, same inputs and
+  // operations -- for [El_t | e_t]).
+#pragma unroll
+  for (int k = 0; k < TR::size; ++k) park(kRt + k, R[k]);
+  if (hl) {
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+      double er[N], xr[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        er[j] = ldEr(i * N + j, t);
+        xr[j] = 0.0;
+      }
+      if (i + 1 < N) pfEr(i + 1, t);
+      else pfEl(0, t);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double c, s;
+        make_rot(R[TR::at(k, k)], er[k], c, s);
+#pragma unroll
+        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], er[j], c, s);
+#pragma unroll
+        for (int j = 0; j < N; ++j) rot(X[k][j], xr[j], c, s);
+      }
+      if (hr) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) sto(EN::Er + i * N + j, xr[j]);   // X~_t
+      }
+    }
+  } else if (hr) {
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) sto(EN::Er + i * N + j, 0.0);
+    }
+  }
+  // T_r = R_tt^{-1} R_{t,t+1}
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    const double inv = 1.0 / R[TR::at(i, i)];
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double sr = X[i][c];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) sr = fma(-R[TR::at(i, k)], X[k][c], sr);
+      X[i][c] = sr * inv;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) str(RR::Tr + i * N + j, X[i][j]);
+
+  // ---- stage 3: [D~_{t+1}; C_{t+1}; Zs] -> the survivor's C'_{t+1}, y' ----
+  if (hr) {
+    const int64_t u = t + 1;
+    double R3[TR::size];
+    double z3[N];
+    if (!L0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = i; j < N; ++j) R3[TR::at(i, j)] = ldC(i * N + j, u);
+        z3[i] = ldY(i, u);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < TR::size; ++k) R3[k] = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) z3[i] = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < in.RC; ++r) {
+        double row[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) row[j] = ldC(r * N + j, u);
+        double yr = ldY(r, u);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double c, s;
+          make_rot(R3[TR::at(k, k)], row[k], c, s);
+#pragma unroll
+          for (int j = k + 1; j < N; ++j) rot(R3[TR::at(k, j)], row[j], c, s);
+          rot(z3[k], yr, c, s);
+        }
+      }
+    }
+    const int nrows = zs_in ? 2 * N : N;    // leftover rows, then the odd level's Zs (reading R5)
+#pragma unroll 1
+    for (int i = 0; i < nrows; ++i) {
+      double row[N], zr;
+      if (i < N) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) row[j] = unpark(kLeft + i * (N + 1) + j);
+        zr = unpark(kLeft + i * (N + 1) + N);
+      } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) row[j] = a.zscratch[(i - N) * (N + 1) + j];
+        zr = a.zscratch[(i - N) * (N + 1) + N];
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double c, s;
+        make_rot(R3[TR::at(k, k)], row[k], c, s);
+#pragma unroll
+        for (int j = k + 1; j < N; ++j) rot(R3[TR::at(k, j)], row[j], c, s);
+        rot(z3[k], zr, c, s);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) sto(EN::C + i * N + j, j >= i ? R3[TR::at(i, j)] : 0.0);
+      sto(EN::y + i, z3[i]);
+    }
+    sto(EN::nrm, sqrt(ref2u));
+  }
+
+  // ---- stage 2, pass A: rows of [Er_t | El_t | e_t] into [R~_t | 0 | z~_t] ----
+#pragma unroll
+  for (int k = 0; k < TR::size; ++k) R[k] = unpark(kRt + k);
+  double Rl[N][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) Rl[i][j] = 0.0;
+  if (hl) {
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+      double er[N], el[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        er[j] = ldEr(i * N + j, t);
+        el[j] = ldEl(i * N + j, t);
+      }
+      double ee = ldE(i, t);
+      if (i + 1 < N) {
+        pfEr(i + 1, t);
+        pfEl(i + 1, t);
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double c, s;
+        make_rot(R[TR::at(k, k)], er[k], c, s);
+#pragma unroll
+        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], er[j], c, s);
+#pragma unroll
+        for (int j = 0; j < N; ++j) rot(Rl[k][j], el[j], c, s);
+        rot(z[k], ee, c, s);
+      }
+      if (hr) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) sto(EN::El + i * N + j, el[j]);   // Z_t
+        sto(EN::e + i, ee);                                           // z^_t
+      } else if (zs_out) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) a.zscratch[i * (N + 1) + j] = el[j];
+        a.zscratch[i * (N + 1) + N] = ee;
+      }
+    }
+  } else if (hr) {
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) sto(EN::El + i * N + j, 0.0);
+      sto(EN::e + i, 0.0);
+    }
+  }
+
+  // ---- post: rank check, T_l = R^{-1} R_l, w = R^{-1} z, P = R^{-1} R^{-T} ----
+  {
+    const double thr = kRankTol * sqrt(ref2);
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < N; ++d) bad |= !(fabs(R[TR::at(d, d)]) > thr);
+    if (bad) report(a.status, (((t + 1) << (a.level - a.lbase)) - 1) + a.step0, kBadRank);
+  }
+  double inv[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) inv[i] = 1.0 / R[TR::at(i, i)];
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double sl = Rl[i][c];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) sl = fma(-R[TR::at(i, k)], Rl[k][c], sl);
+      Rl[i][c] = sl * inv[i];
+    }
+    double sz = z[i];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) sz = fma(-R[TR::at(i, k)], z[k], sz);
+    z[i] = sz * inv[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) str(RR::Tl + i * N + j, Rl[i][j]);
+    str(RR::w + i, z[i]);
+  }
+  // R^{-1} (upper, in place of R): Ri(i,j) = -inv_i sum_{k=i+1..j} R(i,k) Ri(k,j)
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+#pragma unroll
+    for (int j = N - 1; j > i; --j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = i + 1; k <= j; ++k) s = fma(R[TR::at(i, k)], R[TR::at(k, j)], s);
+      R[TR::at(i, j)] = -s * inv[i];
+    }
+    R[TR::at(i, i)] = inv[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int j = i; j < N; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = j; k < N; ++k) s = fma(R[TR::at(i, k)], R[TR::at(j, k)], s);
+      str(RR::P + TR::at(i, j), s);
+    }
+  }
+}
+
+// Resident CTAs (of 64 threads) per SM the register allocation targets.
+constexpr int factor_min_blocks(int n) { return n <= 4 ? 8 : n == 5 ? 7 : n == 6 ? KS_F6_BLOCKS : 4; }
+
+template <int N, bool L0, bool CE, bool CC, bool OAOS>
+__global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(SmallFactorArgs a) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t K = a.K;
+  const int64_t npairs = K >= 2 ? K / 2 : 1;
+  if (p >= npairs) return;
+  const bool single_only = (K == 1);
+  const bool triple = (K >= 3) && (K & 1) && (p == K / 2 - 1);
+  // pass 0: the odd level's last column (no right neighbour), pass 1: the pair.
+  // One inlined call site keeps the (large, fully unrolled) body once in the
+  // instruction cache.
+#pragma unroll 1
+  for (int pass = (single_only || triple) ? 0 : 1; pass < (single_only ? 1 : 2); ++pass) {
+    const int64_t t = pass == 0 ? K - 1 : 2 * p;
+    const bool hl = t + a.t0 > 0;
+    if (pass == 0) small_eliminate<N, L0, CE, CC, OAOS>(a, t, false, hl, 0, false, hl);
+    else small_eliminate<N, L0, CE, CC, OAOS>(a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false);
+  }
+}
+
+// -------------------------------------------------------------- backward ---
+
+// One thread per eliminated column t of level L (P:592-600 and Alg. 2,
+// P:792-824):
+//   x_t    = w - T_l x_l - T_r x_r
+//   S_tl   = -(T_l S_ll + T_r S_lr^T),  S_tr = -(T_l S_lr + T_r S_rr)   (S_{t,I} = -T S_II)
+//   S_tt   = P - S_tl T_l^T - S_tr T_r^T  (upper triangle computed, mirrored)
+// S_lr = S_{t-1,t+1} is the level-(L+1) cross block; S_{t-1,t} = S_tl^T and
+// S_{t,t+1} = S_tr are stored for level L-1.
+constexpr int kBwdT = 64;   // threads (= eliminated columns) per backward CTA
+
+template <int N>
+__global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs a) {
+  using TR = Tri<N>;
+  using RR = Rr<N>;
+  constexpr int NN = N * N, T = kBwdT, NB = T + 1, TS = T + 1;   // odd strides: conflict-free
+  const int tid = threadIdx.x;
+  const int64_t b0 = (int64_t)blockIdx.x * T, b = b0 + tid, t = 2 * b;
+  const bool active = t < a.K;
+  const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
+  const int64_t step = 1ll << a.shift;
+  const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
+  if (a.do_state && active) {
+    double xl[N], xr[N];
+    const double *pl = hl ? (jl < 0 ? a.xhalo : a.x + jl * N) : nullptr;
+    const double *pr = hr ? a.x + jr * N : nullptr;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      xl[k] = pl ? pl[k] : 0.0;
+      xr[k] = pr ? pr[k] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = ldv<32>(a.rec, b, RR::w + i);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s = fma(-ldv<32>(a.rec, b, RR::Tl + i * N + k), xl[k], s);
+        s = fma(-ldv<32>(a.rec, b, RR::Tr + i * N + k), xr[k], s);
+      }
+      a.x[j * N + i] = s;
+    }
+  }
+  if (!a.do_cov) return;
+
+  // Stage the neighbours' covariance blocks through shared memory: the CTA's
+  // 64 columns have 65 distinct neighbours (level-(L+1) columns b0-1 .. b0+63),
+  // each a contiguous 8 n^2-byte block of S in step order, loaded coalesced
+  // and stored element-major so that thread reads are conflict-free.
+  extern __shared__ double bsm[];
+  double *Snb = bsm;              // [NN][NB]
+  double *Stt = bsm + NN * NB;    // [NN][TS]
+  const int64_t Kup = a.K / 2;    // columns of level L+1
+  for (int idx = tid; idx < NB * NN; idx += T) {
+    const int sblk = idx / NN, e = idx - sblk * NN;
+    const int64_t q = b0 - 1 + sblk;
+    const double *src = nullptr;
+    if (q == -1) {
+      if (a.t0 > 0) src = a.Shalo;
+    } else if (q >= 0 && q < Kup) {
+      src = a.S + (((q + 1) << (a.shift + 1)) - 1) * NN;
+    }
+    Snb[e * NB + sblk] = src ? src[e] : 0.0;
+  }
+  __syncthreads();
+  if (active) {
+    double Sll[TR::size], Srr[TR::size], Slr[N][N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+#pragma unroll
+      for (int c = r; c < N; ++c) {
+        Sll[TR::at(r, c)] = Snb[(r * N + c) * NB + tid];
+        Srr[TR::at(r, c)] = Snb[(r * N + c) * NB + tid + 1];
+      }
+#pragma unroll
+      for (int c = 0; c < N; ++c) Slr[r][c] = (hl && hr) ? ldv<32>(a.Xup, b, r * N + c) : 0.0;
+    }
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+      double tl[N], tr[N], A[N], B[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        tl[k] = ldv<32>(a.rec, b, RR::Tl + i * N + k);
+        tr[k] = ldv<32>(a.rec, b, RR::Tr + i * N + k);
+      }
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double sll = k <= c ? Sll[TR::at(k, c)] : Sll[TR::at(c, k)];
+          const double srr = k <= c ? Srr[TR::at(k, c)] : Srr[TR::at(c, k)];
+          sa = fma(tl[k], sll, sa);
+          sa = fma(tr[k], Slr[c][k], sa);
+          sb = fma(tl[k], Slr[k][c], sb);
+          sb = fma(tr[k], srr, sb);
+        }
+        A[c] = -sa;
+        B[c] = -sb;
+      }
+      if (a.Xcur.p) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          if (hl) stv<32>(a.Xcur, t, c * N + i, A[c]);       // slot t-1: S_{t-1,t} = S_tl^T
+          if (hr) stv<32>(a.Xcur, t + 1, i * N + c, B[c]);   // slot t:   S_{t,t+1} = S_tr
+        }
+      }
+      // row i of S_tt (upper part jj >= i, mirrored: exactly symmetric)
+#pragma unroll 1
+      for (int jj = i; jj < N; ++jj) {
+        double s = ldv<32>(a.rec, b, RR::P + TR::at(i, jj));
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          s = fma(-A[k], ldv<32>(a.rec, b, RR::Tl + jj * N + k), s);
+          s = fma(-B[k], ldv<32>(a.rec, b, RR::Tr + jj * N + k), s);
+        }
+        Stt[(i * N + jj) * TS + tid] = s;
+        Stt[(jj * N + i) * TS + tid] = s;
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < T * NN; idx += T) {     // coalesced: one column's block is contiguous
+    const int col = idx / NN, e = idx - col * NN;
+    const int64_t bb = b0 + col;
+    if (2 * bb < a.K) a.S[(((2 * bb + 1) << a.shift) - 1) * NN + e] = Stt[e * TS + col];
+  }
+}
+
+// ---------------------------------------------------------------- whiten ---
+
+// Store element e of column i of a whitened level-0 view (constant: ES = 1).
+__device__ __forceinline__ void wst(const TView &v, int cst, int64_t i, int e, double x) {
+  if (cst) stv<1>(v, i, e, x);
+  else stv<32>(v, i, e, x);
+}
+
+// Evolution blocks: K = Lam Lam^T (Cholesky), El = -Lam^{-1}F,
+// Er = Lam^{-1}, e = Lam^{-1} c.  One thread per distinct block.
+template <int N>
+__global__ void __launch_bounds__(128) small_whiten_evo(SmallWhitenArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.cntE) return;
+  const int64_t g = a.first_global + i;
+  const bool evo = !((a.cntE != 1 && g == 0) || (a.N == 1 && a.first_global == 0));
+  if (!evo) {
+#pragma unroll
+    for (int k = 0; k < N * N; ++k) {
+      wst(a.El, a.cE, i, k, 0.0);
+      wst(a.Er, a.cE, i, k, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) wst(a.e, a.cE, i, k, 0.0);
+    wst(a.nEr, a.cE, i, 0, 0.0);
+    wst(a.nEl, a.cE, i, 0, 0.0);
+    return;
+  }
+  const int64_t iK = (a.cntE == 1) ? 0 : i;
+  const double *K = a.K + iK * a.sK, *F = a.F + iK * a.sF;
+  const double *cc = a.c ? a.c + iK * a.sc : nullptr;
+  double Lm[N][N];
+  bool ok = true;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) Lm[r][c] = K[r * N + c];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double d = Lm[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d = fma(-Lm[j][k], Lm[j][k], d);
+    ok &= d > 0.0;
+    const double ljj = sqrt(d > 0.0 ? d : 1.0), il = 1.0 / ljj;
+    Lm[j][j] = ljj;
+#pragma unroll
+    for (int r = j + 1; r < N; ++r) {
+      double v = Lm[r][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v = fma(-Lm[r][k], Lm[j][k], v);
+      Lm[r][j] = v * il;
+    }
+  }
+  if (!ok) report(a.status, (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i, kBadK);
+  double il[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) il[r] = 1.0 / Lm[r][r];
+  double nel = 0.0, ner = 0.0;
+  // El = -Lam^{-1} F, column by column
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double x[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double s = F[r * N + c];
+#pragma unroll
+      for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
+      x[r] = s * il[r];
+    }
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      wst(a.El, a.cE, i, r * N + c, -x[r]);
+      nel = fma(x[r], x[r], nel);
+    }
+  }
+  // Er = Lam^{-1} (lower triangular)
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double x[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double s = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
+      x[r] = (r < c) ? 0.0 : s * il[r];
+    }
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      wst(a.Er, a.cE, i, r * N + c, x[r]);
+      ner = fma(x[r], x[r], ner);
+    }
+  }
+  {
+    double x[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double s = cc ? cc[r] : 0.0;
+#pragma unroll
+      for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
+      x[r] = s * il[r];
+      wst(a.e, a.cE, i, r, x[r]);
+    }
+  }
+  wst(a.nEr, a.cE, i, 0, ner);
+  wst(a.nEl, a.cE, i, 0, nel);
+}
+
+// Observation blocks: L = M M^T; C = M^{-1} H, y = M^{-1} o (rows >= m_i are 0).
+// One thread per distinct block; m_i <= kSmallMaxM.
+template <int N>
+__global__ void __launch_bounds__(128) small_whiten_obs(SmallWhitenArgs a) {
+  constexpr int MM = kSmallMaxM;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.cntC) return;
+  const int mx = a.m_max;
+  const int mi = a.m ? a.m[i] : mx;
+  const double *L = a.L + i * a.sL, *H = a.H + i * a.sH, *o = a.o + i * a.so;
+  double Lm[MM][MM];
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < MM; ++j) {
+    if (j < mi) {
+      double d = L[j * mx + j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) d = fma(-Lm[j][k], Lm[j][k], d);
+      ok &= d > 0.0;
+      const double ljj = sqrt(d > 0.0 ? d : 1.0), il = 1.0 / ljj;
+      Lm[j][j] = ljj;
+#pragma unroll
+      for (int r = j + 1; r < MM; ++r) {
+        if (r < mi) {
+          double v = L[r * mx + j];
+#pragma unroll
+          for (int k = 0; k < j; ++k) v = fma(-Lm[r][k], Lm[j][k], v);
+          Lm[r][j] = v * il;
+        }
+      }
+    }
+  }
+  if (!ok) report(a.status, i, kBadL);
+  double nc = 0.0;
+#pragma unroll
+  for (int c = 0; c <= N; ++c) {          // N columns of H, then o
+    const bool is_o = (c == N);
+    if (is_o && a.constC) break;
+    double x[MM];
+#pragma unroll
+    for (int r = 0; r < MM; ++r) {
+      if (r < mi) {
+        double s = is_o ? o[r] : H[r * N + c];
+#pragma unroll
+        for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
+        x[r] = s / Lm[r][r];
+      } else {
+        x[r] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < MM; ++r) {
+      if (r < mx) {
+        if (is_o) {
+          wst(a.y, 0, i, r, x[r]);
+        } else {
+          wst(a.C, a.cC, i, r * N + c, x[r]);
+          nc = fma(x[r], x[r], nc);
+        }
+      }
+    }
+  }
+  wst(a.nC, a.cC, i, 0, nc);
+  if (a.constC) {
+#pragma unroll
+    for (int r = 0; r < MM; ++r)
+#pragma unroll
+      for (int k = 0; k < MM; ++k)
+        if (r < mx && k < mx) a.Mchol[r * mx + k] = (k <= r && r < mi) ? Lm[r][k] : 0.0;
+  }
+}
+
+// Constant observation model: y_i = M^{-1} o_i, one thread per step.
+template <int DUMMY>
+__global__ void __launch_bounds__(256) small_whiten_y(SmallWhitenArgs a) {
+  __shared__ double M[kSmallMaxM * kSmallMaxM];
+  const int mx = a.m_max;
+  for (int k = threadIdx.x; k < mx * mx; k += blockDim.x) M[k] = a.Mchol[k];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const double *o = a.o + i * a.so;
+  double y[kSmallMaxM];
+#pragma unroll
+  for (int r = 0; r < kSmallMaxM; ++r) {
+    if (r < mx) {
+      double s = o[r];
+#pragma unroll
+      for (int k = 0; k < r; ++k) s = fma(-M[r * mx + k], y[k], s);
+      y[r] = s / M[r * mx + r];
+      wst(a.y, 0, i, r, y[r]);
+    }
+  }
+}
+
+template <int N, bool L0, bool CE, bool CC, bool OAOS>
+cudaError_t factor_launch(const SmallFactorArgs &a, cudaStream_t s) {
+  const int64_t np = a.K >= 2 ? a.K / 2 : 1;
+  const int T = 64;
+  const unsigned g = (unsigned)((np + T - 1) / T);
+  const size_t smem = (size_t)T * (N * (N + 1) + N * (N + 1) / 2) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(small_factor_kernel<N, L0, CE, CC, OAOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  small_factor_kernel<N, L0, CE, CC, OAOS><<<g, T, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N, bool OAOS>
+cudaError_t factor_oaos(const SmallFactorArgs &a, cudaStream_t s) {
+  if (a.in.ent.p != nullptr) return factor_launch<N, false, false, false, OAOS>(a, s);
+  if (a.cE) {
+    if (a.cC) return factor_launch<N, true, true, true, OAOS>(a, s);
+    return factor_launch<N, true, true, false, OAOS>(a, s);
+  }
+  if (a.cC) return factor_launch<N, true, false, true, OAOS>(a, s);
+  return factor_launch<N, true, false, false, OAOS>(a, s);
+}
+
+template <int N>
+cudaError_t factor_n(const SmallFactorArgs &a, cudaStream_t s) {
+  return a.outAoS ? factor_oaos<N, true>(a, s) : factor_oaos<N, false>(a, s);
+}
+
+template <int N>
+cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
+  const int64_t nc = (a.K + 1) / 2;
+  const int T = kBwdT;
+  const size_t smem = a.do_cov ? (size_t)N * N * (2 * T + 2) * sizeof(double) : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(small_backward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(N * N * (2 * T + 2) * sizeof(double)));
+    attr = true;
+  }
+  small_backward_kernel<N><<<(unsigned)((nc + T - 1) / T), T, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t whiten_n(const SmallWhitenArgs &a, cudaStream_t s, int *nl) {
+  const int T = 128;
+  small_whiten_evo<N><<<(unsigned)((a.cntE + T - 1) / T), T, 0, s>>>(a);
+  *nl = 1;
+  if (a.m_max > 0) {
+    small_whiten_obs<N><<<(unsigned)((a.cntC + T - 1) / T), T, 0, s>>>(a);
+    *nl += 1;
+    if (a.constC) {
+      small_whiten_y<N><<<(unsigned)((a.N + 255) / 256), 256, 0, s>>>(a);
+      *nl += 1;
+    }
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace smalld
+}  // namespace ks
+

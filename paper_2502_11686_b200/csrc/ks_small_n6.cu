@@ -1,0 +1,10 @@
+// Instantiation of the small-n path for n = 6 (see ks_small_impl.cuh).
+#include "ks_small_impl.cuh"
+
+namespace ks {
+namespace smalld {
+template cudaError_t factor_n<6>(const SmallFactorArgs &, cudaStream_t);
+template cudaError_t backward_n<6>(const SmallBackwardArgs &, cudaStream_t);
+template cudaError_t whiten_n<6>(const SmallWhitenArgs &, cudaStream_t, int *);
+}  // namespace smalld
+}  // namespace ks
