@@ -119,6 +119,17 @@ struct Rr {
   static constexpr int Tl = 0, Tr = N * N, w = 2 * N * N, P = 2 * N * N + N;
 };
 
+// Shared memory of the factor kernel: per-thread parking (leftover rows
+// N(N+1) + R~ packed N(N+1)/2, element-major), then the staged constant
+// level-0 blocks (El, Er, e, C with RC <= kSmallMaxM rows).
+template <int N>
+constexpr int kParkDoubles = N * (N + 1) + N * (N + 1) / 2;
+template <int N>
+struct CstOff {
+  static constexpr int El = 0, Er = N * N, e = 2 * N * N, C = 2 * N * N + N,
+                       size = 2 * N * N + N + kSmallMaxM * N;
+};
+
 template <int N, bool L0, bool CE, bool CC, bool OAOS>
 __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_t t, bool hr, bool hl,
                                                 int64_t pnext, bool zs_in, bool zs_out) {
@@ -129,23 +140,37 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // field loads: level 0 per-field views (constant blocks: ES = 1, ts = 0),
   // level >= 1 one tiled entry record view
   constexpr int ESE = CE ? 1 : 32, ESC = CC ? 1 : 32, ESO = OAOS ? 1 : 32;
-  auto ldC = [&](int e, int64_t c) { return L0 ? ldv<ESC>(in.C, c, e) : ldv<32>(in.ent, c, EN::C + e); };
+  // constant level-0 blocks (stride-0 model) are staged once per CTA in
+  // shared memory by the kernel prologue and read there (broadcast)
+  extern __shared__ double smem_park[];
+  const double *cst = smem_park + (size_t)blockDim.x * kParkDoubles<N>;
+  auto ldC = [&](int e, int64_t c) {
+    return L0 ? (CC ? cst[CstOff<N>::C + e] : ldv<32>(in.C, c, e)) : ldv<32>(in.ent, c, EN::C + e);
+  };
   auto ldY = [&](int e, int64_t c) { return L0 ? ldv<32>(in.y, c, e) : ldv<32>(in.ent, c, EN::y + e); };
-  auto ldEl = [&](int e, int64_t c) { return L0 ? ldv<ESE>(in.El, c, e) : ldv<32>(in.ent, c, EN::El + e); };
-  auto ldEr = [&](int e, int64_t c) { return L0 ? ldv<ESE>(in.Er, c, e) : ldv<32>(in.ent, c, EN::Er + e); };
-  auto ldE = [&](int e, int64_t c) { return L0 ? ldv<ESE>(in.e, c, e) : ldv<32>(in.ent, c, EN::e + e); };
+  auto ldEl = [&](int e, int64_t c) {
+    return L0 ? (CE ? cst[CstOff<N>::El + e] : ldv<32>(in.El, c, e)) : ldv<32>(in.ent, c, EN::El + e);
+  };
+  auto ldEr = [&](int e, int64_t c) {
+    return L0 ? (CE ? cst[CstOff<N>::Er + e] : ldv<32>(in.Er, c, e)) : ldv<32>(in.ent, c, EN::Er + e);
+  };
+  auto ldE = [&](int e, int64_t c) {
+    return L0 ? (CE ? cst[CstOff<N>::e + e] : ldv<32>(in.e, c, e)) : ldv<32>(in.ent, c, EN::e + e);
+  };
   auto sto = [&](int e, double v) { stv<ESO>(a.out, pnext, e, v); };
   // prefetch row i of a block field (n elements per row) of column c
   auto pfEl = [&](int i, int64_t c) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      if (L0) pfv<ESE>(in.El, c, i * N + j); else pfv<32>(in.ent, c, EN::El + i * N + j);
+      if (!L0) pfv<32>(in.ent, c, EN::El + i * N + j);
+      else if (!CE) pfv<32>(in.El, c, i * N + j);
     }
   };
   auto pfEr = [&](int i, int64_t c) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      if (L0) pfv<ESE>(in.Er, c, i * N + j); else pfv<32>(in.ent, c, EN::Er + i * N + j);
+      if (!L0) pfv<32>(in.ent, c, EN::Er + i * N + j);
+      else if (!CE) pfv<32>(in.Er, c, i * N + j);
     }
   };
   const int64_t rcol = t >> 1;
@@ -181,7 +206,6 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // thread at sp[e * blockDim.x]): the stage-1 leftover rows (N x (N+1)) and
   // a copy of R~_t (packed), so that at most ~76 doubles are live in
   // registers at any point (stage 1 -> stage 2 pass B -> stage 3 -> pass A).
-  extern __shared__ double smem_park[];
   double *sp = smem_park + threadIdx.x;
   const int bs = blockDim.x;
   auto park = [&](int e, double v) { sp[e * bs] = v; };
@@ -486,6 +510,21 @@ constexpr int factor_min_blocks(int n) { return n <= 4 ? 8 : n == 5 ? 7 : n == 6
 
 template <int N, bool L0, bool CE, bool CC, bool OAOS>
 __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(SmallFactorArgs a) {
+  if (L0 && (CE || CC)) {   // stage the constant (stride-0) level-0 blocks once per CTA
+    extern __shared__ double smem_park[];
+    double *cst = smem_park + (size_t)blockDim.x * kParkDoubles<N>;
+    for (int k = threadIdx.x; k < CstOff<N>::size; k += blockDim.x) {
+      double v = 0.0;
+      if (CE && k < CstOff<N>::e + N) {
+        v = k < CstOff<N>::Er ? a.in.El.p[k] : k < CstOff<N>::e ? a.in.Er.p[k - CstOff<N>::Er]
+                                                              : a.in.e.p[k - CstOff<N>::e];
+      } else if (CC && k >= CstOff<N>::C && k - CstOff<N>::C < a.in.RC * N) {
+        v = a.in.C.p[k - CstOff<N>::C];
+      }
+      cst[k] = v;
+    }
+    __syncthreads();
+  }
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t K = a.K;
   const int64_t npairs = K >= 2 ? K / 2 : 1;
@@ -514,6 +553,12 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
 // S_lr = S_{t-1,t+1} is the level-(L+1) cross block; S_{t-1,t} = S_tl^T and
 // S_{t,t+1} = S_tr are stored for level L-1.
 constexpr int kBwdT = 64;   // threads (= eliminated columns) per backward CTA
+
+// 8-byte asynchronous global -> shared copy (LDGSTS); src_size 0 zero-fills.
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gsrc), "r"(valid ? 8 : 0));
+}
 
 template <int N>
 __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs a) {
@@ -565,8 +610,9 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
     } else if (q >= 0 && q < Kup) {
       src = a.S + (((q + 1) << (a.shift + 1)) - 1) * NN;
     }
-    Snb[e * NB + sblk] = src ? src[e] : 0.0;
+    cp_async8(&Snb[e * NB + sblk], src ? src + e : a.S, src != nullptr);
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (active) {
     double Sll[TR::size], Srr[TR::size], Slr[N][N];
@@ -839,7 +885,7 @@ cudaError_t factor_launch(const SmallFactorArgs &a, cudaStream_t s) {
   const int64_t np = a.K >= 2 ? a.K / 2 : 1;
   const int T = 64;
   const unsigned g = (unsigned)((np + T - 1) / T);
-  const size_t smem = (size_t)T * (N * (N + 1) + N * (N + 1) / 2) * sizeof(double);
+  const size_t smem = ((size_t)T * kParkDoubles<N> + CstOff<N>::size) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(small_factor_kernel<N, L0, CE, CC, OAOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
