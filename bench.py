@@ -121,7 +121,7 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def roofline(launches, N, n, m, strides, p64_tf):
+def roofline(launches, N, n, m, strides, p64_tf, cfg="c5"):
     """Dominant launch (largest total time in the timed region) vs its roofline."""
     from paper_2502_11686_b200 import model
     groups = {}
@@ -142,7 +142,17 @@ def roofline(launches, N, n, m, strides, p64_tf):
         ach = fl / avg_s / 1e12
         r = {"bound": "alu", "achieved": ach, "peak": p64_tf, "unit": "TFLOP/s", "frac": ach / p64_tf,
              "peak_source": "measured fp64 DFMA peak (ks_peak_fp64_tflops, this run)"}
-    r.update({"traffic": None, "kernel": f"{fam}_level_kernel L={lev}", "launch_ms": avg_s * 1e3,
+    traffic, tsrc = None, None
+    try:   # DRAM bytes of this launch from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        rec = tj.get(cfg, {}).get(f"{fam} L={lev}")
+        if rec:
+            traffic, tsrc = rec["bytes"], f"profiles/{rec['round']}_{fam}_L{lev}.txt ({rec['report']})"
+    except Exception:
+        pass
+    r.update({"traffic": traffic, "traffic_source": tsrc, "kernel": f"{fam}_level_kernel L={lev}",
+              "launch_ms": avg_s * 1e3,
               "share_of_step": share, "algorithmic_bytes": by, "algorithmic_flops": fl,
               "units": units,
               "other_roof_frac": (fl / avg_s / 1e12 / p64_tf) if r["bound"] == "hbm"
@@ -251,7 +261,7 @@ def main():
     sm.set_timing(False)
     sm.check()
     value = N / (ms / 1e3)
-    rl = roofline(launches, M, p.n, p.m_max, strides, p64)
+    rl = roofline(launches, M, p.n, p.m_max, strides, p64, a.config if P == 1 and a.N is None else "")
     sb, sf = model.step_totals(M, p.n, p.m_max, strides)
     bw = peaks()[0]
     step_rl = {"algorithmic_bytes": sb, "algorithmic_flops": sf,

@@ -29,7 +29,9 @@ def entry_doubles(n: int) -> int:
 
 
 def rrec_doubles(n: int) -> int:
-    return 3 * n * n + n
+    """R record of an eliminated column: T_l, T_r (n x n), w (n), P (packed
+    upper n(n+1)/2 on the small path; full n x n on the generic path)."""
+    return 2 * n * n + n + (n * (n + 1) // 2 if n <= 8 else n * n)
 
 
 def level0_column_doubles(n: int, RC: int, strides: dict) -> int:
@@ -61,8 +63,13 @@ def solve_level(n: int, K: int):
 
 
 def selinv_level(n: int, K: int, level: int):
+    """Per eliminated column: read T_l, T_r, P and the neighbour blocks S_ll,
+    S_rr (each level-(L+1) block is the neighbour of two columns: one block
+    per column) and S_lr; write S_tt and, for levels >= 1, the two cross
+    blocks the next level down reads."""
     cols = (K + 1) // 2
-    d = 3 * n * n + 3 * n * n + n * n + (2 * n * n if level >= 1 else 0)
+    p = n * (n + 1) // 2 if n <= 8 else n * n
+    d = 2 * n * n + p + n * n + n * n + n * n + (2 * n * n if level >= 1 else 0)
     return 8 * cols * d, cols * 12 * n ** 3, cols
 
 

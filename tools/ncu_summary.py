@@ -27,8 +27,9 @@ STALLS = ["no_instructions", "long_scoreboard", "short_scoreboard", "wait", "mat
           "dispatch_stall", "drain", "tex_throttle", "membar", "sleeping", "imc_miss", "misc"]
 
 
-def main(rep):
-    out = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"]).decode()
+def main(rep, launch=None):
+    flt = [] if launch is None else ["-s", str(launch), "-c", "1"]
+    out = subprocess.check_output(["ncu", "-i", rep, *flt, "--page", "raw", "--csv"]).decode()
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
     for r in rows[2:]:
