@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <algorithm>
 #include <new>
 #include <vector>
 
@@ -303,33 +305,36 @@ SmallIn small_level0(const ks_ctx *c) {
   return v;
 }
 
-int run_small_factor_levels(ks_ctx *c) {
+SmallFactorArgs small_factor_args(ks_ctx *c, size_t i) {
   const int n = c->n;
   const int64_t E = entry_doubles(n), Rs = small_rrec_doubles(n);
   const std::vector<int64_t> &Ks = c->K_;
+  SmallFactorArgs a;
+  const bool last = i + 1 == Ks.size();
+  a.in = small_level0(c);
+  if (i > 0) a.in.ent = tv(c->ent[i], 32 * E);
+  a.outAoS = 0;
+  if (!last) a.out = tv(c->ent[i + 1], 32 * E);
+  else if (c->sharded) { a.out = tv(c->send, E); a.outAoS = 1; }
+  else a.out = tv(nullptr, 0);
+  a.rec = tv(c->rrec[i], 32 * Rs);
+  a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+  a.K = Ks[i];
+  a.level = (int)i;
+  a.lbase = 0;
+  a.step0 = 0;
+  a.status = c->status;
+  a.zscratch = c->zscratch;
+  a.cE = c->cntE == 1;
+  a.cC = c->cntC == 1;
+  return a;
+}
+
+int run_small_factor_levels(ks_ctx *c) {
+  const int n = c->n;
+  const std::vector<int64_t> &Ks = c->K_;
   for (size_t i = 0; i < Ks.size(); ++i) {
-    SmallFactorArgs a;
-    const bool last = i + 1 == Ks.size();
-    if (i == 0) {
-      a.in = small_level0(c);
-    } else {
-      a.in = small_level0(c);
-      a.in.ent = tv(c->ent[i], 32 * E);
-    }
-    a.outAoS = 0;
-    if (!last) a.out = tv(c->ent[i + 1], 32 * E);
-    else if (c->sharded) { a.out = tv(c->send, E); a.outAoS = 1; }
-    else a.out = tv(nullptr, 0);
-    a.rec = tv(c->rrec[i], 32 * Rs);
-    a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
-    a.K = Ks[i];
-    a.level = (int)i;
-    a.lbase = 0;
-    a.step0 = 0;
-    a.status = c->status;
-    a.zscratch = c->zscratch;
-    a.cE = c->cntE == 1;
-    a.cC = c->cntC == 1;
+    SmallFactorArgs a = small_factor_args(c, i);
     Launch l(c, 1, (int)i);
     cudaError_t e = launch_small_factor(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
@@ -337,23 +342,30 @@ int run_small_factor_levels(ks_ctx *c) {
   return KS_OK;
 }
 
-int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
+SmallBackwardArgs small_backward_args(ks_ctx *c, int i, int do_state, int do_cov) {
   const int n = c->n;
   const int64_t nn = (int64_t)n * n, Rs = small_rrec_doubles(n);
   const std::vector<int64_t> &Ks = c->K_;
+  SmallBackwardArgs a;
+  a.rec = tv(c->rrec[i], 32 * Rs);
+  a.K = Ks[i];
+  a.shift = i;
+  a.do_state = do_state;
+  a.do_cov = do_cov;
+  const bool top = i + 1 == (int)Ks.size();
+  a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+  a.x = c->xout; a.S = c->Sout; a.xhalo = c->hx; a.Shalo = c->hS;
+  if (!top) a.Xup = tv(c->X[i + 1], 32 * nn);
+  else a.Xup = c->sharded ? tv(c->Xq_local, 32 * nn) : tv(nullptr, 0);
+  a.Xcur = (i >= 1 && do_cov) ? tv(c->X[i], 32 * nn) : tv(nullptr, 0);
+  return a;
+}
+
+int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
+  const int n = c->n;
+  const std::vector<int64_t> &Ks = c->K_;
   for (int i = (int)Ks.size() - 1; i >= 0; --i) {
-    SmallBackwardArgs a;
-    a.rec = tv(c->rrec[i], 32 * Rs);
-    a.K = Ks[i];
-    a.shift = i;
-    a.do_state = do_state;
-    a.do_cov = do_cov;
-    const bool top = i + 1 == (int)Ks.size();
-    a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
-    a.x = c->xout; a.S = c->Sout; a.xhalo = c->hx; a.Shalo = c->hS;
-    if (!top) a.Xup = tv(c->X[i + 1], 32 * nn);
-    else a.Xup = c->sharded ? tv(c->Xq_local, 32 * nn) : tv(nullptr, 0);
-    a.Xcur = (i >= 1 && do_cov) ? tv(c->X[i], 32 * nn) : tv(nullptr, 0);
+    SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
     Launch l(c, do_cov ? 3 : 2, i);
     cudaError_t e = launch_small_backward(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);

@@ -134,9 +134,11 @@ template <int N, bool L0, bool CE, bool CC, bool OAOS>
 __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_t t, bool hr, bool hl,
                                                 int64_t pnext, bool zs_in, bool zs_out) {
   using TR = Tri<N>;
+  constexpr int UR = 1;   // row loops stay rolled: the unrolled body thrashes the I-cache
   using EN = Ent<N>;
   using RR = Rr<N>;
   const SmallIn &in = a.in;
+  double *zs_ = a.zscratch;
   // field loads: level 0 per-field views (constant blocks: ES = 1, ts = 0),
   // level >= 1 one tiled entry record view
   constexpr int ESE = CE ? 1 : 32, ESC = CC ? 1 : 32, ESO = OAOS ? 1 : 32;
@@ -229,7 +231,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   } else {
 #pragma unroll
     for (int k = 0; k < TR::size; ++k) R[k] = 0.0;
-#pragma unroll 1
+#pragma unroll UR
     for (int r = 0; r < in.RC; ++r) {
       double row[N];
 #pragma unroll
@@ -250,7 +252,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // leftover rows [0 | d | y~] (rows of D~_{t+1}) are parked for stage 3.
   if (hr) {
     const int64_t u = t + 1;
-#pragma unroll 1
+#pragma unroll UR
     for (int i = 0; i < N; ++i) {
       double el[N], er[N];
 #pragma unroll
@@ -287,7 +289,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 #pragma unroll
   for (int k = 0; k < TR::size; ++k) park(kRt + k, R[k]);
   if (hl) {
-#pragma unroll 1
+#pragma unroll UR
     for (int i = 0; i < N; ++i) {
       double er[N], xr[N];
 #pragma unroll
@@ -312,7 +314,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       }
     }
   } else if (hr) {
-#pragma unroll 1
+#pragma unroll UR
     for (int i = 0; i < N; ++i) {
 #pragma unroll
       for (int j = 0; j < N; ++j) sto(EN::Er + i * N + j, 0.0);
@@ -352,7 +354,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       for (int k = 0; k < TR::size; ++k) R3[k] = 0.0;
 #pragma unroll
       for (int i = 0; i < N; ++i) z3[i] = 0.0;
-#pragma unroll 1
+#pragma unroll UR
       for (int r = 0; r < in.RC; ++r) {
         double row[N];
 #pragma unroll
@@ -369,7 +371,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       }
     }
     const int nrows = zs_in ? 2 * N : N;    // leftover rows, then the odd level's Zs (reading R5)
-#pragma unroll 1
+#pragma unroll UR
     for (int i = 0; i < nrows; ++i) {
       double row[N], zr;
       if (i < N) {
@@ -378,8 +380,8 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         zr = unpark(kLeft + i * (N + 1) + N);
       } else {
 #pragma unroll
-        for (int j = 0; j < N; ++j) row[j] = a.zscratch[(i - N) * (N + 1) + j];
-        zr = a.zscratch[(i - N) * (N + 1) + N];
+        for (int j = 0; j < N; ++j) row[j] = zs_[(i - N) * (N + 1) + j];
+        zr = zs_[(i - N) * (N + 1) + N];
       }
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -408,7 +410,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 #pragma unroll
     for (int j = 0; j < N; ++j) Rl[i][j] = 0.0;
   if (hl) {
-#pragma unroll 1
+#pragma unroll UR
     for (int i = 0; i < N; ++i) {
       double er[N], el[N];
 #pragma unroll
@@ -437,12 +439,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         sto(EN::e + i, ee);                                           // z^_t
       } else if (zs_out) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) a.zscratch[i * (N + 1) + j] = el[j];
-        a.zscratch[i * (N + 1) + N] = ee;
+        for (int j = 0; j < N; ++j) zs_[i * (N + 1) + j] = el[j];
+        zs_[i * (N + 1) + N] = ee;
       }
     }
   } else if (hr) {
-#pragma unroll 1
+#pragma unroll UR
     for (int i = 0; i < N; ++i) {
 #pragma unroll
       for (int j = 0; j < N; ++j) sto(EN::El + i * N + j, 0.0);
@@ -508,6 +510,25 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 // Resident CTAs (of 64 threads) per SM the register allocation targets.
 constexpr int factor_min_blocks(int n) { return n <= 4 ? 8 : n == 5 ? 7 : n == 6 ? KS_F6_BLOCKS : 4; }
 
+// One work item of a factor level: pair p (plus, on an odd level, the last
+// column without right neighbour, handled first by the last pair's thread).
+template <int N, bool L0, bool CE, bool CC, bool OAOS>
+__device__ __forceinline__ void factor_item(const SmallFactorArgs &a, int64_t p) {
+  const int64_t K = a.K;
+  const bool single_only = (K == 1);
+  const bool triple = (K >= 3) && (K & 1) && (p == K / 2 - 1);
+  // pass 0: the odd level's last column (no right neighbour), pass 1: the pair.
+  // One inlined call site keeps the (large, fully unrolled) body once in the
+  // instruction cache.
+#pragma unroll 1
+  for (int pass = (single_only || triple) ? 0 : 1; pass < (single_only ? 1 : 2); ++pass) {
+    const int64_t t = pass == 0 ? K - 1 : 2 * p;
+    const bool hl = t + a.t0 > 0;
+    if (pass == 0) small_eliminate<N, L0, CE, CC, OAOS>(a, t, false, hl, 0, false, hl);
+    else small_eliminate<N, L0, CE, CC, OAOS>(a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false);
+  }
+}
+
 template <int N, bool L0, bool CE, bool CC, bool OAOS>
 __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(SmallFactorArgs a) {
   if (L0 && (CE || CC)) {   // stage the constant (stride-0) level-0 blocks once per CTA
@@ -526,21 +547,9 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
     __syncthreads();
   }
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t K = a.K;
-  const int64_t npairs = K >= 2 ? K / 2 : 1;
+  const int64_t npairs = a.K >= 2 ? a.K / 2 : 1;
   if (p >= npairs) return;
-  const bool single_only = (K == 1);
-  const bool triple = (K >= 3) && (K & 1) && (p == K / 2 - 1);
-  // pass 0: the odd level's last column (no right neighbour), pass 1: the pair.
-  // One inlined call site keeps the (large, fully unrolled) body once in the
-  // instruction cache.
-#pragma unroll 1
-  for (int pass = (single_only || triple) ? 0 : 1; pass < (single_only ? 1 : 2); ++pass) {
-    const int64_t t = pass == 0 ? K - 1 : 2 * p;
-    const bool hl = t + a.t0 > 0;
-    if (pass == 0) small_eliminate<N, L0, CE, CC, OAOS>(a, t, false, hl, 0, false, hl);
-    else small_eliminate<N, L0, CE, CC, OAOS>(a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false);
-  }
+  factor_item<N, L0, CE, CC, OAOS>(a, p);
 }
 
 // -------------------------------------------------------------- backward ---
@@ -593,16 +602,20 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
   }
   if (!a.do_cov) return;
 
-  // Stage the neighbours' covariance blocks through shared memory: the CTA's
-  // 64 columns have 65 distinct neighbours (level-(L+1) columns b0-1 .. b0+63),
-  // each a contiguous 8 n^2-byte block of S in step order, loaded coalesced
-  // and stored element-major so that thread reads are conflict-free.
+  // Shared-memory staging (cp.async, coalesced): the 65 distinct neighbour
+  // covariance blocks of the CTA's 64 columns (level-(L+1) columns
+  // b0-1 .. b0+63, each a contiguous n^2 block of S in step order) and the
+  // CTA's R records (T_l, T_r, P).  Everything the compute phase reads then
+  // comes from shared memory or registers; the S_tt blocks go back through
+  // shared memory (overlaying the neighbour blocks) as contiguous stores.
+  constexpr int NT = N * (N + 1) / 2, NR = 2 * NN + NT;   // staged record elements
   extern __shared__ double bsm[];
-  double *Snb = bsm;              // [NN][NB]
-  double *Stt = bsm + NN * NB;    // [NN][TS]
-  const int64_t Kup = a.K / 2;    // columns of level L+1
-  for (int idx = tid; idx < NB * NN; idx += T) {
-    const int sblk = idx / NN, e = idx - sblk * NN;
+  double *Snb = bsm;                 // [NN][NB]   (later: S_tt [NN][TS])
+  double *TP = bsm + NN * NB;        // [NR][NB]   T_l | T_r | P
+  const int64_t Kup = a.K / 2;       // columns of level L+1
+  // neighbour blocks: thread tid stages block sblk = tid (and thread 0 also
+  // the 65th); every element offset is an immediate
+  auto stage_block = [&](int sblk) {
     const int64_t q = b0 - 1 + sblk;
     const double *src = nullptr;
     if (q == -1) {
@@ -610,12 +623,27 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
     } else if (q >= 0 && q < Kup) {
       src = a.S + (((q + 1) << (a.shift + 1)) - 1) * NN;
     }
-    cp_async8(&Snb[e * NB + sblk], src ? src + e : a.S, src != nullptr);
+    const bool ok = src != nullptr;
+    const double *s0 = ok ? src : a.S;
+#pragma unroll
+    for (int e = 0; e < NN; ++e) cp_async8(&Snb[e * NB + sblk], s0 + (ok ? e : 0), ok);
+  };
+  stage_block(tid);
+  if (tid == 0) stage_block(T);
+  // R records: thread tid stages its own column (T_l, T_r, then P)
+  {
+    const int64_t ncol = (a.K + 1) / 2;
+    const bool ok = b < ncol;
+    const double *rc = ok ? cb<32>(a.rec, b) : a.rec.p;
+#pragma unroll
+    for (int e = 0; e < 2 * NN; ++e) cp_async8(&TP[e * NB + tid], rc + (ok ? 32 * e : 0), ok);
+#pragma unroll
+    for (int e = 0; e < NT; ++e) cp_async8(&TP[(2 * NN + e) * NB + tid], rc + (ok ? 32 * (RR::P + e) : 0), ok);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  double Sll[TR::size], Srr[TR::size], Slr[N][N];
   if (active) {
-    double Sll[TR::size], Srr[TR::size], Slr[N][N];
 #pragma unroll
     for (int r = 0; r < N; ++r) {
 #pragma unroll
@@ -626,13 +654,18 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
 #pragma unroll
       for (int c = 0; c < N; ++c) Slr[r][c] = (hl && hr) ? ldv<32>(a.Xup, b, r * N + c) : 0.0;
     }
+  }
+  __syncthreads();                   // Snb is dead: its space becomes S_tt
+  double *Stt = bsm;
+  auto tp = [&](int e) { return TP[e * NB + tid]; };
+  if (active) {
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
       double tl[N], tr[N], A[N], B[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        tl[k] = ldv<32>(a.rec, b, RR::Tl + i * N + k);
-        tr[k] = ldv<32>(a.rec, b, RR::Tr + i * N + k);
+        tl[k] = tp(i * N + k);
+        tr[k] = tp(NN + i * N + k);
       }
 #pragma unroll
       for (int c = 0; c < N; ++c) {
@@ -656,17 +689,17 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
           if (hr) stv<32>(a.Xcur, t + 1, i * N + c, B[c]);   // slot t:   S_{t,t+1} = S_tr
         }
       }
-      // row i of S_tt (upper part jj >= i, mirrored: exactly symmetric)
+      // row i of S_tt = P - S_tl T_l^T - S_tr T_r^T (upper part jj >= i, mirrored)
 #pragma unroll 1
       for (int jj = i; jj < N; ++jj) {
-        double s = ldv<32>(a.rec, b, RR::P + TR::at(i, jj));
+        double sv = tp(2 * NN + TR::at(i, jj));
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          s = fma(-A[k], ldv<32>(a.rec, b, RR::Tl + jj * N + k), s);
-          s = fma(-B[k], ldv<32>(a.rec, b, RR::Tr + jj * N + k), s);
+          sv = fma(-A[k], tp(jj * N + k), sv);
+          sv = fma(-B[k], tp(NN + jj * N + k), sv);
         }
-        Stt[(i * N + jj) * TS + tid] = s;
-        Stt[(jj * N + i) * TS + tid] = s;
+        Stt[(i * N + jj) * TS + tid] = sv;
+        Stt[(jj * N + i) * TS + tid] = sv;
       }
     }
   }
@@ -916,11 +949,11 @@ template <int N>
 cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
   const int64_t nc = (a.K + 1) / 2;
   const int T = kBwdT;
-  const size_t smem = a.do_cov ? (size_t)N * N * (2 * T + 2) * sizeof(double) : 0;
+  const size_t full = (size_t)(N * N + 2 * N * N + N * (N + 1) / 2) * (T + 1) * sizeof(double);
+  const size_t smem = a.do_cov ? full : 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(small_backward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(N * N * (2 * T + 2) * sizeof(double)));
+    cudaFuncSetAttribute(small_backward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)full);
     attr = true;
   }
   small_backward_kernel<N><<<(unsigned)((nc + T - 1) / T), T, smem, s>>>(a);
