@@ -7,7 +7,7 @@ constant-velocity model), time-sharded over N GPUs (strong scaling).
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 One step = ks_whiten + ks_factor (+ boundary allgather + ks_factor_boundary
-on N > 1) + ks_solve + ks_selinv with inputs resident in HBM (outputs bound
+on N > 1) + ks_solve_selinv (solve + SelInv in one backward sweep) with inputs resident in HBM (outputs bound
 to caller buffers, so ks_get is free).  The working set (~11 GB) is far
 larger than L2 (126 MB), so no L2 flush is needed between steps.
 
@@ -222,8 +222,7 @@ def main():
         if P > 1:
             kdist.exchange_boundary(v[0], v[1])
             s.factor_boundary()
-        s.solve()
-        s.selinv()
+        s.solve_selinv()
         if get is not None:
             s.get(*get)
 

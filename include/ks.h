@@ -20,7 +20,9 @@
  *
  * Call order (each returns KS_ERR_ORDER when called out of order):
  *     ks_create -> ks_whiten -> ks_factor -> ks_solve [-> ks_selinv] -> ks_get
- * ks_selinv is optional (the paper's "NC" variant).  All calls only
+ *                                          or ks_solve_selinv        -> ks_get
+ * ks_selinv is optional (the paper's "NC" variant);
+ * ks_solve_selinv does both backward phases in one pass over the factor.  All calls only
  * ENQUEUE work on the stream given to ks_create; only ks_sync_status and
  * ks_get with host destination buffers synchronise.
  */
@@ -131,6 +133,14 @@ int ks_solve(ks_ctx *ctx);
  * reverse: S_{j,I} = -T S_{I,I}, S_jj = P - S_{j,I} T^T, symmetrised. */
 int ks_selinv(ks_ctx *ctx);
 
+/* Phases 3 + 4 fused: the same results as ks_solve followed by ks_selinv
+ * (bitwise), computed in one backward sweep over the levels that reads each
+ * stored R record once (P:592-600 and Alg. 2, P:792-824 share the loop over
+ * the levels in reverse and the operand T = R_jj^{-1}[R_{j,l} R_{j,r}]).
+ * Requires a covariance buffer (cov_out bound, or KS_OUTPUTS_BOUND unset);
+ * KS_ERR_ARG otherwise. */
+int ks_solve_selinv(ks_ctx *ctx);
+
 /* Copy results into caller buffers (device or host; NULL = skip).  A pointer
  * equal to the bound output buffer is a no-op.  Host destinations synchronise
  * the stream.  cov requires a prior ks_selinv. */
@@ -151,10 +161,11 @@ int ks_factor_boundary(ks_ctx *ctx);
 /* Per-kernel-family device timing with CUDA events recorded around every
  * launch on the context's stream (0 = off; ks_set_timing synchronises and
  * resets).  Families: 0 whiten, 1 factor levels, 2 solve levels, 3 selinv
- * levels, 4 multi-GPU boundary system.  ms[f] = summed event time,
- * launches[f] = timed launches (synchronises). */
+ * levels, 4 multi-GPU boundary system, 5 fused solve+selinv levels.
+ * ms[f] = summed event time, launches[f] = timed launches (synchronises). */
+#define KS_NFAMILIES 6
 int ks_set_timing(ks_ctx *ctx, int on);
-int ks_get_timing(ks_ctx *ctx, double ms[5], int64_t launches[5]);
+int ks_get_timing(ks_ctx *ctx, double ms[KS_NFAMILIES], int64_t launches[KS_NFAMILIES]);
 
 /* The individual timed launches since ks_set_timing (synchronises): returns
  * their count (negative = -error code) and fills up to `cap` entries of

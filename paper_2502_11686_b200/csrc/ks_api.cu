@@ -102,8 +102,8 @@ struct ks_ctx {
   std::vector<int> ev_family, ev_level;
   std::vector<int32_t> rec_family, rec_level;
   std::vector<float> rec_ms;
-  double t_ms[5] = {0, 0, 0, 0, 0};
-  int64_t t_cnt[5] = {0, 0, 0, 0, 0};
+  double t_ms[KS_NFAMILIES] = {};
+  int64_t t_cnt[KS_NFAMILIES] = {};
 };
 
 namespace {
@@ -366,7 +366,7 @@ int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
   const std::vector<int64_t> &Ks = c->K_;
   for (int i = (int)Ks.size() - 1; i >= 0; --i) {
     SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
-    Launch l(c, do_cov ? 3 : 2, i);
+    Launch l(c, do_cov ? (do_state ? 5 : 3) : 2, i);
     cudaError_t e = launch_small_backward(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
@@ -411,7 +411,7 @@ int run_factor_levels(ks_ctx *c, bool boundary) {
 }
 
 // Timing families: 0 whiten, 1 factor levels, 2 solve levels, 3 selinv levels,
-// 4 boundary system (multi-GPU).
+// 4 boundary system (multi-GPU), 5 fused solve+selinv levels.
 int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
   if (c->small && !boundary) return run_small_backward_levels(c, do_state, do_cov);
   const int n = c->n;
@@ -443,7 +443,7 @@ int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
       else a.Xup = c->sharded ? c->Xq_local : nullptr;
       a.Xcur = (i >= 1) ? c->X[i] : nullptr;
     }
-    Launch l(c, boundary ? 4 : (do_cov ? 3 : 2), (boundary ? c->q : 0) + i);
+    Launch l(c, boundary ? 4 : (do_cov ? (do_state ? 5 : 3) : 2), (boundary ? c->q : 0) + i);
     cudaError_t e = launch_backward_level(a, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
@@ -652,6 +652,19 @@ int ks_selinv(ks_ctx *c) {
   return KS_OK;
 }
 
+int ks_solve_selinv(ks_ctx *c) {
+  if (!c || !c->Sout) return KS_ERR_ARG;
+  if (c->stage < 3) return KS_ERR_ORDER;
+  int r;
+  if (c->sharded) {
+    if ((r = run_backward_levels(c, true, 1, 1))) return r;
+    if ((r = scatter_boundary(c, true, true))) return r;
+  }
+  if ((r = run_backward_levels(c, false, 1, 1))) return r;
+  c->solved = c->covd = true;
+  return KS_OK;
+}
+
 int ks_get(ks_ctx *c, double *states, double *cov) {
   if (!c) return KS_ERR_ARG;
   if ((states && !c->solved) || (cov && !c->covd)) return KS_ERR_ORDER;
@@ -698,7 +711,7 @@ int ks_set_timing(ks_ctx *c, int on) {
   c->rec_family.clear();
   c->rec_level.clear();
   c->rec_ms.clear();
-  for (int f = 0; f < 5; ++f) { c->t_ms[f] = 0; c->t_cnt[f] = 0; }
+  for (int f = 0; f < KS_NFAMILIES; ++f) { c->t_ms[f] = 0; c->t_cnt[f] = 0; }
   return KS_OK;
 }
 
@@ -722,11 +735,11 @@ int drain_events(ks_ctx *c) {
 }
 }  // namespace
 
-int ks_get_timing(ks_ctx *c, double ms[5], int64_t launches[5]) {
+int ks_get_timing(ks_ctx *c, double ms[KS_NFAMILIES], int64_t launches[KS_NFAMILIES]) {
   if (!c) return KS_ERR_ARG;
   int r = drain_events(c);
   if (r) return r;
-  for (int f = 0; f < 5; ++f) {
+  for (int f = 0; f < KS_NFAMILIES; ++f) {
     if (ms) ms[f] = c->t_ms[f];
     if (launches) launches[f] = c->t_cnt[f];
   }

@@ -62,7 +62,7 @@ __device__ __forceinline__ void report(unsigned long long *st, int64_t step, int
 
 // 1/sqrt(h) for h > 0: the MUFU approximation refined by two Newton steps
 // (each doubles the correct bits: ~2^-22 -> ~2^-44 -> full double).  No
-// special-case branches (h is a sum of squares with b != 0 where it is used).
+// special-case branches.
 __device__ __forceinline__ double rsqrt_nr(double h) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h));
@@ -72,25 +72,49 @@ __device__ __forceinline__ double rsqrt_nr(double h) {
   y = fma(0.5 * y, fma(-hy, y, 1.0), y);
   return y;
 }
-
-// Givens rotation zeroing b against the pivot a: (a, b) <- (r, 0).
-// b == 0 selects the identity (c = 1, s = 0), so zero (padding) rows are exact
-// no-ops; branch-free (selects) so that ragged rows do not diverge.
-__device__ __forceinline__ void make_rot(double &a, double &b, double &c, double &s) {
-  const bool id = (b == 0.0);
-  const double h = fma(a, a, b * b);
-  const double ih = rsqrt_nr(id ? 1.0 : h);
-  c = id ? 1.0 : a * ih;
-  s = id ? 0.0 : b * ih;
-  a = id ? a : h * ih;
-  b = 0.0;
+// sqrt(h) for h >= 0 (0 -> 0), branch-free.
+__device__ __forceinline__ double sqrt_nr(double h) {
+  const bool z = !(h > 0.0);
+  const double r = h * rsqrt_nr(z ? 1.0 : h);
+  return z ? 0.0 : r;
+}
+// 1/x for x != 0: MUFU approximation + two Newton steps.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  return y;
 }
 
-__device__ __forceinline__ void rot(double &x, double &y, double c, double s) {
-  const double nx = fma(c, x, s * y);
-  const double ny = fma(c, y, -(s * x));
-  x = nx;
-  y = ny;
+// Square-root-free Givens rotations (Gentleman, 1973).  Every row of the
+// triangular factor is kept as R_k = sqrt(d_k) [1, u_{k,k+1}, ..., | trailing
+// columns], every streamed row as sqrt(delta) [y_k, y_{k+1}, ...].  Zeroing
+// y_k against row k is the plane rotation with c = sqrt(d/d'),
+// s = sqrt(delta) y_k / sqrt(d') (the same orthogonal Q as the classical
+// Givens / Householder QR of P:424-436, up to row signs: R_kk = +sqrt(d_k)):
+//     d' = d + delta y_k^2,  sbar = delta y_k / d',  delta' = delta d / d'
+//     y_j' = y_j - y_k u_j,  u_j' = u_j + sbar y_j'          (every column j > k)
+// i.e. TWO fma per element and pair instead of four, and one reciprocal
+// instead of a reciprocal square root per rotation.  d' = 0 (an empty row of
+// R meeting a zero pivot) is the identity, so zero padding rows are exact
+// no-ops; the selects keep ragged rows from diverging.
+__device__ __forceinline__ void gmake(double &d, double yk, double &delta, double &sb) {
+  const double dy = delta * yk;
+  const double dn = fma(dy, yk, d);
+  const bool id = (dn == 0.0);
+  const double inv = rcp_nr(id ? 1.0 : dn);
+  sb = id ? 0.0 : dy * inv;
+  delta = id ? delta : (delta * inv) * d;
+  d = dn;
+}
+// Apply to one column: u (row of R) and y (streamed row), yk the pivot value
+// of the streamed row before the rotation.
+__device__ __forceinline__ void gapp(double &u, double &y, double yk, double sb) {
+  y = fma(-yk, u, y);
+  u = fma(sb, y, u);
 }
 
 // ---------------------------------------------------------------- factor ---
@@ -107,6 +131,12 @@ __device__ __forceinline__ void rot(double &x, double &y, double c, double s) {
 //            neighbour: "nothing to do".
 //   post:    T_l = R^{-1} R_{t,t-1}, T_r = R^{-1} R_{t,t+1}, w = R^{-1} z_t,
 //            P = R^{-1} R^{-T} (packed) -> R record.
+// All QRs are square-root-free Givens row streaming (gmake / gapp above), so
+// R = D^{1/2} U with U unit upper triangular and the trailing blocks carry the
+// same D^{1/2}: T = U^{-1} X needs no division and P = U^{-1} D^{-1} U^{-T}.
+// Level >= 1 C-like blocks are stored in that form (d_k on the diagonal, U
+// strictly above, y = D^{-1/2} z); coupling rows are stored as true rows
+// (weight folded in: sqrt(delta) x row), so no weight accumulates over levels.
 // Entry element offsets (entry_doubles layout).
 template <int N>
 struct Ent {
@@ -119,11 +149,11 @@ struct Rr {
   static constexpr int Tl = 0, Tr = N * N, w = 2 * N * N, P = 2 * N * N + N;
 };
 
-// Shared memory of the factor kernel: per-thread parking (leftover rows
-// N(N+1) + R~ packed N(N+1)/2, element-major), then the staged constant
-// level-0 blocks (El, Er, e, C with RC <= kSmallMaxM rows).
+// Shared memory of the factor kernel: per-thread parking (leftover rows with
+// their weights N(N+2) + R~ packed N(N+1)/2, element-major), then the staged
+// constant level-0 blocks (El, Er, e, C with RC <= kSmallMaxM rows).
 template <int N>
-constexpr int kParkDoubles = N * (N + 1) + N * (N + 1) / 2;
+constexpr int kParkDoubles = N * (N + 2) + N * (N + 1) / 2;
 template <int N>
 struct CstOff {
   static constexpr int El = 0, Er = N * N, e = 2 * N * N, C = 2 * N * N + N,
@@ -177,7 +207,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   };
   const int64_t rcol = t >> 1;
   auto str = [&](int e, double v) { stv<32>(a.rec, rcol, e, v); };
-  double R[TR::size];
+  double R[TR::size];   // d_k on the diagonal, U strictly above
   double X[N][N];
   double z[N];
 
@@ -205,14 +235,28 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
     for (int j = 0; j < N; ++j) X[i][j] = 0.0;
   }
   // Per-thread shared-memory parking (element-major: element e of this
-  // thread at sp[e * blockDim.x]): the stage-1 leftover rows (N x (N+1)) and
-  // a copy of R~_t (packed), so that at most ~76 doubles are live in
-  // registers at any point (stage 1 -> stage 2 pass B -> stage 3 -> pass A).
+  // thread at sp[e * blockDim.x]): the stage-1 leftover rows with their
+  // weights (N x (N+2)) and a copy of R~_t (packed), so that at most ~76
+  // doubles are live in registers at any point (stage 1 -> stage 2 pass B ->
+  // stage 3 -> pass A).
   double *sp = smem_park + threadIdx.x;
   const int bs = blockDim.x;
   auto park = [&](int e, double v) { sp[e * bs] = v; };
   auto unpark = [&](int e) { return sp[e * bs]; };
-  constexpr int kLeft = 0, kRt = N * (N + 1);
+  constexpr int kLeft = 0, kRt = N * (N + 2);
+
+  // stream one weighted row [row (pivot part, N) | rhs] into (Rm, zm)
+  auto stream_row = [&](double(&Rm)[TR::size], double(&zm)[N], double(&row)[N], double &rhs, double dl) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double sb;
+      const double yk = row[k];
+      gmake(Rm[TR::at(k, k)], yk, dl, sb);
+#pragma unroll
+      for (int j = k + 1; j < N; ++j) gapp(Rm[TR::at(k, j)], row[j], yk, sb);
+      gapp(zm[k], rhs, yk, sb);
+    }
+  };
 
   // ---- stage 1 base: R = C_t ----
   if (hr) {
@@ -237,19 +281,13 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 #pragma unroll
       for (int j = 0; j < N; ++j) row[j] = ldC(r * N + j, t);
       double yr = ldY(r, t);
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double c, s;
-        make_rot(R[TR::at(k, k)], row[k], c, s);
-#pragma unroll
-        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], row[j], c, s);
-        rot(z[k], yr, c, s);
-      }
+      stream_row(R, z, row, yr, 1.0);
     }
   }
 
   // ---- stage 1: rows of [El_{t+1} | Er_{t+1} | e_{t+1}] into [R | X | z] ----
-  // leftover rows [0 | d | y~] (rows of D~_{t+1}) are parked for stage 3.
+  // leftover rows [0 | d | y~] (rows of D~_{t+1}) are parked, with their
+  // weights, for stage 3.
   if (hr) {
     const int64_t u = t + 1;
 #pragma unroll UR
@@ -267,19 +305,22 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       } else if (hl) {
         pfEr(0, t);
       }
+      double dl = 1.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        double c, s;
-        make_rot(R[TR::at(k, k)], el[k], c, s);
+        double sb;
+        const double yk = el[k];
+        gmake(R[TR::at(k, k)], yk, dl, sb);
 #pragma unroll
-        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], el[j], c, s);
+        for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], el[j], yk, sb);
 #pragma unroll
-        for (int j = 0; j < N; ++j) rot(X[k][j], er[j], c, s);
-        rot(z[k], ee, c, s);
+        for (int j = 0; j < N; ++j) gapp(X[k][j], er[j], yk, sb);
+        gapp(z[k], ee, yk, sb);
       }
 #pragma unroll
-      for (int j = 0; j < N; ++j) park(kLeft + i * (N + 1) + j, er[j]);
-      park(kLeft + i * (N + 1) + N, ee);
+      for (int j = 0; j < N; ++j) park(kLeft + i * (N + 2) + j, er[j]);
+      park(kLeft + i * (N + 2) + N, ee);
+      park(kLeft + i * (N + 2) + N + 1, dl);
     }
   }
 
@@ -299,18 +340,21 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       }
       if (i + 1 < N) pfEr(i + 1, t);
       else pfEl(0, t);
+      double dl = 1.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        double c, s;
-        make_rot(R[TR::at(k, k)], er[k], c, s);
+        double sb;
+        const double yk = er[k];
+        gmake(R[TR::at(k, k)], yk, dl, sb);
 #pragma unroll
-        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], er[j], c, s);
+        for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], er[j], yk, sb);
 #pragma unroll
-        for (int j = 0; j < N; ++j) rot(X[k][j], xr[j], c, s);
+        for (int j = 0; j < N; ++j) gapp(X[k][j], xr[j], yk, sb);
       }
       if (hr) {
+        const double w = sqrt_nr(dl);
 #pragma unroll
-        for (int j = 0; j < N; ++j) sto(EN::Er + i * N + j, xr[j]);   // X~_t
+        for (int j = 0; j < N; ++j) sto(EN::Er + i * N + j, w * xr[j]);   // X~_t
       }
     }
   } else if (hr) {
@@ -320,16 +364,15 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       for (int j = 0; j < N; ++j) sto(EN::Er + i * N + j, 0.0);
     }
   }
-  // T_r = R_tt^{-1} R_{t,t+1}
+  // T_r = R_tt^{-1} R_{t,t+1} = U^{-1} X (unit triangular: no division)
 #pragma unroll
   for (int i = N - 1; i >= 0; --i) {
-    const double inv = 1.0 / R[TR::at(i, i)];
 #pragma unroll
     for (int c = 0; c < N; ++c) {
       double sr = X[i][c];
 #pragma unroll
       for (int k = i + 1; k < N; ++k) sr = fma(-R[TR::at(i, k)], X[k][c], sr);
-      X[i][c] = sr * inv;
+      X[i][c] = sr;
     }
   }
 #pragma unroll
@@ -360,43 +403,42 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 #pragma unroll
         for (int j = 0; j < N; ++j) row[j] = ldC(r * N + j, u);
         double yr = ldY(r, u);
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double c, s;
-          make_rot(R3[TR::at(k, k)], row[k], c, s);
-#pragma unroll
-          for (int j = k + 1; j < N; ++j) rot(R3[TR::at(k, j)], row[j], c, s);
-          rot(z3[k], yr, c, s);
-        }
+        stream_row(R3, z3, row, yr, 1.0);
       }
     }
     const int nrows = zs_in ? 2 * N : N;    // leftover rows, then the odd level's Zs (reading R5)
 #pragma unroll UR
     for (int i = 0; i < nrows; ++i) {
-      double row[N], zr;
+      double row[N], zr, dl;
       if (i < N) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) row[j] = unpark(kLeft + i * (N + 1) + j);
-        zr = unpark(kLeft + i * (N + 1) + N);
+        for (int j = 0; j < N; ++j) row[j] = unpark(kLeft + i * (N + 2) + j);
+        zr = unpark(kLeft + i * (N + 2) + N);
+        dl = unpark(kLeft + i * (N + 2) + N + 1);
       } else {
 #pragma unroll
         for (int j = 0; j < N; ++j) row[j] = zs_[(i - N) * (N + 1) + j];
         zr = zs_[(i - N) * (N + 1) + N];
+        dl = 1.0;
       }
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double c, s;
-        make_rot(R3[TR::at(k, k)], row[k], c, s);
-#pragma unroll
-        for (int j = k + 1; j < N; ++j) rot(R3[TR::at(k, j)], row[j], c, s);
-        rot(z3[k], zr, c, s);
-      }
+      stream_row(R3, z3, row, zr, dl);
     }
+    if (OAOS) {   // the multi-GPU boundary entry: true rows (generic-path layout)
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+      for (int i = 0; i < N; ++i) {
+        const double w = sqrt_nr(R3[TR::at(i, i)]);
 #pragma unroll
-      for (int j = 0; j < N; ++j) sto(EN::C + i * N + j, j >= i ? R3[TR::at(i, j)] : 0.0);
-      sto(EN::y + i, z3[i]);
+        for (int j = 0; j < N; ++j)
+          sto(EN::C + i * N + j, j > i ? w * R3[TR::at(i, j)] : (j == i ? w : 0.0));
+        sto(EN::y + i, w * z3[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) sto(EN::C + i * N + j, j >= i ? R3[TR::at(i, j)] : 0.0);
+        sto(EN::y + i, z3[i]);
+      }
     }
     sto(EN::nrm, sqrt(ref2u));
   }
@@ -423,24 +465,29 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         pfEr(i + 1, t);
         pfEl(i + 1, t);
       }
+      double dl = 1.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        double c, s;
-        make_rot(R[TR::at(k, k)], er[k], c, s);
+        double sb;
+        const double yk = er[k];
+        gmake(R[TR::at(k, k)], yk, dl, sb);
 #pragma unroll
-        for (int j = k + 1; j < N; ++j) rot(R[TR::at(k, j)], er[j], c, s);
+        for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], er[j], yk, sb);
 #pragma unroll
-        for (int j = 0; j < N; ++j) rot(Rl[k][j], el[j], c, s);
-        rot(z[k], ee, c, s);
+        for (int j = 0; j < N; ++j) gapp(Rl[k][j], el[j], yk, sb);
+        gapp(z[k], ee, yk, sb);
       }
-      if (hr) {
+      if (hr || zs_out) {
+        const double w = sqrt_nr(dl);
+        if (hr) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) sto(EN::El + i * N + j, el[j]);   // Z_t
-        sto(EN::e + i, ee);                                           // z^_t
-      } else if (zs_out) {
+          for (int j = 0; j < N; ++j) sto(EN::El + i * N + j, w * el[j]);   // Z_t
+          sto(EN::e + i, w * ee);                                           // z^_t
+        } else {
 #pragma unroll
-        for (int j = 0; j < N; ++j) zs_[i * (N + 1) + j] = el[j];
-        zs_[i * (N + 1) + N] = ee;
+          for (int j = 0; j < N; ++j) zs_[i * (N + 1) + j] = w * el[j];
+          zs_[i * (N + 1) + N] = w * ee;
+        }
       }
     }
   } else if (hr) {
@@ -452,12 +499,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
     }
   }
 
-  // ---- post: rank check, T_l = R^{-1} R_l, w = R^{-1} z, P = R^{-1} R^{-T} ----
+  // ---- post: rank check, T_l = U^{-1} Rl, w = U^{-1} z, P = U^{-1} D^{-1} U^{-T} ----
   {
-    const double thr = kRankTol * sqrt(ref2);
+    const double thr = kRankTol * kRankTol * ref2;   // |R_kk|^2 = d_k vs (tol |col|)^2
     bool bad = false;
 #pragma unroll
-    for (int d = 0; d < N; ++d) bad |= !(fabs(R[TR::at(d, d)]) > thr);
+    for (int d = 0; d < N; ++d) bad |= !(R[TR::at(d, d)] > thr);
     if (bad) report(a.status, (((t + 1) << (a.level - a.lbase)) - 1) + a.step0, kBadRank);
   }
   double inv[N];
@@ -470,12 +517,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       double sl = Rl[i][c];
 #pragma unroll
       for (int k = i + 1; k < N; ++k) sl = fma(-R[TR::at(i, k)], Rl[k][c], sl);
-      Rl[i][c] = sl * inv[i];
+      Rl[i][c] = sl;
     }
     double sz = z[i];
 #pragma unroll
     for (int k = i + 1; k < N; ++k) sz = fma(-R[TR::at(i, k)], z[k], sz);
-    z[i] = sz * inv[i];
+    z[i] = sz;
   }
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -483,25 +530,29 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
     for (int j = 0; j < N; ++j) str(RR::Tl + i * N + j, Rl[i][j]);
     str(RR::w + i, z[i]);
   }
-  // R^{-1} (upper, in place of R): Ri(i,j) = -inv_i sum_{k=i+1..j} R(i,k) Ri(k,j)
+  // V = U^{-1} (unit upper, in place of U): V(i,j) = -sum_{k=i+1..j} U(i,k) V(k,j)
 #pragma unroll
   for (int i = N - 1; i >= 0; --i) {
 #pragma unroll
     for (int j = N - 1; j > i; --j) {
-      double s = 0.0;
+      double s = R[TR::at(i, j)];
 #pragma unroll
-      for (int k = i + 1; k <= j; ++k) s = fma(R[TR::at(i, k)], R[TR::at(k, j)], s);
-      R[TR::at(i, j)] = -s * inv[i];
+      for (int k = i + 1; k < j; ++k) s = fma(R[TR::at(i, k)], R[TR::at(k, j)], s);
+      R[TR::at(i, j)] = -s;
     }
-    R[TR::at(i, i)] = inv[i];
   }
+  // P(i,j) = sum_{k >= j} V(i,k) V(j,k) / d_k   (i <= j, V(k,k) = 1)
 #pragma unroll
   for (int i = 0; i < N; ++i) {
 #pragma unroll
     for (int j = i; j < N; ++j) {
       double s = 0.0;
 #pragma unroll
-      for (int k = j; k < N; ++k) s = fma(R[TR::at(i, k)], R[TR::at(j, k)], s);
+      for (int k = j; k < N; ++k) {
+        const double vik = (k == i) ? 1.0 : R[TR::at(i, k)];
+        const double vjk = (k == j) ? 1.0 : R[TR::at(j, k)];
+        s = fma(vik, vjk * inv[k], s);
+      }
       str(RR::P + TR::at(i, j), s);
     }
   }
@@ -560,8 +611,17 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
 //   S_tl   = -(T_l S_ll + T_r S_lr^T),  S_tr = -(T_l S_lr + T_r S_rr)   (S_{t,I} = -T S_II)
 //   S_tt   = P - S_tl T_l^T - S_tr T_r^T  (upper triangle computed, mirrored)
 // S_lr = S_{t-1,t+1} is the level-(L+1) cross block; S_{t-1,t} = S_tl^T and
-// S_{t,t+1} = S_tr are stored for level L-1.
-constexpr int kBwdT = 64;   // threads (= eliminated columns) per backward CTA
+// S_{t,t+1} = S_tr are stored for level L-1.  With do_state and do_cov both
+// set, one pass over the R records serves the solve and SelInv
+// (ks_solve_selinv).
+template <int N>
+__host__ __device__ constexpr int bwd_threads() { return N <= 6 ? 64 : 32; }   // eliminated columns per CTA
+template <int N>
+__host__ __device__ constexpr int rs_doubles() { return 2 * N * N + N + N * (N + 1) / 2; }
+template <int N>
+__host__ __device__ constexpr size_t bwd_smem_doubles() {
+  return (size_t)bwd_threads<N>() * rs_doubles<N>() + (size_t)N * N * (bwd_threads<N>() + 1);
+}
 
 // 8-byte asynchronous global -> shared copy (LDGSTS); src_size 0 zero-fills.
 __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
@@ -569,19 +629,49 @@ __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gsrc), "r"(valid ? 8 : 0));
 }
 
+// mbarrier + 1-D bulk copy (the TMA engine: UBLKCP in SASS) of a contiguous
+// global range into shared memory.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "KS_MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra KS_MBAR_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 template <int N>
-__global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs a) {
+__global__ void __launch_bounds__(bwd_threads<N>()) small_backward_kernel(SmallBackwardArgs a) {
   using TR = Tri<N>;
   using RR = Rr<N>;
-  constexpr int NN = N * N, T = kBwdT, NB = T + 1, TS = T + 1;   // odd strides: conflict-free
+  constexpr int NN = N * N, T = bwd_threads<N>(), NB = T + 1, TS = T + 1, RS = rs_doubles<N>();
   const int tid = threadIdx.x;
   const int64_t b0 = (int64_t)blockIdx.x * T, b = b0 + tid, t = 2 * b;
   const bool active = t < a.K;
   const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
   const int64_t step = 1ll << a.shift;
   const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
+  double xl[N], xr[N];
   if (a.do_state && active) {
-    double xl[N], xr[N];
     const double *pl = hl ? (jl < 0 ? a.xhalo : a.x + jl * N) : nullptr;
     const double *pr = hr ? a.x + jr * N : nullptr;
 #pragma unroll
@@ -589,6 +679,9 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
       xl[k] = pl ? pl[k] : 0.0;
       xr[k] = pr ? pr[k] : 0.0;
     }
+  }
+  if (!a.do_cov) {   // solve only: direct coalesced record loads, no staging
+    if (!active) return;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = ldv<32>(a.rec, b, RR::w + i);
@@ -599,22 +692,35 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
       }
       a.x[j * N + i] = s;
     }
+    return;
   }
-  if (!a.do_cov) return;
 
-  // Shared-memory staging (cp.async, coalesced): the 65 distinct neighbour
+  // Staging.  (1) The CTA's R records are whole tiles of the tiled record
+  // array (32 columns x RS doubles each, contiguous): ONE bulk copy by the
+  // TMA engine, completion on an mbarrier.  (2) The 65 distinct neighbour
   // covariance blocks of the CTA's 64 columns (level-(L+1) columns
-  // b0-1 .. b0+63, each a contiguous n^2 block of S in step order) and the
-  // CTA's R records (T_l, T_r, P).  Everything the compute phase reads then
-  // comes from shared memory or registers; the S_tt blocks go back through
-  // shared memory (overlaying the neighbour blocks) as contiguous stores.
-  constexpr int NT = N * (N + 1) / 2, NR = 2 * NN + NT;   // staged record elements
-  extern __shared__ double bsm[];
-  double *Snb = bsm;                 // [NN][NB]   (later: S_tt [NN][TS])
-  double *TP = bsm + NN * NB;        // [NR][NB]   T_l | T_r | P
+  // b0-1 .. b0+63, each a contiguous n^2 block of S in step order), strided
+  // in HBM: cp.async, element-major in shared memory.  (3) The cross block
+  // S_lr and the neighbour states go straight to registers, issued before
+  // the waits so that all three overlap.  The S_tt blocks go back through
+  // shared memory (overlaying (2)) as contiguous stores.
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ __align__(8) unsigned long long mbar;
+  double *REC = bsm;                 // [T/32][RS][32]
+  double *Snb = bsm + T * RS;        // [NN][NB]   (later: S_tt [NN][TS])
+  {
+    const int64_t ncol = (a.K + 1) / 2;
+    const int64_t tile0 = b0 >> 5, ntile = (ncol + 31) >> 5;
+    const int mytiles = (int)((ntile - tile0) < T / 32 ? (ntile - tile0) : T / 32);
+    if (tid == 0) mbar_init(&mbar, 1);
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned bytes = (unsigned)mytiles * RS * 32 * 8;
+      mbar_expect_tx(&mbar, bytes);
+      bulk_g2s(REC, a.rec.p + tile0 * a.rec.ts, bytes, &mbar);
+    }
+  }
   const int64_t Kup = a.K / 2;       // columns of level L+1
-  // neighbour blocks: thread tid stages block sblk = tid (and thread 0 also
-  // the 65th); every element offset is an immediate
   auto stage_block = [&](int sblk) {
     const int64_t q = b0 - 1 + sblk;
     const double *src = nullptr;
@@ -630,42 +736,48 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
   };
   stage_block(tid);
   if (tid == 0) stage_block(T);
-  // R records: thread tid stages its own column (T_l, T_r, then P)
-  {
-    const int64_t ncol = (a.K + 1) / 2;
-    const bool ok = b < ncol;
-    const double *rc = ok ? cb<32>(a.rec, b) : a.rec.p;
+  double Slr[N][N];
 #pragma unroll
-    for (int e = 0; e < 2 * NN; ++e) cp_async8(&TP[e * NB + tid], rc + (ok ? 32 * e : 0), ok);
+  for (int r = 0; r < N; ++r)
 #pragma unroll
-    for (int e = 0; e < NT; ++e) cp_async8(&TP[(2 * NN + e) * NB + tid], rc + (ok ? 32 * (RR::P + e) : 0), ok);
-  }
+    for (int c = 0; c < N; ++c) Slr[r][c] = (active && hl && hr) ? ldv<32>(a.Xup, b, r * N + c) : 0.0;
   asm volatile("cp.async.wait_all;" ::: "memory");
+  mbar_wait(&mbar, 0);
   __syncthreads();
-  double Sll[TR::size], Srr[TR::size], Slr[N][N];
+  const double *myrec = REC + (tid >> 5) * (RS * 32) + (tid & 31);
+  auto rec = [&](int e) { return myrec[e * 32]; };
+  if (active && a.do_state) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = rec(RR::w + i);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        s = fma(-rec(RR::Tl + i * N + k), xl[k], s);
+        s = fma(-rec(RR::Tr + i * N + k), xr[k], s);
+      }
+      a.x[j * N + i] = s;
+    }
+  }
+  double Sll[TR::size], Srr[TR::size];
   if (active) {
 #pragma unroll
-    for (int r = 0; r < N; ++r) {
+    for (int r = 0; r < N; ++r)
 #pragma unroll
       for (int c = r; c < N; ++c) {
         Sll[TR::at(r, c)] = Snb[(r * N + c) * NB + tid];
         Srr[TR::at(r, c)] = Snb[(r * N + c) * NB + tid + 1];
       }
-#pragma unroll
-      for (int c = 0; c < N; ++c) Slr[r][c] = (hl && hr) ? ldv<32>(a.Xup, b, r * N + c) : 0.0;
-    }
   }
   __syncthreads();                   // Snb is dead: its space becomes S_tt
-  double *Stt = bsm;
-  auto tp = [&](int e) { return TP[e * NB + tid]; };
+  double *Stt = Snb;
   if (active) {
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
       double tl[N], tr[N], A[N], B[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        tl[k] = tp(i * N + k);
-        tr[k] = tp(NN + i * N + k);
+        tl[k] = rec(RR::Tl + i * N + k);
+        tr[k] = rec(RR::Tr + i * N + k);
       }
 #pragma unroll
       for (int c = 0; c < N; ++c) {
@@ -692,11 +804,11 @@ __global__ void __launch_bounds__(kBwdT) small_backward_kernel(SmallBackwardArgs
       // row i of S_tt = P - S_tl T_l^T - S_tr T_r^T (upper part jj >= i, mirrored)
 #pragma unroll 1
       for (int jj = i; jj < N; ++jj) {
-        double sv = tp(2 * NN + TR::at(i, jj));
+        double sv = rec(RR::P + TR::at(i, jj));
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          sv = fma(-A[k], tp(jj * N + k), sv);
-          sv = fma(-B[k], tp(NN + jj * N + k), sv);
+          sv = fma(-A[k], rec(RR::Tl + jj * N + k), sv);
+          sv = fma(-B[k], rec(RR::Tr + jj * N + k), sv);
         }
         Stt[(i * N + jj) * TS + tid] = sv;
         Stt[(jj * N + i) * TS + tid] = sv;
@@ -948,8 +1060,8 @@ cudaError_t factor_n(const SmallFactorArgs &a, cudaStream_t s) {
 template <int N>
 cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
   const int64_t nc = (a.K + 1) / 2;
-  const int T = kBwdT;
-  const size_t full = (size_t)(N * N + 2 * N * N + N * (N + 1) / 2) * (T + 1) * sizeof(double);
+  constexpr int T = bwd_threads<N>();
+  const size_t full = bwd_smem_doubles<N>() * sizeof(double);
   const size_t smem = a.do_cov ? full : 0;
   static bool attr = false;
   if (!attr) {

@@ -67,6 +67,7 @@ class ShardedSmoother:
         if self.world > 1:
             exchange_boundary(self.views[0], self.views[1])
             s.factor_boundary()
-        s.solve()
         if cov:
-            s.selinv()
+            s.solve_selinv()
+        else:
+            s.solve()

@@ -23,10 +23,10 @@ LIB_PATH = os.path.join(_HERE, "libks.so")
 KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
     KS_ERR_WORKSPACE = range(8)
 KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH = 1, 2, 4
-FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary")
+FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary", "backward")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
-           "ks_get", "ks_sync_status", "ks_boundary_buffers", "ks_factor_boundary",
+           "ks_solve_selinv", "ks_get", "ks_sync_status", "ks_boundary_buffers", "ks_factor_boundary",
            "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info",
            "ks_peak_fp64_tflops", "ks_strerror", "ks_destroy")
 
@@ -67,7 +67,8 @@ def lib():
         L.ks_workspace_bytes.restype = sz
         L.ks_create.argtypes = [C.POINTER(vp), C.POINTER(ks_problem), vp, sz, vp,
                                 C.POINTER(ks_shard), vp, vp]
-        for f in ("ks_whiten", "ks_factor", "ks_solve", "ks_selinv", "ks_factor_boundary"):
+        for f in ("ks_whiten", "ks_factor", "ks_solve", "ks_selinv", "ks_solve_selinv",
+                  "ks_factor_boundary"):
             getattr(L, f).argtypes = [vp]
         L.ks_get.argtypes = [vp, vp, vp]
         L.ks_sync_status.argtypes = [vp, C.POINTER(i64), C.POINTER(i32)]
@@ -212,6 +213,9 @@ class Smoother:
     def selinv(self):
         _check(self.L.ks_selinv(self.ctx), "ks_selinv")
 
+    def solve_selinv(self):
+        _check(self.L.ks_solve_selinv(self.ctx), "ks_solve_selinv")
+
     def get(self, states=None, cov=None):
         """Copy results into torch tensors (device or host)."""
         sp = None if states is None else states.data_ptr()
@@ -233,8 +237,8 @@ class Smoother:
         _check(self.L.ks_set_timing(self.ctx, 1 if on else 0), "ks_set_timing")
 
     def timing(self):
-        ms = (C.c_double * 5)()
-        cnt = (C.c_int64 * 5)()
+        ms = (C.c_double * len(FAMILIES))()
+        cnt = (C.c_int64 * len(FAMILIES))()
         _check(self.L.ks_get_timing(self.ctx, ms, cnt), "ks_get_timing")
         return {f: (ms[i], cnt[i]) for i, f in enumerate(FAMILIES)}
 
@@ -252,10 +256,14 @@ class Smoother:
         _check(self.L.ks_info(self.ctx, C.byref(lv), C.byref(la)), "ks_info")
         return {"levels": lv.value, "launches": la.value}
 
-    def run(self, cov: bool = True):
-        """whiten -> factor -> solve [-> selinv] (enqueue only)."""
+    def run(self, cov: bool = True, fused: bool = True):
+        """whiten -> factor -> solve [-> selinv] (enqueue only); with cov and
+        fused, the two backward phases run as one ks_solve_selinv sweep."""
         self.whiten()
         self.factor()
+        if cov and fused:
+            self.solve_selinv()
+            return
         self.solve()
         if cov:
             self.selinv()

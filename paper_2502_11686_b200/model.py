@@ -73,6 +73,16 @@ def selinv_level(n: int, K: int, level: int):
     return 8 * cols * d, cols * 12 * n ** 3, cols
 
 
+def backward_level(n: int, K: int, level: int):
+    """Fused solve + SelInv (ks_solve_selinv) per eliminated column: the R
+    record read once (T_l, T_r, w, P), one neighbour state and one neighbour
+    covariance block (each level-(L+1) column neighbours two eliminated
+    columns), S_lr; write x_t, S_tt and, for levels >= 1, the two cross blocks."""
+    cols = (K + 1) // 2
+    d = rrec_doubles(n) + n + n * n + n * n + n + n * n + (2 * n * n if level >= 1 else 0)
+    return 8 * cols * d, cols * (12 * n ** 3 + 4 * n * n), cols
+
+
 def whiten(n: int, m: int, N: int, cntE: int, cntC: int, per_step_o: bool = True):
     by = cntE * (2 * n * n + n) + cntE * (3 * n * n + n)            # F,K,c in; El,Er,e out
     by += cntC * (m * n + m * m) + cntC * (m * n)                    # H,L in; C out
@@ -92,8 +102,9 @@ def levels(N: int):
     return Ks
 
 
-def step_totals(N: int, n: int, m: int, strides: dict, cov: bool = True):
-    """Whole-step algorithmic (bytes, flops) on one GPU."""
+def step_totals(N: int, n: int, m: int, strides: dict, cov: bool = True, fused: bool = True):
+    """Whole-step algorithmic (bytes, flops) on one GPU (fused: the backward
+    phases as one ks_solve_selinv sweep)."""
     tb = tf = 0
     cntE = 1 if not strides.get("E", 1) else N
     cntC = 1 if not strides.get("C", 1) else N
@@ -102,6 +113,10 @@ def step_totals(N: int, n: int, m: int, strides: dict, cov: bool = True):
     for L, K in enumerate(levels(N)):
         b, f, _ = factor_level(n, m if L == 0 else n, K, L, strides)
         tb += b; tf += f
+        if cov and fused:
+            b, f, _ = backward_level(n, K, L)
+            tb += b; tf += f
+            continue
         b, f, _ = solve_level(n, K)
         tb += b; tf += f
         if cov:
@@ -119,6 +134,8 @@ def launch_cost(family: str, level: int, N: int, n: int, m: int, strides: dict):
         return solve_level(n, K)
     if family == "selinv":
         return selinv_level(n, K, level)
+    if family == "backward":
+        return backward_level(n, K, level)
     if family == "whiten":
         cntE = 1 if not strides.get("E", 1) else N
         cntC = 1 if not strides.get("C", 1) else N

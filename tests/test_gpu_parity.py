@@ -22,9 +22,9 @@ def ks():
     return _ks
 
 
-def gpu_smooth(p, cov=True, **kw):
+def gpu_smooth(p, cov=True, fused=True, **kw):
     s = ks().Smoother(p, cov=cov, **kw)
-    s.run(cov=cov)
+    s.run(cov=cov, fused=fused)
     s.check()
     x = s.states.cpu().numpy()
     S = s.cov.cpu().numpy() if cov else None
@@ -105,6 +105,24 @@ def test_determinism_bitwise(generic):
     assert np.array_equal(x1, x2) and np.array_equal(S1, S2)
 
 
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("case", ["c2", "c3", "c5", "r1", "r2", "r5", "r7", "r8"])
+def test_fused_backward_matches_separate(case, generic):
+    """ks_solve_selinv (one sweep) gives the same bits as ks_solve + ks_selinv."""
+    if case.startswith("r"):
+        n = int(case[1:])
+        rng = np.random.default_rng(50 + n)
+        p = gen.random_problem(rng, 777, n, m_max=min(n + 1, 8))
+        p.m = np.minimum(p.m, p.m_max)
+    else:
+        p = gen.make(case, N=4097 if case != "c5" else 12345)
+    x1, S1, _ = gpu_smooth(p, fused=True, generic=generic)
+    x2, S2, _ = gpu_smooth(p, fused=False, generic=generic)
+    assert np.array_equal(x1, x2) and np.array_equal(S1, S2)
+    xo, So = oracle.smooth(p)
+    assert rel_state_err(x1, xo) <= TOL_X and rel_cov_err(S1, So) <= TOL_S
+
+
 def test_small_and_generic_paths_agree():
     p = gen.make("c2", N=4097)
     x1, S1, _ = gpu_smooth(p)
@@ -174,7 +192,7 @@ def test_error_order_and_args():
         s.get(torch.empty((64, 2), dtype=torch.float64, device="cuda"))
 
 
-def _virtual_shards(p, P, cov=True, generic=False):
+def _virtual_shards(p, P, cov=True, generic=False, fused=False):
     """The time-sharded multi-GPU algorithm with P ranks emulated on one GPU:
     each rank's local levels run in its own context; the allgather is a
     device copy into every rank's receive buffer (no rank waits on another)."""
@@ -189,6 +207,9 @@ def _virtual_shards(p, P, cov=True, generic=False):
     for s, (_, rcv) in zip(parts, views):
         rcv.copy_(gathered)
         s.factor_boundary()
+        if cov and fused:
+            s.solve_selinv()
+            continue
         s.solve()
         if cov:
             s.selinv()
@@ -206,6 +227,8 @@ def _virtual_shards(p, P, cov=True, generic=False):
 def test_virtual_shards_match_oracle(cfg, N, P, generic):
     p = gen.make(cfg, N=N)
     x, S = _virtual_shards(p, P, generic=generic)
+    xf, Sf = _virtual_shards(p, P, generic=generic, fused=True)
+    assert np.array_equal(x, xf) and np.array_equal(S, Sf)
     xo, So = oracle.smooth(p)
     assert rel_state_err(x, xo) <= TOL_X
     assert rel_cov_err(S, So) <= TOL_S
