@@ -4,8 +4,10 @@ Each translation unit is compiled to an object file in parallel (the small-n
 path is split into one file per state dimension), then linked with
 `nvcc -shared`.  Objects go to paper_2502_11686_b200/build/ (git-ignored).
 
-Development knob: KS_SMALL_NS="6" builds only the n = 6 small-path
+Development knobs: KS_SMALL_NS="6" builds only the n = 6 small-path
 instantiation (faster iteration; other n then report cudaErrorInvalidValue).
+`build.py --variant NAME -DFOO=1 ...` builds an A/B experiment variant
+variants/libks_NAME.so with extra nvcc defines (load it with KS_LIB=path).
 """
 import glob
 import os
@@ -35,8 +37,8 @@ def deps():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [os.path.join(ROOT, "include", "ks.h")]
 
 
-def _compile(src, extra):
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def _compile(src, extra, objdir=OBJ):
+    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
     cmd = [os.environ.get("NVCC", "nvcc"), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"),
            "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -65,5 +67,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines) -> str:
+    objdir = os.path.join(OBJ, "v_" + name)
+    os.makedirs(objdir, exist_ok=True)
+    out = os.path.join(HERE, "variants", f"libks_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    srcs = sources()
+    defines = list(defines) + (["-DKS_SMALL_ONLY6"] if os.environ.get("KS_SMALL_NS") else [])
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 4))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, defines, objdir), srcs))
+    subprocess.check_call([os.environ.get("NVCC", "nvcc"), *ARCH, "-shared", "-cudart", "static", "-o", out,
+                           *objs, "-ldl"])
+    return out
+
+
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], [a for a in sys.argv[i + 2:] if a.startswith("-D")]))
+    else:
+        build(force=True, verbose="-v" in sys.argv)

@@ -89,26 +89,41 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return y;
 }
 
-// Square-root-free Givens rotations (Gentleman, 1973).  Every row of the
-// triangular factor is kept as R_k = sqrt(d_k) [1, u_{k,k+1}, ..., | trailing
-// columns], every streamed row as sqrt(delta) [y_k, y_{k+1}, ...].  Zeroing
-// y_k against row k is the plane rotation with c = sqrt(d/d'),
-// s = sqrt(delta) y_k / sqrt(d') (the same orthogonal Q as the classical
-// Givens / Householder QR of P:424-436, up to row signs: R_kk = +sqrt(d_k)):
-//     d' = d + delta y_k^2,  sbar = delta y_k / d',  delta' = delta d / d'
-//     y_j' = y_j - y_k u_j,  u_j' = u_j + sbar y_j'          (every column j > k)
-// i.e. TWO fma per element and pair instead of four, and one reciprocal
-// instead of a reciprocal square root per rotation.  d' = 0 (an empty row of
-// R meeting a zero pivot) is the identity, so zero padding rows are exact
-// no-ops; the selects keep ragged rows from diverging.
-__device__ __forceinline__ void gmake(double &d, double yk, double &delta, double &sb) {
-  const double dy = delta * yk;
-  const double dn = fma(dy, yk, d);
-  const bool id = (dn == 0.0);
-  const double inv = rcp_nr(id ? 1.0 : dn);
-  sb = id ? 0.0 : dy * inv;
-  delta = id ? delta : (delta * inv) * d;
-  d = dn;
+// Square-root-free Givens rotations (Gentleman, 1973), in inverse-weight
+// form.  Every row of the triangular factor is kept as
+// R_k = sqrt(d_k) [1, u_{k,k+1}, ..., | trailing columns] and stored through
+// rho_k = 1/d_k (+inf: row k still empty); every streamed row as
+// sqrt(delta) [y_k, y_{k+1}, ...], stored through w = 1/delta (+inf: the row
+// has been absorbed).  Zeroing y_k against row k is the plane rotation with
+// c = sqrt(d/d'), s = sqrt(delta) y_k / sqrt(d') (the same orthogonal Q as
+// the classical Givens / Householder QR of P:424-436, up to row signs:
+// R_kk = +sqrt(d_k)).  With d' = d + delta y_k^2:
+//     w'   = w + y_k^2 rho                 (= 1/delta', delta' = delta d/d')
+//     rho' = rho w / w',   sbar = y_k rho / w'   (= delta y_k / d')
+//     y_j' = y_j - y_k u_j,  u_j' = u_j + sbar y_j'      (every column j > k)
+// TWO fma per element and pair instead of four, one reciprocal per rotation,
+// and -- the point of the inverse-weight form -- the serial dependence from
+// one pivot to the next is a single fma (w') instead of a reciprocal (square
+// root) chain: the reciprocals of consecutive pivots overlap.  An empty row
+// absorbs the streamed row (rho' = w / y_k^2, sbar = 1/y_k, w' = inf); y_k = 0
+// or an absorbed row is the identity, so zero padding rows are exact no-ops.
+// The selects keep ragged rows from diverging.
+__device__ __forceinline__ void gmake(double &rho, double yk, double &w, double &sb) {
+  const bool empty = !(rho < __longlong_as_double(0x7ff0000000000000ll));
+  const bool ident = (yk == 0.0) || !(w < __longlong_as_double(0x7ff0000000000000ll));
+  const double rs = empty ? 0.0 : rho;
+  const double yr = yk * rs;
+  const double wn = fma(yk, yr, w);
+  const double q = rcp_nr(ident ? 1.0 : (empty ? yk : wn));
+  sb = ident ? 0.0 : (empty ? q : yr * q);
+  rho = ident ? rho : (empty ? (w * q) * q : rs * (w * q));
+  w = ident ? w : (empty ? __longlong_as_double(0x7ff0000000000000ll) : wn);
+}
+// sqrt(delta) = 1/sqrt(w) of a streamed row (0 once absorbed).
+__device__ __forceinline__ double wscale(double w) {
+  const bool fin = w < __longlong_as_double(0x7ff0000000000000ll);
+  const double r = rsqrt_nr(fin ? w : 1.0);
+  return fin ? r : 0.0;
 }
 // Apply to one column: u (row of R) and y (streamed row), yk the pivot value
 // of the streamed row before the rotation.
@@ -134,10 +149,11 @@ __device__ __forceinline__ void gapp(double &u, double &y, double yk, double sb)
 // All QRs are square-root-free Givens row streaming (gmake / gapp above), so
 // R = D^{1/2} U with U unit upper triangular and the trailing blocks carry the
 // same D^{1/2}: T = U^{-1} X needs no division and P = U^{-1} D^{-1} U^{-T}.
-// Level >= 1 C-like blocks are stored in that form (d_k on the diagonal, U
+// Level >= 1 C-like blocks are stored in that form (1/d_k on the diagonal, U
 // strictly above, y = D^{-1/2} z); coupling rows are stored as true rows
 // (weight folded in: sqrt(delta) x row), so no weight accumulates over levels.
 // Entry element offsets (entry_doubles layout).
+constexpr double kEmptyRow = __builtin_huge_val();   // rho of an empty row of R
 template <int N>
 struct Ent {
   static constexpr int C = 0, y = N * N, El = N * N + N, Er = 2 * N * N + N, e = 3 * N * N + N,
@@ -246,12 +262,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   constexpr int kLeft = 0, kRt = N * (N + 2);
 
   // stream one weighted row [row (pivot part, N) | rhs] into (Rm, zm)
-  auto stream_row = [&](double(&Rm)[TR::size], double(&zm)[N], double(&row)[N], double &rhs, double dl) {
+  auto stream_row = [&](double(&Rm)[TR::size], double(&zm)[N], double(&row)[N], double &rhs, double wl) {
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double sb;
       const double yk = row[k];
-      gmake(Rm[TR::at(k, k)], yk, dl, sb);
+      gmake(Rm[TR::at(k, k)], yk, wl, sb);
 #pragma unroll
       for (int j = k + 1; j < N; ++j) gapp(Rm[TR::at(k, j)], row[j], yk, sb);
       gapp(zm[k], rhs, yk, sb);
@@ -274,7 +290,9 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < TR::size; ++k) R[k] = 0.0;
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = i; j < N; ++j) R[TR::at(i, j)] = (j == i) ? kEmptyRow : 0.0;
 #pragma unroll UR
     for (int r = 0; r < in.RC; ++r) {
       double row[N];
@@ -305,12 +323,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       } else if (hl) {
         pfEr(0, t);
       }
-      double dl = 1.0;
+      double wl = 1.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double sb;
         const double yk = el[k];
-        gmake(R[TR::at(k, k)], yk, dl, sb);
+        gmake(R[TR::at(k, k)], yk, wl, sb);
 #pragma unroll
         for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], el[j], yk, sb);
 #pragma unroll
@@ -320,7 +338,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 #pragma unroll
       for (int j = 0; j < N; ++j) park(kLeft + i * (N + 2) + j, er[j]);
       park(kLeft + i * (N + 2) + N, ee);
-      park(kLeft + i * (N + 2) + N + 1, dl);
+      park(kLeft + i * (N + 2) + N + 1, wl);
     }
   }
 
@@ -340,19 +358,19 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       }
       if (i + 1 < N) pfEr(i + 1, t);
       else pfEl(0, t);
-      double dl = 1.0;
+      double wl = 1.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double sb;
         const double yk = er[k];
-        gmake(R[TR::at(k, k)], yk, dl, sb);
+        gmake(R[TR::at(k, k)], yk, wl, sb);
 #pragma unroll
         for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], er[j], yk, sb);
 #pragma unroll
         for (int j = 0; j < N; ++j) gapp(X[k][j], xr[j], yk, sb);
       }
       if (hr) {
-        const double w = sqrt_nr(dl);
+        const double w = wscale(wl);
 #pragma unroll
         for (int j = 0; j < N; ++j) sto(EN::Er + i * N + j, w * xr[j]);   // X~_t
       }
@@ -394,7 +412,9 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < TR::size; ++k) R3[k] = 0.0;
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i; j < N; ++j) R3[TR::at(i, j)] = (j == i) ? kEmptyRow : 0.0;
 #pragma unroll
       for (int i = 0; i < N; ++i) z3[i] = 0.0;
 #pragma unroll UR
@@ -409,24 +429,24 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
     const int nrows = zs_in ? 2 * N : N;    // leftover rows, then the odd level's Zs (reading R5)
 #pragma unroll UR
     for (int i = 0; i < nrows; ++i) {
-      double row[N], zr, dl;
+      double row[N], zr, wl;
       if (i < N) {
 #pragma unroll
         for (int j = 0; j < N; ++j) row[j] = unpark(kLeft + i * (N + 2) + j);
         zr = unpark(kLeft + i * (N + 2) + N);
-        dl = unpark(kLeft + i * (N + 2) + N + 1);
+        wl = unpark(kLeft + i * (N + 2) + N + 1);
       } else {
 #pragma unroll
         for (int j = 0; j < N; ++j) row[j] = zs_[(i - N) * (N + 1) + j];
         zr = zs_[(i - N) * (N + 1) + N];
-        dl = 1.0;
+        wl = 1.0;
       }
-      stream_row(R3, z3, row, zr, dl);
+      stream_row(R3, z3, row, zr, wl);
     }
     if (OAOS) {   // the multi-GPU boundary entry: true rows (generic-path layout)
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        const double w = sqrt_nr(R3[TR::at(i, i)]);
+        const double w = wscale(R3[TR::at(i, i)]);   // sqrt(d) = 1/sqrt(rho)
 #pragma unroll
         for (int j = 0; j < N; ++j)
           sto(EN::C + i * N + j, j > i ? w * R3[TR::at(i, j)] : (j == i ? w : 0.0));
@@ -465,12 +485,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         pfEr(i + 1, t);
         pfEl(i + 1, t);
       }
-      double dl = 1.0;
+      double wl = 1.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double sb;
         const double yk = er[k];
-        gmake(R[TR::at(k, k)], yk, dl, sb);
+        gmake(R[TR::at(k, k)], yk, wl, sb);
 #pragma unroll
         for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], er[j], yk, sb);
 #pragma unroll
@@ -478,7 +498,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         gapp(z[k], ee, yk, sb);
       }
       if (hr || zs_out) {
-        const double w = sqrt_nr(dl);
+        const double w = wscale(wl);
         if (hr) {
 #pragma unroll
           for (int j = 0; j < N; ++j) sto(EN::El + i * N + j, w * el[j]);   // Z_t
@@ -501,15 +521,15 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 
   // ---- post: rank check, T_l = U^{-1} Rl, w = U^{-1} z, P = U^{-1} D^{-1} U^{-T} ----
   {
-    const double thr = kRankTol * kRankTol * ref2;   // |R_kk|^2 = d_k vs (tol |col|)^2
+    const double thr = kRankTol * kRankTol * ref2;   // |R_kk|^2 = d_k = 1/rho_k vs (tol |col|)^2
     bool bad = false;
 #pragma unroll
-    for (int d = 0; d < N; ++d) bad |= !(R[TR::at(d, d)] > thr);
+    for (int d = 0; d < N; ++d) bad |= !(R[TR::at(d, d)] * thr < 1.0);
     if (bad) report(a.status, (((t + 1) << (a.level - a.lbase)) - 1) + a.step0, kBadRank);
   }
-  double inv[N];
+  double inv[N];   // 1/d_k
 #pragma unroll
-  for (int i = 0; i < N; ++i) inv[i] = 1.0 / R[TR::at(i, i)];
+  for (int i = 0; i < N; ++i) inv[i] = R[TR::at(i, i)];
 #pragma unroll
   for (int i = N - 1; i >= 0; --i) {
 #pragma unroll
@@ -614,13 +634,26 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
 // S_{t,t+1} = S_tr are stored for level L-1.  With do_state and do_cov both
 // set, one pass over the R records serves the solve and SelInv
 // (ks_solve_selinv).
-template <int N>
-__host__ __device__ constexpr int bwd_threads() { return N <= 6 ? 64 : 32; }   // eliminated columns per CTA
+// Backward CTA: BC eliminated columns (one record tile), two threads per
+// column (warp 0: the "left" half of Alg. 2's products, warp 1: the "right").
+constexpr int kBwdCols = 32;
+// resident CTAs per SM the register allocation targets (no spills at n = 6..8)
+constexpr int bwd_min_blocks(int n) { return n <= 5 ? 5 : n == 6 ? 4 : 3; }
 template <int N>
 __host__ __device__ constexpr int rs_doubles() { return 2 * N * N + N + N * (N + 1) / 2; }
+// S_tt staging row: NN doubles padded to a multiple of 2 (16-byte rows for
+// the bulk store) and to an odd number of 16-byte units (fewer bank conflicts)
+template <int N>
+__host__ __device__ constexpr int bwd_sp() { return ((N * N + 1) / 2) % 2 ? 2 * ((N * N + 1) / 2) : 2 * ((N * N + 1) / 2) + 2; }
+// shared memory: record tile | max(neighbour blocks [NN][BC+1],
+//                                  Q_l, Q_r [2][NT][BC+1] + S_tt staging [BC][SP])
 template <int N>
 __host__ __device__ constexpr size_t bwd_smem_doubles() {
-  return (size_t)bwd_threads<N>() * rs_doubles<N>() + (size_t)N * N * (bwd_threads<N>() + 1);
+  return (size_t)kBwdCols * rs_doubles<N>() +
+         ((size_t)N * N * (kBwdCols + 1) >
+                  (size_t)N * (N + 1) * (kBwdCols + 1) + (size_t)kBwdCols * bwd_sp<N>()
+              ? (size_t)N * N * (kBwdCols + 1)
+              : (size_t)N * (N + 1) * (kBwdCols + 1) + (size_t)kBwdCols * bwd_sp<N>());
 }
 
 // 8-byte asynchronous global -> shared copy (LDGSTS); src_size 0 zero-fills.
@@ -660,18 +693,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
 }
 
 template <int N>
-__global__ void __launch_bounds__(bwd_threads<N>()) small_backward_kernel(SmallBackwardArgs a) {
+__global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backward_kernel(SmallBackwardArgs a) {
   using TR = Tri<N>;
   using RR = Rr<N>;
-  constexpr int NN = N * N, T = bwd_threads<N>(), NB = T + 1, TS = T + 1, RS = rs_doubles<N>();
-  const int tid = threadIdx.x;
-  const int64_t b0 = (int64_t)blockIdx.x * T, b = b0 + tid, t = 2 * b;
+  constexpr int NN = N * N, BC = kBwdCols, NB = BC + 1, RS = rs_doubles<N>(), SP = bwd_sp<N>(),
+                NT = N * (N + 1) / 2;
+  const int tid = threadIdx.x, col = tid & (BC - 1);
+  const bool right = tid >= BC;      // warp-uniform
+  const int64_t b0 = (int64_t)blockIdx.x * BC, b = b0 + col, t = 2 * b;
   const bool active = t < a.K;
   const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
   const int64_t step = 1ll << a.shift;
   const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
   double xl[N], xr[N];
-  if (a.do_state && active) {
+  if (a.do_state && active && !right) {
     const double *pl = hl ? (jl < 0 ? a.xhalo : a.x + jl * N) : nullptr;
     const double *pr = hr ? a.x + jr * N : nullptr;
 #pragma unroll
@@ -681,7 +716,7 @@ __global__ void __launch_bounds__(bwd_threads<N>()) small_backward_kernel(SmallB
     }
   }
   if (!a.do_cov) {   // solve only: direct coalesced record loads, no staging
-    if (!active) return;
+    if (!active || right) return;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = ldv<32>(a.rec, b, RR::w + i);
@@ -695,58 +730,56 @@ __global__ void __launch_bounds__(bwd_threads<N>()) small_backward_kernel(SmallB
     return;
   }
 
-  // Staging.  (1) The CTA's R records are whole tiles of the tiled record
-  // array (32 columns x RS doubles each, contiguous): ONE bulk copy by the
-  // TMA engine, completion on an mbarrier.  (2) The 65 distinct neighbour
-  // covariance blocks of the CTA's 64 columns (level-(L+1) columns
-  // b0-1 .. b0+63, each a contiguous n^2 block of S in step order), strided
-  // in HBM: cp.async, element-major in shared memory.  (3) The cross block
-  // S_lr and the neighbour states go straight to registers, issued before
-  // the waits so that all three overlap.  The S_tt blocks go back through
-  // shared memory (overlaying (2)) as contiguous stores.
+  // Staging.  (1) The CTA's R records are one tile of the tiled record array
+  // (32 columns x RS doubles, contiguous): ONE bulk copy by the TMA engine,
+  // completion on an mbarrier.  (2) The 33 distinct neighbour covariance
+  // blocks of the CTA's 32 columns (level-(L+1) columns b0-1 .. b0+31, each a
+  // contiguous n^2 block of S in step order), strided in HBM: cp.async,
+  // element-major in shared memory.  (3) The cross block S_lr and the
+  // neighbour states go straight to registers, issued before the waits.
+  // Alg. 2's products are split between the two threads of a column:
+  //   left:  S_tl = -(T_l S_ll + T_r S_lr^T),  Q_l = S_tl T_l^T, x_t
+  //   right: S_tr = -(T_l S_lr + T_r S_rr),    Q_r = S_tr T_r^T
+  // and S_tt = P + Q_l + Q_r (upper triangle, mirrored) goes back through
+  // shared memory as one bulk store per column.
   extern __shared__ __align__(16) double bsm[];
   __shared__ __align__(8) unsigned long long mbar;
-  double *REC = bsm;                 // [T/32][RS][32]
-  double *Snb = bsm + T * RS;        // [NN][NB]   (later: S_tt [NN][TS])
-  {
-    const int64_t ncol = (a.K + 1) / 2;
-    const int64_t tile0 = b0 >> 5, ntile = (ncol + 31) >> 5;
-    const int mytiles = (int)((ntile - tile0) < T / 32 ? (ntile - tile0) : T / 32);
-    if (tid == 0) mbar_init(&mbar, 1);
-    __syncthreads();
-    if (tid == 0) {
-      const unsigned bytes = (unsigned)mytiles * RS * 32 * 8;
-      mbar_expect_tx(&mbar, bytes);
-      bulk_g2s(REC, a.rec.p + tile0 * a.rec.ts, bytes, &mbar);
-    }
+  double *REC = bsm;                 // [RS][32]
+  double *Snb = bsm + BC * RS;       // [NN][NB]   (later: Q_l, Q_r [2][NT][NB] | S_tt [BC][SP])
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    mbar_expect_tx(&mbar, (unsigned)(RS * 32 * 8));
+    bulk_g2s(REC, a.rec.p + blockIdx.x * a.rec.ts, (unsigned)(RS * 32 * 8), &mbar);
   }
   const int64_t Kup = a.K / 2;       // columns of level L+1
-  auto stage_block = [&](int sblk) {
-    const int64_t q = b0 - 1 + sblk;
-    const double *src = nullptr;
-    if (q == -1) {
-      if (a.t0 > 0) src = a.Shalo;
-    } else if (q >= 0 && q < Kup) {
-      src = a.S + (((q + 1) << (a.shift + 1)) - 1) * NN;
-    }
-    const bool ok = src != nullptr;
-    const double *s0 = ok ? src : a.S;
+  {
+    // neighbour block sblk = tid (0..32) of the CTA, thread tid stages it
+    const int sblk = tid;
+    if (sblk <= BC) {
+      const int64_t q = b0 - 1 + sblk;
+      const double *src = nullptr;
+      if (q == -1) {
+        if (a.t0 > 0) src = a.Shalo;
+      } else if (q >= 0 && q < Kup) {
+        src = a.S + (((q + 1) << (a.shift + 1)) - 1) * NN;
+      }
+      const bool ok = src != nullptr;
+      const double *s0 = ok ? src : a.S;
 #pragma unroll
-    for (int e = 0; e < NN; ++e) cp_async8(&Snb[e * NB + sblk], s0 + (ok ? e : 0), ok);
-  };
-  stage_block(tid);
-  if (tid == 0) stage_block(T);
+      for (int e = 0; e < NN; ++e) cp_async8(&Snb[e * NB + sblk], s0 + (ok ? e : 0), ok);
+    }
+  }
   double Slr[N][N];
 #pragma unroll
   for (int r = 0; r < N; ++r)
 #pragma unroll
     for (int c = 0; c < N; ++c) Slr[r][c] = (active && hl && hr) ? ldv<32>(a.Xup, b, r * N + c) : 0.0;
   asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();                   // mbarrier init visible; neighbour blocks landed
   mbar_wait(&mbar, 0);
-  __syncthreads();
-  const double *myrec = REC + (tid >> 5) * (RS * 32) + (tid & 31);
+  const double *myrec = REC + col;
   auto rec = [&](int e) { return myrec[e * 32]; };
-  if (active && a.do_state) {
+  if (active && a.do_state && !right) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = rec(RR::w + i);
@@ -758,22 +791,22 @@ __global__ void __launch_bounds__(bwd_threads<N>()) small_backward_kernel(SmallB
       a.x[j * N + i] = s;
     }
   }
-  double Sll[TR::size], Srr[TR::size];
+  double Sd[TR::size];               // left: S_ll, right: S_rr
   if (active) {
 #pragma unroll
     for (int r = 0; r < N; ++r)
 #pragma unroll
-      for (int c = r; c < N; ++c) {
-        Sll[TR::at(r, c)] = Snb[(r * N + c) * NB + tid];
-        Srr[TR::at(r, c)] = Snb[(r * N + c) * NB + tid + 1];
-      }
+      for (int c = r; c < N; ++c) Sd[TR::at(r, c)] = Snb[(r * N + c) * NB + col + (right ? 1 : 0)];
   }
-  __syncthreads();                   // Snb is dead: its space becomes S_tt
-  double *Stt = Snb;
+  __syncthreads();                   // Snb is dead: its space becomes Q_r and S_tt
+  double *Qs = Snb + (right ? NT * NB : 0) + col;   // this side's Q [NT][NB]
+  double *Stt = Snb + 2 * NT * NB + col * SP;
   if (active) {
-#pragma unroll 1
+    // the T block this side multiplies from the right: T_l (left) / T_r (right)
+    const int TO = right ? RR::Tr : RR::Tl;
+#pragma unroll(N <= 6 ? N : 1)
     for (int i = 0; i < N; ++i) {
-      double tl[N], tr[N], A[N], B[N];
+      double tl[N], tr[N], A[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         tl[k] = rec(RR::Tl + i * N + k);
@@ -781,45 +814,61 @@ __global__ void __launch_bounds__(bwd_threads<N>()) small_backward_kernel(SmallB
       }
 #pragma unroll
       for (int c = 0; c < N; ++c) {
-        double sa = 0.0, sb = 0.0;
+        double s = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          const double sll = k <= c ? Sll[TR::at(k, c)] : Sll[TR::at(c, k)];
-          const double srr = k <= c ? Srr[TR::at(k, c)] : Srr[TR::at(c, k)];
-          sa = fma(tl[k], sll, sa);
-          sa = fma(tr[k], Slr[c][k], sa);
-          sb = fma(tl[k], Slr[k][c], sb);
-          sb = fma(tr[k], srr, sb);
+          const double sd = k <= c ? Sd[TR::at(k, c)] : Sd[TR::at(c, k)];
+          if (!right) {              // S_tl = -(T_l S_ll + T_r S_lr^T)
+            s = fma(tl[k], sd, s);
+            s = fma(tr[k], Slr[c][k], s);
+          } else {                   // S_tr = -(T_l S_lr + T_r S_rr)
+            s = fma(tl[k], Slr[k][c], s);
+            s = fma(tr[k], sd, s);
+          }
         }
-        A[c] = -sa;
-        B[c] = -sb;
+        A[c] = -s;
       }
       if (a.Xcur.p) {
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-          if (hl) stv<32>(a.Xcur, t, c * N + i, A[c]);       // slot t-1: S_{t-1,t} = S_tl^T
-          if (hr) stv<32>(a.Xcur, t + 1, i * N + c, B[c]);   // slot t:   S_{t,t+1} = S_tr
+          if (!right && hl) stv<32>(a.Xcur, t, c * N + i, A[c]);      // slot t-1: S_{t-1,t} = S_tl^T
+          if (right && hr) stv<32>(a.Xcur, t + 1, i * N + c, A[c]);   // slot t:   S_{t,t+1} = S_tr
         }
       }
-      // row i of S_tt = P - S_tl T_l^T - S_tr T_r^T (upper part jj >= i, mirrored)
-#pragma unroll 1
-      for (int jj = i; jj < N; ++jj) {
-        double sv = rec(RR::P + TR::at(i, jj));
+      // row i of Q = S_t* T_*^T (upper part jj >= i); the jj chains are independent
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-          sv = fma(-A[k], rec(RR::Tl + jj * N + k), sv);
-          sv = fma(-B[k], rec(RR::Tr + jj * N + k), sv);
-        }
-        Stt[(i * N + jj) * TS + tid] = sv;
-        Stt[(jj * N + i) * TS + tid] = sv;
+      for (int jj = 0; jj < N; ++jj) {
+        if (jj < i) continue;
+        double q = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) q = fma(A[k], rec(TO + jj * N + k), q);
+        Qs[(i * N - (i * (i - 1)) / 2 + (jj - i)) * NB] = q;
       }
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < T * NN; idx += T) {     // coalesced: one column's block is contiguous
-    const int col = idx / NN, e = idx - col * NN;
-    const int64_t bb = b0 + col;
-    if (2 * bb < a.K) a.S[(((2 * bb + 1) << a.shift) - 1) * NN + e] = Stt[e * TS + col];
+  if (active && !right) {
+    // S_tt = P - S_tl T_l^T - S_tr T_r^T = P - Q_l - Q_r (upper part, mirrored)
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int jj = i; jj < N; ++jj) {
+        const int e = TR::at(i, jj);
+        const double sv = (rec(RR::P + e) - Qs[e * NB]) - Qs[(NT + e) * NB];
+        Stt[i * N + jj] = sv;
+        Stt[jj * N + i] = sv;
+      }
+    if constexpr (NN % 2 == 0) {   // 16-byte multiple and alignment: one bulk store
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a.S + j * NN),
+                   "r"(smem_u32(Stt)), "r"((unsigned)(NN * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    } else {
+#pragma unroll
+      for (int e = 0; e < NN; ++e) a.S[j * NN + e] = Stt[e];
+    }
   }
 }
 
@@ -1060,7 +1109,6 @@ cudaError_t factor_n(const SmallFactorArgs &a, cudaStream_t s) {
 template <int N>
 cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
   const int64_t nc = (a.K + 1) / 2;
-  constexpr int T = bwd_threads<N>();
   const size_t full = bwd_smem_doubles<N>() * sizeof(double);
   const size_t smem = a.do_cov ? full : 0;
   static bool attr = false;
@@ -1068,7 +1116,7 @@ cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
     cudaFuncSetAttribute(small_backward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)full);
     attr = true;
   }
-  small_backward_kernel<N><<<(unsigned)((nc + T - 1) / T), T, smem, s>>>(a);
+  small_backward_kernel<N><<<(unsigned)((nc + kBwdCols - 1) / kBwdCols), 2 * kBwdCols, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,13 @@
+# ncu --set full of selected launches of a c5 run (see tools/prof_run.py):
+#   prof_c5.sh SKIP COUNT NAME  (launch indices among small_factor|small_backward kernels;
+#   after 2 warm-up runs: factor L0 = 92, L1 = 93, ..., backward L22..L0 = 115..137)
+set -x
+python tools/prof_run.py c5 > gpurun_out/plain.log 2>&1 || exit 1
+K='regex:small_factor|small_backward'
+while [ $# -ge 3 ]; do
+  ncu --set full --clock-control none --import-source on -k $K -s $1 -c $2 -o gpurun_out/$3 python tools/prof_run.py c5 > gpurun_out/ncu_$3.log 2>&1
+  python tools/ncu_summary.py gpurun_out/$3.ncu-rep > gpurun_out/$3.sum.txt 2>&1
+  python tools/ncu_hot.py gpurun_out/$3.ncu-rep 30 0 > gpurun_out/$3.hot0.txt 2>&1
+  shift 3
+done
+du -sh gpurun_out
