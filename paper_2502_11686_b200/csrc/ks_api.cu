@@ -173,7 +173,7 @@ size_t carve(ks_ctx *c, char *base) {
   const int64_t Rs = small_rrec_doubles(n);
   if (sm) {
     const bool cE = c->cntE == 1, cC = c->cntC == 1;
-    auto sz = [&](bool cst, int64_t E) { return cst ? E : tiled_doubles(N, E); };
+    auto sz = [&](bool cst, int64_t E) { return cst ? E : ptiled_doubles(N, E); };
     c->El0 = w.take<double>(sz(cE, nn));
     c->Er0 = w.take<double>(sz(cE, nn));
     c->e0 = w.take<double>(sz(cE, n));
@@ -181,7 +181,7 @@ size_t carve(ks_ctx *c, char *base) {
     c->nEl0 = w.take<double>(sz(cE, 1));
     c->C0 = w.take<double>(sz(cC, (int64_t)mx * n) + 1);
     c->nC0 = w.take<double>(sz(cC, 1));
-    c->y0 = w.take<double>(tiled_doubles(N, mx) + 1);
+    c->y0 = w.take<double>(ptiled_doubles(N, mx) + 1);
     c->zscratch = w.take<double>(nn + n);
   } else {
     c->El0 = w.take<double>(c->cntE * nn);
@@ -197,7 +197,7 @@ size_t carve(ks_ctx *c, char *base) {
   for (int L = 0;; ++L) {
     if (c->sharded && L == c->q) break;
     c->K_.push_back(K);
-    const int64_t ne = sm ? tiled_doubles(K, E) : K * E;
+    const int64_t ne = sm ? ptiled_doubles(K, E) : K * E;
     const int64_t nr = sm ? tiled_doubles((K + 1) / 2, Rs) : ((K + 1) / 2) * Rr;
     const int64_t nx = sm ? tiled_doubles(K + 1, nn) : (K + 1) * nn;
     c->ent.push_back(L == 0 ? nullptr : w.take<double>(ne));
@@ -292,14 +292,14 @@ SmallIn small_level0(const ks_ctx *c) {
   const int64_t nn = (int64_t)n * n;
   const bool cE = c->cntE == 1, cC = c->cntC == 1;
   SmallIn v;
-  v.C = tv(c->C0, cC ? 0 : 32 * (int64_t)mx * n);
-  v.y = tv(c->y0, 32 * (int64_t)mx);
-  v.El = tv(c->El0, cE ? 0 : 32 * nn);
-  v.Er = tv(c->Er0, cE ? 0 : 32 * nn);
-  v.e = tv(c->e0, cE ? 0 : 32 * (int64_t)n);
-  v.nC = tv(c->nC0, cC ? 0 : 32);
-  v.nEr = tv(c->nEr0, cE ? 0 : 32);
-  v.nEl = tv(c->nEl0, cE ? 0 : 32);
+  v.C = tv(c->C0, cC ? 0 : 64 * (int64_t)mx * n);
+  v.y = tv(c->y0, 64 * (int64_t)mx);
+  v.El = tv(c->El0, cE ? 0 : 64 * nn);
+  v.Er = tv(c->Er0, cE ? 0 : 64 * nn);
+  v.e = tv(c->e0, cE ? 0 : 64 * (int64_t)n);
+  v.nC = tv(c->nC0, cC ? 0 : 64);
+  v.nEr = tv(c->nEr0, cE ? 0 : 64);
+  v.nEl = tv(c->nEl0, cE ? 0 : 64);
   v.RC = mx;
   v.ent = tv(nullptr, 0);
   return v;
@@ -312,9 +312,9 @@ SmallFactorArgs small_factor_args(ks_ctx *c, size_t i) {
   SmallFactorArgs a;
   const bool last = i + 1 == Ks.size();
   a.in = small_level0(c);
-  if (i > 0) a.in.ent = tv(c->ent[i], 32 * E);
+  if (i > 0) a.in.ent = tv(c->ent[i], 64 * E);
   a.outAoS = 0;
-  if (!last) a.out = tv(c->ent[i + 1], 32 * E);
+  if (!last) a.out = tv(c->ent[i + 1], 64 * E);
   else if (c->sharded) { a.out = tv(c->send, E); a.outAoS = 1; }
   else a.out = tv(nullptr, 0);
   a.rec = tv(c->rrec[i], 32 * Rs);

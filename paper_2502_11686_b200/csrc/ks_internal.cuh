@@ -93,6 +93,10 @@ struct TView {
   int64_t ts;
 };
 __host__ __device__ inline int64_t tiled_doubles(int64_t cols, int64_t E) { return ((cols + 31) / 32) * 32 * E; }
+// Pair-interleaved tiles (level-0 per-step arrays and level >= 1 entries of
+// the small path): 64 columns per tile, even columns in the first half,
+//   p[(t >> 6) * 64E + (t & 1) * 32E + 32 e + ((t >> 1) & 31)]
+__host__ __device__ inline int64_t ptiled_doubles(int64_t cols, int64_t E) { return ((cols + 63) / 64) * 64 * E; }
 
 struct SmallIn {               // level-L columns
   // level 0 (whitened inputs), one view per field (constant model: ES = 1,
@@ -100,12 +104,12 @@ struct SmallIn {               // level-L columns
   TView C, y, El, Er, e;
   TView nC, nEr, nEl;          // |C_j|^2, |Er_j|^2, |El_j|^2 (rank reference)
   int RC;
-  // level >= 1: tiled entry records [C (n x n, upper tri) | y | El | Er | e | nrm]
+  // level >= 1: pair-interleaved tiled entry records [C (n x n, upper tri) | y | El | Er | e | nrm]
   TView ent;
 };
 struct SmallFactorArgs {
   SmallIn in;
-  TView out;                   // level-(L+1) survivor entries: tiled, or AoS (outAoS)
+  TView out;                   // level-(L+1) survivor entries: pair-interleaved tiled, or AoS (outAoS)
   TView rec;                   // tiled R records [Tl (n x n) | Tr (n x n) | w (n) | P (n(n+1)/2)]
   int64_t K, t0;
   int level, lbase;

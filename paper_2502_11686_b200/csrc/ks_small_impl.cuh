@@ -35,25 +35,34 @@ struct Tri {
   static constexpr __host__ __device__ int at(int i, int j) { return i * N - (i * (i - 1)) / 2 + (j - i); }
 };
 
-// Column base of a tiled (ES = 32) or AoS / constant (ES = 1) view; element e
-// of the column is then at base[ES * e], a compile-time immediate offset.
+// Column base of a tiled (ES = 32), pair-interleaved tiled (ES = 64) or
+// AoS / constant (ES = 1) view; element e of the column is then at
+// base[EST * e] (EST = 32 for both tiled layouts), a compile-time immediate.
+//   ES = 32: p[(t >> 5) ts + 32 e + (t & 31)]
+//   ES = 64: p[(t >> 6) ts + (t & 1) ts/2 + 32 e + ((t >> 1) & 31)]
+// The pair-interleaved layout keeps the even and the odd columns of each 64
+// in separate 32-column halves, so that a warp of pair threads reading
+// column 2p (or 2p+1) of 32 consecutive pairs touches 256 contiguous bytes.
 template <int ES>
 __device__ __forceinline__ double *cb(const TView &v, int64_t t) {
+  if (ES == 64) return v.p + (t >> 6) * v.ts + (t & 1) * (v.ts >> 1) + ((t >> 1) & 31);
   return ES == 32 ? v.p + (t >> 5) * v.ts + (t & 31) : v.p + t * v.ts;
 }
 template <int ES>
+__host__ __device__ constexpr int est() { return ES == 64 ? 32 : ES; }
+template <int ES>
 __device__ __forceinline__ double ldv(const TView &v, int64_t t, int e) {
-  return __ldg(cb<ES>(v, t) + ES * e);
+  return __ldg(cb<ES>(v, t) + est<ES>() * e);
 }
 template <int ES>
 __device__ __forceinline__ void stv(const TView &v, int64_t t, int e, double x) {
-  cb<ES>(v, t)[ES * e] = x;
+  cb<ES>(v, t)[est<ES>() * e] = x;
 }
 // L1 prefetch of element e of column t (no registers): the row loops fetch
-// the next streamed row while rotating the current one.
+// the next streamed rows while rotating the current one.
 template <int ES>
 __device__ __forceinline__ void pfv(const TView &v, int64_t t, int e) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(cb<ES>(v, t) + ES * e));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(cb<ES>(v, t) + est<ES>() * e));
 }
 
 __device__ __forceinline__ void report(unsigned long long *st, int64_t step, int kind) {
@@ -119,17 +128,60 @@ __device__ __forceinline__ void gmake(double &rho, double yk, double &w, double 
   rho = ident ? rho : (empty ? (w * q) * q : rs * (w * q));
   w = ident ? w : (empty ? __longlong_as_double(0x7ff0000000000000ll) : wn);
 }
+constexpr double kEmptyRow = __builtin_huge_val();   // rho of an empty row of R (w of an absorbed row)
 // sqrt(delta) = 1/sqrt(w) of a streamed row (0 once absorbed).
 __device__ __forceinline__ double wscale(double w) {
   const bool fin = w < __longlong_as_double(0x7ff0000000000000ll);
   const double r = rsqrt_nr(fin ? w : 1.0);
   return fin ? r : 0.0;
 }
+// The same rotation when row k of R is not empty and the streamed row is
+// not absorbed (rho, w finite): no selects.  y_k = 0 changes rho by at most
+// an ulp (rho w / w).  Once every row of R is non-empty it stays so, so the
+// row loops switch to this form after a per-row check (rows_full).
+__device__ __forceinline__ void gmake_fast(double &rho, double yk, double &w, double &sb) {
+  const double yr = yk * rho;
+  const double wn = fma(yk, yr, w);
+  const double q = rcp_nr(wn);
+  sb = yr * q;
+  rho = rho * (w * q);
+  w = wn;
+}
 // Apply to one column: u (row of R) and y (streamed row), yk the pivot value
 // of the streamed row before the rotation.
 __device__ __forceinline__ void gapp(double &u, double &y, double yk, double sb) {
   y = fma(-yk, u, y);
   u = fma(sb, y, u);
+}
+
+// Rotate one streamed row into R (row streaming): pivot part
+// row[0..N), weight w; trail(k, y_k, sbar) applies rotation k to the row's
+// trailing columns.  FAST: every row of R non-empty and the row not absorbed.
+template <bool FAST, int N, class Trail>
+__device__ __forceinline__ void rot_row(double (&R)[Tri<N>::size], double (&row)[N], double &w, Trail &&trail) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double sb;
+    const double yk = row[k];
+    if (FAST) gmake_fast(R[Tri<N>::at(k, k)], yk, w, sb);
+    else gmake(R[Tri<N>::at(k, k)], yk, w, sb);
+#pragma unroll
+    for (int j = k + 1; j < N; ++j) gapp(R[Tri<N>::at(k, j)], row[j], yk, sb);
+    trail(k, yk, sb);
+  }
+}
+template <int N>
+__device__ __forceinline__ bool rows_full(const double (&R)[Tri<N>::size], double w) {
+  bool f = w < kEmptyRow;
+#pragma unroll
+  for (int k = 0; k < N; ++k) f &= R[Tri<N>::at(k, k)] < kEmptyRow;
+  return f;
+}
+// dispatch: the select-free form when R is full and the row live
+template <int N, class Trail>
+__device__ __forceinline__ void rot_row_any(double (&R)[Tri<N>::size], double (&row)[N], double &w, Trail &&trail) {
+  if (rows_full<N>(R, w)) rot_row<true, N>(R, row, w, trail);
+  else rot_row<false, N>(R, row, w, trail);
 }
 
 // ---------------------------------------------------------------- factor ---
@@ -153,7 +205,6 @@ __device__ __forceinline__ void gapp(double &u, double &y, double yk, double sb)
 // strictly above, y = D^{-1/2} z); coupling rows are stored as true rows
 // (weight folded in: sqrt(delta) x row), so no weight accumulates over levels.
 // Entry element offsets (entry_doubles layout).
-constexpr double kEmptyRow = __builtin_huge_val();   // rho of an empty row of R
 template <int N>
 struct Ent {
   static constexpr int C = 0, y = N * N, El = N * N + N, Er = 2 * N * N + N, e = 3 * N * N + N,
@@ -187,38 +238,38 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   double *zs_ = a.zscratch;
   // field loads: level 0 per-field views (constant blocks: ES = 1, ts = 0),
   // level >= 1 one tiled entry record view
-  constexpr int ESE = CE ? 1 : 32, ESC = CC ? 1 : 32, ESO = OAOS ? 1 : 32;
+  constexpr int ESE = CE ? 1 : 64, ESC = CC ? 1 : 64, ESO = OAOS ? 1 : 64;
   // constant level-0 blocks (stride-0 model) are staged once per CTA in
   // shared memory by the kernel prologue and read there (broadcast)
   extern __shared__ double smem_park[];
   const double *cst = smem_park + (size_t)blockDim.x * kParkDoubles<N>;
   auto ldC = [&](int e, int64_t c) {
-    return L0 ? (CC ? cst[CstOff<N>::C + e] : ldv<32>(in.C, c, e)) : ldv<32>(in.ent, c, EN::C + e);
+    return L0 ? (CC ? cst[CstOff<N>::C + e] : ldv<64>(in.C, c, e)) : ldv<64>(in.ent, c, EN::C + e);
   };
-  auto ldY = [&](int e, int64_t c) { return L0 ? ldv<32>(in.y, c, e) : ldv<32>(in.ent, c, EN::y + e); };
+  auto ldY = [&](int e, int64_t c) { return L0 ? ldv<64>(in.y, c, e) : ldv<64>(in.ent, c, EN::y + e); };
   auto ldEl = [&](int e, int64_t c) {
-    return L0 ? (CE ? cst[CstOff<N>::El + e] : ldv<32>(in.El, c, e)) : ldv<32>(in.ent, c, EN::El + e);
+    return L0 ? (CE ? cst[CstOff<N>::El + e] : ldv<64>(in.El, c, e)) : ldv<64>(in.ent, c, EN::El + e);
   };
   auto ldEr = [&](int e, int64_t c) {
-    return L0 ? (CE ? cst[CstOff<N>::Er + e] : ldv<32>(in.Er, c, e)) : ldv<32>(in.ent, c, EN::Er + e);
+    return L0 ? (CE ? cst[CstOff<N>::Er + e] : ldv<64>(in.Er, c, e)) : ldv<64>(in.ent, c, EN::Er + e);
   };
   auto ldE = [&](int e, int64_t c) {
-    return L0 ? (CE ? cst[CstOff<N>::e + e] : ldv<32>(in.e, c, e)) : ldv<32>(in.ent, c, EN::e + e);
+    return L0 ? (CE ? cst[CstOff<N>::e + e] : ldv<64>(in.e, c, e)) : ldv<64>(in.ent, c, EN::e + e);
   };
   auto sto = [&](int e, double v) { stv<ESO>(a.out, pnext, e, v); };
   // prefetch row i of a block field (n elements per row) of column c
   auto pfEl = [&](int i, int64_t c) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      if (!L0) pfv<32>(in.ent, c, EN::El + i * N + j);
-      else if (!CE) pfv<32>(in.El, c, i * N + j);
+      if (!L0) pfv<64>(in.ent, c, EN::El + i * N + j);
+      else if (!CE) pfv<64>(in.El, c, i * N + j);
     }
   };
   auto pfEr = [&](int i, int64_t c) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      if (!L0) pfv<32>(in.ent, c, EN::Er + i * N + j);
-      else if (!CE) pfv<32>(in.Er, c, i * N + j);
+      if (!L0) pfv<64>(in.ent, c, EN::Er + i * N + j);
+      else if (!CE) pfv<64>(in.Er, c, i * N + j);
     }
   };
   const int64_t rcol = t >> 1;
@@ -230,10 +281,10 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // rank reference: |block column of UA|_F (reading R9)
   double ref2, ref2u = 0.0;
   if (!L0) {
-    const double v = ldv<32>(in.ent, t, EN::nrm);
+    const double v = ldv<64>(in.ent, t, EN::nrm);
     ref2 = v * v;
     if (hr) {
-      const double u = ldv<32>(in.ent, t + 1, EN::nrm);
+      const double u = ldv<64>(in.ent, t + 1, EN::nrm);
       ref2u = u * u;
     }
   } else {
@@ -263,15 +314,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 
   // stream one weighted row [row (pivot part, N) | rhs] into (Rm, zm)
   auto stream_row = [&](double(&Rm)[TR::size], double(&zm)[N], double(&row)[N], double &rhs, double wl) {
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double sb;
-      const double yk = row[k];
-      gmake(Rm[TR::at(k, k)], yk, wl, sb);
-#pragma unroll
-      for (int j = k + 1; j < N; ++j) gapp(Rm[TR::at(k, j)], row[j], yk, sb);
-      gapp(zm[k], rhs, yk, sb);
-    }
+    rot_row_any<N>(Rm, row, wl, [&](int k, double yk, double sb) { gapp(zm[k], rhs, yk, sb); });
   };
 
   // ---- stage 1 base: R = C_t ----
@@ -324,17 +367,11 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         pfEr(0, t);
       }
       double wl = 1.0;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double sb;
-        const double yk = el[k];
-        gmake(R[TR::at(k, k)], yk, wl, sb);
-#pragma unroll
-        for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], el[j], yk, sb);
+      rot_row_any<N>(R, el, wl, [&](int k, double yk, double sb) {
 #pragma unroll
         for (int j = 0; j < N; ++j) gapp(X[k][j], er[j], yk, sb);
         gapp(z[k], ee, yk, sb);
-      }
+      });
 #pragma unroll
       for (int j = 0; j < N; ++j) park(kLeft + i * (N + 2) + j, er[j]);
       park(kLeft + i * (N + 2) + N, ee);
@@ -359,16 +396,10 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       if (i + 1 < N) pfEr(i + 1, t);
       else pfEl(0, t);
       double wl = 1.0;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double sb;
-        const double yk = er[k];
-        gmake(R[TR::at(k, k)], yk, wl, sb);
-#pragma unroll
-        for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], er[j], yk, sb);
+      rot_row_any<N>(R, er, wl, [&](int k, double yk, double sb) {
 #pragma unroll
         for (int j = 0; j < N; ++j) gapp(X[k][j], xr[j], yk, sb);
-      }
+      });
       if (hr) {
         const double w = wscale(wl);
 #pragma unroll
@@ -486,17 +517,11 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         pfEl(i + 1, t);
       }
       double wl = 1.0;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double sb;
-        const double yk = er[k];
-        gmake(R[TR::at(k, k)], yk, wl, sb);
-#pragma unroll
-        for (int j = k + 1; j < N; ++j) gapp(R[TR::at(k, j)], er[j], yk, sb);
+      rot_row_any<N>(R, er, wl, [&](int k, double yk, double sb) {
 #pragma unroll
         for (int j = 0; j < N; ++j) gapp(Rl[k][j], el[j], yk, sb);
         gapp(z[k], ee, yk, sb);
-      }
+      });
       if (hr || zs_out) {
         const double w = wscale(wl);
         if (hr) {
@@ -877,7 +902,7 @@ __global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backwar
 // Store element e of column i of a whitened level-0 view (constant: ES = 1).
 __device__ __forceinline__ void wst(const TView &v, int cst, int64_t i, int e, double x) {
   if (cst) stv<1>(v, i, e, x);
-  else stv<32>(v, i, e, x);
+  else stv<64>(v, i, e, x);
 }
 
 // Evolution blocks: K = Lam Lam^T (Cholesky), El = -Lam^{-1}F,
