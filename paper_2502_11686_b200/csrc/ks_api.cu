@@ -189,6 +189,7 @@ size_t carve(ks_ctx *c, char *base) {
     c->e0 = w.take<double>(c->cntE * n);
     c->C0 = w.take<double>(c->cntC * mx * n + 1);
     c->y0 = w.take<double>(N * mx + 1);
+    c->zscratch = w.take<double>(nn + n);
   }
   c->Mchol = w.take<double>((size_t)mx * mx + 1);
   // local levels
@@ -391,6 +392,7 @@ int run_factor_levels(ks_ctx *c, bool boundary) {
     a.level = L;
     a.lbase = boundary ? c->q : 0;
     a.status = c->status;
+    a.zscratch = c->zscratch;
     if (boundary) {
       a.t0 = 0;
       a.step0 = 0;  // reported as boundary-domain index

@@ -44,6 +44,7 @@ struct FactorLevelArgs {
   int lbase;
   int64_t step0;         // for status reporting only
   unsigned long long *status;
+  double *zscratch;      // n (n + 1) doubles: the odd level's last-column leftover Z (row-major)
 };
 
 struct BackwardLevelArgs {
@@ -148,7 +149,7 @@ cudaError_t launch_small_whiten(const SmallWhitenArgs &a, cudaStream_t s, int *n
 cudaError_t launch_small_factor(const SmallFactorArgs &a, int n, cudaStream_t s);
 cudaError_t launch_small_backward(const SmallBackwardArgs &a, int n, cudaStream_t s);
 
-// kernel launchers (ks_kernels.cu); return cudaGetLastError()
+// kernel launchers of the CTA path (ks_large.cu); return cudaGetLastError()
 cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s);
 cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s);
 cudaError_t launch_backward_level(const BackwardLevelArgs &a, cudaStream_t s);

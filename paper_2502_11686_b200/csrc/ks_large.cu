@@ -1,0 +1,851 @@
+// sm_100a fp64 kernels of the Odd-Even Kalman smoother: the CTA path
+// (every n up to the shared-memory limit, n = m = 48 for BASELINE config 4;
+// also the multi-GPU boundary system and KS_GENERIC_PATH for n <= 8).
+//
+// One CTA (8 warps) per eliminated column (pair), the stage matrices resident
+// in shared memory (column-major, rows and columns zero-padded to multiples
+// of 8, leading dimension = 4 mod 16 so that DMMA fragment loads are bank-
+// conflict free).  Every QR is a blocked Householder QR (LAPACK geqrf order:
+// panels of 8 columns, compact-WY Q = I - V T V^T): the panel is factored by
+// one warp (lanes over rows, shuffle reductions), the trailing update
+// W = V^T C, W = T^T W, C -= V W runs on the FP64 tensor cores
+// (mma.sync.m8n8k4.f64, DMMA) -- the real dense contractions of the method
+// at large n (north_star).  Triangular solves (T = R^{-1}[R_l R_r],
+// w = R^{-1} z, R^{-1}), the SelInv products S_{t,I} = -T S_II and
+// S_tt = P - S_{t,I} T^T, and the whitening solves are blocked the same way:
+// 8x8 diagonal blocks by threads, off-diagonal updates as DMMA GEMMs.
+//
+// P:n = line n of the paper text.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ks_internal.cuh"
+
+namespace ks {
+
+namespace {
+
+constexpr int kThreads = 256, kWarps = kThreads / 32;
+constexpr int kLdw = 12;   // leading dimension of the 8 x 8 warp tiles (12 = conflict-free)
+
+__host__ __device__ constexpr int pad8(int x) { return (x + 7) & ~7; }
+// leading dimension for `rows` padded rows: >= pad8(rows) and = 4 (mod 16)
+__host__ __device__ constexpr int ldpad(int rows) { return pad8(rows) + ((4 - pad8(rows) % 16) + 16) % 16; }
+
+__device__ __forceinline__ void report(unsigned long long *st, int64_t step, int kind) {
+  if (st) atomicMin(st, ((unsigned long long)(step + 1) << 8) | (unsigned long long)kind);
+}
+
+// D = A B + D on one 8x8 tile: A 8x4 (row-major fragment: lane holds
+// A[lane/4][lane%4]), B 4x8 (B[lane%4][lane/4]), D 8x8 (D[lane/4][2(lane%4)+i]).
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// C = beta C + alpha op(A) op(B) on shared-memory column-major operands.
+// M, N multiples of 8, K a multiple of 4 (operands zero-padded).  Each warp
+// owns pairs of vertically adjacent 8x8 output tiles (two independent DMMA
+// chains sharing the B fragment).  No aliasing between C and A / B.
+template <bool TA, bool TB>
+__device__ void gemm(int M, int N, int K, double alpha, const double *A, int lda, const double *B, int ldb,
+                     double beta, double *C, int ldc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int mt = M >> 3, nt = N >> 3, mp = (mt + 1) >> 1;
+  for (int tile = warp; tile < mp * nt; tile += kWarps) {
+    const int m0 = (tile % mp) * 16, n0 = (tile / mp) * 8;
+    const bool two = m0 + 8 < M;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const double b = TB ? B[(n0 + g) + (k0 + q) * ldb] : B[(k0 + q) + (n0 + g) * ldb];
+      const double a0 = TA ? A[(k0 + q) + (m0 + g) * lda] : A[(m0 + g) + (k0 + q) * lda];
+      dmma(c00, c01, a0, b);
+      if (two) {
+        const double a1 = TA ? A[(k0 + q) + (m0 + 8 + g) * lda] : A[(m0 + 8 + g) + (k0 + q) * lda];
+        dmma(c10, c11, a1, b);
+      }
+    }
+    double *c = C + (m0 + g) + (n0 + 2 * q) * ldc;
+    if (beta == 0.0) {
+      c[0] = alpha * c00;
+      c[ldc] = alpha * c01;
+      if (two) {
+        c[8] = alpha * c10;
+        c[8 + ldc] = alpha * c11;
+      }
+    } else {
+      c[0] = fma(alpha, c00, beta * c[0]);
+      c[ldc] = fma(alpha, c01, beta * c[ldc]);
+      if (two) {
+        c[8] = fma(alpha, c10, beta * c[8]);
+        c[8 + ldc] = fma(alpha, c11, beta * c[8 + ldc]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
+// Workspace of the blocked QR (shared memory).
+struct QrWs {
+  double *V;      // [ldv x 8]  the panel's reflectors (explicit, zero padded)
+  int ldv;
+  double *T;      // [kLdw x 8] compact-WY factor
+  double *G;      // [kLdw x 8] V^T V
+  double *beta;   // [8]
+  double *tile;   // [kWarps][kLdw x 8] per-warp 8x8 scratch
+};
+constexpr int kPanelMaxR = 5;   // rows per lane in the panel factorization (rows <= 160)
+
+// Panel factorization by warp 0: columns [k0, k0 + nb) of A, rows [k0, rows).
+// Householder reflector j: x = A[k0+j:, k0+j], alpha = -sign(x1)|x|,
+// v = x - alpha e1, H = I - beta v v^T, beta = 1/(|x|^2 - x1 alpha)
+// (zero column: beta = 0).  Writes R into the panel (zeros below the
+// diagonal), V (explicit, rows local to k0) and beta, then G = V^T V (DMMA)
+// and the compact-WY T (LAPACK larft, forward columnwise).
+__device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int mrow = rows - k0, mpad = pad8(mrow);
+  double a[kPanelMaxR][8];
+#pragma unroll
+  for (int r = 0; r < kPanelMaxR; ++r) {
+    const int li = lane + 32 * r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[r][j] = (li < mrow && j < nb) ? A[(k0 + li) + (k0 + j) * lda] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= nb) {   // non-pivot column of a partial panel: zero reflector
+#pragma unroll
+      for (int r = 0; r < kPanelMaxR; ++r) {
+        const int li = lane + 32 * r;
+        if (li < mpad) w.V[li + j * w.ldv] = 0.0;
+      }
+      if (lane == 0) w.beta[j] = 0.0;
+      continue;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < kPanelMaxR; ++r) {
+      const int li = lane + 32 * r;
+      if (li >= j) s = fma(a[r][j], a[r][j], s);
+    }
+    s = warp_sum(s);
+    const double x1 = __shfl_sync(0xffffffffu, a[0][j], j);
+    double alpha, beta, v1;
+    if (s == 0.0) {
+      alpha = x1;
+      beta = 0.0;
+      v1 = 0.0;
+    } else {
+      const double nrm = sqrt(s);
+      alpha = (x1 > 0.0) ? -nrm : nrm;
+      v1 = x1 - alpha;
+      beta = 1.0 / (s - x1 * alpha);
+    }
+    double v[kPanelMaxR];
+#pragma unroll
+    for (int r = 0; r < kPanelMaxR; ++r) {
+      const int li = lane + 32 * r;
+      v[r] = (li > j) ? a[r][j] : (li == j ? v1 : 0.0);
+      if (beta == 0.0) v[r] = 0.0;
+    }
+    // apply H to the remaining panel columns (batched reductions)
+    double d[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      d[jj] = 0.0;
+      if (jj > j && jj < nb) {
+#pragma unroll
+        for (int r = 0; r < kPanelMaxR; ++r) d[jj] = fma(v[r], a[r][jj], d[jj]);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+      if (jj > j && jj < nb) d[jj] = warp_sum(d[jj]) * beta;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+      if (jj > j && jj < nb) {
+#pragma unroll
+        for (int r = 0; r < kPanelMaxR; ++r) a[r][jj] = fma(-d[jj], v[r], a[r][jj]);
+      }
+#pragma unroll
+    for (int r = 0; r < kPanelMaxR; ++r) {
+      const int li = lane + 32 * r;
+      if (li < mpad) w.V[li + j * w.ldv] = (li < mrow) ? v[r] : 0.0;
+      if (li == j) a[r][j] = alpha;
+      else if (li > j) a[r][j] = 0.0;
+    }
+    if (lane == 0) w.beta[j] = beta;
+  }
+#pragma unroll
+  for (int r = 0; r < kPanelMaxR; ++r) {
+    const int li = lane + 32 * r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (li < mrow && j < nb) A[(k0 + li) + (k0 + j) * lda] = a[r][j];
+  }
+  __syncwarp();
+  // G = V^T V (one 8x8 DMMA tile, K = mpad)
+  {
+    double g0 = 0.0, g1 = 0.0;
+    for (int kk = 0; kk < mpad; kk += 4) {
+      const double x = w.V[(kk + q) + g * w.ldv];
+      const double y = w.V[(kk + q) + g * w.ldv];
+      dmma(g0, g1, x, y);
+    }
+    w.G[g + (2 * q) * kLdw] = g0;
+    w.G[g + (2 * q + 1) * kLdw] = g1;
+  }
+  __syncwarp();
+  // T: T_jj = beta_j, T[0:j, j] = -beta_j T[0:j, 0:j] G[0:j, j]
+  for (int j = 0; j < 8; ++j) {
+    double t = 0.0;
+    if (lane < j) {
+      for (int l = lane; l < j; ++l) t = fma(w.T[lane + l * kLdw], w.G[l + j * kLdw], t);
+      t *= -w.beta[j];
+    }
+    __syncwarp();
+    if (lane < 8) w.T[lane + j * kLdw] = (lane < j) ? t : (lane == j ? w.beta[j] : 0.0);
+    __syncwarp();
+  }
+}
+
+// Q^T C for C = A[k0:k0+mpad, c0:c0+ncp] with Q = I - V T V^T:
+// W = V^T C, W = T^T W, C -= V W, one 8-column tile per warp iteration
+// (all three products of a tile in the same warp: no CTA barrier).
+__device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, const QrWs &w) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  double *sc = w.tile + warp * (kLdw * 8);
+  for (int n0 = warp * 8; n0 < ncp; n0 += kWarps * 8) {
+    double *C = A + k0 + (c0 + n0) * lda;
+    double w0 = 0.0, w1 = 0.0;
+    for (int kk = 0; kk < mpad; kk += 4) {
+      const double x = w.V[(kk + q) + g * w.ldv];      // V^T[g][kk+q]
+      const double y = C[(kk + q) + g * lda];           // C[kk+q][g]
+      dmma(w0, w1, x, y);
+    }
+    sc[g + (2 * q) * kLdw] = w0;
+    sc[g + (2 * q + 1) * kLdw] = w1;
+    __syncwarp();
+    double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4) {
+      const double x = w.T[(kk + q) + g * kLdw];        // T^T[g][kk+q]
+      const double y = sc[(kk + q) + g * kLdw];         // W[kk+q][g]
+      dmma(u0, u1, x, y);
+    }
+    __syncwarp();
+    sc[g + (2 * q) * kLdw] = u0;
+    sc[g + (2 * q + 1) * kLdw] = u1;
+    __syncwarp();
+    const double y0 = sc[q + g * kLdw], y1 = sc[(4 + q) + g * kLdw];   // W2[kk+q][g]
+    for (int m0 = 0; m0 < mpad; m0 += 8) {
+      double *cp = C + (m0 + g) + (2 * q) * lda;
+      double c0v = cp[0], c1v = cp[lda];
+      dmma(c0v, c1v, -w.V[(m0 + g) + q * w.ldv], y0);
+      dmma(c0v, c1v, -w.V[(m0 + g) + (4 + q) * w.ldv], y1);
+      cp[0] = c0v;
+      cp[lda] = c1v;
+    }
+    __syncwarp();
+  }
+}
+
+// Blocked Householder QR: triangularise columns [0, npiv) of the
+// rows x ncols column-major shared matrix A and apply Q^T to columns
+// [npiv, ncols).  A is zero-padded to pad8(rows) rows (lda >= that) and to
+// pad8(ncols) (+8 when npiv % 8 != 0) columns.  On exit the first npiv
+// columns hold R (zeros below the diagonal).  Ends with __syncthreads.
+__device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w) {
+  const int warp = threadIdx.x >> 5;
+  for (int k0 = 0; k0 < npiv && k0 < rows; k0 += 8) {
+    const int nb = (npiv - k0 < 8) ? npiv - k0 : 8;
+    if (warp == 0) qr_panel(A, lda, k0, rows, nb, w);
+    __syncthreads();
+    const int c0 = k0 + nb;
+    if (c0 < ncols) qr_apply(A, lda, k0, pad8(rows - k0), c0, pad8(ncols - c0), w);
+    __syncthreads();
+  }
+}
+
+// X <- R^{-1} X for R (n x n upper triangular, ldr) and X (n x p, ldx), both
+// zero-padded to 8 rows/columns: 8-row blocks from the bottom, the diagonal
+// block by one thread per right-hand side, the update of the rows above as a
+// DMMA GEMM.  Ends with __syncthreads.
+__device__ void trsm_upper(const double *R, int ldr, int n, double *X, int ldx, int p) {
+  for (int r0 = ((n - 1) / 8) * 8; r0 >= 0; r0 -= 8) {
+    const int h = (n - r0 < 8) ? n - r0 : 8;
+    for (int c = threadIdx.x; c < p; c += blockDim.x) {
+      double *x = X + r0 + c * ldx;
+      for (int i = h - 1; i >= 0; --i) {
+        double s = x[i];
+        for (int l = i + 1; l < h; ++l) s = fma(-R[(r0 + i) + (r0 + l) * ldr], x[l], s);
+        x[i] = s / R[(r0 + i) + (r0 + i) * ldr];
+      }
+    }
+    __syncthreads();
+    if (r0 > 0) gemm<false, false>(r0, pad8(p), 8, -1.0, R + r0 * ldr, ldr, X + r0, ldx, 1.0, X, ldx);
+    __syncthreads();
+  }
+}
+
+// X <- L^{-1} X for L (n x n lower triangular): 8-row blocks from the top.
+__device__ void trsm_lower(const double *L, int ldl, int n, double *X, int ldx, int p) {
+  for (int r0 = 0; r0 < n; r0 += 8) {
+    const int h = (n - r0 < 8) ? n - r0 : 8;
+    for (int c = threadIdx.x; c < p; c += blockDim.x) {
+      double *x = X + r0 + c * ldx;
+      for (int i = 0; i < h; ++i) {
+        double s = x[i];
+        for (int l = 0; l < i; ++l) s = fma(-L[(r0 + i) + (r0 + l) * ldl], x[l], s);
+        x[i] = s / L[(r0 + i) + (r0 + i) * ldl];
+      }
+    }
+    __syncthreads();
+    const int rest = pad8(n) - r0 - 8;
+    if (rest > 0)
+      gemm<false, false>(rest, pad8(p), 8, -1.0, L + (r0 + 8) + r0 * ldl, ldl, X + r0, ldx, 1.0, X + r0 + 8, ldx);
+    __syncthreads();
+  }
+}
+
+// Cholesky (right-looking) of the d x d lower triangle of Lm (ldl) in place;
+// returns false to every thread if a pivot is <= 0 (then continues with 1).
+__device__ bool cta_chol(double *Lm, int ldl, int d, double *sh) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  bool ok = true;
+  for (int j = 0; j < d; ++j) {
+    const double v = Lm[j + j * ldl];
+    ok &= v > 0.0;
+    const double ljj = sqrt(v > 0.0 ? v : 1.0), il = 1.0 / ljj;
+    __syncthreads();                          // every thread has read the pivot
+    for (int i = j + 1 + tid; i < d; i += NT) Lm[i + j * ldl] *= il;
+    if (tid == 0) Lm[j + j * ldl] = ljj;
+    __syncthreads();
+    const int m = d - j - 1;
+    for (int idx = tid; idx < m * m; idx += NT) {
+      const int i = j + 1 + idx % m, k = j + 1 + idx / m;
+      if (k <= i) Lm[i + k * ldl] = fma(-Lm[i + j * ldl], Lm[k + j * ldl], Lm[i + k * ldl]);
+    }
+    __syncthreads();
+  }
+  (void)sh;
+  return ok;
+}
+
+__device__ void zero_smem(double *p, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) p[i] = 0.0;
+}
+
+// smem column-major A(lda)[r0:r0+rows, c0:c0+cols] <- g (row-major, ldg);
+// rows >= valid or g == null stay untouched (caller zeroed the matrix).
+__device__ void ld_blk(double *A, int lda, int r0, int c0, const double *g, int64_t ldg, int rows, int cols,
+                       int valid) {
+  if (g == nullptr) return;
+  const int tot = (valid < rows ? valid : rows) * cols;
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int i = idx / cols, j = idx - i * cols;
+    A[(r0 + i) + (c0 + j) * lda] = g[(int64_t)i * ldg + j];
+  }
+}
+
+// smem (column-major) -> global row-major (ldg); rows >= valid are written as 0
+__device__ void st_blk(double *g, int64_t ldg, const double *A, int lda, int r0, int c0, int rows, int cols,
+                       int valid) {
+  const int tot = rows * cols;
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int i = idx / cols, j = idx - i * cols;
+    g[(int64_t)i * ldg + j] = (i < valid) ? A[(r0 + i) + (c0 + j) * lda] : 0.0;
+  }
+}
+
+// smem -> smem block copy
+__device__ void cp_blk(double *D, int ldd, int dr, int dc, const double *A, int lda, int r0, int c0, int rows,
+                       int cols) {
+  const int tot = rows * cols;
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int i = idx % rows, j = idx / rows;
+    D[(dr + i) + (dc + j) * ldd] = A[(r0 + i) + (c0 + j) * lda];
+  }
+}
+
+// Sum of squares of `count` contiguous doubles, reduced by warp 0 and
+// returned to every thread through sh[0].
+__device__ double cta_sumsq(const double *g, int count, double *sh) {
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < count; i += 32) s = fma(g[i], g[i], s);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) sh[0] = s;
+  }
+  __syncthreads();
+  return sh[0];
+}
+
+// |UA block column of level-0 column t|_F^2 = |C_t|^2 + |Er_t|^2 + |El_{t+1}|^2.
+__device__ double col_norm2_l0(const EntryView &in, int n, int64_t t, bool hl, bool hr, double *sh) {
+  double s = cta_sumsq(in.C + t * in.sC, in.RC * n, sh);
+  if (hl) s += cta_sumsq(in.Er + t * in.sEr, n * n, sh);
+  if (hr) s += cta_sumsq(in.El + (t + 1) * in.sEl, n * n, sh);
+  return s;
+}
+
+// ---- shared-memory plan of the factor kernel ----
+struct FactorPlan {
+  int ld1, cols1, ld2, cols2, ld3, cols3, ldv;
+  int off2, offws, total;   // doubles
+};
+__host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
+  FactorPlan f;
+  const int extra = (n % 8) ? 8 : 0;
+  f.ld1 = ldpad(RC + n);
+  f.cols1 = pad8(2 * n + 1) + extra;
+  f.ld2 = ldpad(2 * n);
+  f.cols2 = pad8(3 * n + 1) + extra;
+  f.ld3 = ldpad(2 * RC + n);
+  f.cols3 = pad8(n + 1) + extra;
+  const int rmax = (2 * n > 2 * RC + n) ? 2 * n : 2 * RC + n;   // >= RC + n
+  f.ldv = ldpad(rmax);
+  const int s1 = f.ld1 * f.cols1;
+  // post-processing reuses S1 for R^{-1}, P and a padded copy of R (3 x ldpad(n) x pad8(n))
+  const int s1p = 3 * ldpad(n) * pad8(n);
+  const int s2 = f.ld2 * f.cols2, s3 = f.ld3 * f.cols3;
+  f.off2 = ((s1 > s1p ? s1 : s1p) + 1) & ~1;
+  f.offws = f.off2 + (((s2 > s3 ? s2 : s3) + 1) & ~1);
+  f.total = f.offws + f.ldv * 8 + 2 * kLdw * 8 + 8 + kWarps * kLdw * 8 + 8;
+  return f;
+}
+
+__device__ QrWs carve_ws(double *p, int ldv) {
+  QrWs w;
+  w.V = p;
+  w.ldv = ldv;
+  w.T = w.V + ldv * 8;
+  w.G = w.T + kLdw * 8;
+  w.beta = w.G + kLdw * 8;
+  w.tile = w.beta + 8;
+  return w;
+}
+
+// Eliminate column t of the level:
+//   stage 1  QR [C_t; El_{t+1}] -> R~_t, applied to [0; Er_{t+1}] and the RHS
+//            giving X_t (top) and D~_{t+1} (bottom, acts on t+1 only)
+//   stage 3  QR [D~_{t+1}; C_{t+1}; Zs] -> C'_{t+1} (survivor's C-like block)
+//   stage 2  QR [Er_t; R~_t] applied to [El_t, 0, e_t; 0, X_t, z~_t] ->
+//            R_tt, R_{t,t-1}, R_{t,t+1}, z_t (top) and the survivor's new
+//            coupling row [Z_t | X~_t | z^_t] (bottom).  No left neighbour:
+//            "nothing to do": R_tt = R~_t, R_{t,t+1} = X_t.
+// A column without right neighbour (last column of an odd level, or the base
+// case) has an empty right neighbour; its stage-2 leftover Z (acting on t-1
+// only) goes to zscratch to join the left pair's stage 3 (reading R5).
+// Writes the R record T = R^{-1}[R_l R_r], P = R^{-1}R^{-T}, w = R^{-1} z.
+__device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan &f, int64_t t, bool hr, bool hl,
+                          int64_t pnext, bool zs_in, bool zs_out) {
+  const int n = a.n, RC = a.in.RC, tid = threadIdx.x;
+  const EntryView &in = a.in;
+  double *S1 = sm, *P2 = sm + f.off2, *sh = sm + f.total - 8;
+  QrWs w = carve_ws(sm + f.offws, f.ldv);
+  const int ld1 = f.ld1, ld2 = f.ld2, ld3 = f.ld3;
+
+  double nrm_t, nrm_u = 0.0;
+  if (in.nrm) {
+    nrm_t = in.nrm[t * in.snrm];
+    if (hr) nrm_u = in.nrm[(t + 1) * in.snrm];
+  } else {
+    nrm_t = sqrt(col_norm2_l0(in, n, t, hl, hr, sh));
+    if (hr) nrm_u = sqrt(col_norm2_l0(in, n, t + 1, true, t + 2 < a.K, sh));
+  }
+
+  // ---- stage 1 ----
+  zero_smem(S1, ld1 * f.cols1);
+  __syncthreads();
+  ld_blk(S1, ld1, 0, 0, in.C + t * in.sC, n, RC, n, RC);
+  ld_blk(S1, ld1, 0, 2 * n, in.y + t * in.sy, 1, RC, 1, RC);
+  if (hr) {
+    const int64_t u = t + 1;
+    ld_blk(S1, ld1, RC, 0, in.El + u * in.sEl, n, n, n, n);
+    ld_blk(S1, ld1, RC, n, in.Er + u * in.sEr, n, n, n, n);
+    ld_blk(S1, ld1, RC, 2 * n, in.e + u * in.se, 1, n, 1, n);
+  }
+  __syncthreads();
+  qr_blocked(S1, ld1, RC + n, n, 2 * n + 1, w);
+
+  // ---- stage 3 (before stage 2: its matrix B3 shares memory with B2) ----
+  if (hr) {
+    const int64_t u = t + 1;
+    zero_smem(P2, ld3 * f.cols3);
+    __syncthreads();
+    cp_blk(P2, ld3, 0, 0, S1, ld1, n, n, RC, n);          // D~_{t+1}
+    cp_blk(P2, ld3, 0, n, S1, ld1, n, 2 * n, RC, 1);      // y~_{t+1}
+    ld_blk(P2, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
+    ld_blk(P2, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
+    int rows3 = 2 * RC;
+    if (zs_in) {
+      ld_blk(P2, ld3, rows3, 0, a.zscratch, n + 1, n, n + 1, n);
+      rows3 += n;
+    }
+    __syncthreads();
+    qr_blocked(P2, ld3, rows3, n, n + 1, w);
+    double *ent = a.next + pnext * entry_doubles(n);
+    const int valid = rows3 < n ? rows3 : n;
+    st_blk(ent, n, P2, ld3, 0, 0, n, n, valid);             // C'
+    st_blk(ent + n * n, 1, P2, ld3, 0, n, n, 1, valid);     // y'
+    if (tid == 0) ent[3 * n * n + 2 * n] = nrm_u;
+    __syncthreads();
+  }
+
+  // ---- stage 2 ----
+  zero_smem(P2, ld2 * f.cols2);
+  __syncthreads();
+  if (hl) {
+    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
+    ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
+    ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
+    cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
+    cp_blk(P2, ld2, n, 2 * n, S1, ld1, 0, n, n, n + 1);    // X_t, z~_t
+    __syncthreads();
+    qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w);
+    if (hr) {
+      double *ent = a.next + pnext * entry_doubles(n);
+      st_blk(ent + n * n + n, n, P2, ld2, n, n, n, n, n);               // El' = Z_t
+      st_blk(ent + 2 * n * n + n, n, P2, ld2, n, 2 * n, n, n, n);       // Er' = X~_t
+      st_blk(ent + 3 * n * n + n, 1, P2, ld2, n, 3 * n, n, 1, n);       // e'  = z^_t
+    } else if (zs_out) {
+      st_blk(a.zscratch, n + 1, P2, ld2, n, n, n, n, n);                // Z_t
+      st_blk(a.zscratch + n, n + 1, P2, ld2, n, 3 * n, n, 1, n);        // z^_t
+    }
+  } else {
+    cp_blk(P2, ld2, 0, 0, S1, ld1, 0, 0, n, n);
+    cp_blk(P2, ld2, 0, 2 * n, S1, ld1, 0, n, n, n + 1);
+    if (hr) {
+      double *ent = a.next + pnext * entry_doubles(n);
+      for (int i = tid; i < 2 * n * n + n; i += blockDim.x) ent[n * n + n + i] = 0.0;
+    }
+  }
+  __syncthreads();
+
+  // ---- R record: rank check, T = R^{-1}[R_l R_r], w = R^{-1} z, P = R^{-1} R^{-T} ----
+  if (tid == 0) {
+    const double thr = kRankTol * nrm_t;
+    bool bad = false;
+    for (int d = 0; d < n; ++d) bad |= !(fabs(P2[d + d * ld2]) > thr);
+    if (bad) report(a.status, (((t + 1) << (a.level - a.lbase)) - 1) + a.step0, kBadRank);
+  }
+  const int ldr = ldpad(n), np = pad8(n);
+  // R_tt copied into a zero-padded block (the blocked solves read whole 8x8
+  // blocks; B2's columns next to R hold the right-hand sides)
+  double *Ri = S1, *Pm = S1 + ldr * np, *Rc = S1 + 2 * ldr * np;
+  zero_smem(Ri, 3 * ldr * np);
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) Ri[i + i * ldr] = 1.0;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int i = idx % n, j = idx / n;
+    if (i <= j) Rc[i + j * ldr] = P2[i + j * ld2];
+  }
+  __syncthreads();
+  // RHS [R_l | R_r | z] (columns n .. 3n of B2) and I (R^{-1}) in two solves
+  trsm_upper(Rc, ldr, n, P2 + n * ld2, ld2, 2 * n + 1);
+  trsm_upper(Rc, ldr, n, Ri, ldr, n);
+  gemm<false, true>(np, np, np, 1.0, Ri, ldr, Ri, ldr, 0.0, Pm, ldr);
+  __syncthreads();
+  double *rec = a.rrec + (t >> 1) * rrec_doubles(n);
+  const int nn = n * n;
+  for (int idx = tid; idx < nn; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    rec[idx] = P2[r + (n + c) * ld2];                  // Tl
+    rec[nn + idx] = P2[r + (2 * n + c) * ld2];         // Tr
+    rec[2 * nn + idx] = Pm[r + c * ldr];               // P
+  }
+  for (int r = tid; r < n; r += blockDim.x) rec[3 * nn + r] = P2[r + 3 * n * ld2];   // w
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const FactorPlan f = factor_plan(a.n, a.in.RC);
+  const int64_t K = a.K, p = blockIdx.x;
+  const bool single_only = (K == 1);
+  const bool triple = (K >= 3) && (K & 1) && (p == K / 2 - 1);
+  bool zs = false;
+  if (single_only || triple) {
+    const int64_t ts = K - 1;
+    const bool hl = (ts + a.t0) > 0;
+    eliminate(a, sm, f, ts, false, hl, 0, false, hl);
+    zs = hl && triple;
+  }
+  if (!single_only) {
+    const int64_t t = 2 * p;
+    eliminate(a, sm, f, t, true, (t + a.t0) > 0, p, zs, false);
+  }
+}
+
+// ---- backward ----
+struct BwdPlan {
+  int ldt, ldS, ldp, offS, offStI, offP, offx, total;
+};
+__host__ __device__ inline BwdPlan bwd_plan(int n) {
+  BwdPlan b;
+  b.ldt = ldpad(n);
+  b.ldS = ldpad(2 * n);
+  b.ldp = ldpad(n);
+  const int ct = pad8(2 * n);
+  b.offS = b.ldt * ct;
+  b.offStI = b.offS + b.ldS * ct;
+  b.offP = b.offStI + b.ldt * ct;
+  b.offx = b.offP + b.ldp * pad8(n);
+  b.total = b.offx + 4 * pad8(n);
+  return b;
+}
+
+// Backward level (P:592-600 and Alg. 2) for eliminated column t:
+//   x_t     = w - T_l x_l - T_r x_r
+//   S_{t,I} = -T S_II      (T = [T_l T_r], S_II = [S_ll S_lr; S_lr^T S_rr])
+//   S_tt    = P - S_{t,I} T^T, symmetrised (reading R13)
+// both products on the FP64 tensor cores.  S_lr (= S_{t-1,t+1}) is the cross
+// block stored at level L+1; S_{t-1,t} = S_tl^T and S_{t,t+1} = S_tr are
+// stored for level L-1.
+__global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int n = a.n, nn = n * n, tid = threadIdx.x;
+  const BwdPlan bp = bwd_plan(n);
+  const int64_t b = blockIdx.x, t = 2 * b;
+  if (t >= a.K) return;
+  const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
+  double *TT = sm, *SII = sm + bp.offS, *StI = sm + bp.offStI, *Pm = sm + bp.offP, *xv = sm + bp.offx;
+  const int ldt = bp.ldt, ldS = bp.ldS, ldp = bp.ldp, np = pad8(n), n2p = pad8(2 * n);
+  const double *rec = a.rrec + b * rrec_doubles(n);
+  const int64_t step = 1ll << a.shift;
+  const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
+  zero_smem(sm, bp.total);
+  __syncthreads();
+  for (int idx = tid; idx < nn; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    TT[r + c * ldt] = rec[idx];
+    TT[r + (n + c) * ldt] = rec[nn + idx];
+    Pm[r + c * ldp] = rec[2 * nn + idx];
+  }
+  if (a.do_state) {
+    const double *xlp = hl ? (jl < 0 ? a.xhalo : a.x + jl * n) : nullptr;
+    const double *xrp = hr ? a.x + jr * n : nullptr;
+    for (int i = tid; i < n; i += blockDim.x) {
+      xv[i] = xlp ? xlp[i] : 0.0;
+      xv[n + i] = xrp ? xrp[i] : 0.0;
+    }
+  }
+  if (a.do_cov) {
+    const double *Sl = hl ? (jl < 0 ? a.Shalo : a.S + jl * nn) : nullptr;
+    const double *Sr = hr ? a.S + jr * nn : nullptr;
+    const double *Sx = (hl && hr) ? a.Xup + b * nn : nullptr;   // slot b-1: S_{t-1,t+1}
+    for (int idx = tid; idx < nn; idx += blockDim.x) {
+      const int r = idx / n, c = idx - r * n;
+      if (Sl) SII[r + c * ldS] = Sl[idx];
+      if (Sr) SII[(n + r) + (n + c) * ldS] = Sr[idx];
+      if (Sx) {
+        const double v = Sx[idx];
+        SII[r + (n + c) * ldS] = v;
+        SII[(n + c) + r * ldS] = v;
+      }
+    }
+  }
+  __syncthreads();
+  if (a.do_state) {
+    for (int i = tid; i < n; i += blockDim.x) {
+      double s = rec[3 * nn + i];
+      for (int k = 0; k < 2 * n; ++k) s = fma(-TT[i + k * ldt], xv[k], s);
+      a.x[j * n + i] = s;
+    }
+  }
+  if (!a.do_cov) return;
+  gemm<false, false>(np, n2p, n2p, -1.0, TT, ldt, SII, ldS, 0.0, StI, ldt);   // S_{t,I} = -T S_II
+  __syncthreads();
+  gemm<false, true>(np, np, n2p, -1.0, StI, ldt, TT, ldt, 1.0, Pm, ldp);     // S_tt = P - S_{t,I} T^T
+  __syncthreads();
+  double *So = a.S + j * nn;
+  for (int idx = tid; idx < nn; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    So[idx] = 0.5 * (Pm[r + c * ldp] + Pm[c + r * ldp]);
+  }
+  if (a.Xcur) {
+    if (hl) {
+      double *X = a.Xcur + t * nn;                   // slot t-1: S_{t-1,t} = S_tl^T
+      for (int idx = tid; idx < nn; idx += blockDim.x) {
+        const int r = idx / n, c = idx - r * n;
+        X[idx] = StI[c + r * ldt];
+      }
+    }
+    if (hr) {
+      double *X = a.Xcur + (t + 1) * nn;             // slot t: S_{t,t+1} = S_tr
+      for (int idx = tid; idx < nn; idx += blockDim.x) {
+        const int r = idx / n, c = idx - r * n;
+        X[idx] = StI[r + (n + c) * ldt];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- whiten ---
+
+// Evolution blocks: K = Lam Lam^T; El = -Lam^{-1} F,
+// Er = Lam^{-1}, e = Lam^{-1} c.  One CTA per distinct block; the solve with
+// the 2n+1 right-hand sides [F | I | c] is blocked (DMMA updates).
+__global__ void __launch_bounds__(kThreads) whiten_evo_kernel(WhitenArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int n = a.n, nn = n * n, tid = threadIdx.x;
+  const int64_t i = blockIdx.x;
+  double *El = a.El + i * (a.cntE == 1 ? 0 : nn), *Er = a.Er + i * (a.cntE == 1 ? 0 : nn);
+  double *e = a.e + i * (a.cntE == 1 ? 0 : n);
+  const int64_t g = a.first_global + i;
+  if ((a.cntE != 1 && g == 0) || (a.N == 1 && a.first_global == 0)) {   // no evolution row
+    for (int k = tid; k < nn; k += blockDim.x) { El[k] = 0.0; Er[k] = 0.0; }
+    for (int k = tid; k < n; k += blockDim.x) e[k] = 0.0;
+    return;
+  }
+  const int64_t iK = (a.cntE == 1) ? 0 : i;
+  const int ld = ldpad(n), p = 2 * n + 1, cp = pad8(p) + 8;
+  double *Lm = sm, *X = Lm + ld * pad8(n), *sh = X + ld * cp;
+  const double *K = a.K + iK * a.sK, *F = a.F + iK * a.sF;
+  const double *c = a.c ? a.c + iK * a.sc : nullptr;
+  zero_smem(sm, ld * pad8(n) + ld * cp);
+  __syncthreads();
+  for (int k = tid; k < nn; k += blockDim.x) {
+    const int r = k / n, cc = k - r * n;
+    Lm[r + cc * ld] = K[k];
+    X[r + cc * ld] = F[k];
+  }
+  for (int r = tid; r < n; r += blockDim.x) {
+    X[r + (n + r) * ld] = 1.0;
+    X[r + 2 * n * ld] = c ? c[r] : 0.0;
+  }
+  __syncthreads();
+  const bool ok = cta_chol(Lm, ld, n, sh);
+  if (tid == 0 && !ok) {
+    const int64_t step = (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i;
+    report(a.status, step, kBadK);
+  }
+  trsm_lower(Lm, ld, n, X, ld, p);
+  for (int k = tid; k < nn; k += blockDim.x) {
+    const int r = k / n, cc = k - r * n;
+    El[k] = -X[r + cc * ld];
+    Er[k] = X[r + (n + cc) * ld];
+  }
+  for (int r = tid; r < n; r += blockDim.x) e[r] = X[r + 2 * n * ld];
+}
+
+// Observation blocks: L = M M^T; C = M^{-1} H, y = M^{-1} o (rows >= m_i zero).
+__global__ void __launch_bounds__(kThreads) whiten_obs_kernel(WhitenArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int n = a.n, mx = a.m_max, tid = threadIdx.x;
+  const int64_t i = blockIdx.x;
+  const int mi = a.m ? a.m[i] : mx;
+  double *C = a.C + i * (int64_t)mx * n;
+  const int ld = ldpad(mx), p = n + 1, cp = pad8(p) + 8;
+  double *Lm = sm, *X = Lm + ld * pad8(mx), *sh = X + ld * cp;
+  const double *L = a.L + i * a.sL, *H = a.H + i * a.sH, *o = a.o + i * a.so;
+  zero_smem(sm, ld * pad8(mx) + ld * cp);
+  __syncthreads();
+  for (int k = tid; k < mi * mi; k += blockDim.x) {
+    const int r = k / mi, cc = k - r * mi;
+    Lm[r + cc * ld] = L[r * mx + cc];
+  }
+  for (int k = tid; k < mi * n; k += blockDim.x) {
+    const int r = k / n, cc = k - r * n;
+    X[r + cc * ld] = H[r * n + cc];
+  }
+  for (int r = tid; r < mi; r += blockDim.x) X[r + n * ld] = o[r];
+  __syncthreads();
+  const bool ok = cta_chol(Lm, ld, mi, sh);
+  if (tid == 0 && !ok) report(a.status, i, kBadL);
+  trsm_lower(Lm, ld, mi, X, ld, p);
+  for (int k = tid; k < mx * n; k += blockDim.x) {
+    const int r = k / n, cc = k - r * n;
+    C[k] = (r < mi) ? X[r + cc * ld] : 0.0;
+  }
+  if (!a.constC) {
+    for (int r = tid; r < mx; r += blockDim.x) a.y[i * mx + r] = (r < mi) ? X[r + n * ld] : 0.0;
+  } else {
+    for (int k = tid; k < mi * mi; k += blockDim.x) {
+      const int r = k / mi, cc = k - r * mi;
+      a.Mchol[r * mx + cc] = (cc <= r) ? Lm[r + cc * ld] : 0.0;
+    }
+  }
+}
+
+// Constant observation model: y_i = M^{-1} o_i, one thread per step.
+__global__ void whiten_y_kernel(WhitenArgs a) {
+  extern __shared__ double sm[];
+  const int mx = a.m_max;
+  for (int k = threadIdx.x; k < mx * mx; k += blockDim.x) sm[k] = a.Mchol[k];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const double *o = a.o + i * a.so;
+  double *y = a.y + i * mx;
+  for (int r = 0; r < mx; ++r) {
+    double s = o[r];
+    for (int k = 0; k < r; ++k) s = fma(-sm[r * mx + k], y[k], s);
+    y[r] = s / sm[r * mx + r];
+  }
+}
+
+size_t whiten_evo_smem(int n) { return 8 * ((size_t)ldpad(n) * pad8(n) + (size_t)ldpad(n) * (pad8(2 * n + 1) + 8) + 8); }
+size_t whiten_obs_smem(int n, int mx) {
+  return 8 * ((size_t)ldpad(mx) * pad8(mx) + (size_t)ldpad(mx) * (pad8(n + 1) + 8) + 8);
+}
+
+}  // namespace
+
+size_t factor_smem_bytes(int n, int RC) { return 8 * (size_t)factor_plan(n, RC).total; }
+
+size_t backward_smem_bytes(int n) { return 8 * (size_t)bwd_plan(n).total; }
+
+cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  const int64_t grid = a.K >= 2 ? a.K / 2 : 1;
+  factor_level_kernel<<<(unsigned)grid, kThreads, factor_smem_bytes(a.n, a.in.RC), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backward_level(const BackwardLevelArgs &a, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  const int64_t grid = (a.K + 1) / 2;
+  backward_level_kernel<<<(unsigned)grid, kThreads, backward_smem_bytes(a.n), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(whiten_evo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(whiten_obs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  const int n = a.n, mx = a.m_max;
+  whiten_evo_kernel<<<(unsigned)a.cntE, kThreads, whiten_evo_smem(n), s>>>(a);
+  if (mx > 0) {
+    whiten_obs_kernel<<<(unsigned)a.cntC, kThreads, whiten_obs_smem(n, mx), s>>>(a);
+    if (a.constC) {
+      const int T = 256;
+      whiten_y_kernel<<<(unsigned)((a.N + T - 1) / T), T, 8 * (size_t)mx * mx, s>>>(a);
+    }
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ks
