@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "ks_internal.cuh"
 
@@ -27,6 +28,26 @@ namespace ks {
 namespace {
 
 constexpr int kThreads = 256, kWarps = kThreads / 32;
+
+// Development instrumentation (-DKS_LARGE_PROF, variant builds only): phase
+// cycle counts of CTA 0, printed by its thread 0.
+#ifdef KS_LARGE_PROF
+#define KS_PROF_DECL long long _pt = clock64(), _acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define KS_PROF(i)                                   \
+  {                                                  \
+    const long long _now = clock64();                \
+    _acc[i] += _now - _pt;                           \
+    _pt = _now;                                      \
+  }
+#define KS_PROF_PRINT(tag)                                                                          \
+  if (blockIdx.x == 0 && threadIdx.x == 0)                                                          \
+    printf("[%s] %lld %lld %lld %lld %lld %lld %lld %lld\n", tag, _acc[0], _acc[1], _acc[2], _acc[3], \
+           _acc[4], _acc[5], _acc[6], _acc[7]);
+#else
+#define KS_PROF_DECL
+#define KS_PROF(i)
+#define KS_PROF_PRINT(tag)
+#endif
 constexpr int kLdw = 12;   // leading dimension of the 8 x 8 warp tiles (12 = conflict-free)
 
 __host__ __device__ constexpr int pad8(int x) { return (x + 7) & ~7; }
@@ -86,6 +107,54 @@ __device__ void gemm(int M, int N, int K, double alpha, const double *A, int lda
   }
 }
 
+// 1/sqrt(h) (h > 0) and 1/x (x != 0): MUFU approximation + two Newton steps.
+__device__ __forceinline__ double rsqrt_nr(double h) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(h));
+  double hy = h * y;
+  y = fma(0.5 * y, fma(-hy, y, 1.0), y);
+  hy = h * y;
+  y = fma(0.5 * y, fma(-hy, y, 1.0), y);
+  return y;
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  return y;
+}
+
+// Warp all-reduce of 8 values at once: reduce-scatter (xor 16, 8, 4), full
+// reduce of the remaining value (xor 2, 1), then broadcast of the 8 sums:
+// 17 double shuffles instead of 40.
+__device__ __forceinline__ void warp_sum8(double (&p)[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b2 = lane & 8, b1 = lane & 4;
+  double h[4], qd[2], o;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = b4 ? p[i] : p[i + 4];
+    h[i] = (b4 ? p[i + 4] : p[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = b2 ? h[i] : h[i + 2];
+    qd[i] = (b2 ? h[i + 2] : h[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const double send = b1 ? qd[0] : qd[1];
+    o = (b1 ? qd[1] : qd[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  o += __shfl_xor_sync(0xffffffffu, o, 2);
+  o += __shfl_xor_sync(0xffffffffu, o, 1);
+  // lane holds the sum of value (lane >> 2) & 7
+#pragma unroll
+  for (int v = 0; v < 8; ++v) p[v] = __shfl_sync(0xffffffffu, o, 4 * v);
+}
+
 __device__ __forceinline__ double warp_sum(double s) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -103,89 +172,76 @@ struct QrWs {
 };
 constexpr int kPanelMaxR = 5;   // rows per lane in the panel factorization (rows <= 160)
 
-// Panel factorization by warp 0: columns [k0, k0 + nb) of A, rows [k0, rows).
-// Householder reflector j: x = A[k0+j:, k0+j], alpha = -sign(x1)|x|,
-// v = x - alpha e1, H = I - beta v v^T, beta = 1/(|x|^2 - x1 alpha)
-// (zero column: beta = 0).  Writes R into the panel (zeros below the
-// diagonal), V (explicit, rows local to k0) and beta, then G = V^T V (DMMA)
-// and the compact-WY T (LAPACK larft, forward columnwise).
+// Panel factorization by warp 0: columns [k0, k0 + nb) of A, rows [k0, rows)
+// (MR rows per lane).  Householder reflector j: x = A[k0+j:, k0+j],
+// alpha = -sign(x1)|x|, v = x - alpha e1, H = I - beta v v^T,
+// beta = 1/(|x|^2 - x1 alpha) (zero column: beta = 0).  The norm and the
+// products x.a_jj of every later panel column are reduced in ONE batched
+// warp reduction (v.a_jj = x.a_jj - alpha a_jj[j]).  Writes R into the panel
+// (zeros below the diagonal), V (explicit, rows local to k0) and beta, then
+// G = V^T V (DMMA) and the compact-WY T (LAPACK larft, forward columnwise).
+template <int MR>
 __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) {
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int mrow = rows - k0, mpad = pad8(mrow);
-  double a[kPanelMaxR][8];
+  double a[MR][8];
 #pragma unroll
-  for (int r = 0; r < kPanelMaxR; ++r) {
+  for (int r = 0; r < MR; ++r) {
     const int li = lane + 32 * r;
 #pragma unroll
     for (int j = 0; j < 8; ++j) a[r][j] = (li < mrow && j < nb) ? A[(k0 + li) + (k0 + j) * lda] : 0.0;
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    if (j >= nb) {   // non-pivot column of a partial panel: zero reflector
-#pragma unroll
-      for (int r = 0; r < kPanelMaxR; ++r) {
-        const int li = lane + 32 * r;
-        if (li < mpad) w.V[li + j * w.ldv] = 0.0;
-      }
-      if (lane == 0) w.beta[j] = 0.0;
-      continue;
-    }
-    double s = 0.0;
-#pragma unroll
-    for (int r = 0; r < kPanelMaxR; ++r) {
-      const int li = lane + 32 * r;
-      if (li >= j) s = fma(a[r][j], a[r][j], s);
-    }
-    s = warp_sum(s);
-    const double x1 = __shfl_sync(0xffffffffu, a[0][j], j);
-    double alpha, beta, v1;
-    if (s == 0.0) {
-      alpha = x1;
-      beta = 0.0;
-      v1 = 0.0;
-    } else {
-      const double nrm = sqrt(s);
-      alpha = (x1 > 0.0) ? -nrm : nrm;
-      v1 = x1 - alpha;
-      beta = 1.0 / (s - x1 * alpha);
-    }
-    double v[kPanelMaxR];
-#pragma unroll
-    for (int r = 0; r < kPanelMaxR; ++r) {
-      const int li = lane + 32 * r;
-      v[r] = (li > j) ? a[r][j] : (li == j ? v1 : 0.0);
-      if (beta == 0.0) v[r] = 0.0;
-    }
-    // apply H to the remaining panel columns (batched reductions)
-    double d[8];
+    // p[j] = |x|^2, p[jj] = x . a_jj (jj > j), rows li >= j
+    double p[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
-      d[jj] = 0.0;
-      if (jj > j && jj < nb) {
+      p[jj] = 0.0;
+      if (jj >= j) {
 #pragma unroll
-        for (int r = 0; r < kPanelMaxR; ++r) d[jj] = fma(v[r], a[r][jj], d[jj]);
+        for (int r = 0; r < MR; ++r) {
+          const int li = lane + 32 * r;
+          if (li >= j) p[jj] = fma(a[r][j], a[r][jj], p[jj]);
+        }
       }
+    }
+    warp_sum8(p);
+    double aj[8];   // row j of the panel (lane j, slot 0)
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) aj[jj] = (jj >= j) ? __shfl_sync(0xffffffffu, a[0][jj], j) : 0.0;
+    const double s = p[j], x1 = aj[j];
+    const bool live = (j < nb) && (s != 0.0);
+    const double nrm = live ? s * rsqrt_nr(s) : 0.0;
+    const double alpha = live ? ((x1 > 0.0) ? -nrm : nrm) : x1;
+    const double beta = live ? rcp_nr(s - x1 * alpha) : 0.0;
+    const double v1 = live ? x1 - alpha : 0.0;
+    double v[MR];
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int li = lane + 32 * r;
+      v[r] = !live ? 0.0 : (li > j ? a[r][j] : (li == j ? v1 : 0.0));
     }
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj)
-      if (jj > j && jj < nb) d[jj] = warp_sum(d[jj]) * beta;
+      if (jj > j) {
+        const double d = beta * (p[jj] - alpha * aj[jj]);
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj)
-      if (jj > j && jj < nb) {
-#pragma unroll
-        for (int r = 0; r < kPanelMaxR; ++r) a[r][jj] = fma(-d[jj], v[r], a[r][jj]);
+        for (int r = 0; r < MR; ++r) a[r][jj] = fma(-d, v[r], a[r][jj]);
       }
 #pragma unroll
-    for (int r = 0; r < kPanelMaxR; ++r) {
+    for (int r = 0; r < MR; ++r) {
       const int li = lane + 32 * r;
       if (li < mpad) w.V[li + j * w.ldv] = (li < mrow) ? v[r] : 0.0;
-      if (li == j) a[r][j] = alpha;
-      else if (li > j) a[r][j] = 0.0;
+      if (j < nb) {
+        if (li == j) a[r][j] = alpha;
+        else if (li > j) a[r][j] = 0.0;
+      }
     }
     if (lane == 0) w.beta[j] = beta;
   }
 #pragma unroll
-  for (int r = 0; r < kPanelMaxR; ++r) {
+  for (int r = 0; r < MR; ++r) {
     const int li = lane + 32 * r;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -204,17 +260,32 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
     w.G[g + (2 * q + 1) * kLdw] = g1;
   }
   __syncwarp();
-  // T: T_jj = beta_j, T[0:j, j] = -beta_j T[0:j, 0:j] G[0:j, j]
-  for (int j = 0; j < 8; ++j) {
-    double t = 0.0;
-    if (lane < j) {
-      for (int l = lane; l < j; ++l) t = fma(w.T[lane + l * kLdw], w.G[l + j * kLdw], t);
-      t *= -w.beta[j];
+  // T = U^{-1}, U = diag(1/beta) + striu(V^T V) (the UT transform of the
+  // compact-WY factor; a zero reflector gets U_jj = 1, its V column is 0):
+  // lane c < 8 solves column c by back-substitution, 1/U_ii = beta_i.
+  if (lane < 8) {
+    const int c = lane;
+    double t[8], bi[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      bi[i] = w.beta[i] == 0.0 ? 1.0 : w.beta[i];
+      t[i] = 0.0;
     }
-    __syncwarp();
-    if (lane < 8) w.T[lane + j * kLdw] = (lane < j) ? t : (lane == j ? w.beta[j] : 0.0);
-    __syncwarp();
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      if (i == c) t[i] = bi[i];
+      else if (i < c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = i + 1; l < 8; ++l)
+          if (l <= c) acc = fma(w.G[i + l * kLdw], t[l], acc);
+        t[i] = -bi[i] * acc;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w.T[i + c * kLdw] = t[i];
   }
+  __syncwarp();
 }
 
 // Q^T C for C = A[k0:k0+mpad, c0:c0+ncp] with Q = I - V T V^T:
@@ -225,14 +296,15 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, 
   double *sc = w.tile + warp * (kLdw * 8);
   for (int n0 = warp * 8; n0 < ncp; n0 += kWarps * 8) {
     double *C = A + k0 + (c0 + n0) * lda;
-    double w0 = 0.0, w1 = 0.0;
-    for (int kk = 0; kk < mpad; kk += 4) {
-      const double x = w.V[(kk + q) + g * w.ldv];      // V^T[g][kk+q]
-      const double y = C[(kk + q) + g * lda];           // C[kk+q][g]
-      dmma(w0, w1, x, y);
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;   // two independent DMMA chains
+    int kk = 0;
+    for (; kk + 8 <= mpad; kk += 8) {
+      dmma(w0, w1, w.V[(kk + q) + g * w.ldv], C[(kk + q) + g * lda]);          // V^T[g][kk+q], C[kk+q][g]
+      dmma(w2, w3, w.V[(kk + 4 + q) + g * w.ldv], C[(kk + 4 + q) + g * lda]);
     }
-    sc[g + (2 * q) * kLdw] = w0;
-    sc[g + (2 * q + 1) * kLdw] = w1;
+    if (kk < mpad) dmma(w0, w1, w.V[(kk + q) + g * w.ldv], C[(kk + q) + g * lda]);
+    sc[g + (2 * q) * kLdw] = w0 + w2;
+    sc[g + (2 * q + 1) * kLdw] = w1 + w3;
     __syncwarp();
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
@@ -246,6 +318,7 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, 
     sc[g + (2 * q + 1) * kLdw] = u1;
     __syncwarp();
     const double y0 = sc[q + g * kLdw], y1 = sc[(4 + q) + g * kLdw];   // W2[kk+q][g]
+#pragma unroll 2
     for (int m0 = 0; m0 < mpad; m0 += 8) {
       double *cp = C + (m0 + g) + (2 * q) * lda;
       double c0v = cp[0], c1v = cp[lda];
@@ -263,32 +336,60 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, 
 // [npiv, ncols).  A is zero-padded to pad8(rows) rows (lda >= that) and to
 // pad8(ncols) (+8 when npiv % 8 != 0) columns.  On exit the first npiv
 // columns hold R (zeros below the diagonal).  Ends with __syncthreads.
-__device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w) {
+__device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w, long long *acc = nullptr) {
   const int warp = threadIdx.x >> 5;
+#ifdef KS_LARGE_PROF
+  long long _t0 = clock64();
+#endif
   for (int k0 = 0; k0 < npiv && k0 < rows; k0 += 8) {
     const int nb = (npiv - k0 < 8) ? npiv - k0 : 8;
-    if (warp == 0) qr_panel(A, lda, k0, rows, nb, w);
+    if (warp == 0) {
+      const int mr = (rows - k0 + 31) >> 5;
+      if (mr <= 1) qr_panel<1>(A, lda, k0, rows, nb, w);
+      else if (mr == 2) qr_panel<2>(A, lda, k0, rows, nb, w);
+      else if (mr == 3) qr_panel<3>(A, lda, k0, rows, nb, w);
+      else if (mr == 4) qr_panel<4>(A, lda, k0, rows, nb, w);
+      else qr_panel<kPanelMaxR>(A, lda, k0, rows, nb, w);
+    }
     __syncthreads();
+#ifdef KS_LARGE_PROF
+    { const long long t1 = clock64(); if (acc) acc[0] += t1 - _t0; _t0 = t1; }
+#endif
     const int c0 = k0 + nb;
     if (c0 < ncols) qr_apply(A, lda, k0, pad8(rows - k0), c0, pad8(ncols - c0), w);
     __syncthreads();
+#ifdef KS_LARGE_PROF
+    { const long long t1 = clock64(); if (acc) acc[1] += t1 - _t0; _t0 = t1; }
+#endif
   }
 }
 
 // X <- R^{-1} X for R (n x n upper triangular, ldr) and X (n x p, ldx), both
 // zero-padded to 8 rows/columns: 8-row blocks from the bottom, the diagonal
-// block by one thread per right-hand side, the update of the rows above as a
-// DMMA GEMM.  Ends with __syncthreads.
-__device__ void trsm_upper(const double *R, int ldr, int n, double *X, int ldx, int p) {
+// block by one thread per right-hand side (values in registers, multiplied
+// by the reciprocal diagonal rinv[0..n) the caller provides), the update of
+// the rows above as a DMMA GEMM.  Ends with __syncthreads.
+__device__ void trsm_upper(const double *R, int ldr, const double *rinv, int n, double *X, int ldx, int p) {
   for (int r0 = ((n - 1) / 8) * 8; r0 >= 0; r0 -= 8) {
     const int h = (n - r0 < 8) ? n - r0 : 8;
     for (int c = threadIdx.x; c < p; c += blockDim.x) {
-      double *x = X + r0 + c * ldx;
-      for (int i = h - 1; i >= 0; --i) {
-        double s = x[i];
-        for (int l = i + 1; l < h; ++l) s = fma(-R[(r0 + i) + (r0 + l) * ldr], x[l], s);
-        x[i] = s / R[(r0 + i) + (r0 + i) * ldr];
+      double *xp = X + r0 + c * ldx;
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = (i < h) ? xp[i] : 0.0;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        if (i < h) {
+          double s = x[i];
+#pragma unroll
+          for (int l = i + 1; l < 8; ++l)
+            if (l < h) s = fma(-R[(r0 + i) + (r0 + l) * ldr], x[l], s);
+          x[i] = s * rinv[r0 + i];
+        }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < h) xp[i] = x[i];
     }
     __syncthreads();
     if (r0 > 0) gemm<false, false>(r0, pad8(p), 8, -1.0, R + r0 * ldr, ldr, X + r0, ldx, 1.0, X, ldx);
@@ -297,16 +398,26 @@ __device__ void trsm_upper(const double *R, int ldr, int n, double *X, int ldx, 
 }
 
 // X <- L^{-1} X for L (n x n lower triangular): 8-row blocks from the top.
-__device__ void trsm_lower(const double *L, int ldl, int n, double *X, int ldx, int p) {
+__device__ void trsm_lower(const double *L, int ldl, const double *rinv, int n, double *X, int ldx, int p) {
   for (int r0 = 0; r0 < n; r0 += 8) {
     const int h = (n - r0 < 8) ? n - r0 : 8;
     for (int c = threadIdx.x; c < p; c += blockDim.x) {
-      double *x = X + r0 + c * ldx;
-      for (int i = 0; i < h; ++i) {
-        double s = x[i];
-        for (int l = 0; l < i; ++l) s = fma(-L[(r0 + i) + (r0 + l) * ldl], x[l], s);
-        x[i] = s / L[(r0 + i) + (r0 + i) * ldl];
+      double *xp = X + r0 + c * ldx;
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = (i < h) ? xp[i] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < h) {
+          double s = x[i];
+#pragma unroll
+          for (int l = 0; l < i; ++l) s = fma(-L[(r0 + i) + (r0 + l) * ldl], x[l], s);
+          x[i] = s * rinv[r0 + i];
+        }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < h) xp[i] = x[i];
     }
     __syncthreads();
     const int rest = pad8(n) - r0 - 8;
@@ -314,6 +425,11 @@ __device__ void trsm_lower(const double *L, int ldl, int n, double *X, int ldx, 
       gemm<false, false>(rest, pad8(p), 8, -1.0, L + (r0 + 8) + r0 * ldl, ldl, X + r0, ldx, 1.0, X + r0 + 8, ldx);
     __syncthreads();
   }
+}
+
+// rinv[i] = 1 / A_ii, i < n (threads; caller synchronises)
+__device__ void diag_rcp(const double *A, int lda, int n, double *rinv) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) rinv[i] = 1.0 / A[i + i * lda];
 }
 
 // Cholesky (right-looking) of the d x d lower triangle of Lm (ldl) in place;
@@ -415,8 +531,9 @@ __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   const int rmax = (2 * n > 2 * RC + n) ? 2 * n : 2 * RC + n;   // >= RC + n
   f.ldv = ldpad(rmax);
   const int s1 = f.ld1 * f.cols1;
-  // post-processing reuses S1 for R^{-1}, P and a padded copy of R (3 x ldpad(n) x pad8(n))
-  const int s1p = 3 * ldpad(n) * pad8(n);
+  // post-processing reuses S1 for R^{-1}, P, a padded copy of R (3 x ldpad(n) x pad8(n))
+  // and the reciprocal diagonal
+  const int s1p = 3 * ldpad(n) * pad8(n) + pad8(n);
   const int s2 = f.ld2 * f.cols2, s3 = f.ld3 * f.cols3;
   f.off2 = ((s1 > s1p ? s1 : s1p) + 1) & ~1;
   f.offws = f.off2 + (((s2 > s3 ? s2 : s3) + 1) & ~1);
@@ -454,6 +571,12 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   double *S1 = sm, *P2 = sm + f.off2, *sh = sm + f.total - 8;
   QrWs w = carve_ws(sm + f.offws, f.ldv);
   const int ld1 = f.ld1, ld2 = f.ld2, ld3 = f.ld3;
+  KS_PROF_DECL
+#ifdef KS_LARGE_PROF
+  long long *qacc = _acc + 6;
+#else
+  long long *qacc = nullptr;
+#endif
 
   double nrm_t, nrm_u = 0.0;
   if (in.nrm) {
@@ -476,7 +599,9 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     ld_blk(S1, ld1, RC, 2 * n, in.e + u * in.se, 1, n, 1, n);
   }
   __syncthreads();
-  qr_blocked(S1, ld1, RC + n, n, 2 * n + 1, w);
+  KS_PROF(0)
+  qr_blocked(S1, ld1, RC + n, n, 2 * n + 1, w, qacc);
+  KS_PROF(1)
 
   // ---- stage 3 (before stage 2: its matrix B3 shares memory with B2) ----
   if (hr) {
@@ -493,7 +618,9 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
       rows3 += n;
     }
     __syncthreads();
-    qr_blocked(P2, ld3, rows3, n, n + 1, w);
+    KS_PROF(0)
+    qr_blocked(P2, ld3, rows3, n, n + 1, w, qacc);
+    KS_PROF(2)
     double *ent = a.next + pnext * entry_doubles(n);
     const int valid = rows3 < n ? rows3 : n;
     st_blk(ent, n, P2, ld3, 0, 0, n, n, valid);             // C'
@@ -512,7 +639,9 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
     cp_blk(P2, ld2, n, 2 * n, S1, ld1, 0, n, n, n + 1);    // X_t, z~_t
     __syncthreads();
-    qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w);
+    KS_PROF(0)
+    qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w, qacc);
+    KS_PROF(3)
     if (hr) {
       double *ent = a.next + pnext * entry_doubles(n);
       st_blk(ent + n * n + n, n, P2, ld2, n, n, n, n, n);               // El' = Z_t
@@ -542,7 +671,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   const int ldr = ldpad(n), np = pad8(n);
   // R_tt copied into a zero-padded block (the blocked solves read whole 8x8
   // blocks; B2's columns next to R hold the right-hand sides)
-  double *Ri = S1, *Pm = S1 + ldr * np, *Rc = S1 + 2 * ldr * np;
+  double *Ri = S1, *Pm = S1 + ldr * np, *Rc = S1 + 2 * ldr * np, *rinv = S1 + 3 * ldr * np;
   zero_smem(Ri, 3 * ldr * np);
   __syncthreads();
   for (int i = tid; i < n; i += blockDim.x) Ri[i + i * ldr] = 1.0;
@@ -550,12 +679,16 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     const int i = idx % n, j = idx / n;
     if (i <= j) Rc[i + j * ldr] = P2[i + j * ld2];
   }
+  diag_rcp(P2, ld2, n, rinv);
   __syncthreads();
   // RHS [R_l | R_r | z] (columns n .. 3n of B2) and I (R^{-1}) in two solves
-  trsm_upper(Rc, ldr, n, P2 + n * ld2, ld2, 2 * n + 1);
-  trsm_upper(Rc, ldr, n, Ri, ldr, n);
+  KS_PROF(0)
+  trsm_upper(Rc, ldr, rinv, n, P2 + n * ld2, ld2, 2 * n + 1);
+  trsm_upper(Rc, ldr, rinv, n, Ri, ldr, n);
+  KS_PROF(4)
   gemm<false, true>(np, np, np, 1.0, Ri, ldr, Ri, ldr, 0.0, Pm, ldr);
   __syncthreads();
+  KS_PROF(5)
   double *rec = a.rrec + (t >> 1) * rrec_doubles(n);
   const int nn = n * n;
   for (int idx = tid; idx < nn; idx += blockDim.x) {
@@ -566,6 +699,8 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   }
   for (int r = tid; r < n; r += blockDim.x) rec[3 * nn + r] = P2[r + 3 * n * ld2];   // w
   __syncthreads();
+  KS_PROF(0)
+  KS_PROF_PRINT("elim: other stage1 stage3 stage2 trsm Pgemm panel apply")
 }
 
 __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs a) {
@@ -730,7 +865,9 @@ __global__ void __launch_bounds__(kThreads) whiten_evo_kernel(WhitenArgs a) {
     const int64_t step = (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i;
     report(a.status, step, kBadK);
   }
-  trsm_lower(Lm, ld, n, X, ld, p);
+  diag_rcp(Lm, ld, n, sh);
+  __syncthreads();
+  trsm_lower(Lm, ld, sh, n, X, ld, p);
   for (int k = tid; k < nn; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
     El[k] = -X[r + cc * ld];
@@ -763,7 +900,9 @@ __global__ void __launch_bounds__(kThreads) whiten_obs_kernel(WhitenArgs a) {
   __syncthreads();
   const bool ok = cta_chol(Lm, ld, mi, sh);
   if (tid == 0 && !ok) report(a.status, i, kBadL);
-  trsm_lower(Lm, ld, mi, X, ld, p);
+  diag_rcp(Lm, ld, mi, sh);
+  __syncthreads();
+  trsm_lower(Lm, ld, sh, mi, X, ld, p);
   for (int k = tid; k < mx * n; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
     C[k] = (r < mi) ? X[r + cc * ld] : 0.0;
@@ -795,9 +934,9 @@ __global__ void whiten_y_kernel(WhitenArgs a) {
   }
 }
 
-size_t whiten_evo_smem(int n) { return 8 * ((size_t)ldpad(n) * pad8(n) + (size_t)ldpad(n) * (pad8(2 * n + 1) + 8) + 8); }
+size_t whiten_evo_smem(int n) { return 8 * ((size_t)ldpad(n) * pad8(n) + (size_t)ldpad(n) * (pad8(2 * n + 1) + 8) + pad8(n) + 8); }
 size_t whiten_obs_smem(int n, int mx) {
-  return 8 * ((size_t)ldpad(mx) * pad8(mx) + (size_t)ldpad(mx) * (pad8(n + 1) + 8) + 8);
+  return 8 * ((size_t)ldpad(mx) * pad8(mx) + (size_t)ldpad(mx) * (pad8(n + 1) + 8) + pad8(mx) + 8);
 }
 
 }  // namespace
