@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "ks_internal.cuh"
 
@@ -120,13 +121,21 @@ __device__ __forceinline__ double rcp_nr(double x) {
 __device__ __forceinline__ void gmake(double &rho, double yk, double &w, double &sb) {
   const bool empty = !(rho < __longlong_as_double(0x7ff0000000000000ll));
   const bool ident = (yk == 0.0) || !(w < __longlong_as_double(0x7ff0000000000000ll));
-  const double rs = empty ? 0.0 : rho;
-  const double yr = yk * rs;
-  const double wn = fma(yk, yr, w);
-  const double q = rcp_nr(ident ? 1.0 : (empty ? yk : wn));
-  sb = ident ? 0.0 : (empty ? q : yr * q);
-  rho = ident ? rho : (empty ? (w * q) * q : rs * (w * q));
-  w = ident ? w : (empty ? __longlong_as_double(0x7ff0000000000000ll) : wn);
+  if (!(empty || ident)) {   // the common case: select-free
+    const double yr = yk * rho;
+    const double wn = fma(yk, yr, w);
+    const double q = rcp_nr(wn);
+    sb = yr * q;
+    rho = rho * (w * q);
+    w = wn;
+  } else if (ident) {
+    sb = 0.0;
+  } else {                   // an empty row absorbs the streamed row
+    const double q = rcp_nr(yk);
+    sb = q;
+    rho = (w * q) * q;
+    w = __longlong_as_double(0x7ff0000000000000ll);
+  }
 }
 constexpr double kEmptyRow = __builtin_huge_val();   // rho of an empty row of R (w of an absorbed row)
 // sqrt(delta) = 1/sqrt(w) of a streamed row (0 once absorbed).
@@ -663,7 +672,10 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
 // column (warp 0: the "left" half of Alg. 2's products, warp 1: the "right").
 constexpr int kBwdCols = 32;
 // resident CTAs per SM the register allocation targets (no spills at n = 6..8)
-constexpr int bwd_min_blocks(int n) { return n <= 5 ? 5 : n == 6 ? 4 : 3; }
+#ifndef KS_BWD6_BLOCKS
+#define KS_BWD6_BLOCKS 4
+#endif
+constexpr int bwd_min_blocks(int n) { return n <= 5 ? 5 : n == 6 ? KS_BWD6_BLOCKS : 3; }
 template <int N>
 __host__ __device__ constexpr int rs_doubles() { return 2 * N * N + N + N * (N + 1) / 2; }
 // S_tt staging row: NN doubles padded to a multiple of 2 (16-byte rows for
@@ -827,49 +839,56 @@ __global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backwar
   double *Qs = Snb + (right ? NT * NB : 0) + col;   // this side's Q [NT][NB]
   double *Stt = Snb + 2 * NT * NB + col * SP;
   if (active) {
-    // the T block this side multiplies from the right: T_l (left) / T_r (right)
-    const int TO = right ? RR::Tr : RR::Tl;
+    // one code path per side (warp-uniform branch), so neither side executes
+    // the other's products
+    auto side = [&](auto right_c) {
+      constexpr bool RIGHT = decltype(right_c)::value;
+      // the T block this side multiplies from the right: T_l (left) / T_r (right)
+      constexpr int TO = RIGHT ? RR::Tr : RR::Tl;
 #pragma unroll(N <= 6 ? N : 1)
-    for (int i = 0; i < N; ++i) {
-      double tl[N], tr[N], A[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        tl[k] = rec(RR::Tl + i * N + k);
-        tr[k] = rec(RR::Tr + i * N + k);
-      }
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        double s = 0.0;
+      for (int i = 0; i < N; ++i) {
+        double tl[N], tr[N], A[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          const double sd = k <= c ? Sd[TR::at(k, c)] : Sd[TR::at(c, k)];
-          if (!right) {              // S_tl = -(T_l S_ll + T_r S_lr^T)
-            s = fma(tl[k], sd, s);
-            s = fma(tr[k], Slr[c][k], s);
-          } else {                   // S_tr = -(T_l S_lr + T_r S_rr)
-            s = fma(tl[k], Slr[k][c], s);
-            s = fma(tr[k], sd, s);
-          }
+          tl[k] = rec(RR::Tl + i * N + k);
+          tr[k] = rec(RR::Tr + i * N + k);
         }
-        A[c] = -s;
-      }
-      if (a.Xcur.p) {
 #pragma unroll
         for (int c = 0; c < N; ++c) {
-          if (!right && hl) stv<32>(a.Xcur, t, c * N + i, A[c]);      // slot t-1: S_{t-1,t} = S_tl^T
-          if (right && hr) stv<32>(a.Xcur, t + 1, i * N + c, A[c]);   // slot t:   S_{t,t+1} = S_tr
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            const double sd = k <= c ? Sd[TR::at(k, c)] : Sd[TR::at(c, k)];
+            if (!RIGHT) {            // S_tl = -(T_l S_ll + T_r S_lr^T)
+              s = fma(tl[k], sd, s);
+              s = fma(tr[k], Slr[c][k], s);
+            } else {                 // S_tr = -(T_l S_lr + T_r S_rr)
+              s = fma(tl[k], Slr[k][c], s);
+              s = fma(tr[k], sd, s);
+            }
+          }
+          A[c] = -s;
+        }
+        if (a.Xcur.p) {
+#pragma unroll
+          for (int c = 0; c < N; ++c) {
+            if (!RIGHT && hl) stv<32>(a.Xcur, t, c * N + i, A[c]);      // slot t-1: S_{t-1,t} = S_tl^T
+            if (RIGHT && hr) stv<32>(a.Xcur, t + 1, i * N + c, A[c]);   // slot t:   S_{t,t+1} = S_tr
+          }
+        }
+        // row i of Q = S_t* T_*^T (upper part jj >= i); the jj chains are independent
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) {
+          if (jj < i) continue;
+          double q = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) q = fma(A[k], rec(TO + jj * N + k), q);
+          Qs[(i * N - (i * (i - 1)) / 2 + (jj - i)) * NB] = q;
         }
       }
-      // row i of Q = S_t* T_*^T (upper part jj >= i); the jj chains are independent
-#pragma unroll
-      for (int jj = 0; jj < N; ++jj) {
-        if (jj < i) continue;
-        double q = 0.0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) q = fma(A[k], rec(TO + jj * N + k), q);
-        Qs[(i * N - (i * (i - 1)) / 2 + (jj - i)) * NB] = q;
-      }
-    }
+    };
+    if (right) side(std::true_type{});
+    else side(std::false_type{});
   }
   __syncthreads();
   if (active && !right) {
