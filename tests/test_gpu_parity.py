@@ -60,7 +60,8 @@ def test_random_small_all_parities(N, n, generic):
 
 
 @pytest.mark.parametrize("const", [False, True])
-@pytest.mark.parametrize("n,mmax", [(4, 9), (8, 3), (12, 12), (24, 5), (48, 48)])
+@pytest.mark.parametrize("n,mmax", [(4, 9), (8, 3), (9, 1), (12, 12), (13, 20), (17, 17), (24, 5),
+                                    (33, 7), (40, 41), (48, 48)])
 def test_random_dims(n, mmax, const):
     rng = np.random.default_rng(n * 7 + mmax)
     N = 45
