@@ -43,10 +43,18 @@ constexpr int kThreads = 256, kWarps = kThreads / 32;
   if (blockIdx.x == 0 && threadIdx.x == 0)                                                          \
     printf("[%s] %lld %lld %lld %lld %lld %lld %lld %lld\n", tag, _acc[0], _acc[1], _acc[2], _acc[3], \
            _acc[4], _acc[5], _acc[6], _acc[7]);
+__device__ long long g_panel_prof[8];
+#define KS_PP(i, t0)                                                        \
+  {                                                                         \
+    const long long _n = clock64();                                         \
+    _ppa[i] += _n - t0;                                                     \
+    t0 = _n;                                                                \
+  }
 #else
 #define KS_PROF_DECL
 #define KS_PROF(i)
 #define KS_PROF_PRINT(tag)
+#define KS_PP(i, t0)
 #endif
 constexpr int kLdw = 12;   // leading dimension of the 8 x 8 warp tiles (12 = conflict-free)
 
@@ -184,6 +192,10 @@ template <int MR>
 __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) {
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int mrow = rows - k0, mpad = pad8(mrow);
+#ifdef KS_LARGE_PROF
+  long long _ppa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long _pp = clock64();
+#endif
   double a[MR][8];
 #pragma unroll
   for (int r = 0; r < MR; ++r) {
@@ -206,7 +218,9 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
         }
       }
     }
+    KS_PP(0, _pp)
     warp_sum8(p);
+    KS_PP(1, _pp)
     double aj[8];   // row j of the panel (lane j, slot 0)
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) aj[jj] = (jj >= j) ? __shfl_sync(0xffffffffu, a[0][jj], j) : 0.0;
@@ -216,6 +230,7 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
     const double alpha = live ? ((x1 > 0.0) ? -nrm : nrm) : x1;
     const double beta = live ? rcp_nr(s - x1 * alpha) : 0.0;
     const double v1 = live ? x1 - alpha : 0.0;
+    KS_PP(2, _pp)
     double v[MR];
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
@@ -239,6 +254,7 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
       }
     }
     if (lane == 0) w.beta[j] = beta;
+    KS_PP(3, _pp)
   }
 #pragma unroll
   for (int r = 0; r < MR; ++r) {
@@ -248,6 +264,7 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
       if (li < mrow && j < nb) A[(k0 + li) + (k0 + j) * lda] = a[r][j];
   }
   __syncwarp();
+  KS_PP(4, _pp)
   // G = V^T V (one 8x8 DMMA tile, K = mpad)
   {
     double g0 = 0.0, g1 = 0.0;
@@ -260,6 +277,7 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
     w.G[g + (2 * q + 1) * kLdw] = g1;
   }
   __syncwarp();
+  KS_PP(5, _pp)
   // T = U^{-1}, U = diag(1/beta) + striu(V^T V) (the UT transform of the
   // compact-WY factor; a zero reflector gets U_jj = 1, its V column is 0):
   // lane c < 8 solves column c by back-substitution, 1/U_ii = beta_i.
@@ -286,6 +304,11 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
     for (int i = 0; i < 8; ++i) w.T[i + c * kLdw] = t[i];
   }
   __syncwarp();
+  KS_PP(6, _pp)
+#ifdef KS_LARGE_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int i = 0; i < 7; ++i) g_panel_prof[i] += _ppa[i];
+#endif
 }
 
 // Q^T C for C = A[k0:k0+mpad, c0:c0+ncp] with Q = I - V T V^T:
@@ -701,6 +724,11 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   __syncthreads();
   KS_PROF(0)
   KS_PROF_PRINT("elim: other stage1 stage3 stage2 trsm Pgemm panel apply")
+#ifdef KS_LARGE_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("[panel: p+load sum8 scalar update store G T] %lld %lld %lld %lld %lld %lld %lld\n", g_panel_prof[0],
+           g_panel_prof[1], g_panel_prof[2], g_panel_prof[3], g_panel_prof[4], g_panel_prof[5], g_panel_prof[6]);
+#endif
 }
 
 __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs a) {
