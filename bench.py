@@ -148,7 +148,7 @@ def roofline(launches, N, n, m, strides, p64_tf, cfg="c5"):
             tj = json.load(f)
         rec = tj.get(cfg, {}).get(f"{fam} L={lev}")
         if rec:
-            traffic, tsrc = rec["bytes"], f"profiles/{rec['round']}_{fam}_L{lev}.txt ({rec['report']})"
+            traffic, tsrc = rec["bytes"], f"profiles/{rec['round']}_{cfg}_{fam}_L{lev}.txt ({rec['report']})"
     except Exception:
         pass
     r.update({"traffic": traffic, "traffic_source": tsrc, "kernel": f"{fam}_level_kernel L={lev}",

@@ -51,7 +51,7 @@ def main():
             ncu_hot.main(rep, 20, launch)
         by, name = dram_bytes(rep, launch)
         print(f"\nDRAM traffic (read+write) of this launch: {by} bytes", file=buf)
-        fn = f"{rnd}_{label}".replace(" ", "_").replace("=", "")
+        fn = f"{rnd}_{cfg}_{label}".replace(" ", "_").replace("=", "")
         with open(os.path.join(ROOT, "profiles", fn + ".txt"), "w") as f:
             f.write(buf.getvalue())
         traffic.setdefault(cfg, {})[label] = {"bytes": by, "kernel": name, "report": os.path.basename(rep),
