@@ -125,14 +125,11 @@ __device__ __forceinline__ double rsqrt_nr(double h) {
   y = fma(0.5 * y, fma(-hy, y, 1.0), y);
   return y;
 }
-__device__ __forceinline__ double rcp_nr(double x) {
+__device__ __forceinline__ double rcp_nr(double x) {   // one third-order Newton step (see ks_small_impl.cuh)
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  return y;
+  const double e = fma(-x, y, 1.0);
+  return fma(y, fma(e, e, e), y);
 }
 
 // Warp all-reduce of 8 values at once: reduce-scatter (xor 16, 8, 4), full

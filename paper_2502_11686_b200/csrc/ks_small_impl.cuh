@@ -88,15 +88,14 @@ __device__ __forceinline__ double sqrt_nr(double h) {
   const double r = h * rsqrt_nr(z ? 1.0 : h);
   return z ? 0.0 : r;
 }
-// 1/x for x != 0: MUFU approximation + two Newton steps.
+// 1/x for x != 0: the MUFU approximation (relative error <= 2^-19.9,
+// measured on B200: tools/micro/rcp_bench.cu) refined by one third-order
+// Newton step y' = y + y (e + e^2), e = 1 - x y: error ~e^3 < 2^-59.
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  return y;
+  const double e = fma(-x, y, 1.0);
+  return fma(y, fma(e, e, e), y);
 }
 
 // Square-root-free Givens rotations (Gentleman, 1973), in inverse-weight
