@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling runs: no e2e / cpu baseline")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     return ap.parse_args()
 
 
@@ -210,10 +211,13 @@ def main():
     local_p = p.slice(lo, hi) if P > 1 else p
     strides = {"C": int(local_p.H.shape[0] > 1 or local_p.L.shape[0] > 1),
                "E": int(local_p.F.shape[0] > 1 or local_p.K.shape[0] > 1 or local_p.c is not None)}
-    stream = torch.cuda.current_stream(dev)
+    # every library call goes to one side stream (CUDA graphs cannot capture
+    # the legacy default stream)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     p64 = ks.peak_fp64_tflops(stream)
 
-    sm = ks.Smoother(local_p, device=dev, shard=(rank, P, None) if P > 1 else None)
+    sm = ks.Smoother(local_p, device=dev, stream=stream, shard=(rank, P, None) if P > 1 else None)
     views = sm.boundary_tensors() if P > 1 else None
 
     def step(s, v, get=None):
@@ -232,8 +236,33 @@ def main():
     torch.cuda.synchronize()
     if P > 1:
         dist.barrier()
+
+    # (1) per-launch device times (library events around every launch): the
+    # phase split and the roofline's dominant launch
     sm.set_timing(True)
     l0 = sm.info()["launches"]
+    for _ in range(a.steps):
+        step(sm, views)
+    launches = sm.launch_times()
+    n_launch = (sm.info()["launches"] - l0) // a.steps
+    fam_ms = {}
+    for fam, lev, t in launches:
+        fam_ms[fam] = fam_ms.get(fam, 0.0) + t / a.steps
+    sm.set_timing(False)
+    sm.check()
+
+    # (2) the headline: K steps as CUDA-graph replays (one graph = one step's
+    # ~50 launches; 1 GPU) or eagerly (N > 1: the step contains the NCCL
+    # boundary allgather), CUDA events on the launching stream
+    graph = None
+    if P == 1 and not a.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step(sm, views)
+        for _ in range(max(a.warmup, 1)):
+            graph.replay()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else (lambda: step(sm, views))
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
@@ -243,7 +272,7 @@ def main():
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(a.steps):
-        step(sm, views)
+        run()
     e1.record(stream)
     torch.cuda.synchronize()
     if P > 1:
@@ -252,12 +281,6 @@ def main():
     ms = e0.elapsed_time(e1) / a.steps
     if P > 1:
         ms = kdist.max_over_ranks(ms, dev)
-    launches = sm.launch_times()
-    n_launch = (sm.info()["launches"] - l0) // a.steps
-    fam_ms = {}
-    for fam, lev, t in launches:
-        fam_ms[fam] = fam_ms.get(fam, 0.0) + t / a.steps
-    sm.set_timing(False)
     sm.check()
     value = N / (ms / 1e3)
     rl = roofline(launches, M, p.n, p.m_max, strides, p64, a.config if P == 1 and a.N is None else "")
@@ -267,7 +290,9 @@ def main():
                "hbm_frac": sb / (ms / 1e3) / 1e9 / bw, "fp64_frac": sf / (ms / 1e3) / 1e12 / p64}
 
     e2e = None
+    timing = "CUDA-graph replay of the whole step" if graph is not None else "eager launches"
     if not (a.no_e2e or a.quick):
+        graph = None
         del sm
         torch.cuda.empty_cache()
         s2 = ks.Smoother(local_p, device=dev, host_inputs=True, bind_outputs=False,
@@ -320,6 +345,7 @@ def main():
                            "parallelism": f"time-shard x{P}" if P > 1 else "1 GPU",
                            "l2": "working set (~11 GB at c5) >> 126 MB L2; no flush"},
                 "roofline": rl, "step_roofline": step_rl, "cpu_baseline": cpu, "e2e": e2e,
+                "timing": timing,
                 "gpu_launches": int(n_launch), "clocks": clocks,
                 "phases_ms": fam_ms, "fp64_peak_tflops": p64}
         print(json.dumps(line), flush=True)

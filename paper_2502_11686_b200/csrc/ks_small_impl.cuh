@@ -186,10 +186,17 @@ __device__ __forceinline__ bool rows_full(const double (&R)[Tri<N>::size], doubl
   return f;
 }
 // dispatch: the select-free form when R is full and the row live
+#ifndef KS_ROW_DISPATCH
+#define KS_ROW_DISPATCH 1
+#endif
 template <int N, class Trail>
 __device__ __forceinline__ void rot_row_any(double (&R)[Tri<N>::size], double (&row)[N], double &w, Trail &&trail) {
+#if KS_ROW_DISPATCH
   if (rows_full<N>(R, w)) rot_row<true, N>(R, row, w, trail);
   else rot_row<false, N>(R, row, w, trail);
+#else
+  rot_row<false, N>(R, row, w, trail);   // one body: the branchy rotation only
+#endif
 }
 
 // ---------------------------------------------------------------- factor ---
@@ -239,7 +246,10 @@ template <int N, bool L0, bool CE, bool CC, bool OAOS>
 __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_t t, bool hr, bool hl,
                                                 int64_t pnext, bool zs_in, bool zs_out) {
   using TR = Tri<N>;
-  constexpr int UR = 1;   // row loops stay rolled: the unrolled body thrashes the I-cache
+#ifndef KS_ROW_UNROLL
+#define KS_ROW_UNROLL 1
+#endif
+  constexpr int UR = KS_ROW_UNROLL;   // row loops stay rolled: the unrolled body thrashes the I-cache
   using EN = Ent<N>;
   using RR = Rr<N>;
   const SmallIn &in = a.in;
