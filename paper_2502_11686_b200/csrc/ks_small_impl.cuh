@@ -501,11 +501,11 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
           sto(EN::C + i * N + j, j > i ? w * R3[TR::at(i, j)] : (j == i ? w : 0.0));
         sto(EN::y + i, w * z3[i]);
       }
-    } else {
+    } else {   // (rho, U) in the upper triangle; the lower triangle is never read
 #pragma unroll
       for (int i = 0; i < N; ++i) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) sto(EN::C + i * N + j, j >= i ? R3[TR::at(i, j)] : 0.0);
+        for (int j = i; j < N; ++j) sto(EN::C + i * N + j, R3[TR::at(i, j)]);
         sto(EN::y + i, z3[i]);
       }
     }
