@@ -59,9 +59,12 @@ enum {
     KS_OUTPUTS_BOUND = 2u,/* the caller binds states_out (and cov_out, unless it
                              never calls ks_selinv) in ks_create, so the
                              workspace holds no output buffers                   */
-    KS_GENERIC_PATH = 4u  /* force the CTA-per-pair shared-memory kernels even
+    KS_GENERIC_PATH = 4u, /* force the CTA-per-pair shared-memory kernels even
                              when n, m_max <= 8 (default there: one thread per
                              pair, registers + Givens; used to cross-check)     */
+    KS_NO_FUSED_TAIL = 8u /* small path: launch every factor level separately
+                             instead of running the recursion's tail (levels
+                             with few columns) in one on-chip kernel (cross-check) */
 };
 
 /* One problem (or, multi-GPU, one rank's contiguous shard of steps).
@@ -82,7 +85,7 @@ typedef struct ks_problem {
     const double *K;         /* [N][n][n]      evolution-noise covariance (SPD)     */
     const double *L;         /* [N][m_max][m_max] observation-noise covariance (SPD) */
     int64_t sF, sH, sc, so, sK, sL;   /* per-step strides in doubles, 0 = constant */
-    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH */
+    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL */
 } ks_problem;
 
 #define KS_MAX_N 64

@@ -131,7 +131,7 @@ int validate(const ks_problem *p, const ks_shard *sh) {
   if ((p->sF && p->sF < n * n) || (p->sK && p->sK < n * n) || (p->sH && p->sH < mx * n) ||
       (p->sL && p->sL < mx * mx) || (p->sc && p->sc < n) || (p->so && p->so < mx))
     return KS_ERR_ARG;
-  if (p->flags & ~(uint32_t)(KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH)) return KS_ERR_ARG;
+  if (p->flags & ~(uint32_t)(KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL)) return KS_ERR_ARG;
   if (!use_small(p)) {
     if (factor_smem_bytes(p->n, p->m_max > p->n ? p->m_max : p->n) > 227 * 1024) return KS_ERR_ARG;
     if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
@@ -331,13 +331,39 @@ SmallFactorArgs small_factor_args(ks_ctx *c, size_t i) {
   return a;
 }
 
+// First level run by the fused tail kernel (levels >= 1 with K <= the
+// kernel's shared-memory capacity, single GPU), or Ks.size() for none.
+size_t small_tail_start(const ks_ctx *c) {
+  const std::vector<int64_t> &Ks = c->K_;
+  const int64_t cap = small_tail_max_cols(c->n);
+  if (c->sharded || cap <= 0 || (c->p.flags & KS_NO_FUSED_TAIL)) return Ks.size();
+  for (size_t i = 1; i < Ks.size(); ++i)
+    if (Ks[i] <= cap) return (Ks.size() - i > (size_t)kMaxTailLevels) ? Ks.size() : i;
+  return Ks.size();
+}
+
 int run_small_factor_levels(ks_ctx *c) {
   const int n = c->n;
   const std::vector<int64_t> &Ks = c->K_;
-  for (size_t i = 0; i < Ks.size(); ++i) {
+  const size_t it = small_tail_start(c);
+  for (size_t i = 0; i < it; ++i) {
     SmallFactorArgs a = small_factor_args(c, i);
     Launch l(c, 1, (int)i);
     cudaError_t e = launch_small_factor(a, n, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  if (it < Ks.size()) {
+    SmallTailArgs t;
+    t.base = small_factor_args(c, it);
+    t.ent0 = c->ent[it];
+    t.nlev = (int)(Ks.size() - it);
+    for (int l = 0; l < t.nlev; ++l) {
+      t.K[l] = Ks[it + l];
+      t.level[l] = (int)(it + l);
+      t.rec[l] = small_factor_args(c, it + l).rec;
+    }
+    Launch l(c, 1, (int)it, 1);
+    cudaError_t e = launch_small_factor_tail(t, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
   return KS_OK;

@@ -119,6 +119,16 @@ struct SmallFactorArgs {
   double *zscratch;            // n (n + 1) doubles: the odd level's last-column leftover Z
   int cE, cC, outAoS;          // level 0: constant evolution / observation blocks
 };
+// The fused recursion tail (small path): levels L_t .. top in one CTA.
+constexpr int kMaxTailLevels = 16;
+struct SmallTailArgs {
+  SmallFactorArgs base;        // common fields (status, zscratch, t0 = 0, ...)
+  const double *ent0;          // level-L_t entries (global, pair-interleaved tiles)
+  int nlev;
+  int64_t K[kMaxTailLevels];
+  int level[kMaxTailLevels];
+  TView rec[kMaxTailLevels];
+};
 struct SmallBackwardArgs {
   TView rec;                   // tiled R records
   int64_t K, t0;
@@ -148,6 +158,8 @@ int64_t small_rrec_doubles(int n);                  // 2 n^2 + n + n(n+1)/2
 cudaError_t launch_small_whiten(const SmallWhitenArgs &a, cudaStream_t s, int *nlaunch);
 cudaError_t launch_small_factor(const SmallFactorArgs &a, int n, cudaStream_t s);
 cudaError_t launch_small_backward(const SmallBackwardArgs &a, int n, cudaStream_t s);
+cudaError_t launch_small_factor_tail(const SmallTailArgs &t, int n, cudaStream_t s);
+int small_tail_max_cols(int n);     // levels with K <= this run in the fused tail kernel
 
 // kernel launchers of the CTA path (ks_large.cu); return cudaGetLastError()
 cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s);

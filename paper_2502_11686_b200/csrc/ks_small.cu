@@ -9,6 +9,8 @@ namespace smalld {
 template <int N> cudaError_t factor_n(const SmallFactorArgs &, cudaStream_t);
 template <int N> cudaError_t backward_n(const SmallBackwardArgs &, cudaStream_t);
 template <int N> cudaError_t whiten_n(const SmallWhitenArgs &, cudaStream_t, int *);
+template <int N> cudaError_t factor_tail_n(const SmallTailArgs &, cudaStream_t);
+template <int N> int tail_cols_n();
 }  // namespace smalld
 
 using namespace smalld;
@@ -42,6 +44,21 @@ cudaError_t launch_small_factor(const SmallFactorArgs &a, int n, cudaStream_t s)
 }
 cudaError_t launch_small_backward(const SmallBackwardArgs &a, int n, cudaStream_t s) {
   KS_SMALL_DISPATCH(backward_n, n, a, s)
+}
+cudaError_t launch_small_factor_tail(const SmallTailArgs &t, int n, cudaStream_t s) {
+  KS_SMALL_DISPATCH(factor_tail_n, n, t, s)
+}
+int small_tail_max_cols(int n) {
+#define KS_TAIL_COLS(k) \
+  if (n == k) return tail_cols_n<k>();
+#ifdef KS_SMALL_ONLY6
+  KS_TAIL_COLS(6)
+#else
+  KS_TAIL_COLS(1) KS_TAIL_COLS(2) KS_TAIL_COLS(3) KS_TAIL_COLS(4) KS_TAIL_COLS(5) KS_TAIL_COLS(6) KS_TAIL_COLS(7)
+  KS_TAIL_COLS(8)
+#endif
+#undef KS_TAIL_COLS
+  return 0;
 }
 cudaError_t launch_small_whiten(const SmallWhitenArgs &a, cudaStream_t s, int *nlaunch) {
   KS_SMALL_DISPATCH(whiten_n, a.n, a, s, nlaunch)

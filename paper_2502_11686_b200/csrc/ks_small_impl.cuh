@@ -242,7 +242,7 @@ struct CstOff {
                        size = 2 * N * N + N + kSmallMaxM * N;
 };
 
-template <int N, bool L0, bool CE, bool CC, bool OAOS>
+template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false>
 __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_t t, bool hr, bool hl,
                                                 int64_t pnext, bool zs_in, bool zs_out) {
   using TR = Tri<N>;
@@ -254,6 +254,9 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   using RR = Rr<N>;
   const SmallIn &in = a.in;
   double *zs_ = a.zscratch;
+  // level >= 1 entry element e of column c: read-only global (__ldg), or
+  // shared memory (SIN: the fused tail kernel keeps its levels on chip)
+  auto lde = [&](int64_t c, int e) { return SIN ? cb<64>(in.ent, c)[32 * e] : ldv<64>(in.ent, c, e); };
   // field loads: level 0 per-field views (constant blocks: ES = 1, ts = 0),
   // level >= 1 one tiled entry record view
   constexpr int ESE = CE ? 1 : 64, ESC = CC ? 1 : 64, ESO = OAOS ? 1 : 64;
@@ -262,31 +265,31 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   extern __shared__ double smem_park[];
   const double *cst = smem_park + (size_t)blockDim.x * kParkDoubles<N>;
   auto ldC = [&](int e, int64_t c) {
-    return L0 ? (CC ? cst[CstOff<N>::C + e] : ldv<64>(in.C, c, e)) : ldv<64>(in.ent, c, EN::C + e);
+    return L0 ? (CC ? cst[CstOff<N>::C + e] : ldv<64>(in.C, c, e)) : lde(c, EN::C + e);
   };
-  auto ldY = [&](int e, int64_t c) { return L0 ? ldv<64>(in.y, c, e) : ldv<64>(in.ent, c, EN::y + e); };
+  auto ldY = [&](int e, int64_t c) { return L0 ? ldv<64>(in.y, c, e) : lde(c, EN::y + e); };
   auto ldEl = [&](int e, int64_t c) {
-    return L0 ? (CE ? cst[CstOff<N>::El + e] : ldv<64>(in.El, c, e)) : ldv<64>(in.ent, c, EN::El + e);
+    return L0 ? (CE ? cst[CstOff<N>::El + e] : ldv<64>(in.El, c, e)) : lde(c, EN::El + e);
   };
   auto ldEr = [&](int e, int64_t c) {
-    return L0 ? (CE ? cst[CstOff<N>::Er + e] : ldv<64>(in.Er, c, e)) : ldv<64>(in.ent, c, EN::Er + e);
+    return L0 ? (CE ? cst[CstOff<N>::Er + e] : ldv<64>(in.Er, c, e)) : lde(c, EN::Er + e);
   };
   auto ldE = [&](int e, int64_t c) {
-    return L0 ? (CE ? cst[CstOff<N>::e + e] : ldv<64>(in.e, c, e)) : ldv<64>(in.ent, c, EN::e + e);
+    return L0 ? (CE ? cst[CstOff<N>::e + e] : ldv<64>(in.e, c, e)) : lde(c, EN::e + e);
   };
   auto sto = [&](int e, double v) { stv<ESO>(a.out, pnext, e, v); };
   // prefetch row i of a block field (n elements per row) of column c
   auto pfEl = [&](int i, int64_t c) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      if (!L0) pfv<64>(in.ent, c, EN::El + i * N + j);
+      if (!L0 && !SIN) pfv<64>(in.ent, c, EN::El + i * N + j);
       else if (!CE) pfv<64>(in.El, c, i * N + j);
     }
   };
   auto pfEr = [&](int i, int64_t c) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      if (!L0) pfv<64>(in.ent, c, EN::Er + i * N + j);
+      if (!L0 && !SIN) pfv<64>(in.ent, c, EN::Er + i * N + j);
       else if (!CE) pfv<64>(in.Er, c, i * N + j);
     }
   };
@@ -299,10 +302,10 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // rank reference: |block column of UA|_F (reading R9)
   double ref2, ref2u = 0.0;
   if (!L0) {
-    const double v = ldv<64>(in.ent, t, EN::nrm);
+    const double v = lde(t, EN::nrm);
     ref2 = v * v;
     if (hr) {
-      const double u = ldv<64>(in.ent, t + 1, EN::nrm);
+      const double u = lde(t + 1, EN::nrm);
       ref2u = u * u;
     }
   } else {
@@ -626,7 +629,7 @@ constexpr int factor_min_blocks(int n) { return n <= 4 ? 8 : n == 5 ? 7 : n == 6
 
 // One work item of a factor level: pair p (plus, on an odd level, the last
 // column without right neighbour, handled first by the last pair's thread).
-template <int N, bool L0, bool CE, bool CC, bool OAOS>
+template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false>
 __device__ __forceinline__ void factor_item(const SmallFactorArgs &a, int64_t p) {
   const int64_t K = a.K;
   const bool single_only = (K == 1);
@@ -638,8 +641,8 @@ __device__ __forceinline__ void factor_item(const SmallFactorArgs &a, int64_t p)
   for (int pass = (single_only || triple) ? 0 : 1; pass < (single_only ? 1 : 2); ++pass) {
     const int64_t t = pass == 0 ? K - 1 : 2 * p;
     const bool hl = t + a.t0 > 0;
-    if (pass == 0) small_eliminate<N, L0, CE, CC, OAOS>(a, t, false, hl, 0, false, hl);
-    else small_eliminate<N, L0, CE, CC, OAOS>(a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false);
+    if (pass == 0) small_eliminate<N, L0, CE, CC, OAOS, SIN>(a, t, false, hl, 0, false, hl);
+    else small_eliminate<N, L0, CE, CC, OAOS, SIN>(a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false);
   }
 }
 
@@ -664,6 +667,57 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
   const int64_t npairs = a.K >= 2 ? a.K / 2 : 1;
   if (p >= npairs) return;
   factor_item<N, L0, CE, CC, OAOS>(a, p);
+}
+
+// The recursion's tail: every level from the first one
+// with K <= tail_max_cols<N>() up to the base case in ONE CTA and one launch.
+// The level entries live in shared memory (ping-pong buffers: level L reads
+// one, writes the other, K halves every level), so the tail pays neither a
+// launch nor an L2/DRAM round trip per level -- only the latency of one pair
+// elimination per level.  R records go to HBM as usual (the backward reads
+// them).  Same per-column code (small_eliminate) as the level kernels.
+// shared memory of the tail kernel with first-level width K0 (a multiple of
+// 64): park | const | buffer A (K0 columns) | buffer B (max(64, K0 / 2))
+template <int N>
+__host__ __device__ constexpr size_t tail_smem_doubles(int K0) {
+  return (size_t)64 * kParkDoubles<N> + CstOff<N>::size +
+         (size_t)(K0 + (K0 / 2 > 64 ? K0 / 2 : 64)) * (3 * N * N + 2 * N + 1);
+}
+template <int N>
+__host__ __device__ constexpr int tail_max_cols() {
+  return tail_smem_doubles<N>(128) * 8 <= 227 * 1024 ? 128 : tail_smem_doubles<N>(64) * 8 <= 227 * 1024 ? 64 : 0;
+}
+template <int N>
+__host__ __device__ constexpr size_t tail_smem_bytes() {
+  return tail_max_cols<N>() ? tail_smem_doubles<N>(tail_max_cols<N>()) * sizeof(double) : 0;
+}
+template <int N>
+__global__ void __launch_bounds__(64, 1) small_factor_tail_kernel(SmallTailArgs t) {
+  extern __shared__ double smem_park[];
+  constexpr int64_t E = 3 * N * N + 2 * N + 1;
+  double *bufA = smem_park + (size_t)blockDim.x * kParkDoubles<N> + CstOff<N>::size;
+  const int64_t K0 = t.K[0];
+  double *bufB = bufA + ptiled_doubles(K0, E);
+  {   // level-L_t entries: global (written by the last level kernel) -> buffer A
+    const int64_t cnt = ptiled_doubles(K0, E);
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) bufA[i] = t.ent0[i];
+  }
+  __syncthreads();
+  double *in = bufA, *out = bufB;
+  for (int lv = 0; lv < t.nlev; ++lv) {
+    SmallFactorArgs a = t.base;
+    a.K = t.K[lv];
+    a.level = t.level[lv];
+    a.rec = t.rec[lv];
+    a.in.ent = TView{in, 64 * E};
+    a.out = (lv + 1 < t.nlev) ? TView{out, 64 * E} : TView{nullptr, 0};
+    const int64_t npairs = a.K >= 2 ? a.K / 2 : 1;
+    for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x) factor_item<N, false, false, false, false, true>(a, p);
+    __syncthreads();
+    double *tmp = in;
+    in = out;
+    out = tmp;
+  }
 }
 
 // -------------------------------------------------------------- backward ---
@@ -1158,6 +1212,20 @@ template <int N>
 cudaError_t factor_n(const SmallFactorArgs &a, cudaStream_t s) {
   return a.outAoS ? factor_oaos<N, true>(a, s) : factor_oaos<N, false>(a, s);
 }
+
+template <int N>
+cudaError_t factor_tail_n(const SmallTailArgs &t, cudaStream_t s) {
+  const size_t smem = tail_smem_bytes<N>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(small_factor_tail_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  small_factor_tail_kernel<N><<<1, 64, smem, s>>>(t);
+  return cudaGetLastError();
+}
+template <int N>
+int tail_cols_n() { return tail_max_cols<N>(); }
 
 template <int N>
 cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {

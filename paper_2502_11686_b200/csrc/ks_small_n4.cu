@@ -6,5 +6,7 @@ namespace smalld {
 template cudaError_t factor_n<4>(const SmallFactorArgs &, cudaStream_t);
 template cudaError_t backward_n<4>(const SmallBackwardArgs &, cudaStream_t);
 template cudaError_t whiten_n<4>(const SmallWhitenArgs &, cudaStream_t, int *);
+template cudaError_t factor_tail_n<4>(const SmallTailArgs &, cudaStream_t);
+template int tail_cols_n<4>();
 }  // namespace smalld
 }  // namespace ks

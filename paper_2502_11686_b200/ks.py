@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_HERE, "libks.so")   # KS_LI
 
 KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
     KS_ERR_WORKSPACE = range(8)
-KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH = 1, 2, 4
+KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH, KS_NO_FUSED_TAIL = 1, 2, 4, 8
 FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary", "backward")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
@@ -133,7 +133,7 @@ class Smoother:
 
     def __init__(self, problem, device="cuda", stream: Optional[torch.cuda.Stream] = None,
                  host_inputs: bool = False, bind_outputs: bool = True, cov: bool = True,
-                 shard=None, inputs=None, generic: bool = False):
+                 shard=None, inputs=None, generic: bool = False, fused_tail: bool = True):
         self.L = lib()
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -158,7 +158,7 @@ class Smoother:
         pr.F, pr.H, pr.c, pr.o, pr.K, pr.L = (ptr(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
         pr.sF, pr.sH, pr.sc, pr.so, pr.sK, pr.sL = (_stride(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
         pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0) | \
-            (KS_GENERIC_PATH if generic else 0)
+            (KS_GENERIC_PATH if generic else 0) | (0 if fused_tail else KS_NO_FUSED_TAIL)
         self.problem = pr
         self.shard = None
         if shard is not None:

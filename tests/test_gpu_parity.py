@@ -124,6 +124,24 @@ def test_fused_backward_matches_separate(case, generic):
     assert rel_state_err(x1, xo) <= TOL_X and rel_cov_err(S1, So) <= TOL_S
 
 
+@pytest.mark.parametrize("case", [("c5", 12345), ("c5", 1 << 14), ("c2", 5000), ("c3", 777), ("c1", None),
+                                  ("r1", 300), ("r3", 129), ("r7", 1000), ("r8", 500)])
+def test_fused_tail_matches_level_launches(case):
+    """The recursion tail in one on-chip kernel gives the same bits as one
+    launch per level (KS_NO_FUSED_TAIL)."""
+    name, N = case
+    if name.startswith("r"):
+        n = int(name[1:])
+        rng = np.random.default_rng(7 * n + N)
+        p = gen.random_problem(rng, N, n, m_max=min(n + 1, 8))
+        p.m = np.minimum(p.m, p.m_max)
+    else:
+        p = gen.make(name, N=N)
+    x1, S1, s1 = gpu_smooth(p)
+    x2, S2, _ = gpu_smooth(p, fused_tail=False)
+    assert np.array_equal(x1, x2) and np.array_equal(S1, S2)
+
+
 def test_small_and_generic_paths_agree():
     p = gen.make("c2", N=4097)
     x1, S1, _ = gpu_smooth(p)
