@@ -339,6 +339,31 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   };
 
   // ---- stage 1 base: R = C_t ----
+  // Prefetch into L1 what the stage-1 base and stage 3 read first (their row
+  // loops are rolled, so each row's loads would otherwise wait a full memory
+  // round trip): the observations (and per-step C rows) of both columns at
+  // level 0, C_t / y_t of the entry at level >= 1 (C_{t+1} / y_{t+1}: pass B).
+  if (L0) {
+#pragma unroll 1
+    for (int r = 0; r < in.RC; ++r) {
+      pfv<64>(in.y, t, r);
+      if (hr) pfv<64>(in.y, t + 1, r);
+      if (!CC) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          pfv<64>(in.C, t, r * N + j);
+          if (hr) pfv<64>(in.C, t + 1, r * N + j);
+        }
+      }
+    }
+  } else if (!SIN) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i; j < N; ++j) pfv<64>(in.ent, t, EN::C + i * N + j);
+      pfv<64>(in.ent, t, EN::y + i);
+    }
+  }
   if (hr) {
     pfEl(0, t + 1);
     pfEr(0, t + 1);
@@ -405,6 +430,14 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // operations -- for [El_t | e_t]).
 #pragma unroll
   for (int k = 0; k < TR::size; ++k) park(kRt + k, R[k]);
+  if (!L0 && !SIN && hr) {   // stage 3's base block C_{t+1}, y_{t+1}
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+      for (int j = i; j < N; ++j) pfv<64>(in.ent, t + 1, EN::C + i * N + j);
+      pfv<64>(in.ent, t + 1, EN::y + i);
+    }
+  }
   if (hl) {
 #pragma unroll UR
     for (int i = 0; i < N; ++i) {
