@@ -594,7 +594,7 @@ int ks_whiten(ks_ctx *c) {
     a.Mchol = c->Mchol; a.status = c->status;
     int nl = 0;
     {
-      Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
+      Launch l(c, 0, 0, 1 + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
       e = launch_small_whiten(a, c->stream, &nl);
     }
     if (e != cudaSuccess) return cuda_fail(e);

@@ -1023,8 +1023,7 @@ __device__ __forceinline__ void wst(const TView &v, int cst, int64_t i, int e, d
 // Evolution blocks: K = Lam Lam^T (Cholesky), El = -Lam^{-1}F,
 // Er = Lam^{-1}, e = Lam^{-1} c.  One thread per distinct block.
 template <int N>
-__global__ void __launch_bounds__(128) small_whiten_evo(SmallWhitenArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_t i) {
   if (i >= a.cntE) return;
   const int64_t g = a.first_global + i;
   const bool evo = !((a.cntE != 1 && g == 0) || (a.N == 1 && a.first_global == 0));
@@ -1122,9 +1121,8 @@ __global__ void __launch_bounds__(128) small_whiten_evo(SmallWhitenArgs a) {
 // Observation blocks: L = M M^T; C = M^{-1} H, y = M^{-1} o (rows >= m_i are 0).
 // One thread per distinct block; m_i <= kSmallMaxM.
 template <int N>
-__global__ void __launch_bounds__(128) small_whiten_obs(SmallWhitenArgs a) {
+__device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_t i) {
   constexpr int MM = kSmallMaxM;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.cntC) return;
   const int mx = a.m_max;
   const int mi = a.m ? a.m[i] : mx;
@@ -1189,6 +1187,14 @@ __global__ void __launch_bounds__(128) small_whiten_obs(SmallWhitenArgs a) {
       for (int k = 0; k < MM; ++k)
         if (r < mx && k < mx) a.Mchol[r * mx + k] = (k <= r && r < mi) ? Lm[r][k] : 0.0;
   }
+}
+
+// Evolution and observation blocks in one launch (independent): CTAs
+// [0, gE) whiten the evolution blocks, the rest the observation blocks.
+template <int N>
+__global__ void __launch_bounds__(128) small_whiten_eo(SmallWhitenArgs a, unsigned gE) {
+  if (blockIdx.x < gE) whiten_evo_body<N>(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  else whiten_obs_body<N>(a, (int64_t)(blockIdx.x - gE) * blockDim.x + threadIdx.x);
 }
 
 // Constant observation model: y_i = M^{-1} o_i, one thread per step.
@@ -1277,11 +1283,11 @@ cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
 template <int N>
 cudaError_t whiten_n(const SmallWhitenArgs &a, cudaStream_t s, int *nl) {
   const int T = 128;
-  small_whiten_evo<N><<<(unsigned)((a.cntE + T - 1) / T), T, 0, s>>>(a);
+  const unsigned gE = (unsigned)((a.cntE + T - 1) / T);
+  const unsigned gC = a.m_max > 0 ? (unsigned)((a.cntC + T - 1) / T) : 0u;
+  small_whiten_eo<N><<<gE + gC, T, 0, s>>>(a, gE);
   *nl = 1;
   if (a.m_max > 0) {
-    small_whiten_obs<N><<<(unsigned)((a.cntC + T - 1) / T), T, 0, s>>>(a);
-    *nl += 1;
     if (a.constC) {
       small_whiten_y<N><<<(unsigned)((a.N + 255) / 256), 256, 0, s>>>(a);
       *nl += 1;
