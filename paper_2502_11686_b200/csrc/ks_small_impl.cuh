@@ -23,6 +23,9 @@
 
 #include "ks_internal.cuh"
 
+#ifndef KS_PF_ROWS
+#define KS_PF_ROWS 2   // L1 prefetch distance of the streamed rows
+#endif
 #ifndef KS_F6_BLOCKS
 #define KS_F6_BLOCKS 4
 #endif
@@ -364,11 +367,22 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       pfv<64>(in.ent, t, EN::y + i);
     }
   }
-  if (hr) {
-    pfEl(0, t + 1);
-    pfEr(0, t + 1);
-  } else if (hl) {
-    pfEr(0, t);
+  // row prefetch schedule (distance PD rows): stage 1 streams El/Er/e of
+  // t+1, pass B Er of t, pass A Er/El/e of t.
+  constexpr int PD = KS_PF_ROWS;
+  auto pfE = [&](int i, int64_t c) {
+    if (!L0 && !SIN) pfv<64>(in.ent, c, EN::e + i);
+    else if (L0 && !CE) pfv<64>(in.e, c, i);
+  };
+#pragma unroll
+  for (int i = 0; i < PD; ++i) {
+    if (hr) {
+      pfEl(i, t + 1);
+      pfEr(i, t + 1);
+      pfE(i, t + 1);
+    } else if (hl) {
+      pfEr(i, t);
+    }
   }
   if (!L0) {
 #pragma unroll
@@ -406,11 +420,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         er[j] = ldEr(i * N + j, u);
       }
       double ee = ldE(i, u);
-      if (i + 1 < N) {
-        pfEl(i + 1, u);
-        pfEr(i + 1, u);
+      if (i + PD < N) {
+        pfEl(i + PD, u);
+        pfEr(i + PD, u);
+        pfE(i + PD, u);
       } else if (hl) {
-        pfEr(0, t);
+        pfEr(i + PD - N, t);
       }
       double wl = 1.0;
       rot_row_any<N>(R, el, wl, [&](int k, double yk, double sb) {
@@ -447,8 +462,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         er[j] = ldEr(i * N + j, t);
         xr[j] = 0.0;
       }
-      if (i + 1 < N) pfEr(i + 1, t);
-      else pfEl(0, t);
+      if (i + PD < N) pfEr(i + PD, t);
+      else {
+        pfEr(i + PD - N, t);
+        pfEl(i + PD - N, t);
+        pfE(i + PD - N, t);
+      }
       double wl = 1.0;
       rot_row_any<N>(R, er, wl, [&](int k, double yk, double sb) {
 #pragma unroll
@@ -566,9 +585,10 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         el[j] = ldEl(i * N + j, t);
       }
       double ee = ldE(i, t);
-      if (i + 1 < N) {
-        pfEr(i + 1, t);
-        pfEl(i + 1, t);
+      if (i + PD < N) {
+        pfEr(i + PD, t);
+        pfEl(i + PD, t);
+        pfE(i + PD, t);
       }
       double wl = 1.0;
       rot_row_any<N>(R, er, wl, [&](int k, double yk, double sb) {
