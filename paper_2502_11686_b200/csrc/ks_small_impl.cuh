@@ -1170,6 +1170,9 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
     }
   }
   if (!ok) report(a.status, i, kBadL);
+  double ild[MM];   // reciprocal diagonal (multiplications in the solves below)
+#pragma unroll
+  for (int r = 0; r < MM; ++r) ild[r] = (r < mi) ? 1.0 / Lm[r][r] : 0.0;
   double nc = 0.0;
 #pragma unroll
   for (int c = 0; c <= N; ++c) {          // N columns of H, then o
@@ -1182,7 +1185,7 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
         double s = is_o ? o[r] : H[r * N + c];
 #pragma unroll
         for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
-        x[r] = s / Lm[r][r];
+        x[r] = s * ild[r];
       } else {
         x[r] = 0.0;
       }
@@ -1220,9 +1223,10 @@ __global__ void __launch_bounds__(128) small_whiten_eo(SmallWhitenArgs a, unsign
 // Constant observation model: y_i = M^{-1} o_i, one thread per step.
 template <int DUMMY>
 __global__ void __launch_bounds__(256) small_whiten_y(SmallWhitenArgs a) {
-  __shared__ double M[kSmallMaxM * kSmallMaxM];
+  __shared__ double M[kSmallMaxM * kSmallMaxM], Mi[kSmallMaxM];
   const int mx = a.m_max;
   for (int k = threadIdx.x; k < mx * mx; k += blockDim.x) M[k] = a.Mchol[k];
+  for (int k = threadIdx.x; k < mx; k += blockDim.x) Mi[k] = 1.0 / a.Mchol[k * mx + k];
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N) return;
@@ -1234,7 +1238,7 @@ __global__ void __launch_bounds__(256) small_whiten_y(SmallWhitenArgs a) {
       double s = o[r];
 #pragma unroll
       for (int k = 0; k < r; ++k) s = fma(-M[r * mx + k], y[k], s);
-      y[r] = s / M[r * mx + r];
+      y[r] = s * Mi[r];
       wst(a.y, 0, i, r, y[r]);
     }
   }
