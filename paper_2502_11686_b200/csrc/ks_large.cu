@@ -452,23 +452,62 @@ __device__ void diag_rcp(const double *A, int lda, int n, double *rinv) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) rinv[i] = 1.0 / A[i + i * lda];
 }
 
-// Cholesky (right-looking) of the d x d lower triangle of Lm (ldl) in place;
-// returns false to every thread if a pivot is <= 0 (then continues with 1).
+// Blocked right-looking Cholesky of the d x d lower triangle of Lm (ldl,
+// zero-padded to 8): 8-column panels factored by warp 0 (lanes over rows,
+// pivots and panel rows by shuffles, d <= 64), the trailing update
+// A22 -= L21 L21^T as a DMMA GEMM.  Returns (to warp 0) false if a pivot is
+// <= 0 (then continues with 1).  Ends with __syncthreads.
 __device__ bool cta_chol(double *Lm, int ldl, int d, double *sh) {
-  const int tid = threadIdx.x, NT = blockDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bool ok = true;
-  for (int j = 0; j < d; ++j) {
-    const double v = Lm[j + j * ldl];
-    ok &= v > 0.0;
-    const double ljj = sqrt(v > 0.0 ? v : 1.0), il = 1.0 / ljj;
-    __syncthreads();                          // every thread has read the pivot
-    for (int i = j + 1 + tid; i < d; i += NT) Lm[i + j * ldl] *= il;
-    if (tid == 0) Lm[j + j * ldl] = ljj;
+  for (int k0 = 0; k0 < d; k0 += 8) {
+    const int nb = (d - k0 < 8) ? d - k0 : 8;
+    if (warp == 0) {
+      double a[2][8];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int r = k0 + lane + 32 * s;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) a[s][c] = (r < d && c < nb) ? Lm[r + (k0 + c) * ldl] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < nb) {
+          const double v = __shfl_sync(0xffffffffu, a[0][c], c);
+          ok &= v > 0.0;
+          const double l = sqrt(v > 0.0 ? v : 1.0), il = 1.0 / l;
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const int r = k0 + lane + 32 * s;
+            if (r == k0 + c) a[s][c] = l;
+            else if (r > k0 + c) a[s][c] *= il;
+          }
+#pragma unroll
+          for (int cc = c + 1; cc < 8; ++cc) {
+            const double lcc = __shfl_sync(0xffffffffu, a[0][c], cc);   // L[k0+cc][k0+c]
+            if (cc < nb) {
+#pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                const int r = k0 + lane + 32 * s;
+                if (r >= k0 + cc) a[s][cc] = fma(-a[s][c], lcc, a[s][cc]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int r = k0 + lane + 32 * s;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (r < d && c < nb && r >= k0 + c) Lm[r + (k0 + c) * ldl] = a[s][c];
+      }
+    }
     __syncthreads();
-    const int m = d - j - 1;
-    for (int idx = tid; idx < m * m; idx += NT) {
-      const int i = j + 1 + idx % m, k = j + 1 + idx / m;
-      if (k <= i) Lm[i + k * ldl] = fma(-Lm[i + j * ldl], Lm[k + j * ldl], Lm[i + k * ldl]);
+    const int rest = pad8(d) - k0 - 8;
+    if (rest > 0) {
+      const double *L21 = Lm + (k0 + 8) + k0 * ldl;
+      gemm<false, true>(rest, rest, 8, -1.0, L21, ldl, L21, ldl, 1.0, Lm + (k0 + 8) + (k0 + 8) * ldl, ldl);
     }
     __syncthreads();
   }
