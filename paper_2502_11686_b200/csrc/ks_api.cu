@@ -391,7 +391,27 @@ SmallBackwardArgs small_backward_args(ks_ctx *c, int i, int do_state, int do_cov
 int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
   const int n = c->n;
   const std::vector<int64_t> &Ks = c->K_;
-  for (int i = (int)Ks.size() - 1; i >= 0; --i) {
+  const int it = (int)small_tail_start(c);   // the levels the fused factor tail ran
+  int top = (int)Ks.size() - 1;
+  if (it < (int)Ks.size()) {
+    SmallBwdTailArgs t;
+    t.base = small_backward_args(c, top, do_state, do_cov);
+    t.nlev = 0;
+    for (int i = top; i >= it; --i) {
+      const SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
+      t.K[t.nlev] = a.K;
+      t.shift[t.nlev] = a.shift;
+      t.rec[t.nlev] = a.rec;
+      t.Xup[t.nlev] = a.Xup;
+      t.Xcur[t.nlev] = a.Xcur;
+      ++t.nlev;
+    }
+    Launch l(c, do_cov ? (do_state ? 5 : 3) : 2, it);
+    cudaError_t e = launch_small_backward_tail(t, n, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+    top = it - 1;
+  }
+  for (int i = top; i >= 0; --i) {
     SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
     Launch l(c, do_cov ? (do_state ? 5 : 3) : 2, i);
     cudaError_t e = launch_small_backward(a, n, c->stream);

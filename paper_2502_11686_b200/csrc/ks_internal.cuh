@@ -139,6 +139,14 @@ struct SmallBackwardArgs {
   TView Xcur;                  // tiled level-L cross blocks to write (p null: skip)
   int do_state, do_cov;
 };
+// The backward of the fused tail: levels top .. L_t in one CTA (top first).
+struct SmallBwdTailArgs {
+  SmallBackwardArgs base;      // common fields (x, S, do_state, do_cov, t0 = 0, ...)
+  int nlev;
+  int64_t K[kMaxTailLevels];
+  int shift[kMaxTailLevels];
+  TView rec[kMaxTailLevels], Xup[kMaxTailLevels], Xcur[kMaxTailLevels];
+};
 struct SmallWhitenArgs {
   int64_t N;
   int n, m_max;
@@ -159,6 +167,7 @@ cudaError_t launch_small_whiten(const SmallWhitenArgs &a, cudaStream_t s, int *n
 cudaError_t launch_small_factor(const SmallFactorArgs &a, int n, cudaStream_t s);
 cudaError_t launch_small_backward(const SmallBackwardArgs &a, int n, cudaStream_t s);
 cudaError_t launch_small_factor_tail(const SmallTailArgs &t, int n, cudaStream_t s);
+cudaError_t launch_small_backward_tail(const SmallBwdTailArgs &t, int n, cudaStream_t s);
 int small_tail_max_cols(int n);     // levels with K <= this run in the fused tail kernel
 
 // kernel launchers of the CTA path (ks_large.cu); return cudaGetLastError()

@@ -11,6 +11,7 @@ template <int N> cudaError_t backward_n(const SmallBackwardArgs &, cudaStream_t)
 template <int N> cudaError_t whiten_n(const SmallWhitenArgs &, cudaStream_t, int *);
 template <int N> cudaError_t factor_tail_n(const SmallTailArgs &, cudaStream_t);
 template <int N> int tail_cols_n();
+template <int N> cudaError_t backward_tail_n(const SmallBwdTailArgs &, cudaStream_t);
 }  // namespace smalld
 
 using namespace smalld;
@@ -47,6 +48,9 @@ cudaError_t launch_small_backward(const SmallBackwardArgs &a, int n, cudaStream_
 }
 cudaError_t launch_small_factor_tail(const SmallTailArgs &t, int n, cudaStream_t s) {
   KS_SMALL_DISPATCH(factor_tail_n, n, t, s)
+}
+cudaError_t launch_small_backward_tail(const SmallBwdTailArgs &t, int n, cudaStream_t s) {
+  KS_SMALL_DISPATCH(backward_tail_n, n, t, s)
 }
 int small_tail_max_cols(int n) {
 #define KS_TAIL_COLS(k) \

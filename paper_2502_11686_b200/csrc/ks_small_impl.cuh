@@ -845,15 +845,22 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
       : "memory");
 }
 
-template <int N>
-__global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backward_kernel(SmallBackwardArgs a) {
+// One tile of eliminated columns (32 columns, 64 threads: see the kernel
+// below).  TAIL: called once per level by the fused backward tail kernel --
+// the mbarrier is initialised by the caller and reused (phase bit), S_tt goes
+// out with plain stores (the next level of the same kernel reads it), and a
+// tile index beyond the level only takes part in the CTA barriers.
+template <int N, bool TAIL>
+__device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t tile, int tid, double *bsm,
+                                         unsigned long long *mbarp, unsigned phase) {
   using TR = Tri<N>;
   using RR = Rr<N>;
   constexpr int NN = N * N, BC = kBwdCols, NB = BC + 1, RS = rs_doubles<N>(), SP = bwd_sp<N>(),
                 NT = N * (N + 1) / 2;
-  const int tid = threadIdx.x, col = tid & (BC - 1);
+  const int col = tid & (BC - 1);
   const bool right = tid >= BC;      // warp-uniform
-  const int64_t b0 = (int64_t)blockIdx.x * BC, b = b0 + col, t = 2 * b;
+  const int64_t b0 = tile * BC, b = b0 + col, t = 2 * b;
+  const bool tile_live = b0 < (a.K + 1) / 2;
   const bool active = t < a.K;
   const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
   const int64_t step = 1ll << a.shift;
@@ -895,14 +902,12 @@ __global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backwar
   //   right: S_tr = -(T_l S_lr + T_r S_rr),    Q_r = S_tr T_r^T
   // and S_tt = P + Q_l + Q_r (upper triangle, mirrored) goes back through
   // shared memory as one bulk store per column.
-  extern __shared__ __align__(16) double bsm[];
-  __shared__ __align__(8) unsigned long long mbar;
   double *REC = bsm;                 // [RS][32]
   double *Snb = bsm + BC * RS;       // [NN][NB]   (later: Q_l, Q_r [2][NT][NB] | S_tt [BC][SP])
-  if (tid == 0) {
-    mbar_init(&mbar, 1);
-    mbar_expect_tx(&mbar, (unsigned)(RS * 32 * 8));
-    bulk_g2s(REC, a.rec.p + blockIdx.x * a.rec.ts, (unsigned)(RS * 32 * 8), &mbar);
+  if (tid == 0 && tile_live) {
+    if (!TAIL) mbar_init(mbarp, 1);
+    mbar_expect_tx(mbarp, (unsigned)(RS * 32 * 8));
+    bulk_g2s(REC, a.rec.p + tile * a.rec.ts, (unsigned)(RS * 32 * 8), mbarp);
   }
   const int64_t Kup = a.K / 2;       // columns of level L+1
   {
@@ -929,7 +934,7 @@ __global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backwar
     for (int c = 0; c < N; ++c) Slr[r][c] = (active && hl && hr) ? ldv<32>(a.Xup, b, r * N + c) : 0.0;
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();                   // mbarrier init visible; neighbour blocks landed
-  mbar_wait(&mbar, 0);
+  if (tile_live) mbar_wait(mbarp, phase);
   const double *myrec = REC + col;
   auto rec = [&](int e) { return myrec[e * 32]; };
   if (active && a.do_state && !right) {
@@ -1018,16 +1023,53 @@ __global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backwar
         Stt[i * N + jj] = sv;
         Stt[jj * N + i] = sv;
       }
-    if constexpr (NN % 2 == 0) {   // 16-byte multiple and alignment: one bulk store
+    if constexpr (TAIL || NN % 2 != 0) {
+#pragma unroll
+      for (int e = 0; e < NN; ++e) a.S[j * NN + e] = Stt[e];
+    } else {   // 16-byte multiple and alignment: one bulk store
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a.S + j * NN),
                    "r"(smem_u32(Stt)), "r"((unsigned)(NN * 8))
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    } else {
-#pragma unroll
-      for (int e = 0; e < NN; ++e) a.S[j * NN + e] = Stt[e];
+    }
+  }
+}
+
+
+template <int N>
+__global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N)) small_backward_kernel(SmallBackwardArgs a) {
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ __align__(8) unsigned long long mbar;
+  bwd_tile<N, false>(a, blockIdx.x, threadIdx.x, bsm, &mbar, 0);
+}
+
+// The backward of the recursion's tail (the levels the fused factor tail ran)
+// in one CTA and one launch, top level first: two tiles (4 warps) per round,
+// a CTA barrier between levels (each level reads what the one above wrote).
+template <int N>
+__global__ void __launch_bounds__(4 * kBwdCols, 1) small_backward_tail_kernel(SmallBwdTailArgs t) {
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int half = threadIdx.x / (2 * kBwdCols), tid = threadIdx.x % (2 * kBwdCols);
+  double *my = bsm + half * bwd_smem_doubles<N>();
+  if (tid == 0) mbar_init(&mbar[half], 1);
+  __syncthreads();
+  unsigned phase = 0;
+  for (int lv = 0; lv < t.nlev; ++lv) {
+    SmallBackwardArgs a = t.base;
+    a.rec = t.rec[lv];
+    a.K = t.K[lv];
+    a.shift = t.shift[lv];
+    a.Xup = t.Xup[lv];
+    a.Xcur = t.Xcur[lv];
+    const int64_t ntile = ((a.K + 1) / 2 + kBwdCols - 1) / kBwdCols;
+    for (int64_t r = 0; 2 * r < ntile; ++r) {
+      const int64_t tile = 2 * r + half;
+      bwd_tile<N, true>(a, tile, tid, my, &mbar[half], phase);
+      if (tile < ntile) phase ^= 1u;
+      __syncthreads();
     }
   }
 }
@@ -1301,6 +1343,18 @@ cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
     attr = true;
   }
   small_backward_kernel<N><<<(unsigned)((nc + kBwdCols - 1) / kBwdCols), 2 * kBwdCols, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t backward_tail_n(const SmallBwdTailArgs &t, cudaStream_t s) {
+  const size_t smem = 2 * bwd_smem_doubles<N>() * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(small_backward_tail_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  small_backward_tail_kernel<N><<<1, 4 * kBwdCols, smem, s>>>(t);
   return cudaGetLastError();
 }
 

@@ -8,5 +8,6 @@ template cudaError_t backward_n<3>(const SmallBackwardArgs &, cudaStream_t);
 template cudaError_t whiten_n<3>(const SmallWhitenArgs &, cudaStream_t, int *);
 template cudaError_t factor_tail_n<3>(const SmallTailArgs &, cudaStream_t);
 template int tail_cols_n<3>();
+template cudaError_t backward_tail_n<3>(const SmallBwdTailArgs &, cudaStream_t);
 }  // namespace smalld
 }  // namespace ks
