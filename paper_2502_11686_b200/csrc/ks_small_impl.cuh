@@ -104,53 +104,33 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // Square-root-free Givens rotations (Gentleman, 1973), in inverse-weight
 // form.  Every row of the triangular factor is kept as
 // R_k = sqrt(d_k) [1, u_{k,k+1}, ..., | trailing columns] and stored through
-// rho_k = 1/d_k (+inf: row k still empty); every streamed row as
-// sqrt(delta) [y_k, y_{k+1}, ...], stored through w = 1/delta (+inf: the row
-// has been absorbed).  Zeroing y_k against row k is the plane rotation with
-// c = sqrt(d/d'), s = sqrt(delta) y_k / sqrt(d') (the same orthogonal Q as
-// the classical Givens / Householder QR of P:424-436, up to row signs:
-// R_kk = +sqrt(d_k)).  With d' = d + delta y_k^2:
+// rho_k = 1/d_k; every streamed row as sqrt(delta) [y_k, y_{k+1}, ...],
+// stored through w = 1/delta.  Zeroing y_k against row k is the plane
+// rotation with c = sqrt(d/d'), s = sqrt(delta) y_k / sqrt(d') (the same
+// orthogonal Q as the classical Givens / Householder QR of P:424-436, up to
+// row signs: R_kk = +sqrt(d_k)).  With d' = d + delta y_k^2:
 //     w'   = w + y_k^2 rho                 (= 1/delta', delta' = delta d/d')
 //     rho' = rho w / w',   sbar = y_k rho / w'   (= delta y_k / d')
 //     y_j' = y_j - y_k u_j,  u_j' = u_j + sbar y_j'      (every column j > k)
 // TWO fma per element and pair instead of four, one reciprocal per rotation,
 // and -- the point of the inverse-weight form -- the serial dependence from
 // one pivot to the next is a single fma (w') instead of a reciprocal (square
-// root) chain: the reciprocals of consecutive pivots overlap.  An empty row
-// absorbs the streamed row (rho' = w / y_k^2, sbar = 1/y_k, w' = inf); y_k = 0
-// or an absorbed row is the identity, so zero padding rows are exact no-ops.
-// The selects keep ragged rows from diverging.
+// root) chain: the reciprocals of consecutive pivots overlap.
+//
+// Empty rows.  A row of R that has received no data yet (level 0: R starts
+// empty; m_i < n leaves rows empty after the observation rows) has
+// rho = kEmptyRow, a huge FINITE value (d = 2^-600 ~ 2.4e-181, an initial row
+// weight far below any data), so absorbing a streamed row into it is the same
+// select-free rotation: with y_k != 0, sbar = (1/y_k)(1 - eps),
+// rho' = (w/y_k^2)(1 - eps), w' ~ 2^600 y_k^2 (the streamed row is consumed:
+// later rotations of it are the identity to eps), eps = w / (y_k^2 rho)
+// < 1e-100 for every |y_k| >= 1e-40.  y_k = 0 (zero padding rows) leaves the
+// row unchanged up to an ulp of rho.  Rows still empty at the end (rank
+// deficiency) keep rho ~ 2^600 and fail the rank test.  One branch-free form
+// for every rotation: no guards, one code path (half the code of a guarded
+// version, and the compiler interleaves consecutive pivots).
+constexpr double kEmptyRow = 0x1p600;
 __device__ __forceinline__ void gmake(double &rho, double yk, double &w, double &sb) {
-  const bool empty = !(rho < __longlong_as_double(0x7ff0000000000000ll));
-  const bool ident = (yk == 0.0) || !(w < __longlong_as_double(0x7ff0000000000000ll));
-  if (!(empty || ident)) {   // the common case: select-free
-    const double yr = yk * rho;
-    const double wn = fma(yk, yr, w);
-    const double q = rcp_nr(wn);
-    sb = yr * q;
-    rho = rho * (w * q);
-    w = wn;
-  } else if (ident) {
-    sb = 0.0;
-  } else {                   // an empty row absorbs the streamed row
-    const double q = rcp_nr(yk);
-    sb = q;
-    rho = (w * q) * q;
-    w = __longlong_as_double(0x7ff0000000000000ll);
-  }
-}
-constexpr double kEmptyRow = __builtin_huge_val();   // rho of an empty row of R (w of an absorbed row)
-// sqrt(delta) = 1/sqrt(w) of a streamed row (0 once absorbed).
-__device__ __forceinline__ double wscale(double w) {
-  const bool fin = w < __longlong_as_double(0x7ff0000000000000ll);
-  const double r = rsqrt_nr(fin ? w : 1.0);
-  return fin ? r : 0.0;
-}
-// The same rotation when row k of R is not empty and the streamed row is
-// not absorbed (rho, w finite): no selects.  y_k = 0 changes rho by at most
-// an ulp (rho w / w).  Once every row of R is non-empty it stays so, so the
-// row loops switch to this form after a per-row check (rows_full).
-__device__ __forceinline__ void gmake_fast(double &rho, double yk, double &w, double &sb) {
   const double yr = yk * rho;
   const double wn = fma(yk, yr, w);
   const double q = rcp_nr(wn);
@@ -158,6 +138,8 @@ __device__ __forceinline__ void gmake_fast(double &rho, double yk, double &w, do
   rho = rho * (w * q);
   w = wn;
 }
+// sqrt(delta) = 1/sqrt(w) of a streamed row.
+__device__ __forceinline__ double wscale(double w) { return rsqrt_nr(w); }
 // Apply to one column: u (row of R) and y (streamed row), yk the pivot value
 // of the streamed row before the rotation.
 __device__ __forceinline__ void gapp(double &u, double &y, double yk, double sb) {
@@ -167,39 +149,18 @@ __device__ __forceinline__ void gapp(double &u, double &y, double yk, double sb)
 
 // Rotate one streamed row into R (row streaming): pivot part
 // row[0..N), weight w; trail(k, y_k, sbar) applies rotation k to the row's
-// trailing columns.  FAST: every row of R non-empty and the row not absorbed.
-template <bool FAST, int N, class Trail>
+// trailing columns.
+template <int N, class Trail>
 __device__ __forceinline__ void rot_row(double (&R)[Tri<N>::size], double (&row)[N], double &w, Trail &&trail) {
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     double sb;
     const double yk = row[k];
-    if (FAST) gmake_fast(R[Tri<N>::at(k, k)], yk, w, sb);
-    else gmake(R[Tri<N>::at(k, k)], yk, w, sb);
+    gmake(R[Tri<N>::at(k, k)], yk, w, sb);
 #pragma unroll
     for (int j = k + 1; j < N; ++j) gapp(R[Tri<N>::at(k, j)], row[j], yk, sb);
     trail(k, yk, sb);
   }
-}
-template <int N>
-__device__ __forceinline__ bool rows_full(const double (&R)[Tri<N>::size], double w) {
-  bool f = w < kEmptyRow;
-#pragma unroll
-  for (int k = 0; k < N; ++k) f &= R[Tri<N>::at(k, k)] < kEmptyRow;
-  return f;
-}
-// dispatch: the select-free form when R is full and the row live
-#ifndef KS_ROW_DISPATCH
-#define KS_ROW_DISPATCH 1
-#endif
-template <int N, class Trail>
-__device__ __forceinline__ void rot_row_any(double (&R)[Tri<N>::size], double (&row)[N], double &w, Trail &&trail) {
-#if KS_ROW_DISPATCH
-  if (rows_full<N>(R, w)) rot_row<true, N>(R, row, w, trail);
-  else rot_row<false, N>(R, row, w, trail);
-#else
-  rot_row<false, N>(R, row, w, trail);   // one body: the branchy rotation only
-#endif
 }
 
 // ---------------------------------------------------------------- factor ---
@@ -338,7 +299,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 
   // stream one weighted row [row (pivot part, N) | rhs] into (Rm, zm)
   auto stream_row = [&](double(&Rm)[TR::size], double(&zm)[N], double(&row)[N], double &rhs, double wl) {
-    rot_row_any<N>(Rm, row, wl, [&](int k, double yk, double sb) { gapp(zm[k], rhs, yk, sb); });
+    rot_row<N>(Rm, row, wl, [&](int k, double yk, double sb) { gapp(zm[k], rhs, yk, sb); });
   };
 
   // ---- stage 1 base: R = C_t ----
@@ -428,7 +389,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         pfEr(i + PD - N, t);
       }
       double wl = 1.0;
-      rot_row_any<N>(R, el, wl, [&](int k, double yk, double sb) {
+      rot_row<N>(R, el, wl, [&](int k, double yk, double sb) {
 #pragma unroll
         for (int j = 0; j < N; ++j) gapp(X[k][j], er[j], yk, sb);
         gapp(z[k], ee, yk, sb);
@@ -469,7 +430,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         pfE(i + PD - N, t);
       }
       double wl = 1.0;
-      rot_row_any<N>(R, er, wl, [&](int k, double yk, double sb) {
+      rot_row<N>(R, er, wl, [&](int k, double yk, double sb) {
 #pragma unroll
         for (int j = 0; j < N; ++j) gapp(X[k][j], xr[j], yk, sb);
       });
@@ -591,7 +552,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         pfE(i + PD, t);
       }
       double wl = 1.0;
-      rot_row_any<N>(R, er, wl, [&](int k, double yk, double sb) {
+      rot_row<N>(R, er, wl, [&](int k, double yk, double sb) {
 #pragma unroll
         for (int j = 0; j < N; ++j) gapp(Rl[k][j], el[j], yk, sb);
         gapp(z[k], ee, yk, sb);
