@@ -77,7 +77,7 @@ struct ks_ctx {
   // level 0 (whitened)
   unsigned long long *status = nullptr;
   double *C0 = nullptr, *y0 = nullptr, *El0 = nullptr, *Er0 = nullptr, *e0 = nullptr,
-         *Mchol = nullptr;
+         *Mchol = nullptr, *Minv = nullptr;
   int64_t cntE = 1, cntC = 1;
   // local levels 0..nlev-1 (sharded: 0..q-1)
   std::vector<int64_t> K_;
@@ -192,6 +192,7 @@ size_t carve(ks_ctx *c, char *base) {
     c->zscratch = w.take<double>(nn + n);
   }
   c->Mchol = w.take<double>((size_t)mx * mx + 1);
+  c->Minv = w.take<double>((size_t)mx * mx + 1);
   // local levels
   c->K_.clear(); c->ent.clear(); c->rrec.clear(); c->X.clear();
   int64_t K = N;
@@ -288,6 +289,12 @@ EntryView aos_view(const double *ent, int n) {
 // ---- small-path views (tiled, 32 columns per tile; see TView) ----
 TView tv(const double *p, int64_t ts) { return TView{const_cast<double *>(p), ts}; }
 
+// Constant observation model on the small path: the level-0 factor computes
+// y = M^{-1} o itself (no y pass over HBM).
+int small_yfuse(const ks_ctx *c) {
+  return (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr) ? 1 : 0;
+}
+
 SmallIn small_level0(const ks_ctx *c) {
   const int n = c->n, mx = c->mx;
   const int64_t nn = (int64_t)n * n;
@@ -303,6 +310,10 @@ SmallIn small_level0(const ks_ctx *c) {
   v.nEl = tv(c->nEl0, cE ? 0 : 64);
   v.RC = mx;
   v.ent = tv(nullptr, 0);
+  v.yfuse = small_yfuse(c);
+  v.o = c->o;
+  v.so = c->p.so;
+  v.Minv = c->Minv;
   return v;
 }
 
@@ -612,9 +623,10 @@ int ks_whiten(ks_ctx *c) {
     a.cE = c->cntE == 1;
     a.cC = c->cntC == 1;
     a.Mchol = c->Mchol; a.status = c->status;
+    a.Minv = small_yfuse(c) ? c->Minv : nullptr;
     int nl = 0;
     {
-      Launch l(c, 0, 0, 1 + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
+      Launch l(c, 0, 0, 1);
       e = launch_small_whiten(a, c->stream, &nl);
     }
     if (e != cudaSuccess) return cuda_fail(e);

@@ -105,6 +105,11 @@ struct SmallIn {               // level-L columns
   TView C, y, El, Er, e;
   TView nC, nEr, nEl;          // |C_j|^2, |Er_j|^2, |El_j|^2 (rank reference)
   int RC;
+  // constant observation model: y = M^{-1} o computed by the level-0 factor
+  // (yfuse = 1; Minv [RC][RC] lower triangular, o with stride so), else y
+  int yfuse;
+  const double *o, *Minv;
+  int64_t so;
   // level >= 1: pair-interleaved tiled entry records [C (n x n, upper tri) | y | El | Er | e | nrm]
   TView ent;
 };
@@ -159,6 +164,7 @@ struct SmallWhitenArgs {
   TView C, y, El, Er, e, nC, nEr, nEl;   // tiled per step, or ES = 1 / ts = 0 when constant
   int cE, cC;                  // layout flags of the above (1 = constant block)
   double *Mchol;               // m_max^2 scratch (constant observation model)
+  double *Minv;                // m_max^2: M^{-1} for the factor's fused y (null: small_whiten_y)
   unsigned long long *status;
 };
 size_t small_entry_doubles(int n);                  // = entry_doubles(n)

@@ -69,6 +69,9 @@ __device__ __forceinline__ void pfv(const TView &v, int64_t t, int e) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(cb<ES>(v, t) + est<ES>() * e));
 }
 
+// L1 prefetch of the 128-byte line holding p
+__device__ __forceinline__ void pf_line(const double *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ void report(unsigned long long *st, int64_t step, int kind) {
   if (st) atomicMin(st, ((unsigned long long)(step + 1) << 8) | (unsigned long long)kind);
 }
@@ -203,7 +206,8 @@ constexpr int kParkDoubles = N * (N + 2) + N * (N + 1) / 2;
 template <int N>
 struct CstOff {
   static constexpr int El = 0, Er = N * N, e = 2 * N * N, C = 2 * N * N + N,
-                       size = 2 * N * N + N + kSmallMaxM * N;
+                       Mi = 2 * N * N + N + kSmallMaxM * N,   // M^{-1} (constant observation model)
+      size = 2 * N * N + N + kSmallMaxM * N + kSmallMaxM * kSmallMaxM;
 };
 
 template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false>
@@ -231,7 +235,20 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   auto ldC = [&](int e, int64_t c) {
     return L0 ? (CC ? cst[CstOff<N>::C + e] : ldv<64>(in.C, c, e)) : lde(c, EN::C + e);
   };
-  auto ldY = [&](int e, int64_t c) { return L0 ? ldv<64>(in.y, c, e) : lde(c, EN::y + e); };
+  // level-0 observations: y = M^{-1} o computed here for a
+  // constant observation model (M^{-1} staged in shared memory), else the
+  // whitened y of ks_whiten
+  auto ldY = [&](int e, int64_t c) {
+    if (!L0) return lde(c, EN::y + e);
+    if (CC && in.yfuse) {
+      const double *oc = in.o + c * in.so;
+      double yv = 0.0;
+#pragma unroll 1
+      for (int k = 0; k <= e; ++k) yv = fma(cst[CstOff<N>::Mi + e * kSmallMaxM + k], __ldg(oc + k), yv);
+      return yv;
+    }
+    return ldv<64>(in.y, c, e);
+  };
   auto ldEl = [&](int e, int64_t c) {
     return L0 ? (CE ? cst[CstOff<N>::El + e] : ldv<64>(in.El, c, e)) : lde(c, EN::El + e);
   };
@@ -308,10 +325,16 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // round trip): the observations (and per-step C rows) of both columns at
   // level 0, C_t / y_t of the entry at level >= 1 (C_{t+1} / y_{t+1}: pass B).
   if (L0) {
+    if (CC && in.yfuse) {
+      pf_line(in.o + t * in.so);
+      if (hr) pf_line(in.o + (t + 1) * in.so);
+    }
 #pragma unroll 1
     for (int r = 0; r < in.RC; ++r) {
-      pfv<64>(in.y, t, r);
-      if (hr) pfv<64>(in.y, t + 1, r);
+      if (!(CC && in.yfuse)) {
+        pfv<64>(in.y, t, r);
+        if (hr) pfv<64>(in.y, t + 1, r);
+      }
       if (!CC) {
 #pragma unroll
         for (int j = 0; j < N; ++j) {
@@ -672,6 +695,9 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
                                                               : a.in.e.p[k - CstOff<N>::e];
       } else if (CC && k >= CstOff<N>::C && k - CstOff<N>::C < a.in.RC * N) {
         v = a.in.C.p[k - CstOff<N>::C];
+      } else if (CC && a.in.yfuse && k >= CstOff<N>::Mi) {
+        const int r = (k - CstOff<N>::Mi) / kSmallMaxM, q = (k - CstOff<N>::Mi) % kSmallMaxM;
+        v = (r < a.in.RC && q < a.in.RC) ? a.in.Minv[r * a.in.RC + q] : 0.0;
       }
       cst[k] = v;
     }
@@ -1212,6 +1238,22 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
 #pragma unroll
       for (int k = 0; k < MM; ++k)
         if (r < mx && k < mx) a.Mchol[r * mx + k] = (k <= r && r < mi) ? Lm[r][k] : 0.0;
+    if (a.Minv) {   // M^{-1} (lower triangular) for the factor's fused y = M^{-1} o
+#pragma unroll
+      for (int c = 0; c < MM; ++c) {
+        double x[MM];
+#pragma unroll
+        for (int r = 0; r < MM; ++r) {
+          double sv = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+          for (int k = 0; k < r; ++k) sv = fma(-Lm[r][k], x[k], sv);
+          x[r] = (r < mi && r >= c) ? sv * ild[r] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < MM; ++r)
+          if (r < mx && c < mx) a.Minv[r * mx + c] = x[r];
+      }
+    }
   }
 }
 
@@ -1327,7 +1369,7 @@ cudaError_t whiten_n(const SmallWhitenArgs &a, cudaStream_t s, int *nl) {
   small_whiten_eo<N><<<gE + gC, T, 0, s>>>(a, gE);
   *nl = 1;
   if (a.m_max > 0) {
-    if (a.constC) {
+    if (a.constC && !a.Minv) {   // (with Minv the factor computes y = M^{-1} o itself)
       small_whiten_y<N><<<(unsigned)((a.N + 255) / 256), 256, 0, s>>>(a);
       *nl += 1;
     }

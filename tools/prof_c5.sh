@@ -1,7 +1,7 @@
 # ncu --set full of selected launches of a c5 run (see tools/prof_run.py):
 #   prof_c5.sh SKIP COUNT NAME  (launch indices among small_factor|small_backward kernels;
-#   after 2 warm-up runs of c5: factor L0 = 78, L1 = 79, ... (15 level launches + the fused
-#   tail), backward L22..L0 = 94..116)
+#   after 2 warm-up runs of c5 (32 matching launches per run): factor L0 = 64, L1 = 65, ...,
+#   factor tail 79, backward tail 80, backward L14..L0 = 81..95)
 set -x
 python tools/prof_run.py c5 > gpurun_out/plain.log 2>&1 || exit 1
 K='regex:small_factor|small_backward'
