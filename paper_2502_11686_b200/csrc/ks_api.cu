@@ -339,6 +339,7 @@ SmallFactorArgs small_factor_args(ks_ctx *c, size_t i) {
   a.zscratch = c->zscratch;
   a.cE = c->cntE == 1;
   a.cC = c->cntC == 1;
+  a.ent_off = a.out_off = 0;
   return a;
 }
 
@@ -353,26 +354,59 @@ size_t small_tail_start(const ks_ctx *c) {
   return Ks.size();
 }
 
+// Subtree pass (levels [is, is + kSubLevels)): the first level ≥ 1 below the
+// tail whose K is a multiple of the subtree width with at most one subtree
+// per SM (the subtree kernel needs most of an SM's shared memory), single
+// GPU; returns Ks.size() for none.
+constexpr int kSubLevels = 7;   // subtree width 2^7 = 128 columns (tail_max_cols)
+size_t small_subtree_start(const ks_ctx *c) {
+  const std::vector<int64_t> &Ks = c->K_;
+  const size_t it = small_tail_start(c);
+  const int64_t W = 1ll << kSubLevels;
+  if (it >= Ks.size() || small_tail_max_cols(c->n) < W) return Ks.size();
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (size_t i = 1; i + kSubLevels <= it; ++i)
+    if (Ks[i] % W == 0 && Ks[i] / W <= sms) return i;   // one wave (one subtree per SM)
+  return Ks.size();
+}
+
+SmallTailArgs small_tail_args(ks_ctx *c, size_t i0, int nlev, int64_t W) {
+  SmallTailArgs t;
+  t.base = small_factor_args(c, i0);
+  t.ent0 = c->ent[i0];
+  t.W = W;
+  t.nlev = nlev;
+  for (int l = 0; l < nlev; ++l) {
+    t.K[l] = c->K_[i0 + l];
+    t.level[l] = (int)(i0 + l);
+    t.rec[l] = small_factor_args(c, i0 + l).rec;
+  }
+  t.out_last = small_factor_args(c, i0 + nlev - 1).out;
+  return t;
+}
+
 int run_small_factor_levels(ks_ctx *c) {
   const int n = c->n;
   const std::vector<int64_t> &Ks = c->K_;
-  const size_t it = small_tail_start(c);
-  for (size_t i = 0; i < it; ++i) {
+  const size_t it = small_tail_start(c), is = small_subtree_start(c);
+  for (size_t i = 0; i < it;) {
+    if (i == is) {   // kSubLevels levels in one launch, one subtree per CTA
+      SmallTailArgs t = small_tail_args(c, i, kSubLevels, 1ll << kSubLevels);
+      Launch l(c, 1, (int)i, 1);
+      cudaError_t e = launch_small_factor_tail(t, n, c->stream);
+      if (e != cudaSuccess) return cuda_fail(e);
+      i += kSubLevels;
+      continue;
+    }
     SmallFactorArgs a = small_factor_args(c, i);
     Launch l(c, 1, (int)i);
     cudaError_t e = launch_small_factor(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
+    ++i;
   }
   if (it < Ks.size()) {
-    SmallTailArgs t;
-    t.base = small_factor_args(c, it);
-    t.ent0 = c->ent[it];
-    t.nlev = (int)(Ks.size() - it);
-    for (int l = 0; l < t.nlev; ++l) {
-      t.K[l] = Ks[it + l];
-      t.level[l] = (int)(it + l);
-      t.rec[l] = small_factor_args(c, it + l).rec;
-    }
+    SmallTailArgs t = small_tail_args(c, it, (int)(Ks.size() - it), 0);
     Launch l(c, 1, (int)it, 1);
     cudaError_t e = launch_small_factor_tail(t, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
@@ -399,34 +433,52 @@ SmallBackwardArgs small_backward_args(ks_ctx *c, int i, int do_state, int do_cov
   return a;
 }
 
+SmallBwdTailArgs small_bwd_tail_args(ks_ctx *c, int top, int bottom, int do_state, int do_cov, int64_t W) {
+  SmallBwdTailArgs t;
+  t.base = small_backward_args(c, top, do_state, do_cov);
+  t.W = W;
+  t.nsub = W ? c->K_[bottom] / W : 1;
+  t.nlev = 0;
+  for (int i = top; i >= bottom; --i) {
+    const SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
+    t.K[t.nlev] = a.K;
+    t.shift[t.nlev] = a.shift;
+    t.rec[t.nlev] = a.rec;
+    t.Xup[t.nlev] = a.Xup;
+    t.Xcur[t.nlev] = a.Xcur;
+    ++t.nlev;
+  }
+  return t;
+}
+
 int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
   const int n = c->n;
   const std::vector<int64_t> &Ks = c->K_;
   const int it = (int)small_tail_start(c);   // the levels the fused factor tail ran
+  const int is = (int)small_subtree_start(c);
+  const int fam = do_cov ? (do_state ? 5 : 3) : 2;
   int top = (int)Ks.size() - 1;
   if (it < (int)Ks.size()) {
-    SmallBwdTailArgs t;
-    t.base = small_backward_args(c, top, do_state, do_cov);
-    t.nlev = 0;
-    for (int i = top; i >= it; --i) {
-      const SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
-      t.K[t.nlev] = a.K;
-      t.shift[t.nlev] = a.shift;
-      t.rec[t.nlev] = a.rec;
-      t.Xup[t.nlev] = a.Xup;
-      t.Xcur[t.nlev] = a.Xcur;
-      ++t.nlev;
-    }
-    Launch l(c, do_cov ? (do_state ? 5 : 3) : 2, it);
+    SmallBwdTailArgs t = small_bwd_tail_args(c, top, it, do_state, do_cov, 0);
+    Launch l(c, fam, it);
     cudaError_t e = launch_small_backward_tail(t, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
     top = it - 1;
   }
-  for (int i = top; i >= 0; --i) {
+  for (int i = top; i >= 0;) {
+    if (is < (int)Ks.size() && i == is + kSubLevels - 1) {   // the subtree pass, one subtree per CTA
+      SmallBwdTailArgs t = small_bwd_tail_args(c, i, is, do_state, do_cov, 1ll << kSubLevels);
+      Launch l(c, fam, is);
+      cudaError_t e = launch_small_backward_tail(t, n, c->stream);
+      if (e != cudaSuccess) return cuda_fail(e);
+      i = is - 1;
+      continue;
+    }
     SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
-    Launch l(c, do_cov ? (do_state ? 5 : 3) : 2, i);
+    Launch l(c, fam, i);
     cudaError_t e = launch_small_backward(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
+    --i;
   }
   return KS_OK;
 }

@@ -123,12 +123,15 @@ struct SmallFactorArgs {
   unsigned long long *status;
   double *zscratch;            // n (n + 1) doubles: the odd level's last-column leftover Z
   int cE, cC, outAoS;          // level 0: constant evolution / observation blocks
+  int64_t ent_off, out_off;    // fused kernels: entry / output column offsets of the CTA's buffers
 };
 // The fused recursion tail (small path): levels L_t .. top in one CTA.
 constexpr int kMaxTailLevels = 16;
 struct SmallTailArgs {
   SmallFactorArgs base;        // common fields (status, zscratch, t0 = 0, ...)
   const double *ent0;          // level-L_t entries (global, pair-interleaved tiles)
+  int64_t W;                   // 0: one CTA, whole levels; else subtree width per CTA (power of 2)
+  TView out_last;              // entries of the level after the last fused one (null at the top)
   int nlev;
   int64_t K[kMaxTailLevels];
   int level[kMaxTailLevels];
@@ -147,6 +150,7 @@ struct SmallBackwardArgs {
 // The backward of the fused tail: levels top .. L_t in one CTA (top first).
 struct SmallBwdTailArgs {
   SmallBackwardArgs base;      // common fields (x, S, do_state, do_cov, t0 = 0, ...)
+  int64_t W, nsub;             // 0: one CTA, whole levels; else subtree width (bottom level), CTAs
   int nlev;
   int64_t K[kMaxTailLevels];
   int shift[kMaxTailLevels];

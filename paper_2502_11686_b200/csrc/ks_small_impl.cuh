@@ -224,7 +224,9 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   double *zs_ = a.zscratch;
   // level >= 1 entry element e of column c: read-only global (__ldg), or
   // shared memory (SIN: the fused tail kernel keeps its levels on chip)
-  auto lde = [&](int64_t c, int e) { return SIN ? cb<64>(in.ent, c)[32 * e] : ldv<64>(in.ent, c, e); };
+  auto lde = [&](int64_t c, int e) {
+    return SIN ? cb<64>(in.ent, c - a.ent_off)[32 * e] : ldv<64>(in.ent, c, e);
+  };
   // field loads: level 0 per-field views (constant blocks: ES = 1, ts = 0),
   // level >= 1 one tiled entry record view
   constexpr int ESE = CE ? 1 : 64, ESC = CC ? 1 : 64, ESO = OAOS ? 1 : 64;
@@ -258,7 +260,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   auto ldE = [&](int e, int64_t c) {
     return L0 ? (CE ? cst[CstOff<N>::e + e] : ldv<64>(in.e, c, e)) : lde(c, EN::e + e);
   };
-  auto sto = [&](int e, double v) { stv<ESO>(a.out, pnext, e, v); };
+  auto sto = [&](int e, double v) { stv<ESO>(a.out, pnext - a.out_off, e, v); };
   // prefetch row i of a block field (n elements per row) of column c
   auto pfEl = [&](int i, int64_t c) {
 #pragma unroll
@@ -736,11 +738,17 @@ __global__ void __launch_bounds__(64, 1) small_factor_tail_kernel(SmallTailArgs 
   extern __shared__ double smem_park[];
   constexpr int64_t E = 3 * N * N + 2 * N + 1;
   double *bufA = smem_park + (size_t)blockDim.x * kParkDoubles<N> + CstOff<N>::size;
-  const int64_t K0 = t.K[0];
+  // W == 0: one CTA runs whole levels; W > 0: CTA c owns the subtree of the W
+  // columns [cW, cW + W) of the first level (W a power of two, every level
+  // halving exactly), so all its levels are local (a column's
+  // left neighbour in another subtree is only a target of blocks stored here)
+  const int64_t c = blockIdx.x;
+  const int64_t K0 = t.W ? t.W : t.K[0];
   double *bufB = bufA + ptiled_doubles(K0, E);
-  {   // level-L_t entries: global (written by the last level kernel) -> buffer A
+  {   // first-level entries: global (written by the last level kernel) -> buffer A
     const int64_t cnt = ptiled_doubles(K0, E);
-    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) bufA[i] = t.ent0[i];
+    const double *src = t.ent0 + (t.W ? c * t.W * E : 0);
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) bufA[i] = src[i];
   }
   __syncthreads();
   double *in = bufA, *out = bufB;
@@ -750,9 +758,14 @@ __global__ void __launch_bounds__(64, 1) small_factor_tail_kernel(SmallTailArgs 
     a.level = t.level[lv];
     a.rec = t.rec[lv];
     a.in.ent = TView{in, 64 * E};
-    a.out = (lv + 1 < t.nlev) ? TView{out, 64 * E} : TView{nullptr, 0};
-    const int64_t npairs = a.K >= 2 ? a.K / 2 : 1;
-    for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x) factor_item<N, false, false, false, false, true>(a, p);
+    const int64_t kloc = t.W ? (t.W >> lv) : a.K;            // this CTA's columns
+    a.ent_off = t.W ? c * kloc : 0;
+    const bool last = lv + 1 == t.nlev;
+    a.out = last ? t.out_last : TView{out, 64 * E};
+    a.out_off = (t.W && !last) ? c * (kloc / 2) : 0;
+    const int64_t npairs = t.W ? kloc / 2 : (a.K >= 2 ? a.K / 2 : 1);
+    for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x)
+      factor_item<N, false, false, false, false, true>(a, (t.W ? c * (kloc / 2) : 0) + p);
     __syncthreads();
     double *tmp = in;
     in = out;
@@ -839,7 +852,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phas
 // tile index beyond the level only takes part in the CTA barriers.
 template <int N, bool TAIL>
 __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t tile, int tid, double *bsm,
-                                         unsigned long long *mbarp, unsigned phase) {
+                                         unsigned long long *mbarp, unsigned phase, int64_t bbeg = 0,
+                                         int64_t bend = INT64_MAX) {
   using TR = Tri<N>;
   using RR = Rr<N>;
   constexpr int NN = N * N, BC = kBwdCols, NB = BC + 1, RS = rs_doubles<N>(), SP = bwd_sp<N>(),
@@ -848,7 +862,9 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
   const bool right = tid >= BC;      // warp-uniform
   const int64_t b0 = tile * BC, b = b0 + col, t = 2 * b;
   const bool tile_live = b0 < (a.K + 1) / 2;
-  const bool active = t < a.K;
+  // columns outside [bbeg, bend) belong to another CTA's subtree: staged
+  // (harmless) but neither computed nor written
+  const bool active = t < a.K && b >= bbeg && b < bend;
   const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
   const int64_t step = 1ll << a.shift;
   const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
@@ -1044,6 +1060,7 @@ __global__ void __launch_bounds__(4 * kBwdCols, 1) small_backward_tail_kernel(Sm
   if (tid == 0) mbar_init(&mbar[half], 1);
   __syncthreads();
   unsigned phase = 0;
+  const int64_t c = blockIdx.x;
   for (int lv = 0; lv < t.nlev; ++lv) {
     SmallBackwardArgs a = t.base;
     a.rec = t.rec[lv];
@@ -1051,11 +1068,22 @@ __global__ void __launch_bounds__(4 * kBwdCols, 1) small_backward_tail_kernel(Sm
     a.shift = t.shift[lv];
     a.Xup = t.Xup[lv];
     a.Xcur = t.Xcur[lv];
-    const int64_t ntile = ((a.K + 1) / 2 + kBwdCols - 1) / kBwdCols;
-    for (int64_t r = 0; 2 * r < ntile; ++r) {
-      const int64_t tile = 2 * r + half;
-      bwd_tile<N, true>(a, tile, tid, my, &mbar[half], phase);
-      if (tile < ntile) phase ^= 1u;
+    // W == 0: the whole level; else this CTA's subtree (W columns at the
+    // bottom level, W >> (nlev-1-lv) at this one): eliminated columns
+    // [bbeg, bend), inside one or more 32-column record tiles
+    int64_t bbeg = 0, bend = (a.K + 1) / 2;
+    if (t.W) {
+      const int64_t ne = (t.W >> (t.nlev - 1 - lv)) / 2;
+      bbeg = c * ne;
+      bend = bbeg + ne;
+    }
+    const int64_t tb = bbeg / kBwdCols, te = (bend + kBwdCols - 1) / kBwdCols;
+    for (int64_t r = 0; tb + 2 * r < te; ++r) {
+      const int64_t tile = tb + 2 * r + half;
+      const bool live = tile < te;
+      bwd_tile<N, true>(a, live ? tile : ((a.K + 1) / 2 + kBwdCols) / kBwdCols, tid, my, &mbar[half], phase, bbeg,
+                        bend);
+      if (live && tile * kBwdCols < (a.K + 1) / 2) phase ^= 1u;
       __syncthreads();
     }
   }
@@ -1329,7 +1357,7 @@ cudaError_t factor_tail_n(const SmallTailArgs &t, cudaStream_t s) {
     cudaFuncSetAttribute(small_factor_tail_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  small_factor_tail_kernel<N><<<1, 64, smem, s>>>(t);
+  small_factor_tail_kernel<N><<<(unsigned)(t.W ? t.K[0] / t.W : 1), 64, smem, s>>>(t);
   return cudaGetLastError();
 }
 template <int N>
@@ -1357,7 +1385,7 @@ cudaError_t backward_tail_n(const SmallBwdTailArgs &t, cudaStream_t s) {
     cudaFuncSetAttribute(small_backward_tail_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  small_backward_tail_kernel<N><<<1, 4 * kBwdCols, smem, s>>>(t);
+  small_backward_tail_kernel<N><<<(unsigned)(t.W ? t.nsub : 1), 4 * kBwdCols, smem, s>>>(t);
   return cudaGetLastError();
 }
 
