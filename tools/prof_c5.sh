@@ -1,7 +1,7 @@
 # ncu --set full of selected launches of a c5 run (see tools/prof_run.py):
 #   prof_c5.sh SKIP COUNT NAME  (launch indices among small_factor|small_backward kernels;
-#   after 2 warm-up runs of c5 (32 matching launches per run): factor L0 = 64, L1 = 65, ...,
-#   factor tail 79, backward tail 80, backward L14..L0 = 81..95)
+#   after 2 warm-up runs of c5 (20 matching launches per run: factor L0..L7, subtree pass,
+#   tail; backward tail, subtree pass, L7..L0): factor L0 = 40, L1 = 41, backward L1 = 58, L0 = 59)
 set -x
 python tools/prof_run.py c5 > gpurun_out/plain.log 2>&1 || exit 1
 K='regex:small_factor|small_backward'
