@@ -25,7 +25,11 @@ def post_flops(n: int) -> int:
 
 
 def entry_doubles(n: int) -> int:
-    return 3 * n * n + 2 * n + 1
+    """Doubles of one level >= 1 entry that are read / written: the C-like
+    block is upper triangular (its lower triangle is never stored on the
+    small path; the CTA path stores full blocks), y, El, Er, e, |col|."""
+    c = n * (n + 1) // 2 if n <= 8 else n * n
+    return c + 2 * n * n + 2 * n + 1
 
 
 def rrec_doubles(n: int) -> int:
