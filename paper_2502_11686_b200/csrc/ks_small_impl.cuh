@@ -869,7 +869,10 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
   const int64_t step = 1ll << a.shift;
   const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
   double xl[N], xr[N];
-  if (a.do_state && active && !right) {
+  // the state x_t: the left thread of a column in the solve-only path, the
+  // right one (the half with less SelInv work) when both are computed
+  const bool xside = a.do_cov ? right : !right;
+  if (a.do_state && active && xside) {
     const double *pl = hl ? (jl < 0 ? a.xhalo : a.x + jl * N) : nullptr;
     const double *pr = hr ? a.x + jr * N : nullptr;
 #pragma unroll
@@ -940,7 +943,7 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
   if (tile_live) mbar_wait(mbarp, phase);
   const double *myrec = REC + col;
   auto rec = [&](int e) { return myrec[e * 32]; };
-  if (active && a.do_state && !right) {
+  if (active && a.do_state && xside) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = rec(RR::w + i);
@@ -1015,17 +1018,25 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
     else side(std::false_type{});
   }
   __syncthreads();
-  if (active && !right) {
-    // S_tt = P - S_tl T_l^T - S_tr T_r^T = P - Q_l - Q_r (upper part, mirrored)
+  if (active) {
+    // S_tt = P - S_tl T_l^T - S_tr T_r^T = P - Q_l - Q_r (upper part,
+    // mirrored), the upper-triangle entries split between the two threads
+    constexpr int ES = (NT + 1) / 2;
+    const double *Q0 = Snb + col;    // Q_l [NT][NB] then Q_r [NT][NB]
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
       for (int jj = i; jj < N; ++jj) {
         const int e = TR::at(i, jj);
-        const double sv = (rec(RR::P + e) - Qs[e * NB]) - Qs[(NT + e) * NB];
-        Stt[i * N + jj] = sv;
-        Stt[jj * N + i] = sv;
+        if ((e < ES) != right) {
+          const double sv = (rec(RR::P + e) - Q0[e * NB]) - Q0[(NT + e) * NB];
+          Stt[i * N + jj] = sv;
+          Stt[jj * N + i] = sv;
+        }
       }
+  }
+  __syncthreads();
+  if (active && !right) {
     if constexpr (TAIL || NN % 2 != 0) {
 #pragma unroll
       for (int e = 0; e < NN; ++e) a.S[j * NN + e] = Stt[e];
