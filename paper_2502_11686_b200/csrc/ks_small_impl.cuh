@@ -16,6 +16,8 @@
 // consecutive columns with one coalesced 256-byte access.
 //
 // P:n = line n of the paper text.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -25,6 +27,9 @@
 
 #ifndef KS_PF_ROWS
 #define KS_PF_ROWS 2   // L1 prefetch distance of the streamed rows
+#endif
+#ifndef KS_BWD_TMA
+#define KS_BWD_TMA 1   // regular backward levels of even n: TMA tensor copies
 #endif
 #ifndef KS_F6_BLOCKS
 #define KS_F6_BLOCKS 4
@@ -798,16 +803,15 @@ __host__ __device__ constexpr int rs_doubles() { return 2 * N * N + N + N * (N +
 // the bulk store) and to an odd number of 16-byte units (fewer bank conflicts)
 template <int N>
 __host__ __device__ constexpr int bwd_sp() { return ((N * N + 1) / 2) % 2 ? 2 * ((N * N + 1) / 2) : 2 * ((N * N + 1) / 2) + 2; }
-// shared memory: record tile | max(neighbour blocks [NN][BC+1],
-//                                  Q_l, Q_r [2][NT][BC+1] + S_tt staging [BC][SP])
+// shared memory: record tile [RS][BC] | S_lr tile [NN][BC] | max(neighbour
+// blocks [NN][BC+1], Q_l, Q_r [2][NT][BC+1]); the S_tt staging rows [BC][SP]
+// overlay the record tile's T_l, T_r part (dead once Q_l, Q_r are formed)
 template <int N>
 __host__ __device__ constexpr size_t bwd_smem_doubles() {
-  return (size_t)kBwdCols * rs_doubles<N>() +
-         ((size_t)N * N * (kBwdCols + 1) >
-                  (size_t)N * (N + 1) * (kBwdCols + 1) + (size_t)kBwdCols * bwd_sp<N>()
-              ? (size_t)N * N * (kBwdCols + 1)
-              : (size_t)N * (N + 1) * (kBwdCols + 1) + (size_t)kBwdCols * bwd_sp<N>());
+  return (size_t)kBwdCols * (rs_doubles<N>() + N * N) +
+         ((size_t)N * N > (size_t)N * (N + 1) ? (size_t)N * N : (size_t)N * (N + 1)) * (kBwdCols + 1);
 }
+static_assert(bwd_sp<1>() <= 2 && bwd_sp<6>() <= 72 && bwd_sp<8>() <= 128, "S_tt staging must fit in T_l, T_r");
 
 // 8-byte asynchronous global -> shared copy (LDGSTS); src_size 0 zero-fills.
 __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
@@ -897,23 +901,27 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
   }
 
   // Staging.  (1) The CTA's R records are one tile of the tiled record array
-  // (32 columns x RS doubles, contiguous): ONE bulk copy by the TMA engine,
+  // (32 columns x RS doubles, contiguous) and its cross blocks S_lr one tile
+  // of the tiled level-(L+1) cross array: two bulk copies by the TMA engine,
   // completion on an mbarrier.  (2) The 33 distinct neighbour covariance
   // blocks of the CTA's 32 columns (level-(L+1) columns b0-1 .. b0+31, each a
   // contiguous n^2 block of S in step order), strided in HBM: cp.async,
-  // element-major in shared memory.  (3) The cross block S_lr and the
-  // neighbour states go straight to registers, issued before the waits.
+  // element-major in shared memory.  (3) The neighbour states go straight
+  // to registers, issued before the waits.
   // Alg. 2's products are split between the two threads of a column:
   //   left:  S_tl = -(T_l S_ll + T_r S_lr^T),  Q_l = S_tl T_l^T, x_t
   //   right: S_tr = -(T_l S_lr + T_r S_rr),    Q_r = S_tr T_r^T
   // and S_tt = P + Q_l + Q_r (upper triangle, mirrored) goes back through
   // shared memory as one bulk store per column.
   double *REC = bsm;                 // [RS][32]
-  double *Snb = bsm + BC * RS;       // [NN][NB]   (later: Q_l, Q_r [2][NT][NB] | S_tt [BC][SP])
+  double *SLR = bsm + BC * RS;       // [NN][32]   the tile of the tiled S_lr array
+  double *Snb = SLR + BC * NN;       // [NN][NB]   (later: Q_l, Q_r [2][NT][NB])
+  const bool xs = a.Xup.p != nullptr;
   if (tid == 0 && tile_live) {
     if (!TAIL) mbar_init(mbarp, 1);
-    mbar_expect_tx(mbarp, (unsigned)(RS * 32 * 8));
+    mbar_expect_tx(mbarp, (unsigned)((RS + (xs ? NN : 0)) * 32 * 8));
     bulk_g2s(REC, a.rec.p + tile * a.rec.ts, (unsigned)(RS * 32 * 8), mbarp);
+    if (xs) bulk_g2s(SLR, a.Xup.p + tile * a.Xup.ts, (unsigned)(NN * 32 * 8), mbarp);
   }
   const int64_t Kup = a.K / 2;       // columns of level L+1
   {
@@ -933,11 +941,6 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
       for (int e = 0; e < NN; ++e) cp_async8(&Snb[e * NB + sblk], s0 + (ok ? e : 0), ok);
     }
   }
-  double Slr[N][N];
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) Slr[r][c] = (active && hl && hr) ? ldv<32>(a.Xup, b, r * N + c) : 0.0;
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();                   // mbarrier init visible; neighbour blocks landed
   if (tile_live) mbar_wait(mbarp, phase);
@@ -955,6 +958,11 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
       a.x[j * N + i] = s;
     }
   }
+  double Slr[N][N];
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) Slr[r][c] = (hl && hr) ? SLR[(r * N + c) * BC + col] : 0.0;
   double Sd[TR::size];               // left: S_ll, right: S_rr
   if (active) {
 #pragma unroll
@@ -962,9 +970,9 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
 #pragma unroll
       for (int c = r; c < N; ++c) Sd[TR::at(r, c)] = Snb[(r * N + c) * NB + col + (right ? 1 : 0)];
   }
-  __syncthreads();                   // Snb is dead: its space becomes Q_r and S_tt
+  __syncthreads();                   // Snb is dead: its space becomes Q_l, Q_r
   double *Qs = Snb + (right ? NT * NB : 0) + col;   // this side's Q [NT][NB]
-  double *Stt = Snb + 2 * NT * NB + col * SP;
+  double *Stt = REC + col * SP;      // over T_l, T_r (after the Q barrier)
   if (active) {
     // one code path per side (warp-uniform branch), so neither side executes
     // the other's products
@@ -1034,6 +1042,8 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
           Stt[jj * N + i] = sv;
         }
       }
+    // generic-proxy writes made visible to the bulk (async-proxy) copies
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
   if (active && !right) {
@@ -1041,7 +1051,6 @@ __device__ __forceinline__ void bwd_tile(const SmallBackwardArgs &a, int64_t til
 #pragma unroll
       for (int e = 0; e < NN; ++e) a.S[j * NN + e] = Stt[e];
     } else {   // 16-byte multiple and alignment: one bulk store
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a.S + j * NN),
                    "r"(smem_u32(Stt)), "r"((unsigned)(NN * 8))
                    : "memory");
@@ -1097,6 +1106,225 @@ __global__ void __launch_bounds__(4 * kBwdCols, 1) small_backward_tail_kernel(Sm
       if (live && tile * kBwdCols < (a.K + 1) / 2) phase ^= 1u;
       __syncthreads();
     }
+  }
+}
+
+// ------------------------------------------------ TMA-tensor backward ---
+//
+// The regular-level fused backward for even n (n^2 and n doubles are 16-byte
+// multiples): every strided block of the tile moves as ONE TMA tensor copy.
+// In step order the level-(L+1) neighbours q = b0-1 .. b0+31 of the tile's
+// columns and the tile's own level-L columns are both rows of a 2-D view of
+// S (and x) with row pitch 2^(L+1) blocks, so a [33][n^2] box loads the 33
+// neighbour blocks (row -1 out of bounds: zero-filled, patched from the
+// shard halo) and a [32][n^2] box stores the 32 S_tt blocks (rows past the
+// level end are clipped); the same for the states.  With the record and S_lr
+// tiles (bulk copies) the whole tile arrives on one mbarrier and leaves in
+// two stores, no per-thread global traffic except the cross blocks.
+struct BwdMaps {
+  CUtensorMap Sout, Snb, xout, xnb;   // box [32][n^2], [33][n^2], [32][n], [33][n]
+};
+__host__ __device__ constexpr int rnd16(int d) { return (d + 15) / 16 * 16; }
+template <int N>
+struct BwdT {
+  static constexpr int NN = N * N, NT = N * (N + 1) / 2, BC = kBwdCols, NB = BC + 1, RS = rs_doubles<N>();
+  // doubles: REC [RS][32] | SLR [NN][32] | SNB [33][NN] / Q [2][NT][NB] | XNB [33][N] | XST [32][N]
+  static constexpr int REC = 0, SLR = REC + RS * BC, SNB = SLR + NN * BC,
+                       XNB = SNB + rnd16((BC + 1) * NN > 2 * NT * NB ? (BC + 1) * NN : 2 * NT * NB),
+                       XST = XNB + rnd16((BC + 1) * N), total = XST + rnd16(BC * N);
+};
+__device__ __forceinline__ void tma_load2d(void *dst, const CUtensorMap *m, int c0, int c1, unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store2d(const CUtensorMap *m, int c0, int c1, const void *src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+
+template <int N>
+__global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N))
+    small_backward_tma_kernel(const SmallBackwardArgs a, const __grid_constant__ BwdMaps m) {
+  using TR = Tri<N>;
+  using RR = Rr<N>;
+  using L = BwdT<N>;
+  constexpr int NN = N * N, BC = kBwdCols, NB = BC + 1, RS = L::RS, NT = L::NT;
+  extern __shared__ __align__(128) double tsm[];
+  __shared__ __align__(8) unsigned long long mbar;
+  double *bsm = tsm;
+  const int tid = threadIdx.x, col = tid & (BC - 1);
+  const bool right = tid >= BC;      // warp-uniform
+  const int64_t b0 = (int64_t)blockIdx.x * BC, b = b0 + col, t = 2 * b;
+  const bool active = t < a.K;
+  const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
+  double *REC = bsm + L::REC, *SLR = bsm + L::SLR, *SNB = bsm + L::SNB, *XNB = bsm + L::XNB, *XST = bsm + L::XST;
+  const bool xs = a.Xup.p != nullptr;
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    mbar_expect_tx(&mbar, (unsigned)(8 * (RS * BC + (xs ? NN * BC : 0) + (BC + 1) * NN + (a.do_state ? (BC + 1) * N : 0))));
+    bulk_g2s(REC, a.rec.p + blockIdx.x * a.rec.ts, (unsigned)(RS * BC * 8), &mbar);
+    if (xs) bulk_g2s(SLR, a.Xup.p + blockIdx.x * a.Xup.ts, (unsigned)(NN * BC * 8), &mbar);
+    tma_load2d(SNB, &m.Snb, 0, (int)(b0 - 1), &mbar);
+    if (a.do_state) tma_load2d(XNB, &m.xnb, 0, (int)(b0 - 1), &mbar);
+  }
+  __syncthreads();                   // mbarrier initialised
+  mbar_wait(&mbar, 0);
+  if (b0 == 0 && a.t0 > 0) {         // neighbour q = -1: the shard halo
+    for (int e = tid; e < NN; e += 2 * BC) SNB[e] = a.Shalo[e];
+    if (a.do_state && tid < N) XNB[tid] = a.xhalo[tid];
+    __syncthreads();
+  }
+  const double *myrec = REC + col;
+  auto rec = [&](int e) { return myrec[e * BC]; };
+  if (active && a.do_state && right) {   // x_t = w - T_l x_l - T_r x_r
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double sx = rec(RR::w + i);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        sx = fma(-rec(RR::Tl + i * N + k), XNB[col * N + k], sx);
+        sx = fma(-rec(RR::Tr + i * N + k), XNB[(col + 1) * N + k], sx);
+      }
+      XST[col * N + i] = sx;
+    }
+  }
+  double Slr[N][N];
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) Slr[r][c] = (hl && hr) ? SLR[(r * N + c) * BC + col] : 0.0;
+  double Sd[TR::size];               // left: S_ll, right: S_rr
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = r; c < N; ++c) Sd[TR::at(r, c)] = SNB[(col + (right ? 1 : 0)) * NN + r * N + c];
+  __syncthreads();                   // SNB is dead: its space becomes Q_l, Q_r
+  double *Qs = SNB + (right ? NT * NB : 0) + col;
+  if (active) {
+    auto side = [&](auto right_c) {
+      constexpr bool RIGHT = decltype(right_c)::value;
+      constexpr int TO = RIGHT ? RR::Tr : RR::Tl;
+#pragma unroll(N <= 6 ? N : 1)
+      for (int i = 0; i < N; ++i) {
+        double tl[N], tr[N], A[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          tl[k] = rec(RR::Tl + i * N + k);
+          tr[k] = rec(RR::Tr + i * N + k);
+        }
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            const double sd = k <= c ? Sd[TR::at(k, c)] : Sd[TR::at(c, k)];
+            if (!RIGHT) {            // S_tl = -(T_l S_ll + T_r S_lr^T)
+              sacc = fma(tl[k], sd, sacc);
+              sacc = fma(tr[k], Slr[c][k], sacc);
+            } else {                 // S_tr = -(T_l S_lr + T_r S_rr)
+              sacc = fma(tl[k], Slr[k][c], sacc);
+              sacc = fma(tr[k], sd, sacc);
+            }
+          }
+          A[c] = -sacc;
+        }
+        if (a.Xcur.p) {
+#pragma unroll
+          for (int c = 0; c < N; ++c) {
+            if (!RIGHT && hl) stv<32>(a.Xcur, t, c * N + i, A[c]);      // slot t-1: S_{t-1,t} = S_tl^T
+            if (RIGHT && hr) stv<32>(a.Xcur, t + 1, i * N + c, A[c]);   // slot t:   S_{t,t+1} = S_tr
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) {
+          if (jj < i) continue;
+          double q = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) q = fma(A[k], rec(TO + jj * N + k), q);
+          Qs[TR::at(i, jj) * NB] = q;
+        }
+      }
+    };
+    if (right) side(std::true_type{});
+    else side(std::false_type{});
+  }
+  __syncthreads();                   // Q_l, Q_r complete; T_l, T_r dead
+  double *Stt = REC + col * NN;      // [32][NN] dense rows: the store box
+  if (active) {
+    const double *Q0 = SNB + col;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int jj = i; jj < N; ++jj) {
+        const int e = TR::at(i, jj);
+        if ((e * 2) / NT == (right ? 1 : 0)) {
+          const double sv = (rec(RR::P + e) - Q0[e * NB]) - Q0[(NT + e) * NB];
+          Stt[i * N + jj] = sv;
+          Stt[jj * N + i] = sv;
+        }
+      }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    tma_store2d(&m.Sout, 0, (int)b0, REC);
+    if (a.do_state) tma_store2d(&m.xout, 0, (int)b0, XST);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// Host: the four tensor maps of one level (cuTensorMapEncodeTiled through the
+// runtime's driver entry point: no libcuda link dependency).
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+  if (!f) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return f;
+}
+static bool tmap_rows(CUtensorMap *m, const double *base, int width, int64_t rows, int64_t pitch, int box) {
+  auto enc = tmap_encoder();
+  if (!enc || rows < 1 || rows > INT32_MAX) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(pitch * 8)};
+  const cuuint32_t boxd[2] = {(cuuint32_t)width, (cuuint32_t)box};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// true: launched (even n, a regular level with at least one neighbour column)
+template <int N>
+bool backward_tma(const SmallBackwardArgs &a, cudaStream_t s) {
+  if constexpr (N % 2 != 0) {
+    return false;
+  } else {
+    const int64_t nc = (a.K + 1) / 2, Kup = a.K / 2, st = 2ll << a.shift;
+    if (!KS_BWD_TMA || !a.do_cov || Kup < 1) return false;
+    BwdMaps m;
+    const double *xb = a.x ? a.x : a.S;   // do_state == 0: never dereferenced
+    if (!tmap_rows(&m.Sout, a.S + ((1ll << a.shift) - 1) * N * N, N * N, nc, st * N * N, kBwdCols) ||
+        !tmap_rows(&m.Snb, a.S + (st - 1) * N * N, N * N, Kup, st * N * N, kBwdCols + 1) ||
+        !tmap_rows(&m.xout, xb + ((1ll << a.shift) - 1) * N, N, nc, st * N, kBwdCols) ||
+        !tmap_rows(&m.xnb, xb + (st - 1) * N, N, Kup, st * N, kBwdCols + 1))
+      return false;
+    const size_t smem = BwdT<N>::total * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(small_backward_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    small_backward_tma_kernel<N><<<(unsigned)((nc + kBwdCols - 1) / kBwdCols), 2 * kBwdCols, smem, s>>>(a, m);
+    return true;
   }
 }
 
@@ -1376,6 +1604,7 @@ int tail_cols_n() { return tail_max_cols<N>(); }
 
 template <int N>
 cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
+  if (backward_tma<N>(a, s)) return cudaGetLastError();
   const int64_t nc = (a.K + 1) / 2;
   const size_t full = bwd_smem_doubles<N>() * sizeof(double);
   const size_t smem = a.do_cov ? full : 0;
