@@ -215,9 +215,10 @@ struct CstOff {
       size = 2 * N * N + N + kSmallMaxM * N + kSmallMaxM * kSmallMaxM;
 };
 
-template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false>
+template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false, bool ZS = false>
 __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_t t, bool hr, bool hl,
-                                                int64_t pnext, bool zs_in, bool zs_out) {
+                                                int64_t pnext, bool zs_in, bool zs_out,
+                                                volatile int *zsync = nullptr, int zval = 0) {
   using TR = Tri<N>;
 #ifndef KS_ROW_UNROLL
 #define KS_ROW_UNROLL 1
@@ -531,6 +532,11 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         zr = unpark(kLeft + i * (N + 2) + N);
         wl = unpark(kLeft + i * (N + 2) + N + 1);
       } else {
+        if (ZS && zsync && i == N) {   // the odd level's last column runs in another thread
+          while (*zsync != zval) {
+          }
+          __threadfence_block();
+        }
 #pragma unroll
         for (int j = 0; j < N; ++j) row[j] = zs_[(i - N) * (N + 1) + j];
         zr = zs_[(i - N) * (N + 1) + N];
@@ -608,6 +614,10 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       sto(EN::e + i, 0.0);
     }
   }
+  if (ZS && zs_out && zsync) {   // Z rows published to the last pair's thread
+    __threadfence_block();
+    *zsync = zval;
+  }
 
   // ---- post: rank check, T_l = U^{-1} Rl, w = U^{-1} z, P = U^{-1} D^{-1} U^{-T} ----
   {
@@ -673,24 +683,41 @@ constexpr int factor_min_blocks(int n) { return n <= 4 ? 8 : n == 5 ? 7 : n == 6
 
 // One work item of a factor level: pair p (plus, on an odd level, the last
 // column without right neighbour, handled first by the last pair's thread).
-template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false>
-__device__ __forceinline__ void factor_item(const SmallFactorArgs &a, int64_t p) {
+// split_odd(K, T): on an odd level >= 1 the last column runs in its own thread
+// (index K/2, after the pairs) concurrently with the last pair, whose stage 3
+// waits for its Z rows on the shared-memory word zsync (value zval) -- when
+// that thread is in the same CTA of T threads as the last pair's (the odd
+// level then costs one pair elimination, not two in series).  The fused tail
+// keeps the serial form (the larger ZS body costs it more I-cache than the
+// split saves at n = 6).
+__host__ __device__ inline bool split_odd(int64_t K, int T) { return K >= 3 && (K & 1) && ((K / 2) % T) != 0; }
+template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false, bool ZS = false>
+__device__ __forceinline__ void factor_item(const SmallFactorArgs &a, int64_t p, volatile int *zsync = nullptr,
+                                            int zval = 0) {
+  if (!ZS) zsync = nullptr;   // ZS: compiled with the split-odd-level code
   const int64_t K = a.K;
   const bool single_only = (K == 1);
-  const bool triple = (K >= 3) && (K & 1) && (p == K / 2 - 1);
+  // split odd level (zsync): thread K/2 eliminates the last column, the last
+  // pair waits for its Z rows; else the last pair's thread does both
+  const bool lastcol = zsync && p == K / 2;
+  const bool triple = !zsync && (K >= 3) && (K & 1) && (p == K / 2 - 1);
+  const bool waits = zsync && (p == K / 2 - 1);
   // pass 0: the odd level's last column (no right neighbour), pass 1: the pair.
-  // One inlined call site keeps the (large, fully unrolled) body once in the
-  // instruction cache.
+  // One inlined call site per pass keeps the (large, fully unrolled) body at
+  // most twice in the instruction cache.
 #pragma unroll 1
-  for (int pass = (single_only || triple) ? 0 : 1; pass < (single_only ? 1 : 2); ++pass) {
+  for (int pass = (single_only || triple || lastcol) ? 0 : 1; pass < ((single_only || lastcol) ? 1 : 2); ++pass) {
     const int64_t t = pass == 0 ? K - 1 : 2 * p;
     const bool hl = t + a.t0 > 0;
-    if (pass == 0) small_eliminate<N, L0, CE, CC, OAOS, SIN>(a, t, false, hl, 0, false, hl);
-    else small_eliminate<N, L0, CE, CC, OAOS, SIN>(a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false);
+    if (pass == 0)
+      small_eliminate<N, L0, CE, CC, OAOS, SIN, ZS>(a, t, false, hl, 0, false, hl, zsync, zval);
+    else
+      small_eliminate<N, L0, CE, CC, OAOS, SIN, ZS>(a, t, true, hl, p, (triple || waits) && (K - 1 + a.t0 > 0),
+                                                    false, waits ? zsync : nullptr, zval);
   }
 }
 
-template <int N, bool L0, bool CE, bool CC, bool OAOS>
+template <int N, bool L0, bool CE, bool CC, bool OAOS, bool ZS = false>
 __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(SmallFactorArgs a) {
   if (L0 && (CE || CC)) {   // stage the constant (stride-0) level-0 blocks once per CTA
     extern __shared__ double smem_park[];
@@ -712,6 +739,14 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
   }
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t npairs = a.K >= 2 ? a.K / 2 : 1;
+  if constexpr (ZS) {   // launched only when split_odd(K, 64)
+    __shared__ int zsync;
+    if (threadIdx.x == 0) zsync = 0;
+    __syncthreads();
+    if (p > npairs) return;
+    factor_item<N, L0, CE, CC, OAOS, false, true>(a, p, &zsync, 1);
+    return;
+  }
   if (p >= npairs) return;
   factor_item<N, L0, CE, CC, OAOS>(a, p);
 }
@@ -1556,25 +1591,27 @@ __global__ void __launch_bounds__(256) small_whiten_y(SmallWhitenArgs a) {
   }
 }
 
-template <int N, bool L0, bool CE, bool CC, bool OAOS>
+template <int N, bool L0, bool CE, bool CC, bool OAOS, bool ZS = false>
 cudaError_t factor_launch(const SmallFactorArgs &a, cudaStream_t s) {
-  const int64_t np = a.K >= 2 ? a.K / 2 : 1;
   const int T = 64;
+  const int64_t np = (a.K >= 2 ? a.K / 2 : 1) + (ZS ? 1 : 0);
   const unsigned g = (unsigned)((np + T - 1) / T);
   const size_t smem = ((size_t)T * kParkDoubles<N> + CstOff<N>::size) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(small_factor_kernel<N, L0, CE, CC, OAOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(small_factor_kernel<N, L0, CE, CC, OAOS, ZS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
-  small_factor_kernel<N, L0, CE, CC, OAOS><<<g, T, smem, s>>>(a);
+  small_factor_kernel<N, L0, CE, CC, OAOS, ZS><<<g, T, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int N, bool OAOS>
 cudaError_t factor_oaos(const SmallFactorArgs &a, cudaStream_t s) {
-  if (a.in.ent.p != nullptr) return factor_launch<N, false, false, false, OAOS>(a, s);
+  if (a.in.ent.p != nullptr)   // level >= 1; an odd level splits its last column off (split_odd)
+    return split_odd(a.K, 64) ? factor_launch<N, false, false, false, OAOS, true>(a, s)
+                              : factor_launch<N, false, false, false, OAOS>(a, s);
   if (a.cE) {
     if (a.cC) return factor_launch<N, true, true, true, OAOS>(a, s);
     return factor_launch<N, true, true, false, OAOS>(a, s);
