@@ -155,6 +155,13 @@ __device__ __forceinline__ void gapp(double &u, double &y, double yk, double sb)
   u = fma(sb, y, u);
 }
 
+// A streamed row absorbed by an empty row of R (w ~ 2^600 y_k^2, see above)
+// is consumed: its later rotations are the identity to eps, and as a stage-1
+// leftover it carries no row of D~ (level 0 with m_i < n: the first n - m_i
+// evolution rows fill the empty rows of R), so stage 3 skips it.  (Stopping
+// the rotations of a row at its absorption was measured slower: the per-pivot
+// exit branch serialises the overlapped reciprocals of consecutive pivots.)
+constexpr double kConsumed = 0x1p500;
 // Rotate one streamed row into R (row streaming): pivot part
 // row[0..N), weight w; trail(k, y_k, sbar) applies rotation k to the row's
 // trailing columns.
@@ -531,6 +538,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
         for (int j = 0; j < N; ++j) row[j] = unpark(kLeft + i * (N + 2) + j);
         zr = unpark(kLeft + i * (N + 2) + N);
         wl = unpark(kLeft + i * (N + 2) + N + 1);
+        if (L0 && wl > kConsumed) continue;   // consumed in stage 1: no D~ row
       } else {
         if (ZS && zsync && i == N) {   // the odd level's last column runs in another thread
           while (*zsync != zval) {
