@@ -311,10 +311,11 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) 
 // Q^T C for C = A[k0:k0+mpad, c0:c0+ncp] with Q = I - V T V^T:
 // W = V^T C, W = T^T W, C -= V W, one 8-column tile per warp iteration
 // (all three products of a tile in the same warp: no CTA barrier).
-__device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, const QrWs &w) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+__device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, const QrWs &w, int wbase = 0,
+                         int nw = kWarps) {
+  const int warp = (threadIdx.x >> 5) - wbase, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   double *sc = w.tile + warp * (kLdw * 8);
-  for (int n0 = warp * 8; n0 < ncp; n0 += kWarps * 8) {
+  for (int n0 = warp * 8; n0 < ncp; n0 += nw * 8) {
     double *C = A + k0 + (c0 + n0) * lda;
     double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;   // two independent DMMA chains
     int kk = 0;
@@ -356,8 +357,15 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, 
 // [npiv, ncols).  A is zero-padded to pad8(rows) rows (lda >= that) and to
 // pad8(ncols) (+8 when npiv % 8 != 0) columns.  On exit the first npiv
 // columns hold R (zeros below the diagonal).  Ends with __syncthreads.
-__device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w, long long *acc = nullptr) {
-  const int warp = threadIdx.x >> 5;
+// Warp group [wbase, wbase + nw) with its own named barrier (barid > 0), or
+// the whole CTA (barid 0).
+__device__ __forceinline__ void group_sync(int barid, int nw) {
+  if (barid == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(nw * 32) : "memory");
+}
+__device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w, long long *acc = nullptr,
+                           int wbase = 0, int nw = kWarps, int barid = 0) {
+  const int warp = (threadIdx.x >> 5) - wbase;
 #ifdef KS_LARGE_PROF
   long long _t0 = clock64();
 #endif
@@ -371,13 +379,13 @@ __device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, Qr
       else if (mr == 4) qr_panel<4>(A, lda, k0, rows, nb, w);
       else qr_panel<kPanelMaxR>(A, lda, k0, rows, nb, w);
     }
-    __syncthreads();
+    group_sync(barid, nw);
 #ifdef KS_LARGE_PROF
     { const long long t1 = clock64(); if (acc) acc[0] += t1 - _t0; _t0 = t1; }
 #endif
     const int c0 = k0 + nb;
-    if (c0 < ncols) qr_apply(A, lda, k0, pad8(rows - k0), c0, pad8(ncols - c0), w);
-    __syncthreads();
+    if (c0 < ncols) qr_apply(A, lda, k0, pad8(rows - k0), c0, pad8(ncols - c0), w, wbase, nw);
+    group_sync(barid, nw);
 #ifdef KS_LARGE_PROF
     { const long long t1 = clock64(); if (acc) acc[1] += t1 - _t0; _t0 = t1; }
 #endif
@@ -577,7 +585,9 @@ __device__ double col_norm2_l0(const EntryView &in, int n, int64_t t, bool hl, b
 struct FactorPlan {
   int ld1, cols1, ld2, cols2, ld3, cols3, ldv;
   int off2, offws, total;   // doubles
+  bool conc;                // stages 2 and 3 concurrently (B3 + a second workspace fit in S1's region)
 };
+constexpr int kConcMaxPerThread = 16;   // D~ | y~ values per thread held across the S1 -> B3 rebuild
 __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   FactorPlan f;
   const int extra = (n % 8) ? 8 : 0;
@@ -597,6 +607,10 @@ __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   f.off2 = ((s1 > s1p ? s1 : s1p) + 1) & ~1;
   f.offws = f.off2 + (((s2 > s3 ? s2 : s3) + 1) & ~1);
   f.total = f.offws + f.ldv * 8 + 2 * kLdw * 8 + 8 + kWarps * kLdw * 8 + 8;
+  // stage 3's matrix rebuilt in S1's region (free once stage 2's matrix is
+  // set up) next to a 4-warp workspace: the two QRs run on two warp groups
+  const int wsb = f.ldv * 8 + 2 * kLdw * 8 + 8 + (kWarps / 2) * kLdw * 8;
+  f.conc = ((s3 + 1) & ~1) + wsb <= f.off2 && RC * (n + 1) <= kConcMaxPerThread * kThreads;
   return f;
 }
 
@@ -662,6 +676,60 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   qr_blocked(S1, ld1, RC + n, n, 2 * n + 1, w, qacc);
   KS_PROF(1)
 
+  if (f.conc && hr && hl) {
+    // ---- stages 2 and 3 concurrently: independent QRs once stage 1 is done.
+    // Stage 2's matrix B2 goes to P2 as below; stage 3's B3 is rebuilt in S1's
+    // region (D~ | y~ held in registers across the rebuild) with a second
+    // workspace behind it; warps 0-3 factor B3, warps 4-7 B2, each group with
+    // its own panel warp and named barrier, so the two serial panel chains
+    // overlap.
+    const int64_t u = t + 1;
+    zero_smem(P2, ld2 * f.cols2);
+    __syncthreads();
+    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
+    ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
+    ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
+    cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
+    cp_blk(P2, ld2, n, 2 * n, S1, ld1, 0, n, n, n + 1);    // X_t, z~_t
+    const int nd = RC * (n + 1);                           // D~_{t+1} (RC x n) | y~_{t+1}
+    double dv[kConcMaxPerThread];
+#pragma unroll
+    for (int k = 0; k < kConcMaxPerThread; ++k) {
+      const int idx = tid + k * kThreads;
+      dv[k] = idx < nd ? S1[(n + idx % RC) + (n + idx / RC) * ld1] : 0.0;
+    }
+    __syncthreads();                                       // S1 is dead
+    double *B3 = S1;
+    zero_smem(B3, ld3 * f.cols3);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kConcMaxPerThread; ++k) {
+      const int idx = tid + k * kThreads;
+      if (idx < nd) B3[idx % RC + (idx / RC) * ld3] = dv[k];
+    }
+    ld_blk(B3, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
+    ld_blk(B3, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
+    int rows3 = 2 * RC;
+    if (zs_in) {
+      ld_blk(B3, ld3, rows3, 0, a.zscratch, n + 1, n, n + 1, n);
+      rows3 += n;
+    }
+    __syncthreads();
+    KS_PROF(0)
+    QrWs w3 = carve_ws(S1 + ((ld3 * f.cols3 + 1) & ~1), f.ldv);
+    if (tid < kThreads / 2) qr_blocked(B3, ld3, rows3, n, n + 1, w3, qacc, 0, kWarps / 2, 1);
+    else qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w, qacc, kWarps / 2, kWarps / 2, 2);
+    __syncthreads();
+    KS_PROF(2)
+    double *ent = a.next + pnext * entry_doubles(n);
+    const int valid = rows3 < n ? rows3 : n;
+    st_blk(ent, n, B3, ld3, 0, 0, n, n, valid);              // C'
+    st_blk(ent + n * n, 1, B3, ld3, 0, n, n, 1, valid);      // y'
+    if (tid == 0) ent[3 * n * n + 2 * n] = nrm_u;
+    st_blk(ent + n * n + n, n, P2, ld2, n, n, n, n, n);               // El' = Z_t
+    st_blk(ent + 2 * n * n + n, n, P2, ld2, n, 2 * n, n, n, n);       // Er' = X~_t
+    st_blk(ent + 3 * n * n + n, 1, P2, ld2, n, 3 * n, n, 1, n);       // e'  = z^_t
+  } else {
   // ---- stage 3 (before stage 2: its matrix B3 shares memory with B2) ----
   if (hr) {
     const int64_t u = t + 1;
@@ -717,6 +785,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
       double *ent = a.next + pnext * entry_doubles(n);
       for (int i = tid; i < 2 * n * n + n; i += blockDim.x) ent[n * n + n + i] = 0.0;
     }
+  }
   }
   __syncthreads();
 

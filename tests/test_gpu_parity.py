@@ -80,6 +80,17 @@ def test_configs_reduced(cfg, N, generic):
     assert_parity(gen.make(cfg, N=N), generic=generic)
 
 
+# Odd levels >= 1 above the fused tail (K > 128): K/2 % 64 != 0 runs the last
+# column in its own thread beside the last pair (split_odd: N = 1550 -> K_1 =
+# 775, N = 6300 -> K_2 = 1575, N = 12345 -> K_3 = 1543), K/2 % 64 == 0 keeps
+# both in one thread (N = 258 -> K_1 = 129, N = 33282 -> K_1 = 16641 = 2*8320+1).
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c5"])
+@pytest.mark.parametrize("N", [1550, 6300, 258, 33282])
+def test_odd_levels_split_and_serial(cfg, N):
+    assert_parity(gen.make(cfg, N=N))
+
+
 @pytest.mark.parametrize("n", [6, 48])
 def test_paper_benchmark_class(n):
     """The paper's own problem class."""
