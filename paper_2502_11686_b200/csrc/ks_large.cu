@@ -588,6 +588,10 @@ struct FactorPlan {
   bool conc;                // stages 2 and 3 concurrently (B3 + a second workspace fit in S1's region)
 };
 constexpr int kConcMaxPerThread = 16;   // D~ | y~ values per thread held across the S1 -> B3 rebuild
+#ifndef KS_CONC_W3
+#define KS_CONC_W3 2
+#endif
+constexpr int kConcW3 = KS_CONC_W3;     // warps of the stage-3 group (the rest: stage 2)
 __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   FactorPlan f;
   const int extra = (n % 8) ? 8 : 0;
@@ -609,7 +613,7 @@ __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   f.total = f.offws + f.ldv * 8 + 2 * kLdw * 8 + 8 + kWarps * kLdw * 8 + 8;
   // stage 3's matrix rebuilt in S1's region (free once stage 2's matrix is
   // set up) next to a 4-warp workspace: the two QRs run on two warp groups
-  const int wsb = f.ldv * 8 + 2 * kLdw * 8 + 8 + (kWarps / 2) * kLdw * 8;
+  const int wsb = f.ldv * 8 + 2 * kLdw * 8 + 8 + kConcW3 * kLdw * 8;
   f.conc = ((s3 + 1) & ~1) + wsb <= f.off2 && RC * (n + 1) <= kConcMaxPerThread * kThreads;
   return f;
 }
@@ -717,8 +721,8 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     __syncthreads();
     KS_PROF(0)
     QrWs w3 = carve_ws(S1 + ((ld3 * f.cols3 + 1) & ~1), f.ldv);
-    if (tid < kThreads / 2) qr_blocked(B3, ld3, rows3, n, n + 1, w3, qacc, 0, kWarps / 2, 1);
-    else qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w, qacc, kWarps / 2, kWarps / 2, 2);
+    if (tid < 32 * kConcW3) qr_blocked(B3, ld3, rows3, n, n + 1, w3, qacc, 0, kConcW3, 1);
+    else qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w, qacc, kConcW3, kWarps - kConcW3, 2);
     __syncthreads();
     KS_PROF(2)
     double *ent = a.next + pnext * entry_doubles(n);
