@@ -483,7 +483,7 @@ __device__ bool cta_chol(double *Lm, int ldl, int d, double *sh) {
         if (c < nb) {
           const double v = __shfl_sync(0xffffffffu, a[0][c], c);
           ok &= v > 0.0;
-          const double l = sqrt(v > 0.0 ? v : 1.0), il = 1.0 / l;
+          const double il = rsqrt_nr(v > 0.0 ? v : 1.0), l = (v > 0.0 ? v : 1.0) * il;
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             const int r = k0 + lane + 32 * s;
@@ -559,26 +559,44 @@ __device__ void cp_blk(double *D, int ldd, int dr, int dc, const double *A, int 
   }
 }
 
-// Sum of squares of `count` contiguous doubles, reduced by warp 0 and
-// returned to every thread through sh[0].
-__device__ double cta_sumsq(const double *g, int count, double *sh) {
+// |UA block column of level-0 column t|_F^2 = |C_t|^2 + |Er_t|^2 + |El_{t+1}|^2,
+// for the pair's two columns t (hl: Er_t exists) and t + 1 (hr; hu: El_{t+2}
+// exists) in ONE pass of all threads and one CTA reduction (sh: 2 kWarps
+// doubles; fixed summation order: deterministic).
+__device__ void col_norm2_l0_pair(const EntryView &in, int n, int64_t t, bool hl, bool hr, bool hu, double *sh,
+                                  double &st, double &su) {
+  const int cn = in.RC * n, nn = n * n, tid = threadIdx.x;
+  const double *Ct = in.C + t * in.sC, *Cu = in.C + (t + 1) * in.sC;
+  const double *Ert = in.Er + t * in.sEr, *Eru = in.Er + (t + 1) * in.sEr;
+  const double *Elu = in.El + (t + 1) * in.sEl, *Elv = in.El + (t + 2) * in.sEl;
+  double a = 0.0, b = 0.0;
+  for (int i = tid; i < cn; i += blockDim.x) {
+    a = fma(Ct[i], Ct[i], a);
+    if (hr) b = fma(Cu[i], Cu[i], b);
+  }
+  for (int i = tid; i < nn; i += blockDim.x) {
+    if (hl) a = fma(Ert[i], Ert[i], a);
+    if (hr) {
+      a = fma(Elu[i], Elu[i], a);
+      b = fma(Eru[i], Eru[i], b);
+      if (hu) b = fma(Elv[i], Elv[i], b);
+    }
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
   __syncthreads();
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < count; i += 32) s = fma(g[i], g[i], s);
-    s = warp_sum(s);
-    if (threadIdx.x == 0) sh[0] = s;
+  if ((tid & 31) == 0) {
+    sh[tid >> 5] = a;
+    sh[kWarps + (tid >> 5)] = b;
   }
   __syncthreads();
-  return sh[0];
-}
-
-// |UA block column of level-0 column t|_F^2 = |C_t|^2 + |Er_t|^2 + |El_{t+1}|^2.
-__device__ double col_norm2_l0(const EntryView &in, int n, int64_t t, bool hl, bool hr, double *sh) {
-  double s = cta_sumsq(in.C + t * in.sC, in.RC * n, sh);
-  if (hl) s += cta_sumsq(in.Er + t * in.sEr, n * n, sh);
-  if (hr) s += cta_sumsq(in.El + (t + 1) * in.sEl, n * n, sh);
-  return s;
+  st = 0.0;
+  su = 0.0;
+  for (int w = 0; w < kWarps; ++w) {
+    st += sh[w];
+    su += sh[kWarps + w];
+  }
+  __syncthreads();
 }
 
 // ---- shared-memory plan of the factor kernel ----
@@ -610,7 +628,7 @@ __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   const int s2 = f.ld2 * f.cols2, s3 = f.ld3 * f.cols3;
   f.off2 = ((s1 > s1p ? s1 : s1p) + 1) & ~1;
   f.offws = f.off2 + (((s2 > s3 ? s2 : s3) + 1) & ~1);
-  f.total = f.offws + f.ldv * 8 + 2 * kLdw * 8 + 8 + kWarps * kLdw * 8 + 8;
+  f.total = f.offws + f.ldv * 8 + 2 * kLdw * 8 + 8 + kWarps * kLdw * 8 + 2 * kWarps;
   // stage 3's matrix rebuilt in S1's region (free once stage 2's matrix is
   // set up) next to a 4-warp workspace: the two QRs run on two warp groups
   const int wsb = f.ldv * 8 + 2 * kLdw * 8 + 8 + kConcW3 * kLdw * 8;
@@ -645,7 +663,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
                           int64_t pnext, bool zs_in, bool zs_out) {
   const int n = a.n, RC = a.in.RC, tid = threadIdx.x;
   const EntryView &in = a.in;
-  double *S1 = sm, *P2 = sm + f.off2, *sh = sm + f.total - 8;
+  double *S1 = sm, *P2 = sm + f.off2, *sh = sm + f.total - 2 * kWarps;
   QrWs w = carve_ws(sm + f.offws, f.ldv);
   const int ld1 = f.ld1, ld2 = f.ld2, ld3 = f.ld3;
   KS_PROF_DECL
@@ -660,8 +678,10 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     nrm_t = in.nrm[t * in.snrm];
     if (hr) nrm_u = in.nrm[(t + 1) * in.snrm];
   } else {
-    nrm_t = sqrt(col_norm2_l0(in, n, t, hl, hr, sh));
-    if (hr) nrm_u = sqrt(col_norm2_l0(in, n, t + 1, true, t + 2 < a.K, sh));
+    double st, su;
+    col_norm2_l0_pair(in, n, t, hl, hr, t + 2 < a.K, sh, st, su);
+    nrm_t = sqrt(st);
+    if (hr) nrm_u = sqrt(su);
   }
 
   // ---- stage 1 ----
@@ -968,7 +988,7 @@ __global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelA
 // Evolution blocks: K = Lam Lam^T; El = -Lam^{-1} F,
 // Er = Lam^{-1}, e = Lam^{-1} c.  One CTA per distinct block; the solve with
 // the 2n+1 right-hand sides [F | I | c] is blocked (DMMA updates).
-__global__ void __launch_bounds__(kThreads) whiten_evo_kernel(WhitenArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int n = a.n, nn = n * n, tid = threadIdx.x;
   const int64_t i = blockIdx.x;
@@ -1014,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads) whiten_evo_kernel(WhitenArgs a) {
 }
 
 // Observation blocks: L = M M^T; C = M^{-1} H, y = M^{-1} o (rows >= m_i zero).
-__global__ void __launch_bounds__(kThreads) whiten_obs_kernel(WhitenArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int n = a.n, mx = a.m_max, tid = threadIdx.x;
   const int64_t i = blockIdx.x;
