@@ -40,7 +40,7 @@ constexpr int kThreads = 256, kWarps = kThreads / 32;
     _pt = _now;                                      \
   }
 #define KS_PROF_PRINT(tag)                                                                          \
-  if (blockIdx.x == 0 && threadIdx.x == 0)                                                          \
+  if (blockIdx.x == 1 && threadIdx.x == 0)                                                          \
     printf("[%s] %lld %lld %lld %lld %lld %lld %lld %lld\n", tag, _acc[0], _acc[1], _acc[2], _acc[3], \
            _acc[4], _acc[5], _acc[6], _acc[7]);
 __device__ long long g_panel_prof[8];
@@ -529,14 +529,31 @@ __device__ void zero_smem(double *p, int count) {
 
 // smem column-major A(lda)[r0:r0+rows, c0:c0+cols] <- g (row-major, ldg);
 // rows >= valid or g == null stay untouched (caller zeroed the matrix).
-__device__ void ld_blk(double *A, int lda, int r0, int c0, const double *g, int64_t ldg, int rows, int cols,
-                       int valid) {
-  if (g == nullptr) return;
+// Returns this thread's share of the block's squared Frobenius norm.
+__device__ double ld_blk(double *A, int lda, int r0, int c0, const double *g, int64_t ldg, int rows, int cols,
+                         int valid) {
+  if (g == nullptr) return 0.0;
   const int tot = (valid < rows ? valid : rows) * cols;
+  double s = 0.0;
   for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
     const int i = idx / cols, j = idx - i * cols;
-    A[(r0 + i) + (c0 + j) * lda] = g[(int64_t)i * ldg + j];
+    const double v = __ldg(g + (int64_t)i * ldg + j);
+    A[(r0 + i) + (c0 + j) * lda] = v;
+    s = fma(v, v, s);
   }
+  return s;
+}
+// L2 prefetch of `count` contiguous doubles (one 128-byte line per thread)
+__device__ __forceinline__ void pf_l2(const double *g, int64_t count) {
+  if (g == nullptr) return;
+  for (int64_t off = (int64_t)threadIdx.x * 16; off < count; off += (int64_t)blockDim.x * 16)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(g + off));
+}
+// this thread's share of |g|_F^2 (count contiguous doubles)
+__device__ double part_sumsq(const double *g, int count) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s = fma(__ldg(g + i), __ldg(g + i), s);
+  return s;
 }
 
 // smem (column-major) -> global row-major (ldg); rows >= valid are written as 0
@@ -559,29 +576,10 @@ __device__ void cp_blk(double *D, int ldd, int dr, int dc, const double *A, int 
   }
 }
 
-// |UA block column of level-0 column t|_F^2 = |C_t|^2 + |Er_t|^2 + |El_{t+1}|^2,
-// for the pair's two columns t (hl: Er_t exists) and t + 1 (hr; hu: El_{t+2}
-// exists) in ONE pass of all threads and one CTA reduction (sh: 2 kWarps
-// doubles; fixed summation order: deterministic).
-__device__ void col_norm2_l0_pair(const EntryView &in, int n, int64_t t, bool hl, bool hr, bool hu, double *sh,
-                                  double &st, double &su) {
-  const int cn = in.RC * n, nn = n * n, tid = threadIdx.x;
-  const double *Ct = in.C + t * in.sC, *Cu = in.C + (t + 1) * in.sC;
-  const double *Ert = in.Er + t * in.sEr, *Eru = in.Er + (t + 1) * in.sEr;
-  const double *Elu = in.El + (t + 1) * in.sEl, *Elv = in.El + (t + 2) * in.sEl;
-  double a = 0.0, b = 0.0;
-  for (int i = tid; i < cn; i += blockDim.x) {
-    a = fma(Ct[i], Ct[i], a);
-    if (hr) b = fma(Cu[i], Cu[i], b);
-  }
-  for (int i = tid; i < nn; i += blockDim.x) {
-    if (hl) a = fma(Ert[i], Ert[i], a);
-    if (hr) {
-      a = fma(Elu[i], Elu[i], a);
-      b = fma(Eru[i], Eru[i], b);
-      if (hu) b = fma(Elv[i], Elv[i], b);
-    }
-  }
+// CTA sums of two per-thread partials (sh: 2 kWarps doubles; fixed order:
+// deterministic).  Contains barriers: every thread calls it.
+__device__ void cta_sum2(double a, double b, double *sh, double &sa, double &sb) {
+  const int tid = threadIdx.x;
   a = warp_sum(a);
   b = warp_sum(b);
   __syncthreads();
@@ -590,11 +588,11 @@ __device__ void col_norm2_l0_pair(const EntryView &in, int n, int64_t t, bool hl
     sh[kWarps + (tid >> 5)] = b;
   }
   __syncthreads();
-  st = 0.0;
-  su = 0.0;
+  sa = 0.0;
+  sb = 0.0;
   for (int w = 0; w < kWarps; ++w) {
-    st += sh[w];
-    su += sh[kWarps + w];
+    sa += sh[w];
+    sb += sh[kWarps + w];
   }
   __syncthreads();
 }
@@ -673,30 +671,39 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   long long *qacc = nullptr;
 #endif
 
-  double nrm_t, nrm_u = 0.0;
-  if (in.nrm) {
-    nrm_t = in.nrm[t * in.snrm];
-    if (hr) nrm_u = in.nrm[(t + 1) * in.snrm];
-  } else {
-    double st, su;
-    col_norm2_l0_pair(in, n, t, hl, hr, t + 2 < a.K, sh, st, su);
-    nrm_t = sqrt(st);
-    if (hr) nrm_u = sqrt(su);
+  // rank references |UA block column|_F (reading R9): given at
+  // level >= 1; at level 0 accumulated per thread from the blocks as they
+  // are loaded (column t: C_t, Er_t, El_{t+1}; column t+1: C_{t+1}, Er_{t+1},
+  // El_{t+2} -- the one block this pair does not otherwise read) and reduced
+  // once after the QRs
+  const bool l0n = in.nrm == nullptr;
+  // what stages 2 and 3 read later (Er_t, El_t, e_t; C_{t+1}, y_{t+1}) is
+  // pulled into L2 now, so their loads do not stall the pair's critical path
+  if (hl) {
+    pf_l2(in.Er + t * in.sEr, (int64_t)n * n);
+    pf_l2(in.El + t * in.sEl, (int64_t)n * n);
+    pf_l2(in.e + t * in.se, n);
   }
+  if (hr) {
+    pf_l2(in.C + (t + 1) * in.sC, (int64_t)RC * n);
+    pf_l2(in.y + (t + 1) * in.sy, RC);
+  }
+  double pt = 0.0, pu = 0.0;
+  if (l0n && hr && t + 2 < a.K) pu = part_sumsq(in.El + (t + 2) * in.sEl, n * n);
 
   // ---- stage 1 ----
   zero_smem(S1, ld1 * f.cols1);
   __syncthreads();
-  ld_blk(S1, ld1, 0, 0, in.C + t * in.sC, n, RC, n, RC);
+  pt += ld_blk(S1, ld1, 0, 0, in.C + t * in.sC, n, RC, n, RC);
   ld_blk(S1, ld1, 0, 2 * n, in.y + t * in.sy, 1, RC, 1, RC);
   if (hr) {
     const int64_t u = t + 1;
-    ld_blk(S1, ld1, RC, 0, in.El + u * in.sEl, n, n, n, n);
-    ld_blk(S1, ld1, RC, n, in.Er + u * in.sEr, n, n, n, n);
+    pt += ld_blk(S1, ld1, RC, 0, in.El + u * in.sEl, n, n, n, n);
+    pu += ld_blk(S1, ld1, RC, n, in.Er + u * in.sEr, n, n, n, n);
     ld_blk(S1, ld1, RC, 2 * n, in.e + u * in.se, 1, n, 1, n);
   }
   __syncthreads();
-  KS_PROF(0)
+  KS_PROF(3)
   qr_blocked(S1, ld1, RC + n, n, 2 * n + 1, w, qacc);
   KS_PROF(1)
 
@@ -710,7 +717,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     const int64_t u = t + 1;
     zero_smem(P2, ld2 * f.cols2);
     __syncthreads();
-    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
+    pt += ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
     ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
     ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
     cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
@@ -731,7 +738,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
       const int idx = tid + k * kThreads;
       if (idx < nd) B3[idx % RC + (idx / RC) * ld3] = dv[k];
     }
-    ld_blk(B3, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
+    pu += ld_blk(B3, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
     ld_blk(B3, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
     int rows3 = 2 * RC;
     if (zs_in) {
@@ -749,10 +756,10 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     const int valid = rows3 < n ? rows3 : n;
     st_blk(ent, n, B3, ld3, 0, 0, n, n, valid);              // C'
     st_blk(ent + n * n, 1, B3, ld3, 0, n, n, 1, valid);      // y'
-    if (tid == 0) ent[3 * n * n + 2 * n] = nrm_u;
     st_blk(ent + n * n + n, n, P2, ld2, n, n, n, n, n);               // El' = Z_t
     st_blk(ent + 2 * n * n + n, n, P2, ld2, n, 2 * n, n, n, n);       // Er' = X~_t
     st_blk(ent + 3 * n * n + n, 1, P2, ld2, n, 3 * n, n, 1, n);       // e'  = z^_t
+    KS_PROF(5)
   } else {
   // ---- stage 3 (before stage 2: its matrix B3 shares memory with B2) ----
   if (hr) {
@@ -761,7 +768,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     __syncthreads();
     cp_blk(P2, ld3, 0, 0, S1, ld1, n, n, RC, n);          // D~_{t+1}
     cp_blk(P2, ld3, 0, n, S1, ld1, n, 2 * n, RC, 1);      // y~_{t+1}
-    ld_blk(P2, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
+    pu += ld_blk(P2, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
     ld_blk(P2, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
     int rows3 = 2 * RC;
     if (zs_in) {
@@ -776,7 +783,6 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     const int valid = rows3 < n ? rows3 : n;
     st_blk(ent, n, P2, ld3, 0, 0, n, n, valid);             // C'
     st_blk(ent + n * n, 1, P2, ld3, 0, n, n, 1, valid);     // y'
-    if (tid == 0) ent[3 * n * n + 2 * n] = nrm_u;
     __syncthreads();
   }
 
@@ -784,7 +790,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   zero_smem(P2, ld2 * f.cols2);
   __syncthreads();
   if (hl) {
-    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
+    pt += ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
     ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
     ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
     cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
@@ -812,6 +818,18 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   }
   }
   __syncthreads();
+
+  double nrm_t, nrm_u = 0.0;
+  if (l0n) {
+    double st, su;
+    cta_sum2(pt, pu, sh, st, su);
+    nrm_t = sqrt(st);
+    nrm_u = sqrt(su);
+  } else {
+    nrm_t = in.nrm[t * in.snrm];
+    if (hr) nrm_u = in.nrm[(t + 1) * in.snrm];
+  }
+  if (hr && tid == 0) a.next[pnext * entry_doubles(n) + 3 * n * n + 2 * n] = nrm_u;
 
   // ---- R record: rank check, T = R^{-1}[R_l R_r], w = R^{-1} z, P = R^{-1} R^{-T} ----
   if (tid == 0) {
