@@ -143,16 +143,17 @@ def roofline(launches, N, n, m, strides, p64_tf, cfg="c5"):
         ach = fl / avg_s / 1e12
         r = {"bound": "alu", "achieved": ach, "peak": p64_tf, "unit": "TFLOP/s", "frac": ach / p64_tf,
              "peak_source": "measured fp64 DFMA peak (ks_peak_fp64_tflops, this run)"}
-    traffic, tsrc = None, None
+    traffic, tsrc, kname = None, None, f"{fam} launch L={lev}"
     try:   # DRAM bytes of this launch from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
         rec = tj.get(cfg, {}).get(f"{fam} L={lev}")
         if rec:
             traffic, tsrc = rec["bytes"], f"profiles/{rec['round']}_{cfg}_{fam}_L{lev}.txt ({rec['report']})"
+            kname = f"{rec['kernel']} L={lev}"
     except Exception:
         pass
-    r.update({"traffic": traffic, "traffic_source": tsrc, "kernel": f"{fam}_level_kernel L={lev}",
+    r.update({"traffic": traffic, "traffic_source": tsrc, "kernel": kname,
               "launch_ms": avg_s * 1e3,
               "share_of_step": share, "algorithmic_bytes": by, "algorithmic_flops": fl,
               "units": units,
