@@ -529,16 +529,28 @@ __device__ void zero_smem(double *p, int count) {
 
 // smem column-major A(lda)[r0:r0+rows, c0:c0+cols] <- g (row-major, ldg);
 // rows >= valid or g == null stay untouched (caller zeroed the matrix).
-// Returns this thread's share of the block's squared Frobenius norm.
-__device__ double ld_blk(double *A, int lda, int r0, int c0, const double *g, int64_t ldg, int rows, int cols,
-                         int valid) {
-  if (g == nullptr) return 0.0;
+// Asynchronous (cp.async, global -> shared without registers): every element
+// of every block of a stage's setup is in flight at once; the caller
+// completes them with sync_loads().
+__device__ void ld_blk(double *A, int lda, int r0, int c0, const double *g, int64_t ldg, int rows, int cols,
+                       int valid) {
+  if (g == nullptr) return;
   const int tot = (valid < rows ? valid : rows) * cols;
-  double s = 0.0;
   for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
     const int i = idx / cols, j = idx - i * cols;
-    const double v = __ldg(g + (int64_t)i * ldg + j);
-    A[(r0 + i) + (c0 + j) * lda] = v;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(A + (r0 + i) + (c0 + j) * lda);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g + (int64_t)i * ldg + j) : "memory");
+  }
+}
+__device__ __forceinline__ void sync_loads() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+}
+// this thread's share of |A[r0:r0+rows, c0:c0+cols]|_F^2 (shared memory)
+__device__ double sumsq_blk(const double *A, int lda, int r0, int c0, int rows, int cols) {
+  double s = 0.0;
+  for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
+    const double v = A[(r0 + idx % rows) + (c0 + idx / rows) * lda];
     s = fma(v, v, s);
   }
   return s;
@@ -694,15 +706,20 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   // ---- stage 1 ----
   zero_smem(S1, ld1 * f.cols1);
   __syncthreads();
-  pt += ld_blk(S1, ld1, 0, 0, in.C + t * in.sC, n, RC, n, RC);
+  ld_blk(S1, ld1, 0, 0, in.C + t * in.sC, n, RC, n, RC);
   ld_blk(S1, ld1, 0, 2 * n, in.y + t * in.sy, 1, RC, 1, RC);
   if (hr) {
     const int64_t u = t + 1;
-    pt += ld_blk(S1, ld1, RC, 0, in.El + u * in.sEl, n, n, n, n);
-    pu += ld_blk(S1, ld1, RC, n, in.Er + u * in.sEr, n, n, n, n);
+    ld_blk(S1, ld1, RC, 0, in.El + u * in.sEl, n, n, n, n);
+    ld_blk(S1, ld1, RC, n, in.Er + u * in.sEr, n, n, n, n);
     ld_blk(S1, ld1, RC, 2 * n, in.e + u * in.se, 1, n, 1, n);
   }
-  __syncthreads();
+  sync_loads();
+  if (l0n) {   // |C_t|, |El_{t+1}| (column t), |Er_{t+1}| (column t+1), before the QR overwrites them
+    pt += sumsq_blk(S1, ld1, 0, 0, RC + (hr ? n : 0), n);
+    if (hr) pu += sumsq_blk(S1, ld1, RC, n, n, n);
+    __syncthreads();
+  }
   KS_PROF(3)
   qr_blocked(S1, ld1, RC + n, n, 2 * n + 1, w, qacc);
   KS_PROF(1)
@@ -717,7 +734,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     const int64_t u = t + 1;
     zero_smem(P2, ld2 * f.cols2);
     __syncthreads();
-    pt += ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
+    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
     ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
     ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
     cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
@@ -729,7 +746,8 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
       const int idx = tid + k * kThreads;
       dv[k] = idx < nd ? S1[(n + idx % RC) + (n + idx / RC) * ld1] : 0.0;
     }
-    __syncthreads();                                       // S1 is dead
+    sync_loads();                                          // S1 is dead; B2 loaded
+    if (l0n) pt += sumsq_blk(P2, ld2, 0, 0, n, n);         // |Er_t|
     double *B3 = S1;
     zero_smem(B3, ld3 * f.cols3);
     __syncthreads();
@@ -738,14 +756,18 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
       const int idx = tid + k * kThreads;
       if (idx < nd) B3[idx % RC + (idx / RC) * ld3] = dv[k];
     }
-    pu += ld_blk(B3, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
+    ld_blk(B3, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
     ld_blk(B3, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
     int rows3 = 2 * RC;
     if (zs_in) {
       ld_blk(B3, ld3, rows3, 0, a.zscratch, n + 1, n, n + 1, n);
       rows3 += n;
     }
-    __syncthreads();
+    sync_loads();
+    if (l0n) {   // |C_{t+1}|
+      pu += sumsq_blk(B3, ld3, RC, 0, RC, n);
+      __syncthreads();
+    }
     KS_PROF(0)
     QrWs w3 = carve_ws(S1 + ((ld3 * f.cols3 + 1) & ~1), f.ldv);
     if (tid < 32 * kConcW3) qr_blocked(B3, ld3, rows3, n, n + 1, w3, qacc, 0, kConcW3, 1);
@@ -768,14 +790,18 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     __syncthreads();
     cp_blk(P2, ld3, 0, 0, S1, ld1, n, n, RC, n);          // D~_{t+1}
     cp_blk(P2, ld3, 0, n, S1, ld1, n, 2 * n, RC, 1);      // y~_{t+1}
-    pu += ld_blk(P2, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
+    ld_blk(P2, ld3, RC, 0, in.C + u * in.sC, n, RC, n, RC);
     ld_blk(P2, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
     int rows3 = 2 * RC;
     if (zs_in) {
       ld_blk(P2, ld3, rows3, 0, a.zscratch, n + 1, n, n + 1, n);
       rows3 += n;
     }
-    __syncthreads();
+    sync_loads();
+    if (l0n) {   // |C_{t+1}|
+      pu += sumsq_blk(P2, ld3, RC, 0, RC, n);
+      __syncthreads();
+    }
     KS_PROF(0)
     qr_blocked(P2, ld3, rows3, n, n + 1, w, qacc);
     KS_PROF(2)
@@ -790,12 +816,16 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   zero_smem(P2, ld2 * f.cols2);
   __syncthreads();
   if (hl) {
-    pt += ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
+    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
     ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
     ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
     cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
     cp_blk(P2, ld2, n, 2 * n, S1, ld1, 0, n, n, n + 1);    // X_t, z~_t
-    __syncthreads();
+    sync_loads();
+    if (l0n) {   // |Er_t|
+      pt += sumsq_blk(P2, ld2, 0, 0, n, n);
+      __syncthreads();
+    }
     KS_PROF(0)
     qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w, qacc);
     KS_PROF(3)
