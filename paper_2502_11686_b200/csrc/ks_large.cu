@@ -542,6 +542,10 @@ __device__ void ld_blk(double *A, int lda, int r0, int c0, const double *g, int6
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g + (int64_t)i * ldg + j) : "memory");
   }
 }
+__device__ __forceinline__ void cp8(double *sdst, const double *g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
 __device__ __forceinline__ void sync_loads() {
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
@@ -966,11 +970,11 @@ __global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelA
   const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
   zero_smem(sm, bp.total);
   __syncthreads();
-  for (int idx = tid; idx < nn; idx += blockDim.x) {
+  for (int idx = tid; idx < nn; idx += blockDim.x) {   // asynchronous: all blocks in flight at once
     const int r = idx / n, c = idx - r * n;
-    TT[r + c * ldt] = rec[idx];
-    TT[r + (n + c) * ldt] = rec[nn + idx];
-    Pm[r + c * ldp] = rec[2 * nn + idx];
+    cp8(&TT[r + c * ldt], rec + idx);
+    cp8(&TT[r + (n + c) * ldt], rec + nn + idx);
+    cp8(&Pm[r + c * ldp], rec + 2 * nn + idx);
   }
   if (a.do_state) {
     const double *xlp = hl ? (jl < 0 ? a.xhalo : a.x + jl * n) : nullptr;
@@ -986,16 +990,15 @@ __global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelA
     const double *Sx = (hl && hr) ? a.Xup + b * nn : nullptr;   // slot b-1: S_{t-1,t+1}
     for (int idx = tid; idx < nn; idx += blockDim.x) {
       const int r = idx / n, c = idx - r * n;
-      if (Sl) SII[r + c * ldS] = Sl[idx];
-      if (Sr) SII[(n + r) + (n + c) * ldS] = Sr[idx];
+      if (Sl) cp8(&SII[r + c * ldS], Sl + idx);
+      if (Sr) cp8(&SII[(n + r) + (n + c) * ldS], Sr + idx);
       if (Sx) {
-        const double v = Sx[idx];
-        SII[r + (n + c) * ldS] = v;
-        SII[(n + c) + r * ldS] = v;
+        cp8(&SII[r + (n + c) * ldS], Sx + idx);
+        cp8(&SII[(n + c) + r * ldS], Sx + idx);
       }
     }
   }
-  __syncthreads();
+  sync_loads();
   if (a.do_state) {
     for (int i = tid; i < n; i += blockDim.x) {
       double s = rec[3 * nn + i];
@@ -1055,16 +1058,16 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
   const double *c = a.c ? a.c + iK * a.sc : nullptr;
   zero_smem(sm, ld * pad8(n) + ld * cp);
   __syncthreads();
-  for (int k = tid; k < nn; k += blockDim.x) {
+  for (int k = tid; k < nn; k += blockDim.x) {   // asynchronous loads
     const int r = k / n, cc = k - r * n;
-    Lm[r + cc * ld] = K[k];
-    X[r + cc * ld] = F[k];
+    cp8(&Lm[r + cc * ld], K + k);
+    cp8(&X[r + cc * ld], F + k);
   }
   for (int r = tid; r < n; r += blockDim.x) {
     X[r + (n + r) * ld] = 1.0;
     X[r + 2 * n * ld] = c ? c[r] : 0.0;
   }
-  __syncthreads();
+  sync_loads();
   const bool ok = cta_chol(Lm, ld, n, sh);
   if (tid == 0 && !ok) {
     const int64_t step = (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i;
@@ -1093,16 +1096,16 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   const double *L = a.L + i * a.sL, *H = a.H + i * a.sH, *o = a.o + i * a.so;
   zero_smem(sm, ld * pad8(mx) + ld * cp);
   __syncthreads();
-  for (int k = tid; k < mi * mi; k += blockDim.x) {
+  for (int k = tid; k < mi * mi; k += blockDim.x) {   // asynchronous loads
     const int r = k / mi, cc = k - r * mi;
-    Lm[r + cc * ld] = L[r * mx + cc];
+    cp8(&Lm[r + cc * ld], L + r * mx + cc);
   }
   for (int k = tid; k < mi * n; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
-    X[r + cc * ld] = H[r * n + cc];
+    cp8(&X[r + cc * ld], H + r * n + cc);
   }
-  for (int r = tid; r < mi; r += blockDim.x) X[r + n * ld] = o[r];
-  __syncthreads();
+  for (int r = tid; r < mi; r += blockDim.x) cp8(&X[r + n * ld], o + r);
+  sync_loads();
   const bool ok = cta_chol(Lm, ld, mi, sh);
   if (tid == 0 && !ok) report(a.status, i, kBadL);
   diag_rcp(Lm, ld, mi, sh);
