@@ -396,12 +396,15 @@ __device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, Qr
 // zero-padded to 8 rows/columns: 8-row blocks from the bottom, the diagonal
 // block by one thread per right-hand side (values in registers, multiplied
 // by the reciprocal diagonal rinv[0..n) the caller provides), the update of
-// the rows above as a DMMA GEMM.  Ends with __syncthreads.
-__device__ void trsm_upper(const double *R, int ldr, const double *rinv, int n, double *X, int ldx, int p) {
+// the rows above as a DMMA GEMM.  Ends with __syncthreads.  Two
+// right-hand-side blocks at once, X1 (p1 columns) and X2 (p2): one diagonal
+// pass and one barrier pair per 8-row block for both.
+__device__ void trsm_upper2(const double *R, int ldr, const double *rinv, int n, double *X1, int ldx1, int p1,
+                            double *X2, int ldx2, int p2) {
   for (int r0 = ((n - 1) / 8) * 8; r0 >= 0; r0 -= 8) {
     const int h = (n - r0 < 8) ? n - r0 : 8;
-    for (int c = threadIdx.x; c < p; c += blockDim.x) {
-      double *xp = X + r0 + c * ldx;
+    for (int c = threadIdx.x; c < p1 + p2; c += blockDim.x) {
+      double *xp = c < p1 ? X1 + r0 + c * ldx1 : X2 + r0 + (c - p1) * ldx2;
       double x[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = (i < h) ? xp[i] : 0.0;
@@ -420,7 +423,10 @@ __device__ void trsm_upper(const double *R, int ldr, const double *rinv, int n, 
         if (i < h) xp[i] = x[i];
     }
     __syncthreads();
-    if (r0 > 0) gemm<false, false>(r0, pad8(p), 8, -1.0, R + r0 * ldr, ldr, X + r0, ldx, 1.0, X, ldx);
+    if (r0 > 0) {
+      gemm<false, false>(r0, pad8(p1), 8, -1.0, R + r0 * ldr, ldr, X1 + r0, ldx1, 1.0, X1, ldx1);
+      gemm<false, false>(r0, pad8(p2), 8, -1.0, R + r0 * ldr, ldr, X2 + r0, ldx2, 1.0, X2, ldx2);
+    }
     __syncthreads();
   }
 }
@@ -887,8 +893,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   __syncthreads();
   // RHS [R_l | R_r | z] (columns n .. 3n of B2) and I (R^{-1}) in two solves
   KS_PROF(0)
-  trsm_upper(Rc, ldr, rinv, n, P2 + n * ld2, ld2, 2 * n + 1);
-  trsm_upper(Rc, ldr, rinv, n, Ri, ldr, n);
+  trsm_upper2(Rc, ldr, rinv, n, P2 + n * ld2, ld2, 2 * n + 1, Ri, ldr, n);
   KS_PROF(4)
   gemm<false, true>(np, np, np, 1.0, Ri, ldr, Ri, ldr, 0.0, Pm, ldr);
   __syncthreads();
