@@ -1174,8 +1174,14 @@ struct BwdT {
   // doubles: REC [RS][32] | SLR [NN][32] | SNB [33][NN] / Q [2][NT][NB] | XNB [33][N] | XST [32][N]
   static constexpr int REC = 0, SLR = REC + RS * BC, SNB = SLR + NN * BC,
                        XNB = SNB + rnd16((BC + 1) * NN > 2 * NT * NB ? (BC + 1) * NN : 2 * NT * NB),
-                       XST = XNB + rnd16((BC + 1) * N), total = XST + rnd16(BC * N);
+                       XST = XNB + rnd16((BC + 1) * N), total = XST + rnd16(BC * N),
+                       // levels >= 1 (KS_BWD_XSTAGE): the 64 cross-block slots 2 b0 .. 2 b0 + 63
+                       // of the tile = two tiles of the tiled level-L cross array, one bulk store
+                       XCS = total, total_x = XCS + 2 * NN * BC;
 };
+#ifndef KS_BWD_XSTAGE
+#define KS_BWD_XSTAGE 1
+#endif
 __device__ __forceinline__ void tma_load2d(void *dst, const CUtensorMap *m, int c0, int c1, unsigned long long *bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -1276,10 +1282,16 @@ __global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N))
           A[c] = -sacc;
         }
         if (a.Xcur.p) {
+          if (KS_BWD_XSTAGE) {   // slot 2 col (+1): tile col >> 4, position 2 col & 31 (+1)
+            double *xs = bsm + L::XCS + (col >> 4) * NN * BC + ((2 * col) & 31) + (RIGHT ? 1 : 0);
 #pragma unroll
-          for (int c = 0; c < N; ++c) {
-            if (!RIGHT && hl) stv<32>(a.Xcur, t, c * N + i, A[c]);      // slot t-1: S_{t-1,t} = S_tl^T
-            if (RIGHT && hr) stv<32>(a.Xcur, t + 1, i * N + c, A[c]);   // slot t:   S_{t,t+1} = S_tr
+            for (int c = 0; c < N; ++c) xs[(RIGHT ? i * N + c : c * N + i) * BC] = A[c];
+          } else {
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+              if (!RIGHT && hl) stv<32>(a.Xcur, t, c * N + i, A[c]);      // slot t-1: S_{t-1,t} = S_tl^T
+              if (RIGHT && hr) stv<32>(a.Xcur, t + 1, i * N + c, A[c]);   // slot t:   S_{t,t+1} = S_tr
+            }
           }
         }
 #pragma unroll
@@ -1316,6 +1328,13 @@ __global__ void __launch_bounds__(2 * kBwdCols, bwd_min_blocks(N))
   if (tid == 0) {
     tma_store2d(&m.Sout, 0, (int)b0, REC);
     if (a.do_state) tma_store2d(&m.xout, 0, (int)b0, XST);
+    if (KS_BWD_XSTAGE && a.Xcur.p) {   // the tile's two cross-array tiles (fewer at the level end)
+      const int64_t xt = 2 * (int64_t)blockIdx.x, xtiles = (a.K + 1 + BC - 1) / BC;
+      const int nt = xtiles - xt >= 2 ? 2 : (int)(xtiles - xt);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a.Xcur.p + xt * a.Xcur.ts),
+                   "r"(smem_u32(bsm + L::XCS)), "r"((unsigned)(nt * NN * BC * 8))
+                   : "memory");
+    }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
@@ -1360,10 +1379,12 @@ bool backward_tma(const SmallBackwardArgs &a, cudaStream_t s) {
         !tmap_rows(&m.xout, xb + ((1ll << a.shift) - 1) * N, N, nc, st * N, kBwdCols) ||
         !tmap_rows(&m.xnb, xb + (st - 1) * N, N, Kup, st * N, kBwdCols + 1))
       return false;
-    const size_t smem = BwdT<N>::total * sizeof(double);
+    const bool xst = KS_BWD_XSTAGE && a.Xcur.p;
+    const size_t smem = (xst ? BwdT<N>::total_x : BwdT<N>::total) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(small_backward_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(small_backward_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(BwdT<N>::total_x * sizeof(double)));
       attr = true;
     }
     small_backward_tma_kernel<N><<<(unsigned)((nc + kBwdCols - 1) / kBwdCols), 2 * kBwdCols, smem, s>>>(a, m);
