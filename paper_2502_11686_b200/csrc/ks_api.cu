@@ -182,14 +182,14 @@ size_t carve(ks_ctx *c, char *base) {
     c->C0 = w.take<double>(sz(cC, (int64_t)mx * n) + 1);
     c->nC0 = w.take<double>(sz(cC, 1));
     c->y0 = w.take<double>(ptiled_doubles(N, mx) + 1);
-    c->zscratch = w.take<double>(nn + n);
+    c->zscratch = w.take<double>(nn + n + 2);   // + the split-odd-level flag
   } else {
     c->El0 = w.take<double>(c->cntE * nn);
     c->Er0 = w.take<double>(c->cntE * nn);
     c->e0 = w.take<double>(c->cntE * n);
     c->C0 = w.take<double>(c->cntC * mx * n + 1);
     c->y0 = w.take<double>(N * mx + 1);
-    c->zscratch = w.take<double>(nn + n);
+    c->zscratch = w.take<double>(nn + n + 2);   // + the split-odd-level flag
   }
   c->Mchol = w.take<double>((size_t)mx * mx + 1);
   c->Minv = w.take<double>((size_t)mx * mx + 1);

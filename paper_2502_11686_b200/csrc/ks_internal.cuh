@@ -45,6 +45,8 @@ struct FactorLevelArgs {
   int64_t step0;         // for status reporting only
   unsigned long long *status;
   double *zscratch;      // n (n + 1) doubles: the odd level's last-column leftover Z (row-major)
+                         // (+ one int flag behind it: split odd levels, set by launch_factor_level)
+  int *zflag;            // null: the last pair's CTA also eliminates the last column
 };
 
 struct BackwardLevelArgs {

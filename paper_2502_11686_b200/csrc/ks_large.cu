@@ -619,6 +619,24 @@ __device__ void cta_sum2(double a, double b, double *sh, double &sa, double &sb)
   __syncthreads();
 }
 
+// The odd level's last-column rows Z (n x (n+1), row-major in zscratch) into
+// rows r0.. of the stage-3 matrix.  Split odd level (a.zflag): they come from
+// another CTA -- wait for its flag, then read through L2 (ld.global.cg).
+__device__ void ld_zs(const FactorLevelArgs &a, double *A, int lda, int r0) {
+  const int n = a.n;
+  if (a.zflag) {
+    if (threadIdx.x == 0) {
+      while (atomicAdd(a.zflag, 0) == 0) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < n * (n + 1); idx += blockDim.x) {
+    const int i = idx / (n + 1), j = idx - i * (n + 1);
+    A[(r0 + i) + j * lda] = __ldcg(a.zscratch + idx);
+  }
+}
+
 // ---- shared-memory plan of the factor kernel ----
 struct FactorPlan {
   int ld1, cols1, ld2, cols2, ld3, cols3, ldv;
@@ -770,7 +788,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     ld_blk(B3, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
     int rows3 = 2 * RC;
     if (zs_in) {
-      ld_blk(B3, ld3, rows3, 0, a.zscratch, n + 1, n, n + 1, n);
+      ld_zs(a, B3, ld3, rows3);
       rows3 += n;
     }
     sync_loads();
@@ -804,7 +822,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     ld_blk(P2, ld3, RC, n, in.y + u * in.sy, 1, RC, 1, RC);
     int rows3 = 2 * RC;
     if (zs_in) {
-      ld_blk(P2, ld3, rows3, 0, a.zscratch, n + 1, n, n + 1, n);
+      ld_zs(a, P2, ld3, rows3);
       rows3 += n;
     }
     sync_loads();
@@ -921,18 +939,29 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs 
   extern __shared__ __align__(16) double sm[];
   const FactorPlan f = factor_plan(a.n, a.in.RC);
   const int64_t K = a.K, p = blockIdx.x;
+  // odd level: the last column (no right neighbour) by CTA K/2 beside the
+  // last pair when split (a.zflag), else first by the last pair's CTA
+  const bool split = a.zflag != nullptr;
   const bool single_only = (K == 1);
-  const bool triple = (K >= 3) && (K & 1) && (p == K / 2 - 1);
+  const bool triple = !split && (K >= 3) && (K & 1) && (p == K / 2 - 1);
+  const bool lastcol = split && p == K / 2;
   bool zs = false;
-  if (single_only || triple) {
+  if (single_only || triple || lastcol) {
     const int64_t ts = K - 1;
     const bool hl = (ts + a.t0) > 0;
     eliminate(a, sm, f, ts, false, hl, 0, false, hl);
+    if (lastcol) {
+      __threadfence();   // its Z rows (zscratch) visible device-wide before the flag
+      __syncthreads();
+      if (threadIdx.x == 0) atomicExch(a.zflag, 1);
+      return;
+    }
     zs = hl && triple;
   }
   if (!single_only) {
     const int64_t t = 2 * p;
-    eliminate(a, sm, f, t, true, (t + a.t0) > 0, p, zs, false);
+    const bool waits = split && p == K / 2 - 1 && (K - 1 + a.t0 > 0);
+    eliminate(a, sm, f, t, true, (t + a.t0) > 0, p, zs || waits, false);
   }
 }
 
@@ -1165,8 +1194,16 @@ cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s) {
     cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  const int64_t grid = a.K >= 2 ? a.K / 2 : 1;
-  factor_level_kernel<<<(unsigned)grid, kThreads, factor_smem_bytes(a.n, a.in.RC), s>>>(a);
+  FactorLevelArgs b = a;
+  b.zflag = nullptr;
+  int64_t grid = a.K >= 2 ? a.K / 2 : 1;
+  if (a.K >= 3 && (a.K & 1) && a.zscratch) {   // odd level: the last column in its own CTA
+    b.zflag = reinterpret_cast<int *>(a.zscratch + (int64_t)a.n * (a.n + 1));
+    cudaError_t e = cudaMemsetAsync(b.zflag, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    grid += 1;
+  }
+  factor_level_kernel<<<(unsigned)grid, kThreads, factor_smem_bytes(a.n, a.in.RC), s>>>(b);
   return cudaGetLastError();
 }
 
