@@ -59,7 +59,7 @@
 /* Relative tolerance for a diagonal entry of a final R_ii block, adapting
  * S:158 (the paper assumes full rank): |R_ii[d][d]| <=
  * RANK_TOL * ||stacked block column||_F is reported as rank deficient. */
-#define RANK_TOL 1e-13
+#define RANK_TOL 1e-12
 
 /* ---------------------------------------------------------------- dense ---- */
 
