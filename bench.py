@@ -6,8 +6,9 @@ constant-velocity model), time-sharded over N GPUs (strong scaling).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ks|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-One step = ks_whiten + ks_factor (+ boundary allgather + ks_factor_boundary
-on N > 1) + ks_solve_selinv (solve + SelInv in one backward sweep) with inputs resident in HBM (outputs bound
+One step = ks_whiten + ks_factor (on N > 1 the local levels, the library's
+NCCL allgather of the boundary columns and the boundary system) +
+ks_solve_selinv (solve + SelInv in one backward sweep) with inputs resident in HBM (outputs bound
 to caller buffers, so ks_get is free).  The working set (~11 GB) is far
 larger than L2 (126 MB), so no L2 flush is needed between steps.
 
@@ -53,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling runs: no e2e / cpu baseline")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the c1-c4 per_config block")
     return ap.parse_args()
 
 
@@ -179,6 +181,7 @@ def run_reference(a, world, rank):
     dt = (time.perf_counter() - t0) / a.steps
     v = S / dt
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "resources_used": {"gpus": 0, "host_cores": 1},
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -191,20 +194,100 @@ def run_reference(a, world, rank):
     return 0
 
 
+def relaunch(a):
+    """`--gpus N > 1` without a launcher: re-exec through torch.distributed.run
+    with one rank per GPU (the driver's own launch line)."""
+    import socket
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {a.gpus} but only {have} CUDA device(s) visible",
+                          "n_gpus": a.gpus}), flush=True)
+        return 1
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def timed_graph(run, stream, steps, warmup):
+    """CUDA-graph capture of one step, then `steps` replays timed with CUDA
+    events on the launching stream (ms per step)."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        run()
+    for _ in range(max(warmup, 1)):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, g
+
+
+def per_config(dev, stream, p64, steps=10):
+    """c1-c4 at full size in the same run (parity cases; c5 is the headline):
+    ms/step and steps/s with and without covariances (NC), and
+    the step against its algorithmic roofline (model.step_totals)."""
+    from paper_2502_11686_b200 import generators as gen
+    from paper_2502_11686_b200 import ks, model
+    bw = peaks()[0]
+    out = {}
+    for cfg in ("c1", "c2", "c3", "c4"):
+        p = gen.make(cfg)
+        strides = {"C": int(p.H.shape[0] > 1 or p.L.shape[0] > 1 or not bool((p.m == p.m_max).all())),
+                   "E": int(p.F.shape[0] > 1 or p.K.shape[0] > 1 or p.c is not None)}
+        res = {"N": p.N, "n": p.n, "m": p.m_max}
+        for variant, cov in (("states+cov", True), ("states_nc", False)):
+            sm = ks.Smoother(p, device=dev, stream=stream, cov=cov)
+            for _ in range(3):
+                sm.run(cov=cov)
+            sm.check()
+            l0 = sm.info()["launches"]
+            sm.run(cov=cov)
+            nl = sm.info()["launches"] - l0
+            ms, g = timed_graph(lambda: sm.run(cov=cov), stream, steps, 3)
+            sm.check()
+            sb, sf = model.step_totals(p.N, p.n, p.m_max, strides, cov=cov)
+            t_h, t_f = sb / (bw * 1e9), sf / (p64 * 1e12)
+            res[variant] = {"ms_per_step": ms, "steps_per_s": p.N / (ms / 1e3), "gpu_launches": nl,
+                            "algorithmic_bytes": sb, "algorithmic_flops": sf,
+                            "bound": "hbm" if t_h >= t_f else "fp64",
+                            "roofline_frac": max(t_h, t_f) / (ms / 1e3),
+                            "hbm_frac": t_h / (ms / 1e3), "fp64_frac": t_f / (ms / 1e3)}
+            del g, sm
+            torch.cuda.empty_cache()
+        out[cfg] = res
+    out["_note"] = ("CUDA-graph replay, inputs resident, 1 GPU; roofline_frac = max(bytes/HBM peak, "
+                    "flops/FP64 peak) / step time with the level-synchronous algorithmic totals of "
+                    "paper_2502_11686_b200/model.py (c3 counted at m = m_max, an upper bound)")
+    return out
+
+
 def main():
     a = parse()
     world, rank, local = dist_env()
     if a.impl == "reference":
         return run_reference(a, world, rank)
+    if world == 1 and a.gpus > 1:
+        return relaunch(a)
+    if world != a.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {a.gpus}")
     from paper_2502_11686_b200 import generators as gen
     from paper_2502_11686_b200 import ks, model
     from paper_2502_11686_b200 import dist as kdist
     assert torch.cuda.is_available(), "bench needs a GPU (there is no CPU fallback)"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
     P = world
+    nccl = None
+    if P > 1:
+        dist.init_process_group("nccl", device_id=dev)
     p = gen.make(a.config, N=a.N)
     N = p.N
     lo, hi = kdist.shard_range(N, rank, P)
@@ -218,21 +301,30 @@ def main():
     torch.cuda.set_stream(stream)
     p64 = ks.peak_fp64_tflops(stream)
 
-    sm = ks.Smoother(local_p, device=dev, stream=stream, shard=(rank, P, None) if P > 1 else None)
-    views = sm.boundary_tensors() if P > 1 else None
+    kd = None
+    if P > 1:
+        # the library's own NCCL communicator (ks_dist_*): rank 0's unique id
+        # travels over the torch process group; ks_factor then allgathers the
+        # boundary columns itself, on the context's stream
+        obj = [ks.Dist.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        kd = ks.Dist(rank, P, lo, N, uid=obj[0], device=dev)
+        nccl = kd.info()
+        nccl["torch_nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
+        print(f"[rank {rank}] ks_dist: NCCL communicator with {nccl['nccl_nranks']} ranks", file=sys.stderr,
+              flush=True)
 
-    def step(s, v, get=None):
+    sm = ks.Smoother(local_p, device=dev, stream=stream, dist=kd)
+
+    def step(s, get=None):
         s.whiten()
-        s.factor()
-        if P > 1:
-            kdist.exchange_boundary(v[0], v[1])
-            s.factor_boundary()
+        s.factor()          # P > 1: local levels, NCCL boundary allgather, boundary system
         s.solve_selinv()
         if get is not None:
             s.get(*get)
 
     for _ in range(max(a.warmup, 1)):
-        step(sm, views)
+        step(sm)
     sm.check()
     torch.cuda.synchronize()
     if P > 1:
@@ -243,7 +335,7 @@ def main():
     sm.set_timing(True)
     l0 = sm.info()["launches"]
     for _ in range(a.steps):
-        step(sm, views)
+        step(sm)
     launches = sm.launch_times()
     n_launch = (sm.info()["launches"] - l0) // a.steps
     fam_ms = {}
@@ -253,17 +345,17 @@ def main():
     sm.check()
 
     # (2) the headline: K steps as CUDA-graph replays (one graph = one step's
-    # ~50 launches; 1 GPU) or eagerly (N > 1: the step contains the NCCL
-    # boundary allgather), CUDA events on the launching stream
+    # launches, the NCCL allgather included on N > 1), or eagerly with
+    # --no-graph; CUDA events on the launching stream, max over ranks
     graph = None
-    if P == 1 and not a.no_graph:
+    if not a.no_graph:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
-            step(sm, views)
+            step(sm)
         for _ in range(max(a.warmup, 1)):
             graph.replay()
         torch.cuda.synchronize()
-    run = graph.replay if graph is not None else (lambda: step(sm, views))
+    run = graph.replay if graph is not None else (lambda: step(sm))
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
@@ -296,23 +388,21 @@ def main():
         graph = None
         del sm
         torch.cuda.empty_cache()
-        s2 = ks.Smoother(local_p, device=dev, host_inputs=True, bind_outputs=False,
-                         shard=(rank, P, None) if P > 1 else None)
-        v2 = s2.boundary_tensors() if P > 1 else None
+        s2 = ks.Smoother(local_p, device=dev, stream=stream, host_inputs=True, bind_outputs=False, dist=kd)
         xh = torch.empty((M, p.n), dtype=torch.float64).pin_memory()
         Sh = torch.empty((M, p.n, p.n), dtype=torch.float64).pin_memory()
         h2d = sum(t.numel() * t.element_size() for t in s2.inputs.values() if t is not None)
         d2h = xh.numel() * 8 + Sh.numel() * 8
         ke = max(1, min(a.steps, 5))
         for _ in range(max(a.warmup, 1)):
-            step(s2, v2, (xh, Sh))
+            step(s2, (xh, Sh))
         s2.check()
         if P > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(ke):
-            step(s2, v2, (xh, Sh))
+            step(s2, (xh, Sh))
         e1.record(stream)
         torch.cuda.synchronize()
         mse = e0.elapsed_time(e1) / ke
@@ -322,8 +412,11 @@ def main():
                "d2h_bytes_per_step": int(d2h * P), "ms_per_step": mse, "steps": ke,
                "path": "ks_create(KS_HOST_INPUTS) pinned host inputs -> whiten(H2D) .. selinv -> "
                        "ks_get(pinned host states, cov)"}
+        del s2
+        torch.cuda.empty_cache()
 
     cpu = None
+    cfgs = None
     if rank == 0 and P == 1 and not (a.no_cpu_baseline or a.quick):
         import oracle
         S = min(a.cpu_sample, N)
@@ -336,6 +429,8 @@ def main():
                "sample": f"first {S} of the {N} steps, one pass of the plain-C sequential "
                          f"Paige-Saunders + Alg. 1 oracle ({dt:.1f} s, 1 thread)",
                "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+    if rank == 0 and P == 1 and not (a.quick or a.no_per_config):
+        cfgs = per_config(dev, stream, p64)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps,
@@ -343,14 +438,18 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": f"synthetic: generators.make('{a.config}') (seeded, BASELINE.json recipe)",
                 "config": {"workload": workload_desc(a.config, N), "N": N, "n": p.n, "m": p.m_max,
-                           "parallelism": f"time-shard x{P}" if P > 1 else "1 GPU",
+                           "parallelism": f"time-shard x{P} (NCCL allgather of the boundary columns)"
+                           if P > 1 else "1 GPU",
                            "l2": "working set (~11 GB at c5) >> 126 MB L2; no flush"},
                 "roofline": rl, "step_roofline": step_rl, "cpu_baseline": cpu, "e2e": e2e,
                 "timing": timing,
                 "gpu_launches": int(n_launch), "clocks": clocks,
-                "phases_ms": fam_ms, "fp64_peak_tflops": p64}
+                "phases_ms": fam_ms, "fp64_peak_tflops": p64, "nccl": nccl,
+                "per_config": cfgs}
         print(json.dumps(line), flush=True)
     if P > 1:
+        dist.barrier()
+        del kd
         dist.destroy_process_group()
     return 0
 

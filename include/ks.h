@@ -48,7 +48,7 @@ enum {
     KS_ERR_CUDA = 3,      /* a CUDA launch/runtime call failed                  */
     KS_ERR_NCCL = 4,      /* NCCL missing or an NCCL call failed (multi-GPU)    */
     KS_ERR_NOT_SPD = 5,   /* K_i or L_i not SPD: Cholesky pivot <= 0     */
-    KS_ERR_RANK = 6,      /* UA rank deficient: |R_jj[d][d]| <= 1e-13*|stack|_F */
+    KS_ERR_RANK = 6,      /* UA rank deficient: |R_jj[d][d]| <= 1e-12*|stack|_F */
     KS_ERR_WORKSPACE = 7  /* workspace too small or misaligned                  */
 };
 
@@ -62,9 +62,16 @@ enum {
     KS_GENERIC_PATH = 4u, /* force the CTA-per-pair shared-memory kernels even
                              when n, m_max <= 8 (default there: one thread per
                              pair, registers + Givens; used to cross-check)     */
-    KS_NO_FUSED_TAIL = 8u /* small path: launch every factor level separately
+    KS_NO_FUSED_TAIL = 8u,/* small path: launch every factor level separately
                              instead of running the recursion's tail (levels
                              with few columns) in one on-chip kernel (cross-check) */
+    KS_COV_IS_CHOL = 16u  /* K and L hold lower-triangular Cholesky factors
+                             Lam_i (K_i = Lam Lam^T) and M_i (L_i = M M^T) instead
+                             of the covariances ("whitening factors K_i, L_i",
+                             BASELINE north_star; any V with V^T V = K^{-1} is a
+                             valid whitening).  Only the lower
+                             triangle is read; a zero diagonal entry is recorded
+                             as KS_ERR_NOT_SPD                                   */
 };
 
 /* One problem (or, multi-GPU, one rank's contiguous shard of steps).
@@ -85,26 +92,43 @@ typedef struct ks_problem {
     const double *K;         /* [N][n][n]      evolution-noise covariance (SPD)     */
     const double *L;         /* [N][m_max][m_max] observation-noise covariance (SPD) */
     int64_t sF, sH, sc, so, sK, sL;   /* per-step strides in doubles, 0 = constant */
-    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL */
+    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL | KS_COV_IS_CHOL */
 } ks_problem;
 
 #define KS_MAX_N 64
 #define KS_MAX_M 64
 
-/* Multi-GPU time sharding.  NULL = one GPU owns all steps.
- * Every rank passes nsteps = N_global / nranks, which must be a power of two;
- * rank r owns global steps [r*nsteps, (r+1)*nsteps).  The boundary exchange
- * is one allgather of each rank's reduced boundary column, done by ks_factor
- * through the NCCL communicator given here (an ncclComm_t cast to void*), or,
- * with comm == NULL, through the caller: see ks_boundary_buffers. */
-typedef struct ks_shard {
-    int32_t rank;
-    int32_t nranks;
-    void *nccl_comm;         /* ncclComm_t or NULL (caller-driven exchange)        */
-} ks_shard;
+/* Multi-GPU time sharding.  One process per GPU.
+ * Rank r owns the contiguous global steps [first_global_step,
+ * first_global_step + nsteps) with nsteps = nsteps_global / nranks a power of
+ * two >= 2 and first_global_step = r * nsteps.  Every rank reduces its steps
+ * to one boundary column with no communication (the coupling row of a shard's
+ * first step is stored with that step, so there is no halo); the P boundary
+ * columns are exchanged with ONE allgather of (3n^2+2n+1) doubles per rank,
+ * factored, solved and inverted redundantly on every rank, and each rank then
+ * runs its local backward levels.
+ *
+ * ks_dist_unique_id (rank 0 only; broadcast the 128 bytes through
+ * torch.distributed or any other channel) and ks_dist_create (collective over
+ * the ranks, with the rank's CUDA device current) create a library-owned NCCL
+ * communicator (libnccl.so.2 is dlopen'ed: no link-time dependency); ks_factor
+ * then performs the allgather itself on the context's stream (capturable in a
+ * CUDA graph).  With id == NULL there is no communicator and the caller drives
+ * the exchange: ks_factor returns after the local levels, the caller
+ * allgathers the ks_boundary_buffers `send` buffers into `recv` (rank order)
+ * on the context's stream and calls ks_factor_boundary.  A ks_dist is
+ * borrowed by every context created with it and must outlive them. */
+typedef struct ks_dist ks_dist;
+int ks_dist_unique_id(unsigned char id[128]);                   /* KS_ERR_NCCL: no NCCL */
+int ks_dist_create(ks_dist **out, int rank, int nranks, const unsigned char *id /* 128 bytes or NULL */,
+                   int64_t first_global_step, int64_t nsteps_global);
+/* rank, nranks, and the NCCL communicator's own rank count (ncclCommCount;
+ * 0 without a communicator). */
+int ks_dist_info(const ks_dist *d, int *rank, int *nranks, int *nccl_nranks);
+void ks_dist_destroy(ks_dist *d);
 
 /* Bytes of device workspace a context needs (0 on bad arguments). */
-size_t ks_workspace_bytes(const ks_problem *p, const ks_shard *shard);
+size_t ks_workspace_bytes(const ks_problem *p, const ks_dist *dist /* NULL = one GPU */);
 
 /* Create a context.  `workspace` is a device buffer of >= ks_workspace_bytes
  * bytes, 256-byte aligned, borrowed for the context's lifetime.  `stream` is a
@@ -112,9 +136,9 @@ size_t ks_workspace_bytes(const ks_problem *p, const ks_shard *shard);
  * the work enqueued by ks_whiten has completed.  `states_out` ([N][n]) and
  * `cov_out` ([N][n][n]) are optional DEVICE buffers that ks_solve / ks_selinv
  * write directly (zero-copy); when NULL, results live in the workspace and
- * ks_get copies them out.  The shard struct is copied. */
+ * ks_get copies them out.  `dist` (NULL = one GPU) is borrowed. */
 int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_bytes,
-              void *stream, const ks_shard *shard, double *states_out, double *cov_out);
+              void *stream, const ks_dist *dist, double *states_out, double *cov_out);
 
 /* Phase 1: Cholesky K_i = Lam Lam^T, L_i = M M^T and
  * triangular solves: C_i = M^{-1}H_i, y_i = M^{-1}o_i, -B_i = -Lam^{-1}F_i,
@@ -150,11 +174,13 @@ int ks_solve_selinv(ks_ctx *ctx);
 int ks_get(ks_ctx *ctx, double *states, double *cov);
 
 /* Synchronise the stream and report the first numerical failure:
- * KS_OK, KS_ERR_NOT_SPD (bad_kind 1 = K, 2 = L) or KS_ERR_RANK; bad_step is
- * the local step index (or -1).  Also surfaces asynchronous CUDA errors. */
+ * KS_OK, KS_ERR_NOT_SPD (bad_kind 1 = K, 2 = L), KS_ERR_RANK, or (small path,
+ * n, m_max <= 8) KS_ERR_ARG with bad_kind 3 when a whitened block column's
+ * norm lies outside [1e-80, 1e60] (the Givens kernels' exponent range); bad_step
+ * is the local step index (or -1).  Also surfaces asynchronous CUDA errors. */
 int ks_sync_status(ks_ctx *ctx, int64_t *bad_step, int *bad_kind);
 
-/* Multi-GPU with nccl_comm == NULL: after ks_factor returns KS_OK on every
+/* Multi-GPU without a communicator (ks_dist_create with id == NULL): after ks_factor returns KS_OK on every
  * rank, the caller allgathers `send` (bytes each) from every rank into
  * `recv` (nranks * bytes, rank order) on the context's stream, then calls
  * ks_factor_boundary.  Device pointers inside the workspace. */
@@ -184,6 +210,13 @@ int ks_info(ks_ctx *ctx, int64_t *levels, int64_t *launches);
  * TFLOP/s (a DFMA-chain kernel over all SMs, best of 3, on `stream`), the
  * FP64 roofline denominator (MEASURED_PEAKS.json has none).  <= 0 on error. */
 double ks_peak_fp64_tflops(void *stream);
+
+/* Debug export of the host level plan every context uses (SURVEY §8(a) a2,
+ * P:381-422): level[j] = the recursion level at which step
+ * j < N is eliminated (the number of trailing one bits of j, the last
+ * surviving column at the top level).  Returns the number of levels
+ * (floor(log2 N) + 1), or -KS_ERR_ARG; level may be NULL. */
+int ks_level_of_steps(int64_t N, int32_t *level);
 
 const char *ks_strerror(int code);
 void ks_destroy(ks_ctx *ctx);

@@ -34,14 +34,26 @@ struct Carve {
 };
 
 // ---- NCCL (dlopen'ed: the library has no link-time NCCL dependency) ----
+struct NcclUid {
+  char internal[128];
+};
 typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int /*ncclDataType_t*/, void *,
                                  cudaStream_t);
+typedef int (*nccl_uid_fn)(NcclUid *);
+typedef int (*nccl_init_fn)(void **, int, NcclUid, int);
+typedef int (*nccl_destroy_fn)(void *);
+typedef int (*nccl_count_fn)(void *, int *);
 
 struct Nccl {
   void *h = nullptr;
   nccl_allgather_fn allgather = nullptr;
+  nccl_uid_fn uid = nullptr;
+  nccl_init_fn init = nullptr;
+  nccl_destroy_fn destroy = nullptr;
+  nccl_count_fn count = nullptr;
   bool load() {
-    if (h) return allgather != nullptr;
+    if (h) return allgather && uid && init && destroy && count;
+    // an NCCL already loaded into the process (PyTorch's) is found by its soname
     const char *names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char *nm : names) {
       h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
@@ -49,12 +61,22 @@ struct Nccl {
     }
     if (!h) return false;
     allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
-    return allgather != nullptr;
+    uid = (nccl_uid_fn)dlsym(h, "ncclGetUniqueId");
+    init = (nccl_init_fn)dlsym(h, "ncclCommInitRank");
+    destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
+    count = (nccl_count_fn)dlsym(h, "ncclCommCount");
+    return allgather && uid && init && destroy && count;
   }
 };
 Nccl g_nccl;
 
 }  // namespace
+
+struct ks_dist {
+  int rank = 0, nranks = 1;
+  int64_t first = 0, nglobal = 0;
+  void *comm = nullptr;   // ncclComm_t (library-owned) or null: caller-driven exchange
+};
 
 struct ks_ctx {
   ks_problem p{};
@@ -65,7 +87,7 @@ struct ks_ctx {
   // sharding
   bool sharded = false;
   int rank = 0, nranks = 1, q = 0;
-  void *comm = nullptr;
+  void *comm = nullptr;   // the ks_dist's NCCL communicator (borrowed) or null
   // device views of the inputs
   const int32_t *m = nullptr;
   const double *F = nullptr, *H = nullptr, *c = nullptr, *o = nullptr, *K = nullptr, *L = nullptr;
@@ -87,6 +109,7 @@ struct ks_ctx {
   std::vector<double *> entb, rrecb, Xb;
   double *send = nullptr, *recv = nullptr, *bx = nullptr, *bS = nullptr, *hx = nullptr,
          *hS = nullptr, *Xq_local = nullptr;
+  bool chol = false;      // KS_COV_IS_CHOL
   // small-n path (ks_small.cu): element-major level arrays
   bool small = false;
   double *nC0 = nullptr, *nEr0 = nullptr, *nEl0 = nullptr, *zscratch = nullptr;
@@ -121,7 +144,9 @@ bool use_small(const ks_problem *p) {
 }
 
 
-int validate(const ks_problem *p, const ks_shard *sh) {
+constexpr uint32_t kAllFlags = KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL | KS_COV_IS_CHOL;
+
+int validate(const ks_problem *p, const ks_dist *d) {
   if (!p) return KS_ERR_ARG;
   if (p->nsteps < 1 || p->n < 1 || p->n > KS_MAX_N || p->m_max < 0 || p->m_max > KS_MAX_M)
     return KS_ERR_ARG;
@@ -131,16 +156,34 @@ int validate(const ks_problem *p, const ks_shard *sh) {
   if ((p->sF && p->sF < n * n) || (p->sK && p->sK < n * n) || (p->sH && p->sH < mx * n) ||
       (p->sL && p->sL < mx * mx) || (p->sc && p->sc < n) || (p->so && p->so < mx))
     return KS_ERR_ARG;
-  if (p->flags & ~(uint32_t)(KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL)) return KS_ERR_ARG;
+  if (p->flags & ~kAllFlags) return KS_ERR_ARG;
   if (!use_small(p)) {
     if (factor_smem_bytes(p->n, p->m_max > p->n ? p->m_max : p->n) > 227 * 1024) return KS_ERR_ARG;
     if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
   }
-  if (sh) {
-    if (sh->nranks < 1 || sh->rank < 0 || sh->rank >= sh->nranks) return KS_ERR_ARG;
-    if (sh->nranks > 1 && (!is_pow2(p->nsteps) || p->nsteps < 2)) return KS_ERR_ARG;
+  if (d && d->nranks > 1) {
+    // power-of-two shards in rank order (the local levels then follow the
+    // global trailing-ones rule with no halo)
+    if (!is_pow2(p->nsteps) || p->nsteps < 2) return KS_ERR_ARG;
+    if (d->nglobal != p->nsteps * d->nranks || d->first != p->nsteps * d->rank) return KS_ERR_ARG;
   }
   return KS_OK;
+}
+
+// The level plan: level L has K_L columns,
+// K_0 = N, K_{L+1} = floor(K_L / 2), down to one column (the base case,
+// P:797-799); column t of level L is step ((t + 1) << L) - 1, the even
+// columns (and an odd level's last column) are eliminated at L.  A sharded
+// context stops before level `stop` (= log2 of its power-of-two shard).
+std::vector<int64_t> level_sizes(int64_t N, int stop) {
+  std::vector<int64_t> Ks;
+  for (int64_t K = N, L = 0;; ++L) {
+    if (L == stop) break;
+    Ks.push_back(K);
+    if (K == 1) break;
+    K /= 2;
+  }
+  return Ks;
 }
 
 // Lay out (or just size, when base == nullptr) the workspace.
@@ -194,19 +237,16 @@ size_t carve(ks_ctx *c, char *base) {
   c->Mchol = w.take<double>((size_t)mx * mx + 1);
   c->Minv = w.take<double>((size_t)mx * mx + 1);
   // local levels
-  c->K_.clear(); c->ent.clear(); c->rrec.clear(); c->X.clear();
-  int64_t K = N;
-  for (int L = 0;; ++L) {
-    if (c->sharded && L == c->q) break;
-    c->K_.push_back(K);
+  c->K_ = level_sizes(N, c->sharded ? c->q : -1);
+  c->ent.clear(); c->rrec.clear(); c->X.clear();
+  for (size_t L = 0; L < c->K_.size(); ++L) {
+    const int64_t K = c->K_[L];
     const int64_t ne = sm ? ptiled_doubles(K, E) : K * E;
     const int64_t nr = sm ? tiled_doubles((K + 1) / 2, Rs) : ((K + 1) / 2) * Rr;
     const int64_t nx = sm ? tiled_doubles(K + 1, nn) : (K + 1) * nn;
     c->ent.push_back(L == 0 ? nullptr : w.take<double>(ne));
     c->rrec.push_back(w.take<double>(nr));
     c->X.push_back(L == 0 ? nullptr : w.take<double>(nx));
-    if (K == 1) break;
-    K /= 2;
   }
   if (c->sharded) {
     const int P = c->nranks;
@@ -221,10 +261,15 @@ size_t carve(ks_ctx *c, char *base) {
     int64_t Kb = P;
     for (int L = 0;; ++L) {
       c->Kb.push_back(Kb);
-      // the boundary system (P columns) always runs on the generic AoS kernels
-      c->entb.push_back(L == 0 ? c->recv : w.take<double>(Kb * E));
-      c->rrecb.push_back(w.take<double>(((Kb + 1) / 2) * Rr));
-      c->Xb.push_back(w.take<double>((Kb + 1) * nn));
+      if (sm) {   // the boundary system runs on the small-path kernels (tiled level arrays)
+        c->entb.push_back(w.take<double>(ptiled_doubles(Kb, E)));
+        c->rrecb.push_back(w.take<double>(tiled_doubles((Kb + 1) / 2, Rs)));
+        c->Xb.push_back(w.take<double>(tiled_doubles(Kb + 1, nn)));
+      } else {    // generic AoS kernels
+        c->entb.push_back(L == 0 ? c->recv : w.take<double>(Kb * E));
+        c->rrecb.push_back(w.take<double>(((Kb + 1) / 2) * Rr));
+        c->Xb.push_back(w.take<double>((Kb + 1) * nn));
+      }
       if (Kb == 1) break;
       Kb /= 2;
     }
@@ -317,23 +362,62 @@ SmallIn small_level0(const ks_ctx *c) {
   return v;
 }
 
-SmallFactorArgs small_factor_args(ks_ctx *c, size_t i) {
+// One recursion on the small path: the local domain (levels 0..), or, on a
+// sharded context, the P-column boundary system (global levels q..) that
+// every rank factors redundantly with the same per-column routines (so the
+// multi-GPU elimination order and arithmetic are the single-GPU ones).
+struct SmallPlan {
+  const std::vector<int64_t> *K;
+  const std::vector<double *> *ent, *rrec, *X;
+  bool l0;               // plan level 0 reads the whitened level-0 inputs
+  bool local;            // the local domain (t0 = rank * K; subtree pass allowed)
+  int lbase;             // global level of plan level 0 (status: plan-domain index)
+  double *send;          // AoS output of the last level (sharded local domain), else null
+  double *x, *S;         // plan-domain outputs
+  const double *xhalo, *Shalo;
+  double *Xtop;          // tiled cross blocks above the top level (sharded local: Xq_local)
+  bool xcur0;            // write the level-0 cross blocks (boundary: scattered to the ranks)
+};
+
+SmallPlan local_plan(ks_ctx *c) {
+  SmallPlan p;
+  p.K = &c->K_; p.ent = &c->ent; p.rrec = &c->rrec; p.X = &c->X;
+  p.l0 = true; p.local = true; p.lbase = 0;
+  p.send = c->sharded ? c->send : nullptr;
+  p.x = c->xout; p.S = c->Sout; p.xhalo = c->hx; p.Shalo = c->hS;
+  p.Xtop = c->sharded ? c->Xq_local : nullptr;
+  p.xcur0 = false;
+  return p;
+}
+
+SmallPlan boundary_plan(ks_ctx *c) {
+  SmallPlan p;
+  p.K = &c->Kb; p.ent = &c->entb; p.rrec = &c->rrecb; p.X = &c->Xb;
+  p.l0 = false; p.local = false; p.lbase = c->q;
+  p.send = nullptr;
+  p.x = c->bx; p.S = c->bS; p.xhalo = nullptr; p.Shalo = nullptr;
+  p.Xtop = nullptr;
+  p.xcur0 = true;
+  return p;
+}
+
+SmallFactorArgs small_factor_args(ks_ctx *c, const SmallPlan &pl, size_t i) {
   const int n = c->n;
   const int64_t E = entry_doubles(n), Rs = small_rrec_doubles(n);
-  const std::vector<int64_t> &Ks = c->K_;
+  const std::vector<int64_t> &Ks = *pl.K;
   SmallFactorArgs a;
   const bool last = i + 1 == Ks.size();
   a.in = small_level0(c);
-  if (i > 0) a.in.ent = tv(c->ent[i], 64 * E);
+  if (i > 0 || !pl.l0) a.in.ent = tv((*pl.ent)[i], 64 * E);
   a.outAoS = 0;
-  if (!last) a.out = tv(c->ent[i + 1], 64 * E);
-  else if (c->sharded) { a.out = tv(c->send, E); a.outAoS = 1; }
+  if (!last) a.out = tv((*pl.ent)[i + 1], 64 * E);
+  else if (pl.send) { a.out = tv(pl.send, E); a.outAoS = 1; }
   else a.out = tv(nullptr, 0);
-  a.rec = tv(c->rrec[i], 32 * Rs);
-  a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
+  a.rec = tv((*pl.rrec)[i], 32 * Rs);
+  a.t0 = (pl.local && c->sharded) ? (int64_t)c->rank * Ks[i] : 0;
   a.K = Ks[i];
-  a.level = (int)i;
-  a.lbase = 0;
+  a.level = pl.lbase + (int)i;
+  a.lbase = pl.lbase;
   a.step0 = 0;
   a.status = c->status;
   a.zscratch = c->zscratch;
@@ -343,27 +427,27 @@ SmallFactorArgs small_factor_args(ks_ctx *c, size_t i) {
   return a;
 }
 
-// First level run by the fused tail kernel (levels >= 1 with K <= the
-// kernel's shared-memory capacity, single GPU), or Ks.size() for none.
-size_t small_tail_start(const ks_ctx *c) {
-  const std::vector<int64_t> &Ks = c->K_;
+// First level run by the fused tail kernel (levels reading entries, with K
+// <= the kernel's shared-memory capacity), or Ks.size() for none.
+size_t small_tail_start(const ks_ctx *c, const SmallPlan &pl) {
+  const std::vector<int64_t> &Ks = *pl.K;
   const int64_t cap = small_tail_max_cols(c->n);
-  if (c->sharded || cap <= 0 || (c->p.flags & KS_NO_FUSED_TAIL)) return Ks.size();
-  for (size_t i = 1; i < Ks.size(); ++i)
+  if (cap <= 0 || (c->p.flags & KS_NO_FUSED_TAIL)) return Ks.size();
+  for (size_t i = pl.l0 ? 1 : 0; i < Ks.size(); ++i)
     if (Ks[i] <= cap) return (Ks.size() - i > (size_t)kMaxTailLevels) ? Ks.size() : i;
   return Ks.size();
 }
 
 // Subtree pass (levels [is, is + kSubLevels)): the first level ≥ 1 below the
 // tail whose K is a multiple of the subtree width with at most one subtree
-// per SM (the subtree kernel needs most of an SM's shared memory), single
-// GPU; returns Ks.size() for none.
+// per SM (the subtree kernel needs most of an SM's shared memory), local
+// domain only; returns Ks.size() for none.
 constexpr int kSubLevels = 7;   // subtree width 2^7 = 128 columns (tail_max_cols)
-size_t small_subtree_start(const ks_ctx *c) {
-  const std::vector<int64_t> &Ks = c->K_;
-  const size_t it = small_tail_start(c);
+size_t small_subtree_start(const ks_ctx *c, const SmallPlan &pl) {
+  const std::vector<int64_t> &Ks = *pl.K;
+  const size_t it = small_tail_start(c, pl);
   const int64_t W = 1ll << kSubLevels;
-  if (it >= Ks.size() || small_tail_max_cols(c->n) < W) return Ks.size();
+  if (!pl.l0 || it >= Ks.size() || small_tail_max_cols(c->n) < W) return Ks.size();
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   for (size_t i = 1; i + kSubLevels <= it; ++i)
@@ -371,76 +455,79 @@ size_t small_subtree_start(const ks_ctx *c) {
   return Ks.size();
 }
 
-SmallTailArgs small_tail_args(ks_ctx *c, size_t i0, int nlev, int64_t W) {
+SmallTailArgs small_tail_args(ks_ctx *c, const SmallPlan &pl, size_t i0, int nlev, int64_t W) {
   SmallTailArgs t;
-  t.base = small_factor_args(c, i0);
-  t.ent0 = c->ent[i0];
+  t.base = small_factor_args(c, pl, i0);
+  t.ent0 = (*pl.ent)[i0];
   t.W = W;
   t.nlev = nlev;
   for (int l = 0; l < nlev; ++l) {
-    t.K[l] = c->K_[i0 + l];
-    t.level[l] = (int)(i0 + l);
-    t.rec[l] = small_factor_args(c, i0 + l).rec;
+    t.K[l] = (*pl.K)[i0 + l];
+    t.level[l] = pl.lbase + (int)(i0 + l);
+    t.rec[l] = small_factor_args(c, pl, i0 + l).rec;
   }
-  t.out_last = small_factor_args(c, i0 + nlev - 1).out;
+  const SmallFactorArgs la = small_factor_args(c, pl, i0 + nlev - 1);
+  t.out_last = la.out;
+  t.out_last_aos = la.outAoS;
   return t;
 }
 
-int run_small_factor_levels(ks_ctx *c) {
+int run_small_factor_levels(ks_ctx *c, const SmallPlan &pl, int fam) {
   const int n = c->n;
-  const std::vector<int64_t> &Ks = c->K_;
-  const size_t it = small_tail_start(c), is = small_subtree_start(c);
+  const std::vector<int64_t> &Ks = *pl.K;
+  const size_t it = small_tail_start(c, pl), is = small_subtree_start(c, pl);
   for (size_t i = 0; i < it;) {
     if (i == is) {   // kSubLevels levels in one launch, one subtree per CTA
-      SmallTailArgs t = small_tail_args(c, i, kSubLevels, 1ll << kSubLevels);
-      Launch l(c, 1, (int)i, 1);
+      SmallTailArgs t = small_tail_args(c, pl, i, kSubLevels, 1ll << kSubLevels);
+      Launch l(c, fam, pl.lbase + (int)i, 1);
       cudaError_t e = launch_small_factor_tail(t, n, c->stream);
       if (e != cudaSuccess) return cuda_fail(e);
       i += kSubLevels;
       continue;
     }
-    SmallFactorArgs a = small_factor_args(c, i);
-    Launch l(c, 1, (int)i);
+    SmallFactorArgs a = small_factor_args(c, pl, i);
+    Launch l(c, fam, pl.lbase + (int)i);
     cudaError_t e = launch_small_factor(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
     ++i;
   }
   if (it < Ks.size()) {
-    SmallTailArgs t = small_tail_args(c, it, (int)(Ks.size() - it), 0);
-    Launch l(c, 1, (int)it, 1);
+    SmallTailArgs t = small_tail_args(c, pl, it, (int)(Ks.size() - it), 0);
+    Launch l(c, fam, pl.lbase + (int)it, 1);
     cudaError_t e = launch_small_factor_tail(t, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
   }
   return KS_OK;
 }
 
-SmallBackwardArgs small_backward_args(ks_ctx *c, int i, int do_state, int do_cov) {
+SmallBackwardArgs small_backward_args(ks_ctx *c, const SmallPlan &pl, int i, int do_state, int do_cov) {
   const int n = c->n;
   const int64_t nn = (int64_t)n * n, Rs = small_rrec_doubles(n);
-  const std::vector<int64_t> &Ks = c->K_;
+  const std::vector<int64_t> &Ks = *pl.K;
   SmallBackwardArgs a;
-  a.rec = tv(c->rrec[i], 32 * Rs);
+  a.rec = tv((*pl.rrec)[i], 32 * Rs);
   a.K = Ks[i];
   a.shift = i;
   a.do_state = do_state;
   a.do_cov = do_cov;
   const bool top = i + 1 == (int)Ks.size();
-  a.t0 = c->sharded ? (int64_t)c->rank * Ks[i] : 0;
-  a.x = c->xout; a.S = c->Sout; a.xhalo = c->hx; a.Shalo = c->hS;
-  if (!top) a.Xup = tv(c->X[i + 1], 32 * nn);
-  else a.Xup = c->sharded ? tv(c->Xq_local, 32 * nn) : tv(nullptr, 0);
-  a.Xcur = (i >= 1 && do_cov) ? tv(c->X[i], 32 * nn) : tv(nullptr, 0);
+  a.t0 = (pl.local && c->sharded) ? (int64_t)c->rank * Ks[i] : 0;
+  a.x = pl.x; a.S = pl.S; a.xhalo = pl.xhalo; a.Shalo = pl.Shalo;
+  if (!top) a.Xup = tv((*pl.X)[i + 1], 32 * nn);
+  else a.Xup = tv(pl.Xtop, pl.Xtop ? 32 * nn : 0);
+  a.Xcur = ((i >= 1 || pl.xcur0) && do_cov) ? tv((*pl.X)[i], 32 * nn) : tv(nullptr, 0);
   return a;
 }
 
-SmallBwdTailArgs small_bwd_tail_args(ks_ctx *c, int top, int bottom, int do_state, int do_cov, int64_t W) {
+SmallBwdTailArgs small_bwd_tail_args(ks_ctx *c, const SmallPlan &pl, int top, int bottom, int do_state,
+                                     int do_cov, int64_t W) {
   SmallBwdTailArgs t;
-  t.base = small_backward_args(c, top, do_state, do_cov);
+  t.base = small_backward_args(c, pl, top, do_state, do_cov);
   t.W = W;
-  t.nsub = W ? c->K_[bottom] / W : 1;
+  t.nsub = W ? (*pl.K)[bottom] / W : 1;
   t.nlev = 0;
   for (int i = top; i >= bottom; --i) {
-    const SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
+    const SmallBackwardArgs a = small_backward_args(c, pl, i, do_state, do_cov);
     t.K[t.nlev] = a.K;
     t.shift[t.nlev] = a.shift;
     t.rec[t.nlev] = a.rec;
@@ -451,31 +538,30 @@ SmallBwdTailArgs small_bwd_tail_args(ks_ctx *c, int top, int bottom, int do_stat
   return t;
 }
 
-int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
+int run_small_backward_levels(ks_ctx *c, const SmallPlan &pl, int do_state, int do_cov, int fam) {
   const int n = c->n;
-  const std::vector<int64_t> &Ks = c->K_;
-  const int it = (int)small_tail_start(c);   // the levels the fused factor tail ran
-  const int is = (int)small_subtree_start(c);
-  const int fam = do_cov ? (do_state ? 5 : 3) : 2;
+  const std::vector<int64_t> &Ks = *pl.K;
+  const int it = (int)small_tail_start(c, pl);   // the levels the fused factor tail ran
+  const int is = (int)small_subtree_start(c, pl);
   int top = (int)Ks.size() - 1;
   if (it < (int)Ks.size()) {
-    SmallBwdTailArgs t = small_bwd_tail_args(c, top, it, do_state, do_cov, 0);
-    Launch l(c, fam, it);
+    SmallBwdTailArgs t = small_bwd_tail_args(c, pl, top, it, do_state, do_cov, 0);
+    Launch l(c, fam, pl.lbase + it);
     cudaError_t e = launch_small_backward_tail(t, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
     top = it - 1;
   }
   for (int i = top; i >= 0;) {
     if (is < (int)Ks.size() && i == is + kSubLevels - 1) {   // the subtree pass, one subtree per CTA
-      SmallBwdTailArgs t = small_bwd_tail_args(c, i, is, do_state, do_cov, 1ll << kSubLevels);
-      Launch l(c, fam, is);
+      SmallBwdTailArgs t = small_bwd_tail_args(c, pl, i, is, do_state, do_cov, 1ll << kSubLevels);
+      Launch l(c, fam, pl.lbase + is);
       cudaError_t e = launch_small_backward_tail(t, n, c->stream);
       if (e != cudaSuccess) return cuda_fail(e);
       i = is - 1;
       continue;
     }
-    SmallBackwardArgs a = small_backward_args(c, i, do_state, do_cov);
-    Launch l(c, fam, i);
+    SmallBackwardArgs a = small_backward_args(c, pl, i, do_state, do_cov);
+    Launch l(c, fam, pl.lbase + i);
     cudaError_t e = launch_small_backward(a, n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e);
     --i;
@@ -484,7 +570,16 @@ int run_small_backward_levels(ks_ctx *c, int do_state, int do_cov) {
 }
 
 int run_factor_levels(ks_ctx *c, bool boundary) {
-  if (c->small && !boundary) return run_small_factor_levels(c);
+  if (c->small) {
+    if (!boundary) return run_small_factor_levels(c, local_plan(c), 1);
+    // the gathered AoS boundary entries -> the plan's tiled level-0 array
+    {
+      Launch l(c, 4, c->q);
+      cudaError_t e = launch_boundary_ptile(c->recv, c->entb[0], c->nranks, c->n, c->stream);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+    return run_small_factor_levels(c, boundary_plan(c), 4);
+  }
   const int n = c->n;
   const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
   const int Lb = boundary ? c->q : 0;
@@ -524,7 +619,9 @@ int run_factor_levels(ks_ctx *c, bool boundary) {
 // Timing families: 0 whiten, 1 factor levels, 2 solve levels, 3 selinv levels,
 // 4 boundary system (multi-GPU), 5 fused solve+selinv levels.
 int run_backward_levels(ks_ctx *c, bool boundary, int do_state, int do_cov) {
-  if (c->small && !boundary) return run_small_backward_levels(c, do_state, do_cov);
+  if (c->small)
+    return run_small_backward_levels(c, boundary ? boundary_plan(c) : local_plan(c), do_state, do_cov,
+                                     boundary ? 4 : (do_cov ? (do_state ? 5 : 3) : 2));
   const int n = c->n;
   const std::vector<int64_t> &Ks = boundary ? c->Kb : c->K_;
   for (int i = (int)Ks.size() - 1; i >= 0; --i) {
@@ -577,9 +674,9 @@ int scatter_boundary(ks_ctx *c, bool states, bool cov) {
       e = cudaMemcpyAsync(c->hS, c->bS + (r - 1) * nn, nn * 8, cudaMemcpyDeviceToDevice, c->stream);
       // slot -1 of the local level-q cross array: S_{b_{r-1}, b_r} = boundary X_q slot r-1
       if (e == cudaSuccess) {
-        if (c->small)   // tiled local layout: element e of column 0 (slot -1) at 32 e
-          e = cudaMemcpy2DAsync(c->Xq_local, 32 * 8, c->Xb[0] + (int64_t)r * nn, 8, 8, nn,
-                                cudaMemcpyDeviceToDevice, c->stream);
+        if (c->small)   // tiled layouts: column r of the boundary's level-0 cross array -> local column 0
+          e = cudaMemcpy2DAsync(c->Xq_local, 32 * 8, c->Xb[0] + (int64_t)(r >> 5) * 32 * nn + (r & 31), 32 * 8,
+                                8, nn, cudaMemcpyDeviceToDevice, c->stream);
         else
           e = cudaMemcpyAsync(c->Xq_local, c->Xb[0] + (int64_t)r * nn, nn * 8, cudaMemcpyDeviceToDevice,
                               c->stream);
@@ -593,15 +690,61 @@ int scatter_boundary(ks_ctx *c, bool states, bool cov) {
 
 extern "C" {
 
-size_t ks_workspace_bytes(const ks_problem *p, const ks_shard *sh) {
-  if (validate(p, sh) != KS_OK) return 0;
+int ks_dist_unique_id(unsigned char id[128]) {
+  if (!id) return KS_ERR_ARG;
+  if (!g_nccl.load()) return KS_ERR_NCCL;
+  NcclUid u;
+  if (g_nccl.uid(&u) != 0) return KS_ERR_NCCL;
+  memcpy(id, u.internal, 128);
+  return KS_OK;
+}
+
+int ks_dist_create(ks_dist **out, int rank, int nranks, const unsigned char *id, int64_t first_global_step,
+                   int64_t nsteps_global) {
+  if (!out) return KS_ERR_ARG;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || nsteps_global < 1 || first_global_step < 0 ||
+      first_global_step >= nsteps_global)
+    return KS_ERR_ARG;
+  ks_dist *d = new (std::nothrow) ks_dist;
+  if (!d) return KS_ERR_ARG;
+  d->rank = rank; d->nranks = nranks; d->first = first_global_step; d->nglobal = nsteps_global;
+  if (id && nranks > 1) {
+    if (!g_nccl.load()) { delete d; return KS_ERR_NCCL; }
+    NcclUid u;
+    memcpy(u.internal, id, 128);
+    if (g_nccl.init(&d->comm, nranks, u, rank) != 0) { delete d; return KS_ERR_NCCL; }
+  }
+  *out = d;
+  return KS_OK;
+}
+
+int ks_dist_info(const ks_dist *d, int *rank, int *nranks, int *nccl_nranks) {
+  if (!d) return KS_ERR_ARG;
+  if (rank) *rank = d->rank;
+  if (nranks) *nranks = d->nranks;
+  if (nccl_nranks) {
+    *nccl_nranks = 0;
+    if (d->comm && g_nccl.count(d->comm, nccl_nranks) != 0) return KS_ERR_NCCL;
+  }
+  return KS_OK;
+}
+
+void ks_dist_destroy(ks_dist *d) {
+  if (!d) return;
+  if (d->comm) g_nccl.destroy(d->comm);
+  delete d;
+}
+
+size_t ks_workspace_bytes(const ks_problem *p, const ks_dist *d) {
+  if (validate(p, d) != KS_OK) return 0;
   ks_ctx c;
   c.p = *p;
   c.N = p->nsteps; c.n = p->n; c.mx = p->m_max;
   c.host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
   c.small = use_small(p);
-  if (sh && sh->nranks > 1) {
-    c.sharded = true; c.rank = sh->rank; c.nranks = sh->nranks;
+  if (d && d->nranks > 1) {
+    c.sharded = true; c.rank = d->rank; c.nranks = d->nranks;
     int q = 0;
     while ((1ll << q) < p->nsteps) ++q;
     c.q = q;
@@ -610,13 +753,13 @@ size_t ks_workspace_bytes(const ks_problem *p, const ks_shard *sh) {
 }
 
 int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_bytes, void *stream,
-              const ks_shard *sh, double *states_out, double *cov_out) {
+              const ks_dist *d, double *states_out, double *cov_out) {
   if (!out) return KS_ERR_ARG;
   *out = nullptr;
-  int v = validate(p, sh);
+  int v = validate(p, d);
   if (v) return v;
   if (!workspace || ((uintptr_t)workspace % kAlign) != 0) return KS_ERR_WORKSPACE;
-  size_t need = ks_workspace_bytes(p, sh);
+  size_t need = ks_workspace_bytes(p, d);
   if (ws_bytes + kAlign < need) return KS_ERR_WORKSPACE;
   ks_ctx *c = new (std::nothrow) ks_ctx;
   if (!c) return KS_ERR_ARG;
@@ -624,13 +767,13 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
   c->N = p->nsteps; c->n = p->n; c->mx = p->m_max;
   c->stream = (cudaStream_t)stream;
   c->host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
+  c->chol = (p->flags & KS_COV_IS_CHOL) != 0;
   c->small = use_small(p);
-  if (sh && sh->nranks > 1) {
-    c->sharded = true; c->rank = sh->rank; c->nranks = sh->nranks; c->comm = sh->nccl_comm;
+  if (d && d->nranks > 1) {
+    c->sharded = true; c->rank = d->rank; c->nranks = d->nranks; c->comm = d->comm;
     int q = 0;
     while ((1ll << q) < p->nsteps) ++q;
     c->q = q;
-    if (c->comm && !g_nccl.load()) { delete c; return KS_ERR_NCCL; }
   }
   c->xout = states_out;
   c->Sout = cov_out;
@@ -676,6 +819,7 @@ int ks_whiten(ks_ctx *c) {
     a.cC = c->cntC == 1;
     a.Mchol = c->Mchol; a.status = c->status;
     a.Minv = small_yfuse(c) ? c->Minv : nullptr;
+    a.chol = c->chol;
     int nl = 0;
     {
       Launch l(c, 0, 0, 1);
@@ -693,6 +837,7 @@ int ks_whiten(ks_ctx *c) {
   a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
   a.C = c->C0; a.y = c->y0; a.El = c->El0; a.Er = c->Er0; a.e = c->e0;
   a.cntE = c->cntE; a.cntC = c->cntC; a.Mchol = c->Mchol; a.status = c->status;
+  a.chol = c->chol;
   a.constC = (c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr);
   {
     Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
@@ -808,6 +953,10 @@ int ks_sync_status(ks_ctx *c, int64_t *bad_step, int *bad_kind) {
   const int kind = (int)(st & 0xff);
   if (bad_step) *bad_step = (int64_t)(st >> 8) - 1;
   if (kind == kBadRank) return KS_ERR_RANK;
+  if (kind == kBadScale) {   // small path: whitened data outside its exponent range
+    if (bad_kind) *bad_kind = 3;
+    return KS_ERR_ARG;
+  }
   if (bad_kind) *bad_kind = kind;
   return KS_ERR_NOT_SPD;
 }
@@ -876,6 +1025,15 @@ int ks_info(ks_ctx *c, int64_t *levels, int64_t *launches) {
   if (levels) *levels = (int64_t)c->K_.size() + (int64_t)c->Kb.size();
   if (launches) *launches = c->launches;
   return KS_OK;
+}
+
+int ks_level_of_steps(int64_t N, int32_t *level) {
+  if (N < 1) return -KS_ERR_ARG;
+  const std::vector<int64_t> Ks = level_sizes(N, -1);
+  for (size_t L = 0; L < Ks.size(); ++L)
+    for (int64_t t = 0; t < Ks[L]; t += 2)
+      if (level) level[((t + 1) << L) - 1] = (int32_t)L;
+  return (int)Ks.size();
 }
 
 const char *ks_strerror(int code) {

@@ -7,13 +7,13 @@
 namespace ks {
 
 // Status word: min over (step+1) << 8 | kind, written with atomicMin.
-enum BadKind : int { kBadK = 1, kBadL = 2, kBadRank = 3 };
+enum BadKind : int { kBadK = 1, kBadL = 2, kBadRank = 3, kBadScale = 4 };
 constexpr unsigned long long kStatusOk = ~0ull;
 
-// Relative rank tolerance: |R_jj[d][d]| <= 1e-13 * |block column j of UA|_F
+// Relative rank tolerance: |R_jj[d][d]| <= 1e-12 * |block column j of UA|_F
 // (the Frobenius norm of the original whitened block column, which Q^T
 // preserves; reading R9).
-constexpr double kRankTol = 1e-13;
+constexpr double kRankTol = 1e-12;
 
 // A level's reduced system: column t owns a C-like block
 // C_t [RC x n] with RHS y_t [RC], and (if it has a left neighbour) the
@@ -75,6 +75,7 @@ struct WhitenArgs {
   int64_t cntE, cntC;    // number of distinct evolution / observation blocks (1 or N)
   int constC;            // constant observation model (H, L stride 0, m = NULL): y by a separate kernel
   double *Mchol;         // [m_max x m_max] scratch when constC
+  int chol;              // KS_COV_IS_CHOL: K, L already hold the lower Cholesky factors
   unsigned long long *status;
 };
 
@@ -134,6 +135,7 @@ struct SmallTailArgs {
   const double *ent0;          // level-L_t entries (global, pair-interleaved tiles)
   int64_t W;                   // 0: one CTA, whole levels; else subtree width per CTA (power of 2)
   TView out_last;              // entries of the level after the last fused one (null at the top)
+  int out_last_aos;            // out_last is an AoS entry (the sharded rank's boundary send buffer)
   int nlev;
   int64_t K[kMaxTailLevels];
   int level[kMaxTailLevels];
@@ -171,6 +173,7 @@ struct SmallWhitenArgs {
   int cE, cC;                  // layout flags of the above (1 = constant block)
   double *Mchol;               // m_max^2 scratch (constant observation model)
   double *Minv;                // m_max^2: M^{-1} for the factor's fused y (null: small_whiten_y)
+  int chol;                    // KS_COV_IS_CHOL: K, L already hold the lower Cholesky factors
   unsigned long long *status;
 };
 size_t small_entry_doubles(int n);                  // = entry_doubles(n)
@@ -181,6 +184,13 @@ cudaError_t launch_small_backward(const SmallBackwardArgs &a, int n, cudaStream_
 cudaError_t launch_small_factor_tail(const SmallTailArgs &t, int n, cudaStream_t s);
 cudaError_t launch_small_backward_tail(const SmallBwdTailArgs &t, int n, cudaStream_t s);
 int small_tail_max_cols(int n);     // levels with K <= this run in the fused tail kernel
+// Multi-GPU boundary system on the small path: the P gathered AoS boundary
+// entries (rank order) -> a pair-interleaved tiled level array of P columns.
+cudaError_t launch_boundary_ptile(const double *recv, double *out, int P, int n, cudaStream_t s);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute belongs to a device context, so a per-process flag is wrong
+// with several devices.  Thread-safe; kernels are identified by address.
+cudaError_t set_smem_attr(const void *func, int bytes);
 
 // kernel launchers of the CTA path (ks_large.cu); return cudaGetLastError()
 cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s);

@@ -529,6 +529,18 @@ __device__ bool cta_chol(double *Lm, int ldl, int d, double *sh) {
   return ok;
 }
 
+// KS_COV_IS_CHOL: the loaded lower triangle already is the factor; valid iff
+// every diagonal entry is nonzero and finite.  Result valid in every thread
+// (ends with __syncthreads).
+__device__ bool chol_diag_ok(const double *Lm, int ldl, int d, double *sh) {
+  __syncthreads();
+  const bool bad = threadIdx.x < d && !(Lm[threadIdx.x + threadIdx.x * ldl] != 0.0 &&
+                                        Lm[threadIdx.x + threadIdx.x * ldl] - Lm[threadIdx.x + threadIdx.x * ldl] == 0.0);
+  const int any = __syncthreads_or(bad);
+  (void)sh;
+  return !any;
+}
+
 __device__ void zero_smem(double *p, int count) {
   for (int i = threadIdx.x; i < count; i += blockDim.x) p[i] = 0.0;
 }
@@ -938,13 +950,16 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
 __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs a) {
   extern __shared__ __align__(16) double sm[];
   const FactorPlan f = factor_plan(a.n, a.in.RC);
-  const int64_t K = a.K, p = blockIdx.x;
-  // odd level: the last column (no right neighbour) by CTA K/2 beside the
-  // last pair when split (a.zflag), else first by the last pair's CTA
+  const int64_t K = a.K;
+  // odd level: the last column (no right neighbour) by CTA 0 beside the last
+  // pair (CTA K/2) when split (a.zflag), else first by the last pair's CTA.
+  // The flag-setting CTA has the LOWEST index, so it is dispatched before
+  // the CTA that waits for it even when only one CTA is resident at a time.
   const bool split = a.zflag != nullptr;
+  const int64_t p = split ? (int64_t)blockIdx.x - 1 : (int64_t)blockIdx.x;
   const bool single_only = (K == 1);
   const bool triple = !split && (K >= 3) && (K & 1) && (p == K / 2 - 1);
-  const bool lastcol = split && p == K / 2;
+  const bool lastcol = split && p < 0;
   bool zs = false;
   if (single_only || triple || lastcol) {
     const int64_t ts = K - 1;
@@ -1094,7 +1109,7 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
   __syncthreads();
   for (int k = tid; k < nn; k += blockDim.x) {   // asynchronous loads
     const int r = k / n, cc = k - r * n;
-    cp8(&Lm[r + cc * ld], K + k);
+    if (!a.chol || cc <= r) cp8(&Lm[r + cc * ld], K + k);   // KS_COV_IS_CHOL: lower triangle only
     cp8(&X[r + cc * ld], F + k);
   }
   for (int r = tid; r < n; r += blockDim.x) {
@@ -1102,7 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
     X[r + 2 * n * ld] = c ? c[r] : 0.0;
   }
   sync_loads();
-  const bool ok = cta_chol(Lm, ld, n, sh);
+  const bool ok = a.chol ? chol_diag_ok(Lm, ld, n, sh) : cta_chol(Lm, ld, n, sh);
   if (tid == 0 && !ok) {
     const int64_t step = (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i;
     report(a.status, step, kBadK);
@@ -1132,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   __syncthreads();
   for (int k = tid; k < mi * mi; k += blockDim.x) {   // asynchronous loads
     const int r = k / mi, cc = k - r * mi;
-    cp8(&Lm[r + cc * ld], L + r * mx + cc);
+    if (!a.chol || cc <= r) cp8(&Lm[r + cc * ld], L + r * mx + cc);   // KS_COV_IS_CHOL: lower only
   }
   for (int k = tid; k < mi * n; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
@@ -1140,7 +1155,7 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   }
   for (int r = tid; r < mi; r += blockDim.x) cp8(&X[r + n * ld], o + r);
   sync_loads();
-  const bool ok = cta_chol(Lm, ld, mi, sh);
+  const bool ok = a.chol ? chol_diag_ok(Lm, ld, mi, sh) : cta_chol(Lm, ld, mi, sh);
   if (tid == 0 && !ok) report(a.status, i, kBadL);
   diag_rcp(Lm, ld, mi, sh);
   __syncthreads();
@@ -1188,12 +1203,7 @@ size_t factor_smem_bytes(int n, int RC) { return 8 * (size_t)factor_plan(n, RC).
 size_t backward_smem_bytes(int n) { return 8 * (size_t)bwd_plan(n).total; }
 
 cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  set_smem_attr((const void *)factor_level_kernel, 227 * 1024);
   FactorLevelArgs b = a;
   b.zflag = nullptr;
   int64_t grid = a.K >= 2 ? a.K / 2 : 1;
@@ -1208,23 +1218,15 @@ cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_backward_level(const BackwardLevelArgs &a, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  set_smem_attr((const void *)backward_level_kernel, 227 * 1024);
   const int64_t grid = (a.K + 1) / 2;
   backward_level_kernel<<<(unsigned)grid, kThreads, backward_smem_bytes(a.n), s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(whiten_evo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(whiten_obs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  set_smem_attr((const void *)whiten_evo_kernel, 227 * 1024);
+  set_smem_attr((const void *)whiten_obs_kernel, 227 * 1024);
   const int n = a.n, mx = a.m_max;
   whiten_evo_kernel<<<(unsigned)a.cntE, kThreads, whiten_evo_smem(n), s>>>(a);
   if (mx > 0) {

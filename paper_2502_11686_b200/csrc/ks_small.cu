@@ -2,6 +2,10 @@
 // (ks_small_n<n>.cu); the kernels themselves are in ks_small_impl.cuh.
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "ks_internal.cuh"
 
 namespace ks {
@@ -66,6 +70,35 @@ int small_tail_max_cols(int n) {
 }
 cudaError_t launch_small_whiten(const SmallWhitenArgs &a, cudaStream_t s, int *nlaunch) {
   KS_SMALL_DISPATCH(whiten_n, a.n, a, s, nlaunch)
+}
+
+// Gathered AoS boundary entries (rank r at recv + r E) -> pair-interleaved
+// tiles: element e of column t at (t >> 6) 64E + (t & 1) 32E + 32 e + ((t >> 1) & 31).
+__global__ void boundary_ptile_kernel(const double *__restrict__ recv, double *__restrict__ out, int P, int E) {
+  const int64_t total = (int64_t)P * E;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx / E, e = idx - t * E;
+    out[(t >> 6) * 64 * E + (t & 1) * 32 * E + 32 * e + ((t >> 1) & 31)] = recv[idx];
+  }
+}
+cudaError_t launch_boundary_ptile(const double *recv, double *out, int P, int n, cudaStream_t s) {
+  const int E = (int)entry_doubles(n);
+  const int64_t total = (int64_t)P * E;
+  boundary_ptile_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(recv, out, P, E);
+  return cudaGetLastError();
+}
+
+cudaError_t set_smem_attr(const void *func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({func, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({func, dev});
+  return e;
 }
 
 }  // namespace ks

@@ -273,7 +273,12 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   auto ldE = [&](int e, int64_t c) {
     return L0 ? (CE ? cst[CstOff<N>::e + e] : ldv<64>(in.e, c, e)) : lde(c, EN::e + e);
   };
-  auto sto = [&](int e, double v) { stv<ESO>(a.out, pnext - a.out_off, e, v); };
+  // survivor entry store; the fused tail's last level may write the sharded
+  // rank's AoS boundary send entry (a.outAoS, a runtime choice there only)
+  auto sto = [&](int e, double v) {
+    if (SIN && a.outAoS) a.out.p[(pnext - a.out_off) * a.out.ts + e] = v;
+    else stv<ESO>(a.out, pnext - a.out_off, e, v);
+  };
   // prefetch row i of a block field (n elements per row) of column c
   auto pfEl = [&](int i, int64_t c) {
 #pragma unroll
@@ -552,22 +557,14 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       }
       stream_row(R3, z3, row, zr, wl);
     }
-    if (OAOS) {   // the multi-GPU boundary entry: true rows (generic-path layout)
+    // (rho, U) in the upper triangle; the lower triangle is never read.  The
+    // multi-GPU boundary entry (OAOS: AoS layout) has the same form: the
+    // boundary system runs on these kernels too (SURVEY §8(e) invariant).
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const double w = wscale(R3[TR::at(i, i)]);   // sqrt(d) = 1/sqrt(rho)
+    for (int i = 0; i < N; ++i) {
 #pragma unroll
-        for (int j = 0; j < N; ++j)
-          sto(EN::C + i * N + j, j > i ? w * R3[TR::at(i, j)] : (j == i ? w : 0.0));
-        sto(EN::y + i, w * z3[i]);
-      }
-    } else {   // (rho, U) in the upper triangle; the lower triangle is never read
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-#pragma unroll
-        for (int j = i; j < N; ++j) sto(EN::C + i * N + j, R3[TR::at(i, j)]);
-        sto(EN::y + i, z3[i]);
-      }
+      for (int j = i; j < N; ++j) sto(EN::C + i * N + j, R3[TR::at(i, j)]);
+      sto(EN::y + i, z3[i]);
     }
     sto(EN::nrm, sqrt(ref2u));
   }
@@ -810,6 +807,7 @@ __global__ void __launch_bounds__(64, 1) small_factor_tail_kernel(SmallTailArgs 
     a.ent_off = t.W ? c * kloc : 0;
     const bool last = lv + 1 == t.nlev;
     a.out = last ? t.out_last : TView{out, 64 * E};
+    a.outAoS = last ? t.out_last_aos : 0;
     a.out_off = (t.W && !last) ? c * (kloc / 2) : 0;
     const int64_t npairs = t.W ? kloc / 2 : (a.K >= 2 ? a.K / 2 : 1);
     for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x)
@@ -1381,12 +1379,7 @@ bool backward_tma(const SmallBackwardArgs &a, cudaStream_t s) {
       return false;
     const bool xst = KS_BWD_XSTAGE && a.Xcur.p;
     const size_t smem = (xst ? BwdT<N>::total_x : BwdT<N>::total) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(small_backward_tma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(BwdT<N>::total_x * sizeof(double)));
-      attr = true;
-    }
+    set_smem_attr((const void *)small_backward_tma_kernel<N>, (int)(BwdT<N>::total_x * sizeof(double)));
     small_backward_tma_kernel<N><<<(unsigned)((nc + kBwdCols - 1) / kBwdCols), 2 * kBwdCols, smem, s>>>(a, m);
     return true;
   }
@@ -1399,6 +1392,14 @@ __device__ __forceinline__ void wst(const TView &v, int cst, int64_t i, int e, d
   if (cst) stv<1>(v, i, e, x);
   else stv<64>(v, i, e, x);
 }
+
+// Exponent range of the Givens path (the empty-row prior d = 2^-600, see
+// kEmptyRow): a whitened block column with squared norm outside
+// [1e-160, 1e120] (norm outside [1e-80, 1e60]) could be biased by the prior
+// (relative 2^-600 / |y|^2 > 1e-21) or overflow y_k^2 rho (|y| > 6.6e63);
+// such a problem is rejected (KS_ERR_ARG from ks_sync_status) instead of
+// being solved inaccurately.  Zero blocks (no rows) are fine.
+__device__ __forceinline__ bool out_of_range(double sq) { return sq != 0.0 && !(sq >= 1e-160 && sq <= 1e120); }
 
 // Evolution blocks: K = Lam Lam^T (Cholesky), El = -Lam^{-1}F,
 // Er = Lam^{-1}, e = Lam^{-1} c.  One thread per distinct block.
@@ -1428,20 +1429,25 @@ __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_
   for (int r = 0; r < N; ++r)
 #pragma unroll
     for (int c = 0; c <= r; ++c) Lm[r][c] = K[r * N + c];
+  if (a.chol) {   // KS_COV_IS_CHOL: K holds Lam itself (nonzero diagonal)
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
-    double d = Lm[j][j];
+    for (int j = 0; j < N; ++j) ok &= Lm[j][j] != 0.0 && Lm[j][j] - Lm[j][j] == 0.0;
+  } else {
 #pragma unroll
-    for (int k = 0; k < j; ++k) d = fma(-Lm[j][k], Lm[j][k], d);
-    ok &= d > 0.0;
-    const double ljj = sqrt(d > 0.0 ? d : 1.0), il = 1.0 / ljj;
-    Lm[j][j] = ljj;
+    for (int j = 0; j < N; ++j) {
+      double d = Lm[j][j];
 #pragma unroll
-    for (int r = j + 1; r < N; ++r) {
-      double v = Lm[r][j];
+      for (int k = 0; k < j; ++k) d = fma(-Lm[j][k], Lm[j][k], d);
+      ok &= d > 0.0;
+      const double ljj = sqrt(d > 0.0 ? d : 1.0), il = 1.0 / ljj;
+      Lm[j][j] = ljj;
 #pragma unroll
-      for (int k = 0; k < j; ++k) v = fma(-Lm[r][k], Lm[j][k], v);
-      Lm[r][j] = v * il;
+      for (int r = j + 1; r < N; ++r) {
+        double v = Lm[r][j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) v = fma(-Lm[r][k], Lm[j][k], v);
+        Lm[r][j] = v * il;
+      }
     }
   }
   if (!ok) report(a.status, (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i, kBadK);
@@ -1496,6 +1502,8 @@ __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_
   }
   wst(a.nEr, a.cE, i, 0, ner);
   wst(a.nEl, a.cE, i, 0, nel);
+  if (out_of_range(ner) || out_of_range(nel))
+    report(a.status, (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i, kBadScale);
 }
 
 // Observation blocks: L = M M^T; C = M^{-1} H, y = M^{-1} o (rows >= m_i are 0).
@@ -1509,22 +1517,33 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
   const double *L = a.L + i * a.sL, *H = a.H + i * a.sH, *o = a.o + i * a.so;
   double Lm[MM][MM];
   bool ok = true;
+  if (a.chol) {   // KS_COV_IS_CHOL: L holds M itself (nonzero diagonal)
 #pragma unroll
-  for (int j = 0; j < MM; ++j) {
-    if (j < mi) {
-      double d = L[j * mx + j];
+    for (int r = 0; r < MM; ++r)
 #pragma unroll
-      for (int k = 0; k < j; ++k) d = fma(-Lm[j][k], Lm[j][k], d);
-      ok &= d > 0.0;
-      const double ljj = sqrt(d > 0.0 ? d : 1.0), il = 1.0 / ljj;
-      Lm[j][j] = ljj;
-#pragma unroll
-      for (int r = j + 1; r < MM; ++r) {
+      for (int k = 0; k <= r; ++k)
         if (r < mi) {
-          double v = L[r * mx + j];
+          Lm[r][k] = L[r * mx + k];
+          if (k == r) ok &= Lm[r][r] != 0.0 && Lm[r][r] - Lm[r][r] == 0.0;
+        }
+  } else {
 #pragma unroll
-          for (int k = 0; k < j; ++k) v = fma(-Lm[r][k], Lm[j][k], v);
-          Lm[r][j] = v * il;
+    for (int j = 0; j < MM; ++j) {
+      if (j < mi) {
+        double d = L[j * mx + j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) d = fma(-Lm[j][k], Lm[j][k], d);
+        ok &= d > 0.0;
+        const double ljj = sqrt(d > 0.0 ? d : 1.0), il = 1.0 / ljj;
+        Lm[j][j] = ljj;
+#pragma unroll
+        for (int r = j + 1; r < MM; ++r) {
+          if (r < mi) {
+            double v = L[r * mx + j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) v = fma(-Lm[r][k], Lm[j][k], v);
+            Lm[r][j] = v * il;
+          }
         }
       }
     }
@@ -1563,6 +1582,7 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
     }
   }
   wst(a.nC, a.cC, i, 0, nc);
+  if (out_of_range(nc)) report(a.status, i, kBadScale);
   if (a.constC) {
 #pragma unroll
     for (int r = 0; r < MM; ++r)
@@ -1626,12 +1646,7 @@ cudaError_t factor_launch(const SmallFactorArgs &a, cudaStream_t s) {
   const int64_t np = (a.K >= 2 ? a.K / 2 : 1) + (ZS ? 1 : 0);
   const unsigned g = (unsigned)((np + T - 1) / T);
   const size_t smem = ((size_t)T * kParkDoubles<N> + CstOff<N>::size) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(small_factor_kernel<N, L0, CE, CC, OAOS, ZS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
+  set_smem_attr((const void *)small_factor_kernel<N, L0, CE, CC, OAOS, ZS>, (int)smem);
   small_factor_kernel<N, L0, CE, CC, OAOS, ZS><<<g, T, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -1657,11 +1672,7 @@ cudaError_t factor_n(const SmallFactorArgs &a, cudaStream_t s) {
 template <int N>
 cudaError_t factor_tail_n(const SmallTailArgs &t, cudaStream_t s) {
   const size_t smem = tail_smem_bytes<N>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(small_factor_tail_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  set_smem_attr((const void *)small_factor_tail_kernel<N>, (int)smem);
   small_factor_tail_kernel<N><<<(unsigned)(t.W ? t.K[0] / t.W : 1), 64, smem, s>>>(t);
   return cudaGetLastError();
 }
@@ -1674,11 +1685,7 @@ cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
   const int64_t nc = (a.K + 1) / 2;
   const size_t full = bwd_smem_doubles<N>() * sizeof(double);
   const size_t smem = a.do_cov ? full : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(small_backward_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)full);
-    attr = true;
-  }
+  set_smem_attr((const void *)small_backward_kernel<N>, (int)full);
   small_backward_kernel<N><<<(unsigned)((nc + kBwdCols - 1) / kBwdCols), 2 * kBwdCols, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -1686,11 +1693,7 @@ cudaError_t backward_n(const SmallBackwardArgs &a, cudaStream_t s) {
 template <int N>
 cudaError_t backward_tail_n(const SmallBwdTailArgs &t, cudaStream_t s) {
   const size_t smem = 2 * bwd_smem_doubles<N>() * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(small_backward_tail_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  set_smem_attr((const void *)small_backward_tail_kernel<N>, (int)smem);
   small_backward_tail_kernel<N><<<(unsigned)(t.W ? t.nsub : 1), 4 * kBwdCols, smem, s>>>(t);
   return cudaGetLastError();
 }

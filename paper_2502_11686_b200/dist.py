@@ -2,10 +2,13 @@
 
 One process per GPU.  Rank r owns steps [r*M, (r+1)*M) with M = N / world a
 power of two; every rank runs its local levels (ks_factor), the ranks
-allgather their single boundary column (3n^2+2n+1 doubles each) through
-torch.distributed (NCCL on GPUs, gloo on CPU tests), and every rank factors
-the P-column boundary system redundantly (ks_factor_boundary) before its
-local backward levels.  This module holds only that host-side plumbing.
+allgather their single boundary column (3n^2+2n+1 doubles each), and every
+rank factors the P-column boundary system redundantly before its local
+backward levels.  On GPUs the library does the allgather itself over its own
+NCCL communicator (ks.Dist with a unique id, bench.py); the caller-driven
+exchange below (torch.distributed, e.g. gloo through pinned host memory) is
+what tests/test_gpu_multiproc.py and tests/test_dist_cpu.py use.  This module
+holds only that host-side plumbing.
 """
 from __future__ import annotations
 
@@ -45,29 +48,3 @@ def max_over_ranks(x: float, device: Optional[torch.device] = None, group=None) 
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
-
-
-class ShardedSmoother:
-    """A rank's context plus the boundary exchange: run() = whiten, local
-    factor, allgather, boundary factor, solve [, selinv]."""
-
-    def __init__(self, problem, rank: int, world: int, device="cuda", cov: bool = True, **kw):
-        from . import ks
-        lo, hi = shard_range(problem.N, rank, world)
-        self.local = problem.slice(lo, hi) if world > 1 else problem
-        self.world = world
-        self.sm = ks.Smoother(self.local, device=device, cov=cov,
-                              shard=(rank, world, None) if world > 1 else None, **kw)
-        self.views = self.sm.boundary_tensors() if world > 1 else None
-
-    def run(self, cov: bool = True):
-        s = self.sm
-        s.whiten()
-        s.factor()
-        if self.world > 1:
-            exchange_boundary(self.views[0], self.views[1])
-            s.factor_boundary()
-        if cov:
-            s.solve_selinv()
-        else:
-            s.solve()

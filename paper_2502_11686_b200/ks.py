@@ -22,13 +22,15 @@ LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_HERE, "libks.so")   # KS_LI
 
 KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
     KS_ERR_WORKSPACE = range(8)
-KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH, KS_NO_FUSED_TAIL = 1, 2, 4, 8
+KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH, KS_NO_FUSED_TAIL, KS_COV_IS_CHOL = 1, 2, 4, 8, 16
 FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary", "backward")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
            "ks_solve_selinv", "ks_get", "ks_sync_status", "ks_boundary_buffers", "ks_factor_boundary",
            "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info",
-           "ks_peak_fp64_tflops", "ks_strerror", "ks_destroy")
+           "ks_peak_fp64_tflops", "ks_strerror", "ks_destroy",
+           "ks_dist_unique_id", "ks_dist_create", "ks_dist_info", "ks_dist_destroy",
+           "ks_level_of_steps")
 
 
 class KsError(RuntimeError):
@@ -48,10 +50,6 @@ class ks_problem(C.Structure):
                 ("sK", C.c_int64), ("sL", C.c_int64), ("flags", C.c_uint32)]
 
 
-class ks_shard(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_comm", C.c_void_p)]
-
-
 _lib = None
 
 
@@ -63,10 +61,15 @@ def lib():
             raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
         L = C.CDLL(LIB_PATH)
         vp, i64, i32, sz = C.c_void_p, C.c_int64, C.c_int, C.c_size_t
-        L.ks_workspace_bytes.argtypes = [C.POINTER(ks_problem), C.POINTER(ks_shard)]
+        L.ks_workspace_bytes.argtypes = [C.POINTER(ks_problem), vp]
         L.ks_workspace_bytes.restype = sz
-        L.ks_create.argtypes = [C.POINTER(vp), C.POINTER(ks_problem), vp, sz, vp,
-                                C.POINTER(ks_shard), vp, vp]
+        L.ks_create.argtypes = [C.POINTER(vp), C.POINTER(ks_problem), vp, sz, vp, vp, vp, vp]
+        L.ks_dist_unique_id.argtypes = [C.c_char_p]
+        L.ks_dist_create.argtypes = [C.POINTER(vp), i32, i32, C.c_char_p, i64, i64]
+        L.ks_dist_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
+        L.ks_dist_destroy.argtypes = [vp]
+        L.ks_dist_destroy.restype = None
+        L.ks_level_of_steps.argtypes = [i64, vp]
         for f in ("ks_whiten", "ks_factor", "ks_solve", "ks_selinv", "ks_solve_selinv",
                   "ks_factor_boundary"):
             getattr(L, f).argtypes = [vp]
@@ -87,7 +90,7 @@ def lib():
         L.ks_destroy.restype = None
         for f in EXPORTS:
             if f not in ("ks_workspace_bytes", "ks_strerror", "ks_destroy", "ks_get_launch_times",
-                         "ks_peak_fp64_tflops"):
+                         "ks_peak_fp64_tflops", "ks_dist_destroy"):
                 getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -122,20 +125,72 @@ def _as_tensor(a, device, pin=False):
     return t.contiguous()
 
 
+class Dist:
+    """One rank's ks_dist (include/ks.h): rank r of `nranks` owns the global
+    steps [first_global_step, first_global_step + nsteps_global / nranks).
+    ``uid`` (128 bytes from ``Dist.unique_id()`` on rank 0, broadcast by the
+    caller) makes the library create its own NCCL communicator -- a collective
+    call, with this rank's CUDA device current -- and ks_factor then does the
+    boundary allgather itself; ``uid=None`` leaves the exchange to the caller
+    (ks_boundary_buffers + ks_factor_boundary)."""
+
+    def __init__(self, rank: int, nranks: int, first_global_step: int, nsteps_global: int,
+                 uid: Optional[bytes] = None, device=None):
+        self.L = lib()
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.first, self.nglobal = int(first_global_step), int(nsteps_global)
+        if uid is not None and len(uid) != 128:
+            raise ValueError("uid must be 128 bytes")
+        d = C.c_void_p()
+        if device is not None:
+            with torch.cuda.device(torch.device(device)):
+                rc = self.L.ks_dist_create(C.byref(d), self.rank, self.nranks, uid, self.first, self.nglobal)
+        else:
+            rc = self.L.ks_dist_create(C.byref(d), self.rank, self.nranks, uid, self.first, self.nglobal)
+        _check(rc, "ks_dist_create")
+        self.ptr = d
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().ks_dist_unique_id(buf), "ks_dist_unique_id")
+        return buf.raw
+
+    def info(self):
+        r, n, nc = C.c_int(), C.c_int(), C.c_int()
+        _check(self.L.ks_dist_info(self.ptr, C.byref(r), C.byref(n), C.byref(nc)), "ks_dist_info")
+        return {"rank": r.value, "nranks": n.value, "nccl_nranks": nc.value}
+
+    def __del__(self):
+        try:
+            if getattr(self, "ptr", None):
+                self.L.ks_dist_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
 class Smoother:
     """One ks_ctx over a problem whose arrays are torch tensors (or numpy).
 
     ``problem`` is any object with N, n, m_max, m, F, H, K, L, o, c attributes
     (e.g. ``generators.Problem``).  ``host_inputs=True`` keeps the inputs in
     pinned host memory and lets ks_whiten copy them (end-to-end path).
-    ``shard=(rank, nranks, nccl_comm_or_None)`` for time-sharded multi-GPU.
+    Time-sharded multi-GPU: ``dist=Dist(...)`` (this rank's shard of the
+    global problem; ``problem`` is the local shard), or the shorthand
+    ``shard=(rank, nranks)`` for a caller-driven exchange with power-of-two
+    shards.  ``chol=True``: K and L hold lower Cholesky factors
+    (KS_COV_IS_CHOL).
     """
 
     def __init__(self, problem, device="cuda", stream: Optional[torch.cuda.Stream] = None,
                  host_inputs: bool = False, bind_outputs: bool = True, cov: bool = True,
-                 shard=None, inputs=None, generic: bool = False, fused_tail: bool = True):
+                 shard=None, inputs=None, generic: bool = False, fused_tail: bool = True,
+                 dist: Optional[Dist] = None, chol: bool = False):
         self.L = lib()
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         p = problem
         self.N, self.n, self.m_max = int(p.N), int(p.n), int(p.m_max)
@@ -158,40 +213,45 @@ class Smoother:
         pr.F, pr.H, pr.c, pr.o, pr.K, pr.L = (ptr(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
         pr.sF, pr.sH, pr.sc, pr.so, pr.sK, pr.sL = (_stride(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
         pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0) | \
-            (KS_GENERIC_PATH if generic else 0) | (0 if fused_tail else KS_NO_FUSED_TAIL)
+            (KS_GENERIC_PATH if generic else 0) | (0 if fused_tail else KS_NO_FUSED_TAIL) | \
+            (KS_COV_IS_CHOL if chol else 0)
         self.problem = pr
-        self.shard = None
-        if shard is not None:
-            sh = ks_shard()
-            sh.rank, sh.nranks = int(shard[0]), int(shard[1])
-            sh.nccl_comm = shard[2] if len(shard) > 2 else None
-            self.shard = sh
-        shp = C.byref(self.shard) if self.shard is not None else None
-        nbytes = self.L.ks_workspace_bytes(C.byref(pr), shp)
-        if nbytes == 0:
-            raise KsError(KS_ERR_ARG, "ks_workspace_bytes")
-        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        self.states = self.cov = None
-        if bind_outputs:
-            self.states = torch.empty((self.N, self.n), dtype=torch.float64, device=self.device)
-            if cov:
-                self.cov = torch.empty((self.N, self.n, self.n), dtype=torch.float64, device=self.device)
-        ctx = C.c_void_p()
-        _check(self.L.ks_create(C.byref(ctx), C.byref(pr), self.workspace.data_ptr(), nbytes,
-                                self.stream.cuda_stream, shp,
-                                None if self.states is None else self.states.data_ptr(),
-                                None if self.cov is None else self.cov.data_ptr()), "ks_create")
+        if dist is None and shard is not None:
+            r, P = int(shard[0]), int(shard[1])
+            dist = Dist(r, P, r * self.N, P * self.N)
+        self.dist = dist   # keep alive (borrowed by the context)
+        dp = dist.ptr if dist is not None else None
+        with torch.cuda.device(self.device):
+            nbytes = self.L.ks_workspace_bytes(C.byref(pr), dp)
+            if nbytes == 0:
+                raise KsError(KS_ERR_ARG, "ks_workspace_bytes")
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self.states = self.cov = None
+            if bind_outputs:
+                self.states = torch.empty((self.N, self.n), dtype=torch.float64, device=self.device)
+                if cov:
+                    self.cov = torch.empty((self.N, self.n, self.n), dtype=torch.float64, device=self.device)
+            ctx = C.c_void_p()
+            _check(self.L.ks_create(C.byref(ctx), C.byref(pr), self.workspace.data_ptr(), nbytes,
+                                    self.stream.cuda_stream, dp,
+                                    None if self.states is None else self.states.data_ptr(),
+                                    None if self.cov is None else self.cov.data_ptr()), "ks_create")
         self.ctx = ctx
+
+    def _call(self, fn, what):
+        # the library launches on the current device: make this context's current
+        with torch.cuda.device(self.device):
+            _check(fn(self.ctx), what)
 
     # --- the ABI calls -------------------------------------------------------
     def whiten(self):
-        _check(self.L.ks_whiten(self.ctx), "ks_whiten")
+        self._call(self.L.ks_whiten, "ks_whiten")
 
     def factor(self):
-        _check(self.L.ks_factor(self.ctx), "ks_factor")
+        self._call(self.L.ks_factor, "ks_factor")
 
     def factor_boundary(self):
-        _check(self.L.ks_factor_boundary(self.ctx), "ks_factor_boundary")
+        self._call(self.L.ks_factor_boundary, "ks_factor_boundary")
 
     def boundary_buffers(self):
         s, r, b = C.c_void_p(), C.c_void_p(), C.c_size_t()
@@ -204,17 +264,17 @@ class Smoother:
         boundary allgather is dist.all_gather_into_tensor(recv, send)."""
         s, r, nb = self.boundary_buffers()
         base = self.workspace.data_ptr()
-        P = self.shard.nranks
+        P = self.dist.nranks
         return (self.workspace[s - base:s - base + nb], self.workspace[r - base:r - base + P * nb])
 
     def solve(self):
-        _check(self.L.ks_solve(self.ctx), "ks_solve")
+        self._call(self.L.ks_solve, "ks_solve")
 
     def selinv(self):
-        _check(self.L.ks_selinv(self.ctx), "ks_selinv")
+        self._call(self.L.ks_selinv, "ks_selinv")
 
     def solve_selinv(self):
-        _check(self.L.ks_solve_selinv(self.ctx), "ks_solve_selinv")
+        self._call(self.L.ks_solve_selinv, "ks_solve_selinv")
 
     def get(self, states=None, cov=None):
         """Copy results into torch tensors (device or host)."""
@@ -275,6 +335,16 @@ class Smoother:
                 self.ctx = None
         except Exception:
             pass
+
+
+def level_of_steps(N: int):
+    """(number of levels, elimination level of every step) from the library's
+    host level plan (ks_level_of_steps; no GPU needed)."""
+    lv = np.zeros(N, np.int32)
+    nl = lib().ks_level_of_steps(int(N), lv.ctypes.data)
+    if nl < 0:
+        raise KsError(-nl, "ks_level_of_steps")
+    return nl, lv
 
 
 def peak_fp64_tflops(stream=None) -> float:

@@ -68,14 +68,54 @@ def test_workspace_sizing_host_logic(ks):
     assert ws(_problem(ks, 10, 0, 6)) == 0
     assert ws(_problem(ks, 10, 6, 6, sF=5)) == 0         # stride smaller than a block
     assert ws(_problem(ks, 10, 6, 6, flags=64)) == 0     # unknown flag
+    assert ws(_problem(ks, 10, 6, 6, flags=ks.KS_COV_IS_CHOL)) > 0
     assert ws(_problem(ks, 10, 200, 6)) == 0             # n > KS_MAX_N
-    sh = ks.ks_shard(); sh.rank, sh.nranks = 1, 4
-    assert ws(_problem(ks, 1024, 6, 3, so=3), sh) > 0
-    assert ws(_problem(ks, 1000, 6, 3, so=3), sh) == 0   # shard size must be a power of two
-    sh.rank = 4
-    assert ws(_problem(ks, 1024, 6, 3, so=3), sh) == 0   # bad rank
+    # multi-GPU: a ks_dist without a communicator (caller-driven exchange)
+    def dist(rank, nranks, first, total):
+        d = C.c_void_p()
+        rc = L.ks_dist_create(C.byref(d), rank, nranks, None, first, total)
+        return rc, d
+    rc, d = dist(1, 4, 1024, 4096)
+    assert rc == ks.KS_OK
+    wsd = lambda pr: L.ks_workspace_bytes(C.byref(pr), d)
+    assert wsd(_problem(ks, 1024, 6, 3, so=3)) > 0
+    assert wsd(_problem(ks, 1000, 6, 3, so=3)) == 0     # shard size must match (power of two, rank order)
+    r, n, nc = C.c_int(), C.c_int(), C.c_int()
+    assert L.ks_dist_info(d, C.byref(r), C.byref(n), C.byref(nc)) == ks.KS_OK
+    assert (r.value, n.value, nc.value) == (1, 4, 0)
+    L.ks_dist_destroy(d)
+    rc, d2 = dist(1, 4, 1000, 4000)                      # a 1000-step shard: accepted by ks_dist_create ...
+    assert rc == ks.KS_OK
+    assert L.ks_workspace_bytes(C.byref(_problem(ks, 1000, 6, 3, so=3)), d2) == 0   # ... not by the context
+    L.ks_dist_destroy(d2)
+    assert dist(4, 4, 0, 4096)[0] == ks.KS_ERR_ARG        # bad rank
+    assert dist(0, 4, 4096, 4096)[0] == ks.KS_ERR_ARG     # first step outside the problem
 
 
 def test_strerror(ks):
     assert ks.strerror(ks.KS_ERR_RANK) == "least-squares matrix rank deficient"
     assert ks.strerror(99) == "unknown"
+
+
+def test_level_plan_matches_golden(ks):
+    """The library's host level plan (the permutation P of SURVEY §8(a) a2)
+    against the worked examples of S:195-197 (tests/golden/oddeven_order.json):
+    which step is eliminated at which level, and the elimination order
+    (by level, ascending steps within a level)."""
+    import json
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "oddeven_order.json")))
+    for case in g["cases"]:
+        N = case["N"]
+        nl, lv = ks.level_of_steps(N)
+        assert nl == int(np.floor(np.log2(N))) + 1
+        order = sorted(range(N), key=lambda j: (lv[j], j))
+        assert order == case["order"], (N, order)
+        assert [int(lv[j]) for j in order] == case["levels"], N
+    # the trailing-ones rule at larger N (odd levels included)
+    for N in (5, 6, 7, 100, 1000, 1023, 4097):
+        nl, lv = ks.level_of_steps(N)
+        for j in range(N):
+            t = (j + 1) >> int(lv[j])
+            assert ((j + 1) & ((1 << int(lv[j])) - 1)) == 0
+            K = N >> int(lv[j])
+            assert (t - 1) % 2 == 0 or (t - 1 == K - 1), (N, j)

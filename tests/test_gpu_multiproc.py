@@ -1,0 +1,89 @@
+"""Two real processes, one rank each, on the single leased GPU.
+
+Each process owns its context over a power-of-two shard of the steps
+(ks_dist_create with no communicator) and runs its local levels; the
+boundary exchange is the caller-driven path of include/ks.h: the rank's
+`send` entry goes device -> pinned host, a world-size-2 gloo allgather,
+host -> the rank's `recv` buffer, then ks_factor_boundary and the local
+backward levels.  The kernels of the two processes never wait on each other
+(the exchange is host-mediated), so one GPU is a faithful stand-in for two.
+The gathered shards must match the oracle and, the shards being powers of
+two, the single-GPU result bit for bit.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, cfg, N, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    from paper_2502_11686_b200 import dist as kdist
+    from paper_2502_11686_b200 import generators as gen
+    from paper_2502_11686_b200 import ks
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = gen.make(cfg, N=N)
+        lo, hi = kdist.shard_range(N, rank, world)
+        d = ks.Dist(rank, world, lo, N)
+        s = ks.Smoother(p.slice(lo, hi), device="cuda:0", dist=d)
+        s.whiten()
+        s.factor()
+        send, recv = s.boundary_tensors()
+        send_h = send.cpu()
+        recv_h = torch.empty(world * send_h.numel(), dtype=torch.uint8)
+        kdist.exchange_boundary(send_h, recv_h)       # gloo, host memory
+        recv.copy_(recv_h.to(recv.device))
+        s.factor_boundary()
+        s.solve_selinv()
+        s.check()
+        q.put((rank, s.states.cpu().numpy(), s.cov.cpu().numpy(), d.info()))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, None, repr(e), None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,N", [("c5", 1 << 14), ("c2", 1 << 12), ("c3", 1 << 11)])
+def test_two_processes_gloo_staged_exchange(cfg, N):
+    import oracle
+    from paper_2502_11686_b200 import generators as gen
+    from paper_2502_11686_b200 import ks
+    from tests.dense import rel_cov_err, rel_state_err
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, cfg, N, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=120)
+    for r, x, S, info in res:
+        assert x is not None, f"rank {r}: {S}"
+        assert info == {"rank": r, "nranks": world, "nccl_nranks": 0}
+    x = np.concatenate([r[1] for r in res])
+    S = np.concatenate([r[2] for r in res])
+    p = gen.make(cfg, N=N)
+    xo, So = oracle.smooth(p)
+    assert rel_state_err(x, xo) <= 1e-9 and rel_cov_err(S, So) <= 1e-8
+    s1 = ks.Smoother(p)
+    s1.run()
+    s1.check()
+    assert np.array_equal(x, s1.states.cpu().numpy()) and np.array_equal(S, s1.cov.cpu().numpy())
