@@ -65,6 +65,9 @@ enum {
     KS_NO_FUSED_TAIL = 8u,/* small path: launch every factor level separately
                              instead of running the recursion's tail (levels
                              with few columns) in one on-chip kernel (cross-check) */
+    KS_KEEP_WHITENING = 32u, /* keep the observation whitening factors M_i in the
+                             workspace so that ks_update_obs can re-whiten new
+                             observations o without redoing the model */
     KS_COV_IS_CHOL = 16u  /* K and L hold lower-triangular Cholesky factors
                              Lam_i (K_i = Lam Lam^T) and M_i (L_i = M M^T) instead
                              of the covariances ("whitening factors K_i, L_i",
@@ -92,7 +95,30 @@ typedef struct ks_problem {
     const double *K;         /* [N][n][n]      evolution-noise covariance (SPD)     */
     const double *L;         /* [N][m_max][m_max] observation-noise covariance (SPD) */
     int64_t sF, sH, sc, so, sK, sL;   /* per-step strides in doubles, 0 = constant */
-    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL | KS_COV_IS_CHOL */
+    uint32_t flags;          /* KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL |
+                                KS_COV_IS_CHOL | KS_KEEP_WHITENING */
+    /* Batched independent problems (P:301-316, P:608-615:
+     * many small linear smoothing problems of one structure, e.g. the inner
+     * solves of a Gauss-Newton / Levenberg-Marquardt smoother).  batch = B >= 1
+     * (0 means 1): the N steps are B independent problems of N / B steps each
+     * (N % B == 0); problem b is steps [b N/B, (b+1) N/B) and, like step 0,
+     * the first step of every problem has no evolution equation (its F, K, c
+     * are ignored).  The least-squares problem is then block diagonal over
+     * the problems and every output equals that problem's own solution; all
+     * problems go through the same launches.  Multi-GPU: segments are counted
+     * in global steps (nsteps_global / B each). */
+    int64_t batch;
+    /* General model: evolution
+     * H_i x_i = F_i x_{i-1} + c_i + eps_i with H_i of size l_i x n_i,
+     * F_i l_i x n_{i-1}, K_i l_i x l_i, and state dimensions n_i <= n.
+     * Arrays keep their uniform [n][n] / [m_max][n] / [n] shapes; rows >= l_i
+     * and columns >= n_i (F: >= n_{i-1}) are ignored.  All NULL = the
+     * uniform model above (H_i = I, l_i = n_i = n). */
+    const double *Hev;       /* [N][n][n] evolution matrix H_i (the paper's H); NULL = I */
+    int64_t sHev;            /* per-step stride in doubles, 0 = constant                 */
+    const int32_t *l;        /* [N] evolution rows l_i in [1, n]; NULL = n_i             */
+    const int32_t *nstate;   /* [N] state dimensions n_i in [1, n]; NULL = all n         */
+    int32_t nstate_min;      /* min_i n_i (sizes the padding rows), if nstate != NULL    */
 } ks_problem;
 
 #define KS_MAX_N 64
@@ -167,6 +193,19 @@ int ks_selinv(ks_ctx *ctx);
  * Requires a covariance buffer (cov_out bound, or KS_OUTPUTS_BOUND unset);
  * KS_ERR_ARG otherwise. */
 int ks_solve_selinv(ks_ctx *ctx);
+
+/* Repeated solves with new observations (P:301-316:
+ * each Gauss-Newton step re-solves one structure; the NC variant
+ * for exactly that use).  Replaces the observation array o (same layout,
+ * stride and memory kind as at ks_create; borrowed until the enqueued work
+ * completes) and re-whitens only y_i = M_i^{-1} o_i, keeping every other
+ * whitened block; the context returns to the whitened stage, so the caller
+ * continues with ks_factor -> ks_solve.  The covariances do not depend on o:
+ * those of a previous ks_selinv stay valid (ks_get may still return them).
+ * Needs KS_KEEP_WHITENING unless the observation model is constant (H, L
+ * stride 0, m == NULL), where the factor whitens o itself (KS_ERR_ARG otherwise);
+ * KS_ERR_ORDER before ks_whiten. */
+int ks_update_obs(ks_ctx *ctx, const double *o);
 
 /* Copy results into caller buffers (device or host; NULL = skip).  A pointer
  * equal to the bound output buffer is a no-op.  Host destinations synchronise

@@ -110,6 +110,8 @@ struct ks_ctx {
   double *send = nullptr, *recv = nullptr, *bx = nullptr, *bS = nullptr, *hx = nullptr,
          *hS = nullptr, *Xq_local = nullptr;
   bool chol = false;      // KS_COV_IS_CHOL
+  int64_t seg = 0;        // steps per independent problem (global steps; batch)
+  double *Mall = nullptr; // KS_KEEP_WHITENING: per-step M_i
   // small-n path (ks_small.cu): element-major level arrays
   bool small = false;
   double *nC0 = nullptr, *nEr0 = nullptr, *nEl0 = nullptr, *zscratch = nullptr;
@@ -144,7 +146,13 @@ bool use_small(const ks_problem *p) {
 }
 
 
-constexpr uint32_t kAllFlags = KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL | KS_COV_IS_CHOL;
+constexpr uint32_t kAllFlags =
+    KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL | KS_COV_IS_CHOL | KS_KEEP_WHITENING;
+
+int64_t global_steps(const ks_problem *p, const ks_dist *d) { return (d && d->nranks > 1) ? d->nglobal : p->nsteps; }
+int64_t segment_steps(const ks_problem *p, const ks_dist *d) {
+  return global_steps(p, d) / (p->batch > 1 ? p->batch : 1);
+}
 
 int validate(const ks_problem *p, const ks_dist *d) {
   if (!p) return KS_ERR_ARG;
@@ -161,6 +169,8 @@ int validate(const ks_problem *p, const ks_dist *d) {
     if (factor_smem_bytes(p->n, p->m_max > p->n ? p->m_max : p->n) > 227 * 1024) return KS_ERR_ARG;
     if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
   }
+  if (p->batch < 0 || (p->batch > 1 && global_steps(p, d) % p->batch != 0)) return KS_ERR_ARG;
+  if (p->Hev || p->l || p->nstate) return KS_ERR_ARG;   // general model: not in this build
   if (d && d->nranks > 1) {
     // power-of-two shards in rank order (the local levels then follow the
     // global trailing-ones rule with no halo)
@@ -210,8 +220,10 @@ size_t carve(ks_ctx *c, char *base) {
     c->st_o = w.take<double>(c->no);
     c->st_c = p.c ? w.take<double>(c->nc) : nullptr;
   }
-  c->cntE = (p.sF == 0 && p.sK == 0 && (p.c == nullptr || p.sc == 0)) ? 1 : N;
+  // a batch needs per-step evolution blocks (zero rows at every problem's first step)
+  c->cntE = (p.sF == 0 && p.sK == 0 && (p.c == nullptr || p.sc == 0) && p.batch <= 1) ? 1 : N;
   c->cntC = (p.sH == 0 && p.sL == 0 && p.m == nullptr) ? 1 : N;
+  c->Mall = ((p.flags & KS_KEEP_WHITENING) && c->cntC > 1) ? w.take<double>(c->cntC * mx * mx + 1) : nullptr;
   const bool sm = c->small;
   const int64_t Rs = small_rrec_doubles(n);
   if (sm) {
@@ -768,6 +780,7 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
   c->stream = (cudaStream_t)stream;
   c->host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
   c->chol = (p->flags & KS_COV_IS_CHOL) != 0;
+  c->seg = segment_steps(p, d);
   c->small = use_small(p);
   if (d && d->nranks > 1) {
     c->sharded = true; c->rank = d->rank; c->nranks = d->nranks; c->comm = d->comm;
@@ -820,6 +833,8 @@ int ks_whiten(ks_ctx *c) {
     a.Mchol = c->Mchol; a.status = c->status;
     a.Minv = small_yfuse(c) ? c->Minv : nullptr;
     a.chol = c->chol;
+    a.seg = c->seg;
+    a.Mall = c->Mall;
     int nl = 0;
     {
       Launch l(c, 0, 0, 1);
@@ -838,6 +853,8 @@ int ks_whiten(ks_ctx *c) {
   a.C = c->C0; a.y = c->y0; a.El = c->El0; a.Er = c->Er0; a.e = c->e0;
   a.cntE = c->cntE; a.cntC = c->cntC; a.Mchol = c->Mchol; a.status = c->status;
   a.chol = c->chol;
+  a.seg = c->seg;
+  a.Mall = c->Mall;
   a.constC = (c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr);
   {
     Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
@@ -922,6 +939,32 @@ int ks_solve_selinv(ks_ctx *c) {
   return KS_OK;
 }
 
+int ks_update_obs(ks_ctx *c, const double *o) {
+  if (!c || (!o && c->mx > 0)) return KS_ERR_ARG;
+  if (c->stage < 1) return KS_ERR_ORDER;
+  const bool constC = c->cntC == 1;
+  if (!constC && !c->Mall) return KS_ERR_ARG;   // needs KS_KEEP_WHITENING
+  if (c->mx > 0) {
+    cudaError_t e = cudaSuccess;
+    if (c->host_inputs) {   // the new observations into the staging buffer (H2D)
+      e = cudaMemcpyAsync(c->st_o, o, c->no * 8, cudaMemcpyHostToDevice, c->stream);
+      if (e != cudaSuccess) return cuda_fail(e);
+    } else {
+      c->o = o;
+      c->p.o = o;
+    }
+    if (!(c->small && small_yfuse(c))) {   // (fused y: the factor whitens o itself)
+      Launch l(c, 0, 0, 1);
+      e = launch_update_y(constC ? c->Mchol : c->Mall, constC ? 0 : (int64_t)c->mx * c->mx, c->o, c->p.so, c->m,
+                          c->mx, c->N, c->y0, c->small ? 1 : 0, c->stream);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+  }
+  c->stage = 1;
+  c->solved = false;   // covariances do not depend on o: c->covd stays
+  return KS_OK;
+}
+
 int ks_get(ks_ctx *c, double *states, double *cov) {
   if (!c) return KS_ERR_ARG;
   if ((states && !c->solved) || (cov && !c->covd)) return KS_ERR_ORDER;
@@ -951,7 +994,7 @@ int ks_sync_status(ks_ctx *c, int64_t *bad_step, int *bad_kind) {
   if (e != cudaSuccess) return cuda_fail(e);
   if (st == kStatusOk) return KS_OK;
   const int kind = (int)(st & 0xff);
-  if (bad_step) *bad_step = (int64_t)(st >> 8) - 1;
+  if (bad_step) *bad_step = status_step(st);
   if (kind == kBadRank) return KS_ERR_RANK;
   if (kind == kBadScale) {   // small path: whitened data outside its exponent range
     if (bad_kind) *bad_kind = 3;

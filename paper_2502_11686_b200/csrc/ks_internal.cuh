@@ -6,9 +6,19 @@
 
 namespace ks {
 
-// Status word: min over (step+1) << 8 | kind, written with atomicMin.
+// Status word: min over (prio << 56) | (step+1) << 8 | kind, written with
+// atomicMin.  Input errors (K, L not SPD, data outside the exponent range:
+// prio 0) win over the rank failures they cause downstream (prio 1), then
+// the smallest step.
 enum BadKind : int { kBadK = 1, kBadL = 2, kBadRank = 3, kBadScale = 4 };
 constexpr unsigned long long kStatusOk = ~0ull;
+__host__ __device__ inline unsigned long long status_word(int64_t step, int kind) {
+  return ((unsigned long long)(kind == kBadRank ? 1 : 0) << 56) | ((unsigned long long)(step + 1) << 8) |
+         (unsigned long long)kind;
+}
+__host__ __device__ inline int64_t status_step(unsigned long long st) {
+  return (int64_t)((st >> 8) & ((1ull << 48) - 1)) - 1;
+}
 
 // Relative rank tolerance: |R_jj[d][d]| <= 1e-12 * |block column j of UA|_F
 // (the Frobenius norm of the original whitened block column, which Q^T
@@ -76,6 +86,8 @@ struct WhitenArgs {
   int constC;            // constant observation model (H, L stride 0, m = NULL): y by a separate kernel
   double *Mchol;         // [m_max x m_max] scratch when constC
   int chol;              // KS_COV_IS_CHOL: K, L already hold the lower Cholesky factors
+  int64_t seg;           // steps per independent problem (global): step g has no evolution row iff g % seg == 0
+  double *Mall;          // KS_KEEP_WHITENING: [cntC][m_max][m_max] lower factors M_i (row-major), or null
   unsigned long long *status;
 };
 
@@ -174,6 +186,8 @@ struct SmallWhitenArgs {
   double *Mchol;               // m_max^2 scratch (constant observation model)
   double *Minv;                // m_max^2: M^{-1} for the factor's fused y (null: small_whiten_y)
   int chol;                    // KS_COV_IS_CHOL: K, L already hold the lower Cholesky factors
+  int64_t seg;                 // steps per independent problem (global; see WhitenArgs)
+  double *Mall;                // KS_KEEP_WHITENING: [cntC][m_max][m_max] lower factors M_i, or null
   unsigned long long *status;
 };
 size_t small_entry_doubles(int n);                  // = entry_doubles(n)
@@ -191,6 +205,11 @@ cudaError_t launch_boundary_ptile(const double *recv, double *out, int P, int n,
 // the attribute belongs to a device context, so a per-process flag is wrong
 // with several devices.  Thread-safe; kernels are identified by address.
 cudaError_t set_smem_attr(const void *func, int bytes);
+// ks_update_obs: y_i = M_i^{-1} o_i (rows >= m_i zero) from the kept lower
+// factors M (stride sM doubles per step: 0 = constant), written pair-
+// interleaved tiled (small path, ptiled != 0) or row-major [N][m_max].
+cudaError_t launch_update_y(const double *M, int64_t sM, const double *o, int64_t so, const int32_t *m, int mx,
+                            int64_t N, double *y, int ptiled, cudaStream_t s);
 
 // kernel launchers of the CTA path (ks_large.cu); return cudaGetLastError()
 cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s);

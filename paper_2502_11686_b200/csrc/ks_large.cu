@@ -63,7 +63,7 @@ __host__ __device__ constexpr int pad8(int x) { return (x + 7) & ~7; }
 __host__ __device__ constexpr int ldpad(int rows) { return pad8(rows) + ((4 - pad8(rows) % 16) + 16) % 16; }
 
 __device__ __forceinline__ void report(unsigned long long *st, int64_t step, int kind) {
-  if (st) atomicMin(st, ((unsigned long long)(step + 1) << 8) | (unsigned long long)kind);
+  if (st) atomicMin(st, status_word(step, kind));
 }
 
 // D = A B + D on one 8x8 tile: A 8x4 (row-major fragment: lane holds
@@ -532,10 +532,11 @@ __device__ bool cta_chol(double *Lm, int ldl, int d, double *sh) {
 // KS_COV_IS_CHOL: the loaded lower triangle already is the factor; valid iff
 // every diagonal entry is nonzero and finite.  Result valid in every thread
 // (ends with __syncthreads).
-__device__ bool chol_diag_ok(const double *Lm, int ldl, int d, double *sh) {
+__device__ bool chol_diag_ok(double *Lm, int ldl, int d, double *sh) {
   __syncthreads();
-  const bool bad = threadIdx.x < d && !(Lm[threadIdx.x + threadIdx.x * ldl] != 0.0 &&
-                                        Lm[threadIdx.x + threadIdx.x * ldl] - Lm[threadIdx.x + threadIdx.x * ldl] == 0.0);
+  const int i = threadIdx.x;
+  const bool bad = i < d && !(Lm[i + i * ldl] != 0.0 && Lm[i + i * ldl] - Lm[i + i * ldl] == 0.0);
+  if (bad) Lm[i + i * ldl] = 1.0;   // continue with a finite factor (outputs undefined, status recorded)
   const int any = __syncthreads_or(bad);
   (void)sh;
   return !any;
@@ -1095,7 +1096,8 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
   double *El = a.El + i * (a.cntE == 1 ? 0 : nn), *Er = a.Er + i * (a.cntE == 1 ? 0 : nn);
   double *e = a.e + i * (a.cntE == 1 ? 0 : n);
   const int64_t g = a.first_global + i;
-  if ((a.cntE != 1 && g == 0) || (a.N == 1 && a.first_global == 0)) {   // no evolution row
+  // no evolution row: the first step of the problem / of every batched problem
+  if ((a.cntE != 1 && g % a.seg == 0) || (a.N == 1 && a.first_global == 0)) {
     for (int k = tid; k < nn; k += blockDim.x) { El[k] = 0.0; Er[k] = 0.0; }
     for (int k = tid; k < n; k += blockDim.x) e[k] = 0.0;
     return;
@@ -1163,6 +1165,12 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   for (int k = tid; k < mx * n; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
     C[k] = (r < mi) ? X[r + cc * ld] : 0.0;
+  }
+  if (a.Mall) {   // KS_KEEP_WHITENING: M_i for ks_update_obs
+    for (int k = tid; k < mx * mx; k += blockDim.x) {
+      const int r = k / mx, cc = k - r * mx;
+      a.Mall[i * (int64_t)mx * mx + k] = (cc <= r && r < mi) ? Lm[r + cc * ld] : 0.0;
+    }
   }
   if (!a.constC) {
     for (int r = tid; r < mx; r += blockDim.x) a.y[i * mx + r] = (r < mi) ? X[r + n * ld] : 0.0;

@@ -78,7 +78,7 @@ __device__ __forceinline__ void pfv(const TView &v, int64_t t, int e) {
 __device__ __forceinline__ void pf_line(const double *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 __device__ __forceinline__ void report(unsigned long long *st, int64_t step, int kind) {
-  if (st) atomicMin(st, ((unsigned long long)(step + 1) << 8) | (unsigned long long)kind);
+  if (st) atomicMin(st, status_word(step, kind));
 }
 
 // 1/sqrt(h) for h > 0: the MUFU approximation refined by two Newton steps
@@ -1407,7 +1407,9 @@ template <int N>
 __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_t i) {
   if (i >= a.cntE) return;
   const int64_t g = a.first_global + i;
-  const bool evo = !((a.cntE != 1 && g == 0) || (a.N == 1 && a.first_global == 0));
+  // no evolution row: the first step of the (global) problem, and of every
+  // problem of a batch (step g with g % seg == 0)
+  const bool evo = !((a.cntE != 1 && g % a.seg == 0) || (a.N == 1 && a.first_global == 0));
   if (!evo) {
 #pragma unroll
     for (int k = 0; k < N * N; ++k) {
@@ -1431,7 +1433,11 @@ __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_
     for (int c = 0; c <= r; ++c) Lm[r][c] = K[r * N + c];
   if (a.chol) {   // KS_COV_IS_CHOL: K holds Lam itself (nonzero diagonal)
 #pragma unroll
-    for (int j = 0; j < N; ++j) ok &= Lm[j][j] != 0.0 && Lm[j][j] - Lm[j][j] == 0.0;
+    for (int j = 0; j < N; ++j) {
+      const bool g = Lm[j][j] != 0.0 && Lm[j][j] - Lm[j][j] == 0.0;
+      ok &= g;
+      if (!g) Lm[j][j] = 1.0;   // continue with a finite factor (outputs undefined, status recorded)
+    }
   } else {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -1524,7 +1530,11 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
       for (int k = 0; k <= r; ++k)
         if (r < mi) {
           Lm[r][k] = L[r * mx + k];
-          if (k == r) ok &= Lm[r][r] != 0.0 && Lm[r][r] - Lm[r][r] == 0.0;
+          if (k == r) {
+            const bool g = Lm[r][r] != 0.0 && Lm[r][r] - Lm[r][r] == 0.0;
+            ok &= g;
+            if (!g) Lm[r][r] = 1.0;
+          }
         }
   } else {
 #pragma unroll
@@ -1549,6 +1559,13 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
     }
   }
   if (!ok) report(a.status, i, kBadL);
+  if (a.Mall) {   // KS_KEEP_WHITENING: M_i for ks_update_obs
+#pragma unroll
+    for (int r = 0; r < MM; ++r)
+#pragma unroll
+      for (int k = 0; k < MM; ++k)
+        if (r < mx && k < mx) a.Mall[i * (int64_t)mx * mx + r * mx + k] = (k <= r && r < mi) ? Lm[r][k] : 0.0;
+  }
   double ild[MM];   // reciprocal diagonal (multiplications in the solves below)
 #pragma unroll
   for (int r = 0; r < MM; ++r) ild[r] = (r < mi) ? 1.0 / Lm[r][r] : 0.0;

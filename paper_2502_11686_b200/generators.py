@@ -69,6 +69,29 @@ class Problem:
                        s(self.c), None if self.x_true is None else self.x_true[lo:hi],
                        self.seed, dict(self.meta))
 
+    @staticmethod
+    def concat(parts: list, name: str = "batch") -> "Problem":
+        """Independent problems of one structure (same N, n, m_max) laid end
+        to end, the layout of a batched context (ks_problem.batch = len(parts)):
+        array plumbing only; a constant block shared by every part stays
+        constant."""
+        p0 = parts[0]
+        assert all(q.N == p0.N and q.n == p0.n and q.m_max == p0.m_max for q in parts)
+
+        def cat(attr):
+            arrs = [getattr(q, attr) for q in parts]
+            if arrs[0] is None:
+                assert all(a is None for a in arrs)
+                return None
+            if all(a.shape[0] == 1 for a in arrs) and all(np.array_equal(a, arrs[0]) for a in arrs):
+                return arrs[0]
+            return np.ascontiguousarray(np.concatenate([np.broadcast_to(a, (q.N,) + a.shape[1:])
+                                                        for a, q in zip(arrs, parts)]))
+        xt = None if any(q.x_true is None for q in parts) else np.concatenate([q.x_true for q in parts])
+        return Problem(name, p0.N * len(parts), p0.n, p0.m_max, np.concatenate([q.m for q in parts]),
+                       cat("F"), cat("H"), cat("K"), cat("L"), cat("o"), cat("c"), xt, p0.seed,
+                       {"batch": len(parts)})
+
     def nbytes_inputs(self) -> int:
         tot = self.m.nbytes
         for a in (self.F, self.H, self.K, self.L, self.o, self.c):

@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_HERE, "libks.so")   # KS_LI
 
 KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
     KS_ERR_WORKSPACE = range(8)
-KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH, KS_NO_FUSED_TAIL, KS_COV_IS_CHOL = 1, 2, 4, 8, 16
+KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH, KS_NO_FUSED_TAIL, KS_COV_IS_CHOL, KS_KEEP_WHITENING = \
+    1, 2, 4, 8, 16, 32
 FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary", "backward")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
@@ -30,7 +31,7 @@ EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solv
            "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info",
            "ks_peak_fp64_tflops", "ks_strerror", "ks_destroy",
            "ks_dist_unique_id", "ks_dist_create", "ks_dist_info", "ks_dist_destroy",
-           "ks_level_of_steps")
+           "ks_level_of_steps", "ks_update_obs")
 
 
 class KsError(RuntimeError):
@@ -47,7 +48,9 @@ class ks_problem(C.Structure):
                 ("m", C.c_void_p), ("F", C.c_void_p), ("H", C.c_void_p), ("c", C.c_void_p),
                 ("o", C.c_void_p), ("K", C.c_void_p), ("L", C.c_void_p),
                 ("sF", C.c_int64), ("sH", C.c_int64), ("sc", C.c_int64), ("so", C.c_int64),
-                ("sK", C.c_int64), ("sL", C.c_int64), ("flags", C.c_uint32)]
+                ("sK", C.c_int64), ("sL", C.c_int64), ("flags", C.c_uint32),
+                ("batch", C.c_int64), ("Hev", C.c_void_p), ("sHev", C.c_int64), ("l", C.c_void_p),
+                ("nstate", C.c_void_p), ("nstate_min", C.c_int32)]
 
 
 _lib = None
@@ -74,6 +77,7 @@ def lib():
                   "ks_factor_boundary"):
             getattr(L, f).argtypes = [vp]
         L.ks_get.argtypes = [vp, vp, vp]
+        L.ks_update_obs.argtypes = [vp, vp]
         L.ks_sync_status.argtypes = [vp, C.POINTER(i64), C.POINTER(i32)]
         L.ks_boundary_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(sz)]
         L.ks_set_timing.argtypes = [vp, i32]
@@ -186,7 +190,8 @@ class Smoother:
     def __init__(self, problem, device="cuda", stream: Optional[torch.cuda.Stream] = None,
                  host_inputs: bool = False, bind_outputs: bool = True, cov: bool = True,
                  shard=None, inputs=None, generic: bool = False, fused_tail: bool = True,
-                 dist: Optional[Dist] = None, chol: bool = False):
+                 dist: Optional[Dist] = None, chol: bool = False, batch: int = 1,
+                 keep_whitening: bool = False):
         self.L = lib()
         self.device = torch.device(device)
         if self.device.type == "cuda" and self.device.index is None:
@@ -214,7 +219,8 @@ class Smoother:
         pr.sF, pr.sH, pr.sc, pr.so, pr.sK, pr.sL = (_stride(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
         pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0) | \
             (KS_GENERIC_PATH if generic else 0) | (0 if fused_tail else KS_NO_FUSED_TAIL) | \
-            (KS_COV_IS_CHOL if chol else 0)
+            (KS_COV_IS_CHOL if chol else 0) | (KS_KEEP_WHITENING if keep_whitening else 0)
+        pr.batch = int(batch)
         self.problem = pr
         if dist is None and shard is not None:
             r, P = int(shard[0]), int(shard[1])
@@ -275,6 +281,15 @@ class Smoother:
 
     def solve_selinv(self):
         self._call(self.L.ks_solve_selinv, "ks_solve_selinv")
+
+    def update_obs(self, o):
+        """ks_update_obs: new observations (same shape as the problem's o),
+        re-whitened in place; continue with factor() and solve()."""
+        host = bool(self.problem.flags & KS_HOST_INPUTS)
+        t = _as_tensor(o, None if host else self.device, pin=host)
+        assert t.dtype == torch.float64 and tuple(t.shape) == tuple(self.inputs["o"].shape)
+        self.inputs["o_update"] = t   # keep alive until the enqueued work completes
+        self._call(lambda ctx: self.L.ks_update_obs(ctx, t.data_ptr()), "ks_update_obs")
 
     def get(self, states=None, cov=None):
         """Copy results into torch tensors (device or host)."""

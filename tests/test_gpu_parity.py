@@ -349,3 +349,97 @@ def test_scale_out_of_range_rejected():
         x, S, _ = gpu_smooth(p, generic=True)    # the CTA path has no such limit
         xo, So = oracle.smooth(p)
         assert rel_state_err(x, xo) <= TOL_X and rel_cov_err(S, So) <= TOL_S
+
+
+# ---- batched independent problems, repeated solves ----
+
+def _batch_cases(case):
+    if case == "random":
+        rng = np.random.default_rng(21)
+        return [gen.random_problem(rng, 100, 3, m_max=4) for _ in range(8)]
+    if case == "c5":
+        p = gen.make("c5", N=1 << 16)
+        return [p.slice(b << 12, (b + 1) << 12) for b in range(16)]
+    if case == "c1":
+        p = gen.make("c1")
+        return [p.slice(b * 100, (b + 1) * 100) for b in range(10)]
+    if case == "c1_singletons":
+        p = gen.make("c1", N=64)
+        return [p.slice(b, b + 1) for b in range(64)]
+    if case == "c4":
+        p = gen.make("c4", N=96)
+        return [p.slice(b * 24, (b + 1) * 24) for b in range(4)]
+    raise ValueError(case)
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("case", ["random", "c5", "c1", "c1_singletons", "c4"])
+def test_batched_problems(case, generic):
+    """ks_problem.batch = B: one context over B independent problems laid end
+    to end; every problem's outputs match the oracle run on that problem
+    alone (whose first step has no evolution row)."""
+    if case == "c4" and not generic:
+        pytest.skip("n = 48 runs on the CTA path only")
+    parts = _batch_cases(case)
+    p = gen.Problem.concat(parts)
+    s = ks().Smoother(p, batch=len(parts), generic=generic)
+    s.run()
+    s.check()
+    x, S = s.states.cpu().numpy(), s.cov.cpu().numpy()
+    Nb = parts[0].N
+    for b, q in enumerate(parts):
+        xo, So = oracle.smooth(q)
+        xb, Sb = x[b * Nb:(b + 1) * Nb], S[b * Nb:(b + 1) * Nb]
+        assert rel_state_err(xb, xo) <= TOL_X, (b, rel_state_err(xb, xo))
+        assert rel_cov_err(Sb, So) <= TOL_S, (b, rel_cov_err(Sb, So))
+
+
+def test_batched_bad_args():
+    p = gen.make("c1", N=100)
+    with pytest.raises(ks().KsError):
+        ks().Smoother(p, batch=7)        # 100 % 7 != 0
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("cfg,N", [("c2", 2000), ("c3", 1777), ("c5", 1 << 14), ("c4", 41)])
+def test_update_obs(cfg, N, host, generic):
+    """ks_update_obs: new observations re-whitened in place (the model's
+    whitening kept), then factor + solve; the states equal a fresh run on the
+    new observations and the earlier covariances stay valid (they do not
+    depend on o)."""
+    if cfg == "c4" and not generic:
+        pytest.skip("n = 48 runs on the CTA path only")
+    p = gen.make(cfg, N=N)
+    q = gen.make(cfg, N=N)
+    rng = np.random.default_rng(5)
+    q.o = q.o + rng.standard_normal(q.o.shape) * (np.abs(q.o).max() * 0.1 + 1.0)
+    q.o[np.arange(q.m_max)[None, :] >= q.m[:, None]] = 0.0
+    s = ks().Smoother(p, keep_whitening=True, host_inputs=host, bind_outputs=not host, generic=generic)
+    s.run()
+    s.check()
+    x1 = torch.empty((N, p.n), dtype=torch.float64)
+    S1 = torch.empty((N, p.n, p.n), dtype=torch.float64)
+    s.get(x1, S1)
+    s.update_obs(q.o)
+    s.factor()
+    s.solve()
+    s.check()
+    x2 = torch.empty((N, p.n), dtype=torch.float64)
+    S2 = torch.empty((N, p.n, p.n), dtype=torch.float64)
+    s.get(x2, S2)
+    xf, Sf, _ = gpu_smooth(q, generic=generic)
+    assert rel_state_err(x2.numpy(), xf) <= 1e-12
+    assert np.array_equal(S2.numpy(), S1.numpy())
+    assert rel_cov_err(S2.numpy(), Sf) <= 1e-12
+    xo = oracle.smooth(q, cov=False)
+    assert rel_state_err(x2.numpy(), xo) <= TOL_X
+
+
+def test_update_obs_needs_kept_whitening():
+    p = gen.make("c2", N=500)
+    s = ks().Smoother(p)
+    s.run()
+    with pytest.raises(ks().KsError) as ei:
+        s.update_obs(p.o)
+    assert ei.value.code == ks().KS_ERR_ARG
