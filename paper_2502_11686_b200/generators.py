@@ -29,7 +29,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["Problem", "CONFIGS", "make", "paper_problem", "random_problem"]
+__all__ = ["Problem", "CONFIGS", "make", "paper_problem", "random_problem", "general_problem"]
 
 
 @dataclass
@@ -48,6 +48,11 @@ class Problem:
     x_true: Optional[np.ndarray] = None  # [N, n] simulated trajectory
     seed: int = 0
     meta: dict = field(default_factory=dict)
+    # general model (ks_problem Hev / l / nstate): evolution
+    # H_i x_i = F_i x_{i-1} + c_i + w_i with H_i l_i x n_i; None = uniform
+    Hev: Optional[np.ndarray] = None    # [N|1, n, n]   (rows >= l_i, cols >= n_i are 0)
+    l: Optional[np.ndarray] = None      # int32 [N]     evolution rows l_i
+    nstate: Optional[np.ndarray] = None  # int32 [N]    state dimensions n_i
 
     def stride(self, name: str) -> int:
         """Per-step stride in doubles (0 = the same block every step)."""
@@ -63,11 +68,12 @@ class Problem:
             if a is None:
                 return None
             return a if a.shape[0] == 1 else np.ascontiguousarray(a[lo:hi])
+        v = lambda a: None if a is None else np.ascontiguousarray(a[lo:hi])
         return Problem(self.name + f"[{lo}:{hi}]", hi - lo, self.n, self.m_max,
                        np.ascontiguousarray(self.m[lo:hi]), s(self.F), s(self.H),
                        s(self.K), s(self.L), np.ascontiguousarray(self.o[lo:hi]),
                        s(self.c), None if self.x_true is None else self.x_true[lo:hi],
-                       self.seed, dict(self.meta))
+                       self.seed, dict(self.meta), s(self.Hev), v(self.l), v(self.nstate))
 
     @staticmethod
     def concat(parts: list, name: str = "batch") -> "Problem":
@@ -333,3 +339,46 @@ def random_problem(rng, N: int, n: int, m=None, m_max: Optional[int] = None,
     c = 0.3 * rng.standard_normal((cnt, n)) if with_c else None
     x, o = simulate(rng, F, K, H, L, mm, noise_free=noise_free, c=c)
     return Problem("random", N, n, mx, mm, F, H, K, L, o, c, x, 0)
+
+
+def general_problem(rng, N: int, n: int, m_max: Optional[int] = None, nmin: int = 1,
+                    noise_free: bool = False, rect: bool = True) -> Problem:
+    """The paper's general linear model: state dimensions
+    n_i in [nmin, n], evolution H_i x_i = F_i x_{i-1} + c_i + w_i with a
+    rectangular full-rank H_i (l_i x n_i, l_i in [1, n], possibly != n_i),
+    F_i l_i x n_{i-1}, K_i l_i x l_i, observations G_i (ABI H) m_i x n_i.
+    Stored in the uniform padded arrays of the C ABI (unused rows/columns 0,
+    unused K / L diagonal 1).  Full column rank of UA: m_0 >= n_0 and
+    l_i + m_i >= n_i with generic (Gaussian) blocks.  The data are consistent
+    with a drawn trajectory x_true: c_i = H_i x_i - F_i x_{i-1} (+ w_i),
+    o_i = G_i x_i (+ v_i); noise_free gives an exactly consistent system."""
+    mx = n if m_max is None else int(m_max)
+    ns = rng.integers(nmin, n + 1, N).astype(np.int32)
+    ls = (rng.integers(1, n + 1, N) if rect else ns.copy()).astype(np.int32)
+    ms = rng.integers(0, mx + 1, N).astype(np.int32)
+    ms = np.maximum(ms, np.maximum(ns - ls, 0)).astype(np.int32)
+    ms[0] = max(ms[0], ns[0])
+    assert ms.max() <= mx, "m_max too small for l_i + m_i >= n_i"
+    Hev = np.zeros((N, n, n)); F = np.zeros((N, n, n)); K = np.tile(np.eye(n), (N, 1, 1))
+    H = np.zeros((N, mx, n)); L = np.tile(np.eye(mx), (N, 1, 1)); c = np.zeros((N, n))
+    o = np.zeros((N, mx)); x = np.zeros((N, n))
+    for i in range(N):
+        x[i, :ns[i]] = rng.standard_normal(ns[i])
+    for i in range(N):
+        ni, li, mi = int(ns[i]), int(ls[i]), int(ms[i])
+        Hev[i, :li, :ni] = rng.standard_normal((li, ni)) + np.eye(li, ni)
+        Ki = wishart_bounded(rng, 1, li, 50.0)[0]
+        K[i, :li, :li] = Ki
+        if i > 0:
+            npv = int(ns[i - 1])
+            F[i, :li, :npv] = 0.5 * rng.standard_normal((li, npv))
+            w = np.zeros(li) if noise_free else np.linalg.cholesky(Ki) @ rng.standard_normal(li)
+            c[i, :li] = Hev[i, :li, :ni] @ x[i, :ni] - F[i, :li, :npv] @ x[i - 1, :npv] + w
+        if mi > 0:
+            H[i, :mi, :ni] = rng.standard_normal((mi, ni))
+            Li = wishart_bounded(rng, 1, mi, 50.0)[0]
+            L[i, :mi, :mi] = Li
+            v = np.zeros(mi) if noise_free else np.linalg.cholesky(Li) @ rng.standard_normal(mi)
+            o[i, :mi] = H[i, :mi, :ni] @ x[i, :ni] + v
+    return Problem("general", N, n, mx, ms, F, H, K, L, o, c, x, 0, {"nmin": nmin},
+                   Hev, ls, ns)

@@ -218,3 +218,50 @@ def test_whitening_square_root_invariance():
     p.L = p.L * 4.0
     x2, S2 = oracle.smooth(p)
     np.testing.assert_allclose(x1, x2, rtol=1e-11, atol=1e-12)
+
+
+# ---- the general-model oracle (oracle/general.py) ----
+
+@pytest.mark.parametrize("seed", range(8))
+def test_general_oracle_vs_dense(seed):
+    """Rectangular H_i (l_i x n_i) and per-step n_i: states = dense lstsq of
+    the stacked general UA, covariances = diagonal blocks of inv(UA^T UA)."""
+    from oracle import general as og
+    from tests.dense import dense_solution_general
+    rng = np.random.default_rng(100 + seed)
+    n = 2 + seed % 4
+    p = gen.general_problem(rng, 12 + 3 * seed, n, nmin=1 + seed % 2, rect=seed % 3 != 0)
+    x, S = og.smooth_general(p)
+    xd, Sd, kappa = dense_solution_general(p)
+    assert rel_state_err(x, xd) < 1e-13 * max(kappa, 10.0) * 10
+    err = np.abs(S - Sd).max() / np.abs(Sd).max()
+    assert err < 1e-13 * max(kappa, 10.0) ** 2
+    assert np.all(S[:, :, :] == np.swapaxes(S, 1, 2))
+
+
+def test_general_oracle_noise_free_recovery():
+    from oracle import general as og
+    rng = np.random.default_rng(7)
+    p = gen.general_problem(rng, 200, 6, nmin=2, noise_free=True)
+    x = og.smooth_general(p, cov=False)
+    assert rel_state_err(x, p.x_true) < 1e-10
+
+
+def test_general_oracle_uniform_matches_c_oracle():
+    """With H_i = I and l_i = n_i = n the general oracle solves the problem
+    the plain-C oracle solves."""
+    from oracle import general as og
+    for cfg, N in (("c2", 60), ("c3", 61), ("c1", 40)):
+        p = gen.make(cfg, N=N)
+        x, S = og.smooth_general(p)
+        xo, So = oracle.smooth(p)
+        assert rel_state_err(x, xo) < 1e-12 and rel_cov_err(S, So) < 1e-12
+
+
+def test_general_oracle_rank_deficient():
+    from oracle import general as og
+    rng = np.random.default_rng(3)
+    p = gen.general_problem(rng, 10, 3, nmin=3, rect=False)
+    p.m[:] = 0                   # no observations: x_0 undetermined
+    with pytest.raises(og.GeneralOracleError):
+        og.smooth_general(p)
