@@ -82,6 +82,8 @@ struct ks_ctx {
   ks_problem p{};
   int64_t N = 0;
   int n = 0, mx = 0;
+  int rc = 0;             // rows of the whitened level-0 C blocks: m_max (+ n - nstate_min padding rows)
+  bool general = false;   // the general model (Hev / l / nstate)
   cudaStream_t stream = nullptr;
   bool host_inputs = false;
   // sharding
@@ -89,10 +91,13 @@ struct ks_ctx {
   int rank = 0, nranks = 1, q = 0;
   void *comm = nullptr;   // the ks_dist's NCCL communicator (borrowed) or null
   // device views of the inputs
-  const int32_t *m = nullptr;
-  const double *F = nullptr, *H = nullptr, *c = nullptr, *o = nullptr, *K = nullptr, *L = nullptr;
+  const int32_t *m = nullptr, *l = nullptr, *ns = nullptr;
+  const double *F = nullptr, *H = nullptr, *c = nullptr, *o = nullptr, *K = nullptr, *L = nullptr,
+               *Hev = nullptr;
   // staging for host inputs
-  int32_t *st_m = nullptr;
+  int32_t *st_m = nullptr, *st_l = nullptr, *st_ns = nullptr;
+  double *st_Hev = nullptr;
+  size_t nHev = 0;
   double *st_F = nullptr, *st_H = nullptr, *st_c = nullptr, *st_o = nullptr, *st_K = nullptr,
          *st_L = nullptr;
   size_t nF = 0, nH = 0, nc = 0, no = 0, nK = 0, nL = 0;  // staged doubles
@@ -141,8 +146,13 @@ int cuda_fail(cudaError_t e) {
 
 bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 
+// Rows of the whitened level-0 C blocks: the observation rows, plus (per-step
+// state dimensions n_i < n) the embedding's padding rows e_k^T x_i = 0 that
+// pin the unused components k >= n_i of the uniform n-vector.
+int level0_rows(const ks_problem *p) { return p->m_max + (p->nstate ? p->n - p->nstate_min : 0); }
+
 bool use_small(const ks_problem *p) {
-  return p->n <= kSmallMaxN && p->m_max <= kSmallMaxM && !(p->flags & KS_GENERIC_PATH);
+  return p->n <= kSmallMaxN && level0_rows(p) <= kSmallMaxM && !(p->flags & KS_GENERIC_PATH);
 }
 
 
@@ -166,11 +176,15 @@ int validate(const ks_problem *p, const ks_dist *d) {
     return KS_ERR_ARG;
   if (p->flags & ~kAllFlags) return KS_ERR_ARG;
   if (!use_small(p)) {
-    if (factor_smem_bytes(p->n, p->m_max > p->n ? p->m_max : p->n) > 227 * 1024) return KS_ERR_ARG;
+    const int rc = level0_rows(p);
+    if (factor_smem_bytes(p->n, rc > p->n ? rc : p->n) > 227 * 1024) return KS_ERR_ARG;
     if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
   }
   if (p->batch < 0 || (p->batch > 1 && global_steps(p, d) % p->batch != 0)) return KS_ERR_ARG;
-  if (p->Hev || p->l || p->nstate) return KS_ERR_ARG;   // general model: not in this build
+  if (p->sHev < 0 || (p->sHev && p->sHev < n * n)) return KS_ERR_ARG;
+  if (p->nstate && (p->nstate_min < 1 || p->nstate_min > p->n)) return KS_ERR_ARG;
+  // per-step n_i: the mask of F_i needs n_{i-1}, which a shard's first step does not have
+  if (p->nstate && d && d->nranks > 1) return KS_ERR_ARG;
   if (d && d->nranks > 1) {
     // power-of-two shards in rank order (the local levels then follow the
     // global trailing-ones rule with no halo)
@@ -201,7 +215,7 @@ size_t carve(ks_ctx *c, char *base) {
   Carve w{base};
   const ks_problem &p = c->p;
   const int64_t N = c->N;
-  const int n = c->n, mx = c->mx;
+  const int n = c->n, mx = c->mx, rc = c->rc;
   const int64_t nn = (int64_t)n * n, E = entry_doubles(n), Rr = rrec_doubles(n);
   c->status = w.take<unsigned long long>(2);
   if (c->host_inputs) {
@@ -219,10 +233,16 @@ size_t carve(ks_ctx *c, char *base) {
     c->st_L = w.take<double>(c->nL);
     c->st_o = w.take<double>(c->no);
     c->st_c = p.c ? w.take<double>(c->nc) : nullptr;
+    c->nHev = p.Hev ? cnt(p.sHev, nn) : 0;
+    c->st_Hev = p.Hev ? w.take<double>(c->nHev) : nullptr;
+    c->st_l = p.l ? w.take<int32_t>(N) : nullptr;
+    c->st_ns = p.nstate ? w.take<int32_t>(N) : nullptr;
   }
   // a batch needs per-step evolution blocks (zero rows at every problem's first step)
-  c->cntE = (p.sF == 0 && p.sK == 0 && (p.c == nullptr || p.sc == 0) && p.batch <= 1) ? 1 : N;
-  c->cntC = (p.sH == 0 && p.sL == 0 && p.m == nullptr) ? 1 : N;
+  // (the general model: per-step unless only a constant H_i is given)
+  c->cntE = (p.sF == 0 && p.sK == 0 && (p.c == nullptr || p.sc == 0) && p.batch <= 1 && p.sHev == 0 &&
+             !p.l && !p.nstate) ? 1 : N;
+  c->cntC = (p.sH == 0 && p.sL == 0 && p.m == nullptr && !p.nstate) ? 1 : N;
   c->Mall = ((p.flags & KS_KEEP_WHITENING) && c->cntC > 1) ? w.take<double>(c->cntC * mx * mx + 1) : nullptr;
   const bool sm = c->small;
   const int64_t Rs = small_rrec_doubles(n);
@@ -234,16 +254,16 @@ size_t carve(ks_ctx *c, char *base) {
     c->e0 = w.take<double>(sz(cE, n));
     c->nEr0 = w.take<double>(sz(cE, 1));
     c->nEl0 = w.take<double>(sz(cE, 1));
-    c->C0 = w.take<double>(sz(cC, (int64_t)mx * n) + 1);
+    c->C0 = w.take<double>(sz(cC, (int64_t)rc * n) + 1);
     c->nC0 = w.take<double>(sz(cC, 1));
-    c->y0 = w.take<double>(ptiled_doubles(N, mx) + 1);
+    c->y0 = w.take<double>(ptiled_doubles(N, rc) + 1);
     c->zscratch = w.take<double>(nn + n + 2);   // + the split-odd-level flag
   } else {
     c->El0 = w.take<double>(c->cntE * nn);
     c->Er0 = w.take<double>(c->cntE * nn);
     c->e0 = w.take<double>(c->cntE * n);
-    c->C0 = w.take<double>(c->cntC * mx * n + 1);
-    c->y0 = w.take<double>(N * mx + 1);
+    c->C0 = w.take<double>(c->cntC * rc * n + 1);
+    c->y0 = w.take<double>(N * rc + 1);
     c->zscratch = w.take<double>(nn + n + 2);   // + the split-odd-level flag
   }
   c->Mchol = w.take<double>((size_t)mx * mx + 1);
@@ -321,15 +341,15 @@ struct Launch {
 
 EntryView level0_view(const ks_ctx *c) {
   EntryView v;
-  const int n = c->n, mx = c->mx;
+  const int n = c->n, rc = c->rc;
   const int64_t nn = (int64_t)n * n;
-  v.C = c->C0; v.sC = c->cntC == 1 ? 0 : (int64_t)mx * n;
-  v.y = c->y0; v.sy = mx;
+  v.C = c->C0; v.sC = c->cntC == 1 ? 0 : (int64_t)rc * n;
+  v.y = c->y0; v.sy = rc;
   v.El = c->El0; v.sEl = c->cntE == 1 ? 0 : nn;
   v.Er = c->Er0; v.sEr = c->cntE == 1 ? 0 : nn;
   v.e = c->e0; v.se = c->cntE == 1 ? 0 : n;
   v.nrm = nullptr; v.snrm = 0;
-  v.RC = mx;
+  v.RC = rc;
   return v;
 }
 
@@ -349,23 +369,23 @@ TView tv(const double *p, int64_t ts) { return TView{const_cast<double *>(p), ts
 // Constant observation model on the small path: the level-0 factor computes
 // y = M^{-1} o itself (no y pass over HBM).
 int small_yfuse(const ks_ctx *c) {
-  return (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr) ? 1 : 0;
+  return (c->mx > 0 && c->cntC == 1) ? 1 : 0;
 }
 
 SmallIn small_level0(const ks_ctx *c) {
-  const int n = c->n, mx = c->mx;
+  const int n = c->n, rc = c->rc;
   const int64_t nn = (int64_t)n * n;
   const bool cE = c->cntE == 1, cC = c->cntC == 1;
   SmallIn v;
-  v.C = tv(c->C0, cC ? 0 : 64 * (int64_t)mx * n);
-  v.y = tv(c->y0, 64 * (int64_t)mx);
+  v.C = tv(c->C0, cC ? 0 : 64 * (int64_t)rc * n);
+  v.y = tv(c->y0, 64 * (int64_t)rc);
   v.El = tv(c->El0, cE ? 0 : 64 * nn);
   v.Er = tv(c->Er0, cE ? 0 : 64 * nn);
   v.e = tv(c->e0, cE ? 0 : 64 * (int64_t)n);
   v.nC = tv(c->nC0, cC ? 0 : 64);
   v.nEr = tv(c->nEr0, cE ? 0 : 64);
   v.nEl = tv(c->nEl0, cE ? 0 : 64);
-  v.RC = mx;
+  v.RC = rc;
   v.ent = tv(nullptr, 0);
   v.yfuse = small_yfuse(c);
   v.o = c->o;
@@ -752,7 +772,7 @@ size_t ks_workspace_bytes(const ks_problem *p, const ks_dist *d) {
   if (validate(p, d) != KS_OK) return 0;
   ks_ctx c;
   c.p = *p;
-  c.N = p->nsteps; c.n = p->n; c.mx = p->m_max;
+  c.N = p->nsteps; c.n = p->n; c.mx = p->m_max; c.rc = level0_rows(p);
   c.host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
   c.small = use_small(p);
   if (d && d->nranks > 1) {
@@ -776,7 +796,8 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
   ks_ctx *c = new (std::nothrow) ks_ctx;
   if (!c) return KS_ERR_ARG;
   c->p = *p;
-  c->N = p->nsteps; c->n = p->n; c->mx = p->m_max;
+  c->N = p->nsteps; c->n = p->n; c->mx = p->m_max; c->rc = level0_rows(p);
+  c->general = p->Hev || p->l || p->nstate;
   c->stream = (cudaStream_t)stream;
   c->host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
   c->chol = (p->flags & KS_COV_IS_CHOL) != 0;
@@ -794,9 +815,10 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
   carve(c, (char *)workspace);
   if (c->host_inputs) {
     c->m = c->st_m; c->F = c->st_F; c->K = c->st_K; c->H = c->st_H; c->L = c->st_L;
-    c->o = c->st_o; c->c = c->st_c;
+    c->o = c->st_o; c->c = c->st_c; c->Hev = c->st_Hev; c->l = c->st_l; c->ns = c->st_ns;
   } else {
     c->m = p->m; c->F = p->F; c->K = p->K; c->H = p->H; c->L = p->L; c->o = p->o; c->c = p->c;
+    c->Hev = p->Hev; c->l = p->l; c->ns = p->nstate;
   }
   *out = c;
   return KS_OK;
@@ -811,7 +833,8 @@ int ks_whiten(ks_ctx *c) {
     struct { void *d; const void *h; size_t bytes; } cp[] = {
         {c->st_m, p.m, p.m ? (size_t)c->N * 4 : 0}, {c->st_F, p.F, c->nF * 8}, {c->st_K, p.K, c->nK * 8},
         {c->st_H, p.H, c->nH * 8}, {c->st_L, p.L, c->nL * 8}, {c->st_o, p.o, c->no * 8},
-        {c->st_c, p.c, c->nc * 8}};
+        {c->st_c, p.c, c->nc * 8}, {c->st_Hev, p.Hev, c->nHev * 8},
+        {c->st_l, p.l, p.l ? (size_t)c->N * 4 : 0}, {c->st_ns, p.nstate, p.nstate ? (size_t)c->N * 4 : 0}};
     for (auto &x : cp)
       if (x.bytes) {
         e = cudaMemcpyAsync(x.d, x.h, x.bytes, cudaMemcpyHostToDevice, c->stream);
@@ -825,7 +848,7 @@ int ks_whiten(ks_ctx *c) {
     a.sF = c->p.sF; a.sH = c->p.sH; a.sc = c->p.sc; a.so = c->p.so; a.sK = c->p.sK; a.sL = c->p.sL;
     a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
     a.cntE = c->cntE; a.cntC = c->cntC;
-    a.constC = (c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr);
+    a.constC = c->cntC == 1;
     const SmallIn v = small_level0(c);
     a.C = v.C; a.y = v.y; a.El = v.El; a.Er = v.Er; a.e = v.e; a.nC = v.nC; a.nEr = v.nEr; a.nEl = v.nEl;
     a.cE = c->cntE == 1;
@@ -835,6 +858,7 @@ int ks_whiten(ks_ctx *c) {
     a.chol = c->chol;
     a.seg = c->seg;
     a.Mall = c->Mall;
+    a.Hev = c->Hev; a.sHev = c->p.sHev; a.l = c->l; a.ns = c->ns; a.RC = c->rc;
     int nl = 0;
     {
       Launch l(c, 0, 0, 1);
@@ -855,9 +879,10 @@ int ks_whiten(ks_ctx *c) {
   a.chol = c->chol;
   a.seg = c->seg;
   a.Mall = c->Mall;
-  a.constC = (c->p.sH == 0 && c->p.sL == 0 && c->p.m == nullptr);
+  a.Hev = c->Hev; a.sHev = c->p.sHev; a.l = c->l; a.ns = c->ns; a.RC = c->rc;
+  a.constC = c->cntC == 1;
   {
-    Launch l(c, 0, 0, 1 + (c->mx > 0) + (c->mx > 0 && c->p.sH == 0 && c->p.sL == 0 && !c->p.m));
+    Launch l(c, 0, 0, 1 + (c->rc > 0) + (c->mx > 0 && c->cntC == 1));
     e = launch_whiten(a, c->stream);
   }
   if (e != cudaSuccess) return cuda_fail(e);
@@ -956,7 +981,7 @@ int ks_update_obs(ks_ctx *c, const double *o) {
     if (!(c->small && small_yfuse(c))) {   // (fused y: the factor whitens o itself)
       Launch l(c, 0, 0, 1);
       e = launch_update_y(constC ? c->Mchol : c->Mall, constC ? 0 : (int64_t)c->mx * c->mx, c->o, c->p.so, c->m,
-                          c->mx, c->N, c->y0, c->small ? 1 : 0, c->stream);
+                          c->mx, c->rc, c->N, c->y0, c->small ? 1 : 0, c->stream);
       if (e != cudaSuccess) return cuda_fail(e);
     }
   }

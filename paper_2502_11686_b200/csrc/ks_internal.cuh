@@ -88,6 +88,11 @@ struct WhitenArgs {
   int chol;              // KS_COV_IS_CHOL: K, L already hold the lower Cholesky factors
   int64_t seg;           // steps per independent problem (global): step g has no evolution row iff g % seg == 0
   double *Mall;          // KS_KEEP_WHITENING: [cntC][m_max][m_max] lower factors M_i (row-major), or null
+  // general model: evolution matrix H_i (null = I), rows l_i, state dims n_i (null: uniform)
+  const double *Hev;
+  int64_t sHev;
+  const int32_t *l, *ns;
+  int RC;                // rows of the whitened C blocks (m_max + padding rows e_k^T x_i = 0, k >= n_i)
   unsigned long long *status;
 };
 
@@ -188,6 +193,10 @@ struct SmallWhitenArgs {
   int chol;                    // KS_COV_IS_CHOL: K, L already hold the lower Cholesky factors
   int64_t seg;                 // steps per independent problem (global; see WhitenArgs)
   double *Mall;                // KS_KEEP_WHITENING: [cntC][m_max][m_max] lower factors M_i, or null
+  const double *Hev;           // general model (see WhitenArgs)
+  int64_t sHev;
+  const int32_t *l, *ns;
+  int RC;
   unsigned long long *status;
 };
 size_t small_entry_doubles(int n);                  // = entry_doubles(n)
@@ -209,7 +218,7 @@ cudaError_t set_smem_attr(const void *func, int bytes);
 // factors M (stride sM doubles per step: 0 = constant), written pair-
 // interleaved tiled (small path, ptiled != 0) or row-major [N][m_max].
 cudaError_t launch_update_y(const double *M, int64_t sM, const double *o, int64_t so, const int32_t *m, int mx,
-                            int64_t N, double *y, int ptiled, cudaStream_t s);
+                            int rc, int64_t N, double *y, int ptiled, cudaStream_t s);
 
 // kernel launchers of the CTA path (ks_large.cu); return cudaGetLastError()
 cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s);

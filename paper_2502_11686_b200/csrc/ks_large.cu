@@ -1119,6 +1119,20 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
     X[r + 2 * n * ld] = c ? c[r] : 0.0;
   }
   sync_loads();
+  if (a.Hev || a.l || a.ns) {   // general model: mask to l_i rows, H_i, n_{i-1} columns of F
+    const int li = a.l ? a.l[i] : (a.ns ? a.ns[i] : n), ni = a.ns ? a.ns[i] : n;
+    const int npv = (a.ns && i > 0) ? a.ns[i - 1] : n;
+    const double *Hv = a.Hev ? a.Hev + iK * a.sHev : nullptr;
+    for (int k = tid; k < nn; k += blockDim.x) {
+      const int r = k / n, cc = k - r * n;
+      if (r >= li || cc >= li) Lm[r + cc * ld] = (r == cc) ? 1.0 : 0.0;   // K_i: leading l_i block
+      if (r >= li || cc >= npv) X[r + cc * ld] = 0.0;
+      X[r + (n + cc) * ld] = (r < li && cc < ni) ? (Hv ? Hv[k] : (r == cc ? 1.0 : 0.0)) : 0.0;
+    }
+    for (int r = tid; r < n; r += blockDim.x)
+      if (r >= li) X[r + 2 * n * ld] = 0.0;
+    __syncthreads();
+  }
   const bool ok = a.chol ? chol_diag_ok(Lm, ld, n, sh) : cta_chol(Lm, ld, n, sh);
   if (tid == 0 && !ok) {
     const int64_t step = (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i;
@@ -1141,11 +1155,14 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   const int n = a.n, mx = a.m_max, tid = threadIdx.x;
   const int64_t i = blockIdx.x;
   const int mi = a.m ? a.m[i] : mx;
-  double *C = a.C + i * (int64_t)mx * n;
-  const int ld = ldpad(mx), p = n + 1, cp = pad8(p) + 8;
-  double *Lm = sm, *X = Lm + ld * pad8(mx), *sh = X + ld * cp;
+  const int ni = a.ns ? a.ns[i] : n;   // general model: columns >= n_i of H_i ignored
+  const int rc = a.RC;
+  double *C = a.C + i * (int64_t)rc * n;
+  const int mx1 = mx > 0 ? mx : 1;   // (m_max = 0 with padding rows: no observation blocks)
+  const int ld = ldpad(mx1), p = n + 1, cp = pad8(p) + 8;
+  double *Lm = sm, *X = Lm + ld * pad8(mx1), *sh = X + ld * cp;
   const double *L = a.L + i * a.sL, *H = a.H + i * a.sH, *o = a.o + i * a.so;
-  zero_smem(sm, ld * pad8(mx) + ld * cp);
+  zero_smem(sm, ld * pad8(mx1) + ld * cp);
   __syncthreads();
   for (int k = tid; k < mi * mi; k += blockDim.x) {   // asynchronous loads
     const int r = k / mi, cc = k - r * mi;
@@ -1153,7 +1170,7 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   }
   for (int k = tid; k < mi * n; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
-    cp8(&X[r + cc * ld], H + r * n + cc);
+    if (cc < ni) cp8(&X[r + cc * ld], H + r * n + cc);
   }
   for (int r = tid; r < mi; r += blockDim.x) cp8(&X[r + n * ld], o + r);
   sync_loads();
@@ -1162,9 +1179,10 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   diag_rcp(Lm, ld, mi, sh);
   __syncthreads();
   trsm_lower(Lm, ld, sh, mi, X, ld, p);
-  for (int k = tid; k < mx * n; k += blockDim.x) {
+  for (int k = tid; k < rc * n; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
-    C[k] = (r < mi) ? X[r + cc * ld] : 0.0;
+    // rows m_i .. m_i + n - n_i - 1: the padding rows e_k^T x_i = 0 (k >= n_i)
+    C[k] = (r < mi) ? X[r + cc * ld] : ((r - mi < n - ni && cc == ni + (r - mi)) ? 1.0 : 0.0);
   }
   if (a.Mall) {   // KS_KEEP_WHITENING: M_i for ks_update_obs
     for (int k = tid; k < mx * mx; k += blockDim.x) {
@@ -1173,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
     }
   }
   if (!a.constC) {
-    for (int r = tid; r < mx; r += blockDim.x) a.y[i * mx + r] = (r < mi) ? X[r + n * ld] : 0.0;
+    for (int r = tid; r < rc; r += blockDim.x) a.y[i * rc + r] = (r < mi) ? X[r + n * ld] : 0.0;
   } else {
     for (int k = tid; k < mi * mi; k += blockDim.x) {
       const int r = k / mi, cc = k - r * mi;
@@ -1237,8 +1255,8 @@ cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s) {
   set_smem_attr((const void *)whiten_obs_kernel, 227 * 1024);
   const int n = a.n, mx = a.m_max;
   whiten_evo_kernel<<<(unsigned)a.cntE, kThreads, whiten_evo_smem(n), s>>>(a);
-  if (mx > 0) {
-    whiten_obs_kernel<<<(unsigned)a.cntC, kThreads, whiten_obs_smem(n, mx), s>>>(a);
+  if (a.RC > 0) {
+    whiten_obs_kernel<<<(unsigned)a.cntC, kThreads, whiten_obs_smem(n, mx > 0 ? mx : 1), s>>>(a);
     if (a.constC) {
       const int T = 256;
       whiten_y_kernel<<<(unsigned)((a.N + T - 1) / T), T, 8 * (size_t)mx * mx, s>>>(a);

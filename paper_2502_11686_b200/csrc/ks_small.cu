@@ -89,14 +89,15 @@ cudaError_t launch_boundary_ptile(const double *recv, double *out, int P, int n,
 }
 
 __global__ void update_y_kernel(const double *__restrict__ M, int64_t sM, const double *__restrict__ o, int64_t so,
-                                const int32_t *__restrict__ m, int mx, int64_t N, double *__restrict__ y, int ptiled) {
+                                const int32_t *__restrict__ m, int mx, int rc, int64_t N, double *__restrict__ y,
+                                int ptiled) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const double *Mi = M + i * sM, *oi = o + i * so;
   const int mi = m ? m[i] : mx;
   // element r of step i (the output doubles as the substitution's scratch)
   auto at = [&](int r) -> double & {
-    return ptiled ? y[(i >> 6) * 64 * mx + (i & 1) * 32 * mx + 32 * r + ((i >> 1) & 31)] : y[i * mx + r];
+    return ptiled ? y[(i >> 6) * 64 * rc + (i & 1) * 32 * rc + 32 * r + ((i >> 1) & 31)] : y[i * rc + r];
   };
   for (int r = 0; r < mx; ++r) {
     double v = 0.0;
@@ -109,8 +110,8 @@ __global__ void update_y_kernel(const double *__restrict__ M, int64_t sM, const 
   }
 }
 cudaError_t launch_update_y(const double *M, int64_t sM, const double *o, int64_t so, const int32_t *m, int mx,
-                            int64_t N, double *y, int ptiled, cudaStream_t s) {
-  update_y_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(M, sM, o, so, m, mx, N, y, ptiled);
+                            int rc, int64_t N, double *y, int ptiled, cudaStream_t s) {
+  update_y_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(M, sM, o, so, m, mx, rc, N, y, ptiled);
   return cudaGetLastError();
 }
 

@@ -1425,12 +1425,19 @@ __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_
   const int64_t iK = (a.cntE == 1) ? 0 : i;
   const double *K = a.K + iK * a.sK, *F = a.F + iK * a.sF;
   const double *cc = a.c ? a.c + iK * a.sc : nullptr;
+  // general model: l_i evolution rows, H_i (l_i x n_i), F_i
+  // (l_i x n_{i-1}); the unused rows / columns of the uniform n x n blocks are
+  // masked to zero (K: identity), so rows >= l_i of El, Er, e come out zero
+  const int li = a.l ? a.l[i] : (a.ns ? a.ns[i] : N);
+  const int ni = a.ns ? a.ns[i] : N;
+  const int npv = (a.ns && i > 0) ? a.ns[i - 1] : N;
+  const double *Hv = a.Hev ? a.Hev + iK * a.sHev : nullptr;
   double Lm[N][N];
   bool ok = true;
 #pragma unroll
   for (int r = 0; r < N; ++r)
 #pragma unroll
-    for (int c = 0; c <= r; ++c) Lm[r][c] = K[r * N + c];
+    for (int c = 0; c <= r; ++c) Lm[r][c] = (r < li) ? K[r * N + c] : (r == c ? 1.0 : 0.0);
   if (a.chol) {   // KS_COV_IS_CHOL: K holds Lam itself (nonzero diagonal)
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -1467,7 +1474,7 @@ __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_
     double x[N];
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      double s = F[r * N + c];
+      double s = (r < li && c < npv) ? F[r * N + c] : 0.0;
 #pragma unroll
       for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
       x[r] = s * il[r];
@@ -1478,16 +1485,16 @@ __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_
       nel = fma(x[r], x[r], nel);
     }
   }
-  // Er = Lam^{-1} (lower triangular)
+  // Er = Lam^{-1} H_i (H_i = I: lower triangular Lam^{-1})
 #pragma unroll
   for (int c = 0; c < N; ++c) {
     double x[N];
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      double s = (r == c) ? 1.0 : 0.0;
+      double s = (r < li && c < ni) ? (Hv ? Hv[r * N + c] : (r == c ? 1.0 : 0.0)) : 0.0;
 #pragma unroll
       for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
-      x[r] = (r < c) ? 0.0 : s * il[r];
+      x[r] = s * il[r];
     }
 #pragma unroll
     for (int r = 0; r < N; ++r) {
@@ -1499,7 +1506,7 @@ __device__ __forceinline__ void whiten_evo_body(const SmallWhitenArgs &a, int64_
     double x[N];
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      double s = cc ? cc[r] : 0.0;
+      double s = (cc && r < li) ? cc[r] : 0.0;
 #pragma unroll
       for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
       x[r] = s * il[r];
@@ -1521,6 +1528,7 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
   const int mx = a.m_max;
   const int mi = a.m ? a.m[i] : mx;
   const double *L = a.L + i * a.sL, *H = a.H + i * a.sH, *o = a.o + i * a.so;
+  const int ni = a.ns ? a.ns[i] : N;   // general model: columns >= n_i of H_i ignored
   double Lm[MM][MM];
   bool ok = true;
   if (a.chol) {   // KS_COV_IS_CHOL: L holds M itself (nonzero diagonal)
@@ -1578,7 +1586,7 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
 #pragma unroll
     for (int r = 0; r < MM; ++r) {
       if (r < mi) {
-        double s = is_o ? o[r] : H[r * N + c];
+        double s = is_o ? o[r] : (c < ni ? H[r * N + c] : 0.0);
 #pragma unroll
         for (int k = 0; k < r; ++k) s = fma(-Lm[r][k], x[k], s);
         x[r] = s * ild[r];
@@ -1588,12 +1596,15 @@ __device__ __forceinline__ void whiten_obs_body(const SmallWhitenArgs &a, int64_
     }
 #pragma unroll
     for (int r = 0; r < MM; ++r) {
-      if (r < mx) {
+      if (r < a.RC) {
         if (is_o) {
           wst(a.y, 0, i, r, x[r]);
         } else {
-          wst(a.C, a.cC, i, r * N + c, x[r]);
-          nc = fma(x[r], x[r], nc);
+          // rows m_i .. m_i + n - n_i - 1: the padding rows e_k^T x_i = 0
+          // (k = n_i ..) of the general model's embedding (y = 0)
+          const double v = (r < mi) ? x[r] : ((r - mi < N - ni && c == ni + (r - mi)) ? 1.0 : 0.0);
+          wst(a.C, a.cC, i, r * N + c, v);
+          nc = fma(v, v, nc);
         }
       }
     }
@@ -1719,7 +1730,7 @@ template <int N>
 cudaError_t whiten_n(const SmallWhitenArgs &a, cudaStream_t s, int *nl) {
   const int T = 128;
   const unsigned gE = (unsigned)((a.cntE + T - 1) / T);
-  const unsigned gC = a.m_max > 0 ? (unsigned)((a.cntC + T - 1) / T) : 0u;
+  const unsigned gC = a.RC > 0 ? (unsigned)((a.cntC + T - 1) / T) : 0u;
   small_whiten_eo<N><<<gE + gC, T, 0, s>>>(a, gE);
   *nl = 1;
   if (a.m_max > 0) {

@@ -94,9 +94,10 @@ class Problem:
             return np.ascontiguousarray(np.concatenate([np.broadcast_to(a, (q.N,) + a.shape[1:])
                                                         for a, q in zip(arrs, parts)]))
         xt = None if any(q.x_true is None for q in parts) else np.concatenate([q.x_true for q in parts])
+        vec = lambda attr: None if getattr(p0, attr) is None else np.concatenate([getattr(q, attr) for q in parts])
         return Problem(name, p0.N * len(parts), p0.n, p0.m_max, np.concatenate([q.m for q in parts]),
                        cat("F"), cat("H"), cat("K"), cat("L"), cat("o"), cat("c"), xt, p0.seed,
-                       {"batch": len(parts)})
+                       {"batch": len(parts)}, cat("Hev"), vec("l"), vec("nstate"))
 
     def nbytes_inputs(self) -> int:
         tot = self.m.nbytes
@@ -353,8 +354,10 @@ def general_problem(rng, N: int, n: int, m_max: Optional[int] = None, nmin: int 
     with a drawn trajectory x_true: c_i = H_i x_i - F_i x_{i-1} (+ w_i),
     o_i = G_i x_i (+ v_i); noise_free gives an exactly consistent system."""
     mx = n if m_max is None else int(m_max)
+    assert mx >= nmin, "m_max >= min n_i needed for m_0 >= n_0"
     ns = rng.integers(nmin, n + 1, N).astype(np.int32)
-    ls = (rng.integers(1, n + 1, N) if rect else ns.copy()).astype(np.int32)
+    ns[0] = min(ns[0], mx)
+    ls = (rng.integers(np.maximum(1, ns - mx), n + 1) if rect else ns.copy()).astype(np.int32)
     ms = rng.integers(0, mx + 1, N).astype(np.int32)
     ms = np.maximum(ms, np.maximum(ns - ls, 0)).astype(np.int32)
     ms[0] = max(ms[0], ns[0])

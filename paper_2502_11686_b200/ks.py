@@ -207,9 +207,15 @@ class Smoother:
             # all m_i == m_max: pass m = NULL (lets a constant observation model
             # be whitened once, stride 0)
             inputs["m"] = None if bool(np.all(m == p.m_max)) else _as_tensor(m, tgt, pin=host_inputs)
+            # the general model: evolution matrix H_i, rows l_i, state dims n_i
+            inputs["Hev"] = _as_tensor(getattr(p, "Hev", None), tgt, pin=host_inputs)
+            for k in ("l", "nstate"):
+                a = getattr(p, k, None)
+                inputs[k] = None if a is None else _as_tensor(np.ascontiguousarray(a, np.int32), tgt,
+                                                              pin=host_inputs)
         self.inputs = inputs  # keep alive (borrowed by the library)
-        for k in ("F", "H", "K", "L", "o", "c"):
-            t = inputs[k]
+        for k in ("F", "H", "K", "L", "o", "c", "Hev"):
+            t = inputs.get(k)
             assert t is None or t.dtype == torch.float64
         pr = ks_problem()
         pr.nsteps, pr.n, pr.m_max = self.N, self.n, self.m_max
@@ -217,6 +223,10 @@ class Smoother:
         pr.m = ptr(inputs["m"])
         pr.F, pr.H, pr.c, pr.o, pr.K, pr.L = (ptr(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
         pr.sF, pr.sH, pr.sc, pr.so, pr.sK, pr.sL = (_stride(inputs[k]) for k in ("F", "H", "c", "o", "K", "L"))
+        pr.Hev, pr.sHev = ptr(inputs.get("Hev")), _stride(inputs.get("Hev"))
+        pr.l, pr.nstate = ptr(inputs.get("l")), ptr(inputs.get("nstate"))
+        if inputs.get("nstate") is not None:
+            pr.nstate_min = int(inputs["nstate"].min().item())
         pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0) | \
             (KS_GENERIC_PATH if generic else 0) | (0 if fused_tail else KS_NO_FUSED_TAIL) | \
             (KS_COV_IS_CHOL if chol else 0) | (KS_KEEP_WHITENING if keep_whitening else 0)

@@ -443,3 +443,81 @@ def test_update_obs_needs_kept_whitening():
     with pytest.raises(ks().KsError) as ei:
         s.update_obs(p.o)
     assert ei.value.code == ks().KS_ERR_ARG
+
+
+# ---- the general model ----
+
+def _general_parity(p, generic, noise_free=False):
+    from oracle import general as og
+    s = ks().Smoother(p, generic=generic)
+    s.run()
+    s.check()
+    x, S = s.states.cpu().numpy(), s.cov.cpu().numpy()
+    ns = p.nstate if p.nstate is not None else np.full(p.N, p.n)
+    xo, So = og.smooth_general(p)
+    mask_x = np.arange(p.n)[None, :] < ns[:, None]
+    mask_S = mask_x[:, :, None] & mask_x[:, None, :]
+    assert rel_state_err(np.where(mask_x, x, 0.0), xo) <= TOL_X
+    assert rel_cov_err(np.where(mask_S, S, 0.0), So) <= TOL_S
+    # the embedding's padding components: pinned to 0, uncorrelated with the state
+    pad = ~mask_x
+    assert np.abs(x[pad]).max(initial=0.0) <= 1e-12 * np.abs(xo).max()
+    cross = mask_x[:, :, None] & pad[:, None, :]
+    assert np.abs(S[cross]).max(initial=0.0) <= 1e-12 * np.abs(So).max()
+    if noise_free:
+        assert rel_state_err(np.where(mask_x, x, 0.0), p.x_true) <= 1e-9
+    return s
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("n,nmin,mmax,N", [(2, 1, 2, 257), (4, 1, 4, 300), (4, 2, 3, 1000), (6, 4, 4, 513),
+                                           (8, 8, 8, 129), (6, 2, 6, 200), (12, 5, 12, 150)])
+def test_general_model(n, nmin, mmax, N, generic):
+    """Per-step state dimensions n_i and rectangular evolution H_i (l_i x n_i,
+    l_i != n_i) against the general-model oracle; the small path takes the
+    problems whose padded observation blocks fit (m_max + n - min n_i <= 8)."""
+    rng = np.random.default_rng(1000 * n + 10 * nmin + mmax)
+    p = gen.general_problem(rng, N, n, m_max=mmax, nmin=nmin)
+    s = _general_parity(p, generic)
+    if not generic:
+        assert s.problem.n == n
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_general_model_noise_free(generic):
+    rng = np.random.default_rng(77)
+    p = gen.general_problem(rng, 2000, 4, m_max=4, nmin=2, noise_free=True)
+    _general_parity(p, generic, noise_free=True)
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_general_rectangular_only(generic):
+    """Uniform n_i = n, l_i in [1, n] with a per-step H_i; and a constant
+    non-identity H (stride 0, the constant-model path)."""
+    rng = np.random.default_rng(5)
+    p = gen.general_problem(rng, 700, 5, m_max=5, nmin=5)
+    p.nstate = None
+    _general_parity(p, generic)
+    q = gen.make("c2", N=999)
+    q.Hev = (np.eye(6) + 0.3 * rng.standard_normal((6, 6)))[None]
+    _general_parity(q, generic)
+
+
+def test_general_with_batch_and_host_inputs():
+    rng = np.random.default_rng(9)
+    parts = [gen.general_problem(rng, 64, 3, m_max=3, nmin=1) for _ in range(4)]
+    from oracle import general as og
+    p = gen.Problem.concat(parts)
+    s = ks().Smoother(p, batch=4, host_inputs=True, bind_outputs=False)
+    s.run()
+    xs = torch.empty((p.N, p.n), dtype=torch.float64)
+    Ss = torch.empty((p.N, p.n, p.n), dtype=torch.float64)
+    s.get(xs, Ss)
+    s.check()
+    for b, q in enumerate(parts):
+        xo, So = og.smooth_general(q)
+        ns = q.nstate
+        m = np.arange(p.n)[None, :] < ns[:, None]
+        xb = np.where(m, xs.numpy()[b * 64:(b + 1) * 64], 0.0)
+        Sb = np.where(m[:, :, None] & m[:, None, :], Ss.numpy()[b * 64:(b + 1) * 64], 0.0)
+        assert rel_state_err(xb, xo) <= TOL_X and rel_cov_err(Sb, So) <= TOL_S

@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 KEYS = {
-    "gpu__time_duration.sum": "dur_us",
+    "gpu__time_duration.sum": "dur_us",   # printed as dur_ms (base unit ns)
     "launch__grid_size": "grid",
     "launch__registers_per_thread": "regs",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occ%",
@@ -29,15 +29,29 @@ STALLS = ["no_instructions", "long_scoreboard", "short_scoreboard", "wait", "mat
 
 def main(rep, launch=None):
     flt = [] if launch is None else ["-s", str(launch), "-c", "1"]
-    out = subprocess.check_output(["ncu", "-i", rep, *flt, "--page", "raw", "--csv"]).decode()
+    # base units (ns, bytes, ...): ncu's default auto-scales each cell
+    # separately (msecond next to usecond, GB next to MB on one line)
+    out = subprocess.check_output(["ncu", "-i", rep, *flt, "--page", "raw", "--csv",
+                                   "--print-units", "base"]).decode()
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
     for r in rows[2:]:
         name = r[h.index("Kernel Name")][:60]
         vals = {}
         for k, short in KEYS.items():
             if k in h:
-                vals[short] = r[h.index(k)]
+                v, u = r[h.index(k)], units[h.index(k)]
+                try:
+                    x = float(v.replace(",", ""))
+                except ValueError:
+                    vals[short] = v
+                    continue
+                if u in ("nsecond", "ns"):
+                    vals[short.replace("dur_us", "dur_ms") if short == "dur_us" else short] = f"{x / 1e6:.4f}"
+                elif u in ("byte", "bytes"):
+                    vals[short + "_GB"] = f"{x / 1e9:.4f}"
+                else:
+                    vals[short] = v
         st = {}
         for s in STALLS:
             k = f"smsp__pcsamp_warps_issue_stalled_{s}"

@@ -1,0 +1,15 @@
+# Round-2 evidence capture (one GPU): full bench line (per_config), the launch
+# list of the bench command, ncu --set full of the c5 factor/backward L0/L1
+# launches and of the c4 (full N = 20000) CTA-path factor L0 and whitening.
+set -x
+TAG=${1:-r2a}
+mkdir -p gpurun_out
+python bench.py > gpurun_out/${TAG}_bench.log 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
+    python bench.py --steps 1 --warmup 3 --quick --no-graph > gpurun_out/${TAG}_ncu_launches.log 2>&1
+bash tools/prof_c5.sh 40 2 ${TAG}_c5f 58 2 ${TAG}_c5b
+python tools/prof_run.py c4 - 1 > gpurun_out/${TAG}_plain_c4.log 2>&1 || exit 1
+ncu --set full --clock-control none --import-source on -k regex:factor_level -s 15 -c 1 -o gpurun_out/${TAG}_c4f python tools/prof_run.py c4 - 1 > gpurun_out/${TAG}_ncu_c4.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:whiten -s 2 -c 2 -o gpurun_out/${TAG}_c4w python tools/prof_run.py c4 - 1 > gpurun_out/${TAG}_ncu_c4w.log 2>&1
+for r in c4f c4w; do python tools/ncu_summary.py gpurun_out/${TAG}_$r.ncu-rep > gpurun_out/${TAG}_$r.sum.txt 2>&1; python tools/ncu_hot.py gpurun_out/${TAG}_$r.ncu-rep 30 0 > gpurun_out/${TAG}_$r.hot0.txt 2>&1; done
+ls -la gpurun_out | tail -30
