@@ -238,8 +238,11 @@ def per_config(dev, stream, p64, steps=10):
     from paper_2502_11686_b200 import ks, model
     bw = peaks()[0]
     out = {}
-    for cfg in ("c1", "c2", "c3", "c4"):
-        p = gen.make(cfg)
+    for cfg in ("c1", "c2", "c3", "c4", "paper_n500"):
+        # paper_n500: the paper's third size: k = 500
+        # steps, n = m = 500, its benchmark class (fixed orthonormal F and G,
+        # K = L = I, random o) -- the large-n path
+        p = gen.paper_problem(500, 500, seed=0) if cfg == "paper_n500" else gen.make(cfg)
         strides = {"C": int(p.H.shape[0] > 1 or p.L.shape[0] > 1 or not bool((p.m == p.m_max).all())),
                    "E": int(p.F.shape[0] > 1 or p.K.shape[0] > 1 or p.c is not None)}
         res = {"N": p.N, "n": p.n, "m": p.m_max}
@@ -251,7 +254,7 @@ def per_config(dev, stream, p64, steps=10):
             l0 = sm.info()["launches"]
             sm.run(cov=cov)
             nl = sm.info()["launches"] - l0
-            ms, g = timed_graph(lambda: sm.run(cov=cov), stream, steps, 3)
+            ms, g = timed_graph(lambda: sm.run(cov=cov), stream, steps if p.n <= 64 else 3, 3 if p.n <= 64 else 1)
             sm.check()
             sb, sf = model.step_totals(p.N, p.n, p.m_max, strides, cov=cov)
             t_h, t_f = sb / (bw * 1e9), sf / (p64 * 1e12)

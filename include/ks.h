@@ -65,6 +65,10 @@ enum {
     KS_NO_FUSED_TAIL = 8u,/* small path: launch every factor level separately
                              instead of running the recursion's tail (levels
                              with few columns) in one on-chip kernel (cross-check) */
+    KS_BIG_PATH = 64u,    /* force the large-n path (batched HBM-resident block
+                             kernels, the default when the CTA path's shared
+                             memory does not fit, e.g. n = m = 500; one GPU,
+                             uniform model; used to cross-check at small n)      */
     KS_KEEP_WHITENING = 32u, /* keep the observation whitening factors M_i in the
                              workspace so that ks_update_obs can re-whiten new
                              observations o without redoing the model */
@@ -121,8 +125,8 @@ typedef struct ks_problem {
     int32_t nstate_min;      /* min_i n_i (sizes the padding rows), if nstate != NULL    */
 } ks_problem;
 
-#define KS_MAX_N 64
-#define KS_MAX_M 64
+#define KS_MAX_N 512   /* n > ~48: the large-n path (batched HBM-resident kernels) */
+#define KS_MAX_M 512
 
 /* Multi-GPU time sharding.  One process per GPU.
  * Rank r owns the contiguous global steps [first_global_step,

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/ks.h"
+#include "ks_big.cuh"
 #include "ks_internal.cuh"
 
 using namespace ks;
@@ -106,6 +107,7 @@ struct ks_ctx {
   double *C0 = nullptr, *y0 = nullptr, *El0 = nullptr, *Er0 = nullptr, *e0 = nullptr,
          *Mchol = nullptr, *Minv = nullptr;
   int64_t cntE = 1, cntC = 1;
+  bool constC = true;     // constant observation model (H, L stride 0, m == NULL, uniform n_i)
   // local levels 0..nlev-1 (sharded: 0..q-1)
   std::vector<int64_t> K_;
   std::vector<double *> ent, rrec, X;
@@ -119,6 +121,8 @@ struct ks_ctx {
   double *Mall = nullptr; // KS_KEEP_WHITENING: per-step M_i
   // small-n path (ks_small.cu): element-major level arrays
   bool small = false;
+  bool big = false;       // the large-n path (ks_big.cu): blocks beyond shared memory
+  ks::big::Plan bp;
   double *nC0 = nullptr, *nEr0 = nullptr, *nEl0 = nullptr, *zscratch = nullptr;
   // outputs
   double *xout = nullptr, *Sout = nullptr;
@@ -152,12 +156,21 @@ bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 int level0_rows(const ks_problem *p) { return p->m_max + (p->nstate ? p->n - p->nstate_min : 0); }
 
 bool use_small(const ks_problem *p) {
-  return p->n <= kSmallMaxN && level0_rows(p) <= kSmallMaxM && !(p->flags & KS_GENERIC_PATH);
+  return p->n <= kSmallMaxN && level0_rows(p) <= kSmallMaxM && !(p->flags & (KS_GENERIC_PATH | KS_BIG_PATH));
+}
+
+// The large-n path: blocks that do not fit the CTA path's shared memory
+// (n = m = 500), or forced (KS_BIG_PATH, cross-checks).
+bool use_big(const ks_problem *p) {
+  if (use_small(p)) return false;
+  if (p->flags & KS_BIG_PATH) return true;
+  const int rc = level0_rows(p);
+  return factor_smem_bytes(p->n, rc > p->n ? rc : p->n) > 227 * 1024 || backward_smem_bytes(p->n) > 227 * 1024;
 }
 
 
-constexpr uint32_t kAllFlags =
-    KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL | KS_COV_IS_CHOL | KS_KEEP_WHITENING;
+constexpr uint32_t kAllFlags = KS_HOST_INPUTS | KS_OUTPUTS_BOUND | KS_GENERIC_PATH | KS_NO_FUSED_TAIL |
+                               KS_COV_IS_CHOL | KS_KEEP_WHITENING | KS_BIG_PATH;
 
 int64_t global_steps(const ks_problem *p, const ks_dist *d) { return (d && d->nranks > 1) ? d->nglobal : p->nsteps; }
 int64_t segment_steps(const ks_problem *p, const ks_dist *d) {
@@ -175,10 +188,11 @@ int validate(const ks_problem *p, const ks_dist *d) {
       (p->sL && p->sL < mx * mx) || (p->sc && p->sc < n) || (p->so && p->so < mx))
     return KS_ERR_ARG;
   if (p->flags & ~kAllFlags) return KS_ERR_ARG;
-  if (!use_small(p)) {
-    const int rc = level0_rows(p);
-    if (factor_smem_bytes(p->n, rc > p->n ? rc : p->n) > 227 * 1024) return KS_ERR_ARG;
-    if (backward_smem_bytes(p->n) > 227 * 1024) return KS_ERR_ARG;
+  if (use_big(p)) {
+    // one HBM-resident stage stack per pair; the Householder panel of a stack
+    // (16 columns) must fit in shared memory; one GPU, uniform model
+    if (ks::big::max_stack_rows(p->n, p->m_max) > ks::big::kBigMaxRows) return KS_ERR_ARG;
+    if ((d && d->nranks > 1) || p->Hev || p->l || p->nstate || (p->flags & KS_KEEP_WHITENING)) return KS_ERR_ARG;
   }
   if (p->batch < 0 || (p->batch > 1 && global_steps(p, d) % p->batch != 0)) return KS_ERR_ARG;
   if (p->sHev < 0 || (p->sHev && p->sHev < n * n)) return KS_ERR_ARG;
@@ -242,7 +256,9 @@ size_t carve(ks_ctx *c, char *base) {
   // (the general model: per-step unless only a constant H_i is given)
   c->cntE = (p.sF == 0 && p.sK == 0 && (p.c == nullptr || p.sc == 0) && p.batch <= 1 && p.sHev == 0 &&
              !p.l && !p.nstate) ? 1 : N;
-  c->cntC = (p.sH == 0 && p.sL == 0 && p.m == nullptr && !p.nstate) ? 1 : N;
+  // constant observation model: one whitened C block, y = M^{-1} o from the one factor M
+  c->constC = p.sH == 0 && p.sL == 0 && p.m == nullptr && !p.nstate;
+  c->cntC = c->constC ? 1 : N;
   c->Mall = ((p.flags & KS_KEEP_WHITENING) && c->cntC > 1) ? w.take<double>(c->cntC * mx * mx + 1) : nullptr;
   const bool sm = c->small;
   const int64_t Rs = small_rrec_doubles(n);
@@ -279,6 +295,36 @@ size_t carve(ks_ctx *c, char *base) {
     c->ent.push_back(L == 0 ? nullptr : w.take<double>(ne));
     c->rrec.push_back(w.take<double>(nr));
     c->X.push_back(L == 0 ? nullptr : w.take<double>(nx));
+  }
+  if (c->big) {   // the large-n path's whitening and stage scratch (ks_big.cuh Plan)
+    ks::big::Plan &b = c->bp;
+    b.n = n; b.RC = rc; b.mx = mx; b.N = N; b.cntE = c->cntE; b.cntC = c->cntC;
+    b.constC = c->constC; b.chol = c->chol; b.seg = c->seg;
+    b.C0 = c->C0; b.y0 = c->y0; b.El0 = c->El0; b.Er0 = c->Er0; b.e0 = c->e0;
+    b.Ks = c->K_; b.ent = c->ent; b.rec = c->rrec; b.X = c->X;
+    b.Kw = w.take<double>(c->cntE * nn);
+    b.Bw = w.take<double>(c->cntE * nn * 2 + c->cntE * n);
+    b.Lw = w.take<double>(c->cntC * mx * mx + 1);
+    b.Hw = w.take<double>(c->cntC * mx * (n + 1) + 1);
+    b.nC = w.take<double>(c->cntC);
+    b.nEr = w.take<double>(c->cntE);
+    b.nEl = w.take<double>(c->cntE);
+    b.nrm0 = w.take<double>(N);
+    int64_t s1, s2, s3, vu, ww, items;
+    ks::big::scratch_sizes(b, s1, s2, s3, vu, ww, items);
+    b.S1 = w.take<double>(items * s1);
+    b.S2 = w.take<double>(items * s2);
+    b.S3 = w.take<double>(items * s3);
+    b.w.V = w.take<double>(items * vu);
+    b.w.U = w.take<double>(items * vu);
+    b.w.W = w.take<double>(items * ww);
+    b.w.sVU = vu; b.w.sW = ww; b.w.ldv = (int)(vu / ks::big::kBigNB);
+    b.Rinv = w.take<double>(items * nn);
+    b.SII = w.take<double>(items * 4 * nn);
+    b.G = w.take<double>(items * 2 * nn);
+    b.Pt = w.take<double>(items * nn);
+    b.xg = w.take<double>(items * 2 * n);
+    b.xt = w.take<double>(items * n);
   }
   if (c->sharded) {
     const int P = c->nranks;
@@ -369,7 +415,7 @@ TView tv(const double *p, int64_t ts) { return TView{const_cast<double *>(p), ts
 // Constant observation model on the small path: the level-0 factor computes
 // y = M^{-1} o itself (no y pass over HBM).
 int small_yfuse(const ks_ctx *c) {
-  return (c->mx > 0 && c->cntC == 1) ? 1 : 0;
+  return (c->mx > 0 && c->constC) ? 1 : 0;
 }
 
 SmallIn small_level0(const ks_ctx *c) {
@@ -775,6 +821,8 @@ size_t ks_workspace_bytes(const ks_problem *p, const ks_dist *d) {
   c.N = p->nsteps; c.n = p->n; c.mx = p->m_max; c.rc = level0_rows(p);
   c.host_inputs = (p->flags & KS_HOST_INPUTS) != 0;
   c.small = use_small(p);
+  c.big = use_big(p);
+  c.seg = segment_steps(p, d);
   if (d && d->nranks > 1) {
     c.sharded = true; c.rank = d->rank; c.nranks = d->nranks;
     int q = 0;
@@ -803,6 +851,7 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
   c->chol = (p->flags & KS_COV_IS_CHOL) != 0;
   c->seg = segment_steps(p, d);
   c->small = use_small(p);
+  c->big = use_big(p);
   if (d && d->nranks > 1) {
     c->sharded = true; c->rank = d->rank; c->nranks = d->nranks; c->comm = d->comm;
     int q = 0;
@@ -819,6 +868,13 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
   } else {
     c->m = p->m; c->F = p->F; c->K = p->K; c->H = p->H; c->L = p->L; c->o = p->o; c->c = p->c;
     c->Hev = p->Hev; c->l = p->l; c->ns = p->nstate;
+  }
+  if (c->big) {
+    ks::big::Plan &b = c->bp;
+    b.m = c->m; b.F = c->F; b.H = c->H; b.c = c->c; b.o = c->o; b.K = c->K; b.L = c->L;
+    b.sF = p->sF; b.sH = p->sH; b.sc = p->sc; b.so = p->so; b.sK = p->sK; b.sL = p->sL;
+    b.status = c->status;
+    b.x = c->xout; b.S = c->Sout;
   }
   *out = c;
   return KS_OK;
@@ -841,6 +897,15 @@ int ks_whiten(ks_ctx *c) {
         if (e != cudaSuccess) return cuda_fail(e);
       }
   }
+  if (c->big) {
+    const int64_t l0 = ks::big::g_launches.load();
+    e = ks::big::whiten(c->bp, c->stream);
+    c->launches += ks::big::g_launches.load() - l0;
+    if (e != cudaSuccess) return cuda_fail(e);
+    c->stage = 1;
+    c->solved = c->covd = false;
+    return KS_OK;
+  }
   if (c->small) {
     SmallWhitenArgs a;
     a.N = c->N; a.n = c->n; a.m_max = c->mx; a.m = c->m;
@@ -848,7 +913,7 @@ int ks_whiten(ks_ctx *c) {
     a.sF = c->p.sF; a.sH = c->p.sH; a.sc = c->p.sc; a.so = c->p.so; a.sK = c->p.sK; a.sL = c->p.sL;
     a.first_global = c->sharded ? (int64_t)c->rank * c->N : 0;
     a.cntE = c->cntE; a.cntC = c->cntC;
-    a.constC = c->cntC == 1;
+    a.constC = c->constC;
     const SmallIn v = small_level0(c);
     a.C = v.C; a.y = v.y; a.El = v.El; a.Er = v.Er; a.e = v.e; a.nC = v.nC; a.nEr = v.nEr; a.nEl = v.nEl;
     a.cE = c->cntE == 1;
@@ -880,9 +945,9 @@ int ks_whiten(ks_ctx *c) {
   a.seg = c->seg;
   a.Mall = c->Mall;
   a.Hev = c->Hev; a.sHev = c->p.sHev; a.l = c->l; a.ns = c->ns; a.RC = c->rc;
-  a.constC = c->cntC == 1;
+  a.constC = c->constC;
   {
-    Launch l(c, 0, 0, 1 + (c->rc > 0) + (c->mx > 0 && c->cntC == 1));
+    Launch l(c, 0, 0, 1 + (c->rc > 0) + (c->mx > 0 && c->constC));
     e = launch_whiten(a, c->stream);
   }
   if (e != cudaSuccess) return cuda_fail(e);
@@ -894,6 +959,15 @@ int ks_whiten(ks_ctx *c) {
 int ks_factor(ks_ctx *c) {
   if (!c) return KS_ERR_ARG;
   if (c->stage < 1) return KS_ERR_ORDER;
+  if (c->big) {
+    const int64_t l0 = ks::big::g_launches.load();
+    Launch l(c, 1, 0, 0);
+    cudaError_t e = ks::big::factor(c->bp, c->stream);
+    c->launches += ks::big::g_launches.load() - l0;
+    if (e != cudaSuccess) return cuda_fail(e);
+    c->stage = 3;
+    return KS_OK;
+  }
   int r = run_factor_levels(c, false);
   if (r) return r;
   if (!c->sharded) {
@@ -925,9 +999,25 @@ int ks_factor_boundary(ks_ctx *c) {
   return KS_OK;
 }
 
+// the large-n path's backward phases
+static int big_backward(ks_ctx *c, bool st, bool cov) {
+  const int64_t l0 = ks::big::g_launches.load();
+  cudaError_t e;
+  {
+    Launch l(c, (cov && st) ? 5 : (cov ? 3 : 2), 0, 0);
+    e = ks::big::backward(c->bp, st, cov, c->stream);
+  }
+  c->launches += ks::big::g_launches.load() - l0;
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (st) c->solved = true;
+  if (cov) c->covd = true;
+  return KS_OK;
+}
+
 int ks_solve(ks_ctx *c) {
   if (!c) return KS_ERR_ARG;
   if (c->stage < 3) return KS_ERR_ORDER;
+  if (c->big) return big_backward(c, true, false);
   int r;
   if (c->sharded) {
     if ((r = run_backward_levels(c, true, 1, 0))) return r;
@@ -941,6 +1031,7 @@ int ks_solve(ks_ctx *c) {
 int ks_selinv(ks_ctx *c) {
   if (!c || !c->Sout) return KS_ERR_ARG;
   if (c->stage < 3) return KS_ERR_ORDER;
+  if (c->big) return big_backward(c, false, true);
   int r;
   if (c->sharded) {
     if ((r = run_backward_levels(c, true, 0, 1))) return r;
@@ -954,6 +1045,7 @@ int ks_selinv(ks_ctx *c) {
 int ks_solve_selinv(ks_ctx *c) {
   if (!c || !c->Sout) return KS_ERR_ARG;
   if (c->stage < 3) return KS_ERR_ORDER;
+  if (c->big) return big_backward(c, true, true);
   int r;
   if (c->sharded) {
     if ((r = run_backward_levels(c, true, 1, 1))) return r;
@@ -967,7 +1059,8 @@ int ks_solve_selinv(ks_ctx *c) {
 int ks_update_obs(ks_ctx *c, const double *o) {
   if (!c || (!o && c->mx > 0)) return KS_ERR_ARG;
   if (c->stage < 1) return KS_ERR_ORDER;
-  const bool constC = c->cntC == 1;
+  const bool constC = c->constC;
+  if (c->big) return KS_ERR_ARG;                 // not on the large-n path
   if (!constC && !c->Mall) return KS_ERR_ARG;   // needs KS_KEEP_WHITENING
   if (c->mx > 0) {
     cudaError_t e = cudaSuccess;

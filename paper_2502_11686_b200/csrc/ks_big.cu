@@ -1,0 +1,960 @@
+// Large-n path (the paper's third size n = m = 500 with
+// k = 500 steps): block columns far larger than
+// shared memory (a 500 x 500 fp64 block is 2 MB), so every block operation
+// of a level is a BATCHED dense kernel over all the level's pairs at once,
+// with the blocks in HBM / L2:
+//   * big_gemm      strided-batched C = alpha op(A) op(B) + beta C on the FP64
+//                   tensor cores (mma.sync.m8n8k4.f64, DMMA), 64 x 64 tiles,
+//                   cp.async double-buffered operand staging;
+//   * big_qr_panel  Householder panel factorisation (LAPACK geqrf order, the
+//                   paper's QR) of 16 columns of every item, one
+//                   CTA per item, writing the compact-WY factors V and
+//                   U = V T^T so that Q^T C = C - U (V^T C) is two big_gemm;
+//   * big_trsm_diag 64 x 64 triangular diagonal-block solves (the blocked
+//                   TRSMs' off-diagonal parts are big_gemm);
+//   * big_chol      Cholesky of the whitening blocks;
+//   * big_copy      descriptor-driven batched block gathers / scatters that
+//                   assemble the stacked stage matrices of P:424-537.
+// The stage algebra is that of the small and CTA paths:
+// stage 1 QR of [C_t; El_{t+1}] applied to [0 | y_t; Er_{t+1} | e_{t+1}],
+// stage 2 QR of [Er_t; R~_t] applied to [El_t | 0 | e_t; 0 | X_t | z~_t],
+// stage 3 QR of [D~_{t+1}; C_{t+1} (; Z)], and Alg. 2's SelInv backward.
+// Time parallelism (pairs) is the batch dimension; within-block parallelism
+// (the point of this workload) comes from the tiles of every
+// GEMM and the rows of every panel.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <atomic>
+#include <cstdio>
+
+#include "ks_internal.cuh"
+#include "ks_big.cuh"
+
+namespace ks {
+namespace big {
+
+std::atomic<int64_t> g_launches{0};
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+// 8-byte global -> shared asynchronous copy; !valid zero-fills (src-size 0:
+// gsrc must still be a mapped address, callers pass the operand base)
+__device__ __forceinline__ void cp8(double *sdst, const double *gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gsrc), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// ------------------------------------------------------------------ GEMM ---
+// Column-major operands; op(A) is M x K, op(B) is K x N.  CTA tile 64 x 64,
+// K chunks of 16 in two shared-memory stages; 8 warps as 2 (M) x 4 (N), each
+// warp 32 x 16 = 4 x 2 DMMA 8x8 tiles.  Shared tiles are k-major with a
+// leading dimension of 68 doubles: the fragment loads (row g = lane/4,
+// k = lane%4) of a half-warp hit 16 distinct 8-byte bank pairs.
+constexpr int GBM = 64, GBN = 64, GBK = 16, GLD = 68;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) big_gemm_kernel(Gemm g) {
+  __shared__ __align__(16) double As[2][GBK][GLD];
+  __shared__ __align__(16) double Bs[2][GBK][GLD];
+  const int64_t b = blockIdx.z;
+  const double *A = g.A + b * g.sA, *B = g.B + b * g.sB;
+  double *C = g.C + b * g.sC;
+  const int m0 = blockIdx.x * GBM, n0 = blockIdx.y * GBN;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, q = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load = [&](int st, int k0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int idx = tid + 256 * r;
+      int m, k;
+      if (TA) { m = idx / GBK; k = idx % GBK; } else { m = idx % GBM; k = idx / GBM; }
+      const int gm = m0 + m, gk = k0 + k;
+      const bool ok = gm < g.M && gk < g.K;
+      const double *src = TA ? A + gk + (int64_t)gm * g.lda : A + gm + (int64_t)gk * g.lda;
+      cp8(&As[st][k][m], ok ? src : A, ok);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int idx = tid + 256 * r;
+      int nn, k;
+      if (TB) { nn = idx % GBN; k = idx / GBN; } else { nn = idx / GBK; k = idx % GBK; }
+      const int gn = n0 + nn, gk = k0 + k;
+      const bool ok = gn < g.N && gk < g.K;
+      const double *src = TB ? B + gn + (int64_t)gk * g.ldb : B + gk + (int64_t)gn * g.ldb;
+      cp8(&Bs[st][k][nn], ok ? src : B, ok);
+    }
+    cp_commit();
+  };
+  const int nk = (g.K + GBK - 1) / GBK;
+  load(0, 0);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int st = kt & 1;
+    if (kt + 1 < nk) {
+      load(st ^ 1, (kt + 1) * GBK);
+      cp_wait1();
+    } else {
+      cp_wait0();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[st][kk + q][wm + 8 * i + gq];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Bs[st][kk + q][wn + 8 * j + gq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int m = m0 + wm + 8 * i + gq;
+      if (m >= g.M) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wn + 8 * j + 2 * q + h;
+        if (n >= g.N) continue;
+        double *c = C + m + (int64_t)n * g.ldc;
+        *c = (g.beta == 0.0) ? g.alpha * acc[i][j][h] : fma(g.alpha, acc[i][j][h], g.beta * *c);
+      }
+    }
+}
+
+cudaError_t gemm(const Gemm &g, bool ta, bool tb, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  if (g.K <= 0 && g.beta == 1.0) return cudaSuccess;
+  const dim3 grid((g.M + GBM - 1) / GBM, (g.N + GBN - 1) / GBN, (unsigned)g.batch);
+  if (ta && tb) big_gemm_kernel<true, true><<<grid, 256, 0, s>>>(g);
+  else if (ta) big_gemm_kernel<true, false><<<grid, 256, 0, s>>>(g);
+  else if (tb) big_gemm_kernel<false, true><<<grid, 256, 0, s>>>(g);
+  else big_gemm_kernel<false, false><<<grid, 256, 0, s>>>(g);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ copy ---
+// Batched block copies: for every descriptor d and item b,
+//   dst[b sd + r + c ldd] = alpha * (src ? src[b ss + (T ? c + r lds : r + c lds)] : 0)
+// (column-major; T: transpose; upper: entries below the diagonal are 0).
+__global__ void __launch_bounds__(256) big_copy_kernel(CopyList L, int64_t batch) {
+  const CopyDesc &d = L.d[blockIdx.y];
+  const int64_t total = (int64_t)d.rows * d.cols;
+  const int64_t per = total * (batch > 0 ? batch : 1);
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < per;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / total, e = idx - b * total;
+    if (b >= d.count) continue;
+    const int c = (int)(e / d.rows), r = (int)(e - (int64_t)c * d.rows);
+    double v = (d.diag != 0.0 && r == c) ? d.diag : 0.0;
+    if (d.src && !(d.upper && r > c)) {
+      const double *s = d.src + b * d.ss;
+      v = d.alpha * (d.trans ? s[c + (int64_t)r * d.lds] : s[r + (int64_t)c * d.lds]);
+    }
+    d.dst[b * d.sd + r + (int64_t)c * d.ldd] = v;
+  }
+}
+
+cudaError_t copy(const CopyList &L, int64_t batch, cudaStream_t s) {
+  if (L.count == 0 || batch <= 0) return cudaSuccess;
+  int64_t mx = 0;
+  for (int i = 0; i < L.count; ++i) mx = mx > (int64_t)L.d[i].rows * L.d[i].cols ? mx : (int64_t)L.d[i].rows * L.d[i].cols;
+  const int64_t work = mx * batch;
+  const unsigned gx = (unsigned)((work + 255) / 256 < 4096 ? (work + 255) / 256 : 4096);
+  big_copy_kernel<<<dim3(gx > 0 ? gx : 1, (unsigned)L.count), 256, 0, s>>>(L, batch);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ QR panel ---
+// Columns [j0, j0 + nb) of the item's stack S (m rows, ld lds), rows j0..m-1,
+// factored in shared memory by Householder reflections (LAPACK dgeqr2 order:
+// beta = -sign(alpha) |x|, v_0 = 1, tau = (beta - alpha) / beta).  Writes the
+// R part back (zeros below the diagonal), the explicit V (rows x nb, unit
+// lower trapezoidal) and U = V T^T (the compact-WY T of dlarft, forward
+// columnwise), so that Q^T C = C - U (V^T C).  One CTA per item.
+constexpr int kPanelThreads = 256;
+__device__ double block_sum(double v, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kPanelThreads / 32; ++w) s += red[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
+  extern __shared__ __align__(16) double psm[];
+  const int64_t b = blockIdx.x;
+  double *S = a.S + b * a.sS;
+  double *V = a.V + b * a.sVU, *U = a.U + b * a.sVU;
+  const int rows = a.m - a.j0, nb = a.nb, tid = threadIdx.x;
+  double *P = psm;                      // [nb][rows] column-major (ld = rows)
+  double *red = P + (size_t)nb * rows;  // reductions: 8 warps x kBigNB partials
+  double *T = red + 8 * kBigNB;         // [nb][nb] column-major
+  double *tau = T + kBigNB * kBigNB;
+  for (int64_t e = tid; e < (int64_t)nb * rows; e += blockDim.x) {
+    const int c = (int)(e / rows), r = (int)(e - (int64_t)c * rows);
+    P[e] = S[(a.j0 + r) + (int64_t)(a.j0 + c) * a.lds];
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    double *x = P + (size_t)j * rows;
+    double part = 0.0;
+    for (int r = j + 1 + tid; r < rows; r += blockDim.x) part = fma(x[r], x[r], part);
+    const double sigma = block_sum(part, red);
+    const double alpha = x[j];
+    double tj = 0.0, beta = alpha, scal = 0.0;
+    if (sigma > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncthreads();
+    for (int r = j + 1 + tid; r < rows; r += blockDim.x) x[r] *= scal;   // v (v_j = 1 implicit)
+    if (tid == 0) { x[j] = beta; tau[j] = tj; }
+    __syncthreads();
+    // H_j applied to the panel columns c > j: w_c = v^T P[:, c], P[:, c] -= tau v w_c
+    for (int c = j + 1; c < nb; ++c) {
+      double *pc = P + (size_t)c * rows;
+      double pw = (tid == 0) ? pc[j] : 0.0;
+      for (int r = j + 1 + tid; r < rows; r += blockDim.x) pw = fma(x[r], pc[r], pw);
+      const double w = block_sum(pw, red) * tj;
+      if (tid == 0) pc[j] -= w;
+      for (int r = j + 1 + tid; r < rows; r += blockDim.x) pc[r] = fma(-w, x[r], pc[r]);
+      __syncthreads();
+    }
+  }
+  // T (dlarft, forward columnwise): T[j][j] = tau_j,
+  // T[0:j, j] = -tau_j T[0:j, 0:j] (V[:, 0:j]^T v_j)
+  for (int j = 0; j < nb; ++j) {
+    for (int i = 0; i < j; ++i) {   // (V^T v_j)_i = sum_r V[r][i] V[r][j], r >= j (v_j zero above j, 1 at j)
+      const double *vi = P + (size_t)i * rows, *vj = P + (size_t)j * rows;
+      double part = (tid == 0) ? vi[j] : 0.0;
+      for (int r = j + 1 + tid; r < rows; r += blockDim.x) part = fma(vi[r], vj[r], part);
+      const double s = block_sum(part, red);
+      if (tid == 0) T[i + j * kBigNB] = s;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      double y[kBigNB];
+      for (int i = 0; i < j; ++i) y[i] = T[i + j * kBigNB];
+      for (int i = 0; i < j; ++i) {
+        double s = 0.0;
+        for (int k = i; k < j; ++k) s = fma(T[i + k * kBigNB], y[k], s);
+        T[i + j * kBigNB] = -tau[j] * s;
+      }
+      T[j + j * kBigNB] = tau[j];
+    }
+    __syncthreads();
+  }
+  // write back: R (upper part of the panel's first nb rows), zeros below; V, U = V T^T
+  for (int64_t e = tid; e < (int64_t)nb * rows; e += blockDim.x) {
+    const int c = (int)(e / rows), r = (int)(e - (int64_t)c * rows);
+    const double pv = P[e];
+    S[(a.j0 + r) + (int64_t)(a.j0 + c) * a.lds] = (r <= c) ? pv : 0.0;
+    V[r + (int64_t)c * a.ldv] = (r < c) ? 0.0 : (r == c ? 1.0 : pv);
+  }
+  for (int r = tid; r < rows; r += blockDim.x) {
+    double vr[kBigNB];
+#pragma unroll
+    for (int c = 0; c < kBigNB; ++c) vr[c] = (c < nb) ? ((r < c) ? 0.0 : (r == c ? 1.0 : P[r + (size_t)c * rows])) : 0.0;
+#pragma unroll
+    for (int c = 0; c < kBigNB; ++c) {
+      if (c >= nb) break;
+      double s = 0.0;   // (V T^T)[r][c] = sum_{k >= c} V[r][k] T[c][k]
+#pragma unroll
+      for (int k = 0; k < kBigNB; ++k)
+        if (k >= c && k < nb) s = fma(vr[k], T[c + k * kBigNB], s);
+      U[r + (int64_t)c * a.ldv] = s;
+    }
+  }
+}
+
+size_t panel_smem(int rows) {
+  return sizeof(double) * ((size_t)kBigNB * rows + 8 * kBigNB + kBigNB * kBigNB + kBigNB);
+}
+
+cudaError_t qr_panel(const Panel &a, int64_t batch, cudaStream_t s) {
+  const size_t sm = panel_smem(a.m - a.j0);
+  cudaError_t e = set_smem_attr((const void *)big_qr_panel_kernel, (int)panel_smem(kBigMaxRows));
+  if (e != cudaSuccess) return e;
+  big_qr_panel_kernel<<<(unsigned)batch, kPanelThreads, sm, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------- triangular diagonal ---
+// In place X = T^{-1} X for the nb x nb diagonal block T = R[j0:j0+nb, j0:j0+nb]
+// (upper: back substitution; lower: forward), X = B[j0:j0+nb, 0:k]; one
+// thread per right-hand-side column, the block staged in shared memory.
+__global__ void __launch_bounds__(256) big_trsm_diag_kernel(Trsm a, int j0, int nb) {
+  __shared__ double Ts[64][65];
+  const int64_t b = blockIdx.y;
+  const double *R = a.R + b * a.sR;
+  double *B = a.B + b * a.sB;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int c = e / nb, r = e - c * nb;
+    Ts[r][c] = R[(j0 + r) + (int64_t)(j0 + c) * a.ldr];
+  }
+  __syncthreads();
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= a.k) return;
+  double *x = B + j0 + (int64_t)col * a.ldb;
+  double xv[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) xv[i] = (i < nb) ? x[i] : 0.0;
+  if (a.upper) {
+#pragma unroll
+    for (int i = 63; i >= 0; --i) {
+      if (i >= nb) continue;
+      double s = xv[i];
+#pragma unroll
+      for (int k = i + 1; k < 64; ++k)
+        if (k < nb) s = fma(-Ts[i][k], xv[k], s);
+      xv[i] = s / Ts[i][i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      if (i >= nb) continue;
+      double s = xv[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) s = fma(-Ts[i][k], xv[k], s);
+      xv[i] = s / Ts[i][i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < nb) x[i] = xv[i];
+}
+
+// Blocked triangular solve X = R^{-1} B (n x n triangular, B n x k), in place.
+cudaError_t trsm(const Trsm &a, int n, int64_t batch, cudaStream_t s) {
+  const int BS = 64;
+  const int nblk = (n + BS - 1) / BS;
+  for (int t = 0; t < nblk; ++t) {
+    const int jb = a.upper ? nblk - 1 - t : t;
+    const int j0 = jb * BS, nb = (n - j0 < BS) ? n - j0 : BS;
+    big_trsm_diag_kernel<<<dim3((a.k + 255) / 256, (unsigned)batch), 256, 0, s>>>(a, j0, nb);
+  ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // eliminate the solved block from the remaining rows
+    Gemm g;
+    g.batch = batch;
+    g.N = a.k; g.K = nb; g.alpha = -1.0; g.beta = 1.0;
+    g.B = a.B + j0; g.ldb = a.ldb; g.sB = a.sB;
+    g.lda = a.ldr; g.sA = a.sR; g.ldc = a.ldb; g.sC = a.sB;
+    if (a.upper) {   // rows 0..j0-1 -= R[0:j0, j0:j0+nb] X_jb
+      g.M = j0; g.A = a.R + (int64_t)j0 * a.ldr; g.C = a.B;
+    } else {         // rows j0+nb..n-1 -= R[j0+nb:n, j0:j0+nb] X_jb
+      g.M = n - j0 - nb; g.A = a.R + (j0 + nb) + (int64_t)j0 * a.ldr; g.C = a.B + j0 + nb;
+    }
+    if (g.M > 0 && (e = gemm(g, false, false, s)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------ Cholesky ---
+// In place lower Cholesky of the leading d x d block of every item
+// (column-major, ld), right-looking, one CTA per item; the strict upper
+// triangle is zeroed.  A pivot <= 0 is recorded (status, step = item index
+// + step_off) and replaced by 1 (outputs undefined, as on the other paths).
+__global__ void __launch_bounds__(256) big_chol_kernel(double *A, int64_t sA, int ld, int d, int chol_given,
+                                                        unsigned long long *status, int64_t step_off, int kind,
+                                                        int64_t step_mul) {
+  __shared__ double red[8];
+  __shared__ double piv;
+  double *M = A + (int64_t)blockIdx.x * sA;
+  const int tid = threadIdx.x;
+  bool bad = false;
+  for (int j = 0; j < d; ++j) {
+    if (!chol_given) {
+      double part = 0.0;
+      for (int k = tid; k < j; k += blockDim.x) part = fma(M[j + (int64_t)k * ld], M[j + (int64_t)k * ld], part);
+      const double s = block_sum(part, red);
+      if (tid == 0) {
+        double dj = M[j + (int64_t)j * ld] - s;
+        if (!(dj > 0.0)) { bad = true; dj = 1.0; }
+        piv = sqrt(dj);
+        M[j + (int64_t)j * ld] = piv;
+      }
+      __syncthreads();
+      const double il = 1.0 / piv;
+      for (int r = j + 1 + tid; r < d; r += blockDim.x) {
+        double v = M[r + (int64_t)j * ld];
+        for (int k = 0; k < j; ++k) v = fma(-M[r + (int64_t)k * ld], M[j + (int64_t)k * ld], v);
+        M[r + (int64_t)j * ld] = v * il;
+      }
+      __syncthreads();
+    } else if (tid == 0) {   // KS_COV_IS_CHOL: the factor is given
+      const double v = M[j + (int64_t)j * ld];
+      if (!(v != 0.0 && v - v == 0.0)) { bad = true; M[j + (int64_t)j * ld] = 1.0; }
+    }
+  }
+  __syncthreads();
+  for (int64_t e = tid; e < (int64_t)d * d; e += blockDim.x) {
+    const int c = (int)(e / d), r = (int)(e - (int64_t)c * d);
+    if (r < c) M[r + (int64_t)c * ld] = 0.0;
+  }
+  if (tid == 0 && bad && status)
+    atomicMin(status, status_word((int64_t)blockIdx.x * step_mul + step_off, kind));
+}
+
+cudaError_t chol(double *A, int64_t sA, int ld, int d, int64_t batch, bool given, unsigned long long *status,
+                 int64_t step_off, int64_t step_mul, int kind, cudaStream_t s) {
+  if (batch <= 0 || d <= 0) return cudaSuccess;
+  big_chol_kernel<<<(unsigned)batch, 256, 0, s>>>(A, sA, ld, d, given ? 1 : 0, status, step_off, kind, step_mul);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- helpers ---
+// Sum of squares of an rows x cols block per item -> out[b * so] (+= if acc).
+__global__ void __launch_bounds__(256) big_sumsq_kernel(const double *A, int64_t sA, int lda, int rows, int cols,
+                                                         double *out, int64_t so, int acc) {
+  __shared__ double red[8];
+  const double *M = A + (int64_t)blockIdx.x * sA;
+  double part = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)rows * cols; e += blockDim.x) {
+    const int c = (int)(e / rows), r = (int)(e - (int64_t)c * rows);
+    const double v = M[r + (int64_t)c * lda];
+    part = fma(v, v, part);
+  }
+  const double s = block_sum(part, red);
+  if (threadIdx.x == 0) out[(int64_t)blockIdx.x * so] = acc ? out[(int64_t)blockIdx.x * so] + s : s;
+}
+cudaError_t sumsq(const double *A, int64_t sA, int lda, int rows, int cols, double *out, int64_t so, bool acc,
+                  int64_t batch, cudaStream_t s) {
+  if (batch <= 0) return cudaSuccess;
+  big_sumsq_kernel<<<(unsigned)batch, 256, 0, s>>>(A, sA, lda, rows, cols, out, so, acc ? 1 : 0);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// Rank test of the eliminated columns: |R_tt[d][d]| <=
+// 1e-12 |block column of UA|_F -> KS_ERR_RANK at the column's step.
+__global__ void big_rank_kernel(const double *R, int64_t sR, int ldr, int n, const double *nrm2, int64_t snrm,
+                                unsigned long long *status, int64_t step_first, int64_t step_stride) {
+  const int64_t b = blockIdx.x;
+  const double *M = R + b * sR;
+  const double ref = sqrt(nrm2[b * snrm]);
+  bool bad = false;
+  for (int d = threadIdx.x; d < n; d += blockDim.x) bad |= !(fabs(M[d + (int64_t)d * ldr]) > kRankTol * ref);
+  if (__syncthreads_or(bad) && threadIdx.x == 0)
+    atomicMin(status, status_word(step_first + b * step_stride, kBadRank));
+}
+cudaError_t rank_check(const double *R, int64_t sR, int ldr, int n, const double *nrm2, int64_t snrm,
+                       unsigned long long *status, int64_t step_first, int64_t step_stride, int64_t batch,
+                       cudaStream_t s) {
+  if (batch <= 0) return cudaSuccess;
+  big_rank_kernel<<<(unsigned)batch, 128, 0, s>>>(R, sR, ldr, n, nrm2, snrm, status, step_first, step_stride);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// dst = (A + A^T) / 2 (n x n, column-major in, row-major == column-major out)
+__global__ void big_sym_kernel(const double *A, int64_t sA, int lda, double *dst, int64_t sd, int n) {
+  const int64_t b = blockIdx.y;
+  const double *M = A + b * sA;
+  double *D = dst + b * sd;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)n * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n), r = (int)(e - (int64_t)c * n);
+    D[e] = 0.5 * (M[r + (int64_t)c * lda] + M[c + (int64_t)r * lda]);
+  }
+}
+cudaError_t sym_store(const double *A, int64_t sA, int lda, double *dst, int64_t sd, int n, int64_t batch,
+                      cudaStream_t s) {
+  if (batch <= 0) return cudaSuccess;
+  const unsigned gx = (unsigned)(((int64_t)n * n + 255) / 256 < 64 ? ((int64_t)n * n + 255) / 256 : 64);
+  big_sym_kernel<<<dim3(gx, (unsigned)batch), 256, 0, s>>>(A, sA, lda, dst, sd, n);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------- blocked Householder ---
+// In place QR of the first ncols_fac columns of every item's S (m x ncols,
+// ld lds), Q^T applied to all the item's remaining columns (the stage's RHS
+// blocks): per 16-column panel, big_qr_panel then W = V^T C, C -= U W.
+cudaError_t qr_apply(double *S, int64_t sS, int lds, int m, int ncols_fac, int ncols, int64_t batch,
+                     const Work &w, cudaStream_t s) {
+  const int kmax = ncols_fac < m ? ncols_fac : m;
+  for (int j0 = 0; j0 < kmax; j0 += kBigNB) {
+    const int nb = (kmax - j0 < kBigNB) ? kmax - j0 : kBigNB;
+    Panel p;
+    p.S = S; p.sS = sS; p.lds = lds; p.m = m; p.j0 = j0; p.nb = nb;
+    p.V = w.V; p.U = w.U; p.sVU = w.sVU; p.ldv = w.ldv;
+    cudaError_t e = qr_panel(p, batch, s);
+    if (e != cudaSuccess) return e;
+    const int nc = ncols - (j0 + nb), rows = m - j0;
+    if (nc <= 0) continue;
+    double *C = S + j0 + (int64_t)(j0 + nb) * lds;
+    Gemm g1;   // W = V^T C  (nb x nc)
+    g1.batch = batch; g1.M = nb; g1.N = nc; g1.K = rows; g1.alpha = 1.0; g1.beta = 0.0;
+    g1.A = w.V; g1.lda = w.ldv; g1.sA = w.sVU;
+    g1.B = C; g1.ldb = lds; g1.sB = sS;
+    g1.C = w.W; g1.ldc = kBigNB; g1.sC = w.sW;
+    if ((e = gemm(g1, true, false, s)) != cudaSuccess) return e;
+    Gemm g2;   // C -= U W
+    g2.batch = batch; g2.M = rows; g2.N = nc; g2.K = nb; g2.alpha = -1.0; g2.beta = 1.0;
+    g2.A = w.U; g2.lda = w.ldv; g2.sA = w.sVU;
+    g2.B = w.W; g2.ldb = kBigNB; g2.sB = w.sW;
+    g2.C = C; g2.ldc = lds; g2.sC = sS;
+    if ((e = gemm(g2, false, false, s)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace big
+}  // namespace ks
+
+// =================================================================== plan ===
+namespace ks {
+namespace big {
+
+int64_t entry_doubles_big(int n) { return 3ll * n * n + 2ll * n + 1; }
+int64_t rrec_doubles_big(int n) { return 3ll * n * n + n; }
+
+namespace {
+
+// one descriptor: copy an rows x cols block for `count` items
+CopyDesc cd(const double *src, int64_t ss, int lds, double *dst, int64_t sd, int ldd, int rows, int cols, int64_t count,
+            double alpha = 1.0, int trans = 0, int upper = 0, double diag = 0.0) {
+  CopyDesc d;
+  d.src = src; d.ss = ss; d.lds = lds; d.dst = dst; d.sd = sd; d.ldd = ldd;
+  d.rows = rows; d.cols = cols; d.count = count; d.alpha = alpha; d.trans = trans; d.upper = upper; d.diag = diag;
+  return d;
+}
+
+cudaError_t run(CopyList &L, cudaStream_t s) {
+  int64_t mx = 0;
+  for (int i = 0; i < L.count; ++i) mx = L.d[i].count > mx ? L.d[i].count : mx;
+  cudaError_t e = copy(L, mx, s);
+  L.count = 0;
+  return e;
+}
+
+// level-0 masks of the observation blocks (per-step m_i): rows / columns
+// >= m_i of Lw -> identity, rows >= m_i of Hw -> 0 (then the solves give
+// exactly zero rows there)
+__global__ void big_mask_obs_kernel(double *Lw, double *Hw, const int32_t *m, int mx, int ncols, int64_t sL, int64_t sH) {
+  const int64_t i = blockIdx.x;
+  const int mi = m[i];
+  double *L = Lw + i * sL, *H = Hw + i * sH;
+  for (int64_t e = threadIdx.x; e < (int64_t)mx * mx; e += blockDim.x) {
+    const int c = (int)(e / mx), r = (int)(e - (int64_t)c * mx);
+    if (r >= mi || c >= mi) L[e] = (r == c) ? 1.0 : 0.0;
+  }
+  for (int64_t e = threadIdx.x; e < (int64_t)mx * ncols; e += blockDim.x) {
+    const int r = (int)(e % mx);
+    if (r >= mi) H[e] = 0.0;
+  }
+}
+
+// nrm0[t] = |C_t|^2 + |Er_t|^2 [t has an evolution row] + |El_{t+1}|^2
+__global__ void big_nrm0_kernel(const double *nC, int64_t sCn, const double *nEr, const double *nEl, int64_t sEn,
+                                int64_t N, double *out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= N) return;
+  double v = nC[t * sCn] + nEr[t * sEn];
+  if (t + 1 < N) v += nEl[(t + 1) * sEn];
+  out[t] = v;
+}
+
+}  // namespace
+
+// rows of the stage stacks for C-like blocks of r rows (stage 3 and the
+// single-column QRs are padded with zero rows up to n)
+int64_t rows1(int n, int r) { return (int64_t)r + n; }
+int64_t rows3(int n, int r, bool odd) { const int64_t v = 2ll * r + (odd ? n : 0); return v > n ? v : n; }
+
+void scratch_sizes(const Plan &p, int64_t &s1, int64_t &s2, int64_t &s3, int64_t &vu, int64_t &w, int64_t &items) {
+  const int64_t n = p.n, r = p.RC > p.n ? p.RC : p.n;   // level 0: RC rows, then n
+  items = p.N / 2 + 1;
+  s1 = rows1(n, r) * (2 * n + 1);
+  s2 = (2 * n) * (3 * n + 1);
+  s3 = rows3(n, r, true) * (n + 1);
+  int64_t rows = rows1(n, r);
+  if (2 * n > rows) rows = 2 * n;
+  if (rows3(n, r, true) > rows) rows = rows3(n, r, true);
+  vu = rows * kBigNB;
+  w = kBigNB * (3 * n + 1);
+}
+int64_t max_stack_rows(int n, int RC) {
+  const int r = RC > n ? RC : n;
+  int64_t rows = rows1(n, r);
+  if (2 * n > rows) rows = 2 * n;
+  if (rows3(n, r, true) > rows) rows = rows3(n, r, true);
+  return rows;
+}
+
+// ------------------------------------------------------------- whiten ---
+// K_i = Lam Lam^T, L_i = M M^T; El = -Lam^{-1} F,
+// Er = Lam^{-1}, e = Lam^{-1} c, C = M^{-1} H, y = M^{-1} o: batched
+// Cholesky + blocked triangular solves on column-major copies.
+cudaError_t whiten(const Plan &p, cudaStream_t s) {
+  const int n = p.n, mx = p.mx;
+  const int64_t nn = (int64_t)n * n;
+  cudaError_t e;
+  CopyList L;
+  // evolution blocks (row-major inputs -> column-major: transposed copies)
+  const int64_t cE = p.cntE;
+  const int64_t sBw = (int64_t)n * (2 * n + 1);
+  L.add(cd(p.K, p.sK, n, p.Kw, nn, n, n, n, cE, 1.0, 1));
+  L.add(cd(p.F, p.sF, n, p.Bw, sBw, n, n, n, cE, 1.0, 1));
+  L.add(cd(nullptr, 0, 1, p.Bw + nn, sBw, n, n, n, cE, 1.0, 0, 0, 1.0));   // identity
+  L.add(cd(p.c, p.sc, 1, p.Bw + 2 * nn, sBw, n, n, 1, p.c ? cE : 0));
+  L.add(cd(nullptr, 0, 1, p.Bw + 2 * nn, sBw, n, n, 1, p.c ? 0 : cE));
+  if ((e = run(L, s)) != cudaSuccess) return e;
+  if (cE > 1) {   // steps without an evolution row: K -> I (never factored as data), F, c -> 0
+    const int64_t cnt = (p.N + p.seg - 1) / p.seg;
+    L.add(cd(nullptr, 0, 1, p.Kw, p.seg * nn, n, n, n, cnt, 1.0, 0, 0, 1.0));
+    L.add(cd(nullptr, 0, 1, p.Bw, p.seg * sBw, n, n, n, cnt));
+    L.add(cd(nullptr, 0, 1, p.Bw + 2 * nn, p.seg * sBw, n, n, 1, cnt));
+    if ((e = run(L, s)) != cudaSuccess) return e;
+  }
+  // (constant model: the step reported for a bad K is 1, the first step using it)
+  if ((e = chol(p.Kw, nn, n, n, cE, p.chol, p.status, cE == 1 ? 1 : 0, 1, kBadK, s)) != cudaSuccess) return e;
+  Trsm t;
+  t.R = p.Kw; t.sR = nn; t.ldr = n; t.B = p.Bw; t.sB = sBw; t.ldb = n; t.k = 2 * n + 1; t.upper = 0;
+  if ((e = trsm(t, n, cE, s)) != cudaSuccess) return e;
+  L.add(cd(p.Bw, sBw, n, p.El0, nn, n, n, n, cE, -1.0));
+  L.add(cd(p.Bw + nn, sBw, n, p.Er0, nn, n, n, n, cE));
+  L.add(cd(p.Bw + 2 * nn, sBw, n, p.e0, n, n, n, 1, cE));
+  if ((e = run(L, s)) != cudaSuccess) return e;
+  // no evolution row at the first step of every problem (global step 0, batch segments)
+  if (cE > 1) {
+    const int64_t cnt = (p.N + p.seg - 1) / p.seg;
+    L.add(cd(nullptr, 0, 1, p.El0, p.seg * nn, n, n, n, cnt));
+    L.add(cd(nullptr, 0, 1, p.Er0, p.seg * nn, n, n, n, cnt));
+    L.add(cd(nullptr, 0, 1, p.e0, p.seg * n, n, n, 1, cnt));
+    if ((e = run(L, s)) != cudaSuccess) return e;
+  } else if (p.N == 1) {
+    L.add(cd(nullptr, 0, 1, p.El0, 0, n, n, n, 1));
+    L.add(cd(nullptr, 0, 1, p.Er0, 0, n, n, n, 1));
+    L.add(cd(nullptr, 0, 1, p.e0, 0, n, n, 1, 1));
+    if ((e = run(L, s)) != cudaSuccess) return e;
+  }
+  if ((e = sumsq(p.Er0, nn, n, n, n, p.nEr, 1, false, cE, s)) != cudaSuccess) return e;
+  if ((e = sumsq(p.El0, nn, n, n, n, p.nEl, 1, false, cE, s)) != cudaSuccess) return e;
+  // observation blocks
+  if (mx > 0) {
+    const int64_t cC = p.cntC, mm = (int64_t)mx * mx;
+    const int64_t sHw = (int64_t)mx * (n + 1);
+    L.add(cd(p.L, p.sL, mx, p.Lw, mm, mx, mx, mx, cC, 1.0, 1));
+    L.add(cd(p.H, p.sH, n, p.Hw, sHw, mx, mx, n, cC, 1.0, 1));
+    if (!p.constC) L.add(cd(p.o, p.so, 1, p.Hw + (int64_t)mx * n, sHw, mx, mx, 1, cC));
+    if ((e = run(L, s)) != cudaSuccess) return e;
+    if (p.m) {
+      big_mask_obs_kernel<<<(unsigned)cC, 256, 0, s>>>(p.Lw, p.Hw, p.m, mx, n + 1, mm, sHw);
+  ++g_launches;
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if ((e = chol(p.Lw, mm, mx, mx, cC, p.chol, p.status, 0, 1, kBadL, s)) != cudaSuccess) return e;
+    t.R = p.Lw; t.sR = mm; t.ldr = mx; t.B = p.Hw; t.sB = sHw; t.ldb = mx; t.k = p.constC ? n : n + 1; t.upper = 0;
+    if ((e = trsm(t, mx, cC, s)) != cudaSuccess) return e;
+    L.add(cd(p.Hw, sHw, mx, p.C0, (int64_t)mx * n, mx, mx, n, cC));
+    if (!p.constC) L.add(cd(p.Hw + (int64_t)mx * n, sHw, mx, p.y0, mx, mx, mx, 1, cC));
+    else L.add(cd(p.o, 0, (int)p.so, p.y0, 0, mx, mx, (int)p.N, 1));   // o^T as mx x N, ld so
+    if ((e = run(L, s)) != cudaSuccess) return e;
+    if (p.constC) {   // y = M^{-1} [o_0 .. o_{N-1}]: one solve with N right-hand sides
+      t.R = p.Lw; t.sR = 0; t.ldr = mx; t.B = p.y0; t.sB = 0; t.ldb = mx; t.k = (int)p.N; t.upper = 0;
+      if ((e = trsm(t, mx, 1, s)) != cudaSuccess) return e;
+    }
+    if ((e = sumsq(p.C0, (int64_t)mx * n, mx, mx, n, p.nC, 1, false, cC, s)) != cudaSuccess) return e;
+  } else {
+    if ((e = cudaMemsetAsync(p.nC, 0, sizeof(double), s)) != cudaSuccess) return e;
+  }
+  big_nrm0_kernel<<<(unsigned)((p.N + 255) / 256), 256, 0, s>>>(p.nC, p.cntC > 1 ? 1 : 0, p.nEr, p.nEl,
+                                                                p.cntE > 1 ? 1 : 0, p.N, p.nrm0);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- factor ---
+namespace {
+
+// column accessors of level L (0: whitened level-0 arrays; >= 1: entries)
+struct Cols {
+  const double *C, *y, *El, *Er, *e, *nrm;
+  int64_t sC, sy, sE, se, snrm;   // per-column strides (0: constant block)
+  int ldC, r;
+};
+Cols level_cols(const Plan &p, size_t L) {
+  Cols c;
+  const int n = p.n;
+  const int64_t nn = (int64_t)n * n;
+  if (L == 0) {
+    c.C = p.C0; c.sC = p.cntC > 1 ? (int64_t)p.RC * n : 0; c.ldC = p.RC > 0 ? p.RC : 1; c.r = p.RC;
+    c.y = p.y0; c.sy = p.RC;
+    c.El = p.El0; c.Er = p.Er0; c.sE = p.cntE > 1 ? nn : 0;
+    c.e = p.e0; c.se = p.cntE > 1 ? n : 0;
+    c.nrm = p.nrm0; c.snrm = 1;
+  } else {
+    const int64_t E = entry_doubles_big(n);
+    const double *b = p.ent[L];
+    c.C = b; c.sC = E; c.ldC = n; c.r = n;
+    c.y = b + nn; c.sy = E;
+    c.El = b + nn + n; c.Er = b + 2 * nn + n; c.sE = E;
+    c.e = b + 3 * nn + n; c.se = E;
+    c.nrm = b + 3 * nn + 2 * n; c.snrm = E;
+  }
+  return c;
+}
+
+// post-processing of eliminated columns whose stage-2 stack top rows hold
+// [R | R_l | R_r | z] (items [0, cnt) of S2): rank test, T = R^{-1}[R_l R_r z],
+// P = R^{-1} R^{-T}, into the records
+cudaError_t post(const Plan &p, size_t L, const double *nrm, int64_t snrm, int64_t cnt, double *rec,
+                 int64_t step_first, int64_t step_stride, cudaStream_t s) {
+  const int n = p.n;
+  const int64_t nn = (int64_t)n * n, ld2 = 2 * n, s2 = ld2 * (3 * n + 1), Rr = rrec_doubles_big(n);
+  cudaError_t e = rank_check(p.S2, s2, (int)ld2, n, nrm, snrm, p.status, step_first, step_stride, cnt, s);
+  if (e != cudaSuccess) return e;
+  Trsm t;
+  t.R = p.S2; t.sR = s2; t.ldr = (int)ld2; t.B = p.S2 + (int64_t)n * ld2; t.sB = s2; t.ldb = (int)ld2;
+  t.k = 2 * n + 1; t.upper = 1;
+  if ((e = trsm(t, n, cnt, s)) != cudaSuccess) return e;
+  CopyList Lc;
+  Lc.add(cd(nullptr, 0, 1, p.Rinv, nn, n, n, n, cnt, 1.0, 0, 0, 1.0));
+  if ((e = run(Lc, s)) != cudaSuccess) return e;
+  t.B = p.Rinv; t.sB = nn; t.ldb = n; t.k = n;
+  if ((e = trsm(t, n, cnt, s)) != cudaSuccess) return e;
+  Gemm g;   // P = R^{-1} R^{-T}
+  g.batch = cnt; g.M = n; g.N = n; g.K = n; g.A = p.Rinv; g.lda = n; g.sA = nn; g.B = p.Rinv; g.ldb = n; g.sB = nn;
+  g.C = rec + 2 * nn + n; g.ldc = n; g.sC = Rr;
+  if ((e = gemm(g, false, true, s)) != cudaSuccess) return e;
+  Lc.add(cd(p.S2 + (int64_t)n * ld2, s2, (int)ld2, rec, Rr, n, n, n, cnt));           // T_l
+  Lc.add(cd(p.S2 + (int64_t)2 * n * ld2, s2, (int)ld2, rec + nn, Rr, n, n, n, cnt));  // T_r
+  Lc.add(cd(p.S2 + (int64_t)3 * n * ld2, s2, (int)ld2, rec + 2 * nn, Rr, n, n, 1, cnt));  // w
+  return run(Lc, s);
+}
+
+}  // namespace
+
+cudaError_t factor(const Plan &p, cudaStream_t s) {
+  const int n = p.n;
+  const int64_t nn = (int64_t)n * n, E = entry_doubles_big(n), Rr = rrec_doubles_big(n);
+  cudaError_t e;
+  CopyList Lc;
+  for (size_t L = 0; L < p.Ks.size(); ++L) {
+    const int64_t K = p.Ks[L];
+    const Cols c = level_cols(p, L);
+    const int r = c.r;
+    const int ld1 = r + n, ld2 = 2 * n;
+    const int64_t s1 = (int64_t)ld1 * (2 * n + 1), s2 = (int64_t)ld2 * (3 * n + 1);
+    const int rb = r > n ? r : n;   // single-column stacks: zero rows up to n
+    if (K == 1) {   // base case: R_00 = qr(C_0), w = R^{-1} z
+      Lc.add(cd(nullptr, 0, 1, p.S1, 0, ld1, ld1, n + 1, 1));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      Lc.add(cd(c.C, 0, c.ldC, p.S1, 0, ld1, r, n, 1));
+      Lc.add(cd(c.y, 0, 1, p.S1 + (int64_t)n * ld1, 0, ld1, r, 1, 1));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      if ((e = qr_apply(p.S1, s1, ld1, rb, n, n + 1, 1, p.w, s)) != cudaSuccess) return e;
+      Lc.add(cd(p.S1, 0, ld1, p.S2, 0, ld2, n, n, 1, 1.0, 0, 1));
+      Lc.add(cd(nullptr, 0, 1, p.S2 + (int64_t)n * ld2, 0, ld2, n, 2 * n, 1));
+      Lc.add(cd(p.S1 + (int64_t)n * ld1, 0, ld1, p.S2 + (int64_t)3 * n * ld2, 0, ld2, n, 1, 1));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      if ((e = post(p, L, c.nrm, 0, 1, p.rec[L], ((int64_t)1 << L) - 1, 0, s)) != cudaSuccess) return e;
+      break;
+    }
+    const int64_t P = K / 2;
+    const bool odd = (K & 1) != 0;
+    const int ld3 = (int)rows3(n, r, odd);
+    const int64_t s3 = (int64_t)ld3 * (n + 1);
+    // ---- stage 1 (pairs): [C_t; El_u | 0; Er_u | y_t; e_u], t = 2p, u = 2p + 1 ----
+    Lc.add(cd(c.C, 2 * c.sC, c.ldC, p.S1, s1, ld1, r, n, P));
+    Lc.add(cd(c.El + c.sE, 2 * c.sE, n, p.S1 + r, s1, ld1, n, n, P));
+    Lc.add(cd(nullptr, 0, 1, p.S1 + (int64_t)n * ld1, s1, ld1, r, n, P));
+    Lc.add(cd(c.Er + c.sE, 2 * c.sE, n, p.S1 + (int64_t)n * ld1 + r, s1, ld1, n, n, P));
+    Lc.add(cd(c.y, 2 * c.sy, 1, p.S1 + (int64_t)2 * n * ld1, s1, ld1, r, 1, P));
+    Lc.add(cd(c.e + c.se, 2 * c.se, 1, p.S1 + (int64_t)2 * n * ld1 + r, s1, ld1, n, 1, P));
+    if (odd) {   // the last column (no right neighbour): [C_t | y_t] in item P (zero rows up to n)
+      const int64_t t = K - 1;
+      if (r < n) {
+        Lc.add(cd(nullptr, 0, 1, p.S1 + P * s1, 0, ld1, ld1, n + 1, 1));
+        if ((e = run(Lc, s)) != cudaSuccess) return e;
+      }
+      Lc.add(cd(c.C + t * c.sC, 0, c.ldC, p.S1 + P * s1, 0, ld1, r, n, 1));
+      Lc.add(cd(c.y + t * c.sy, 0, 1, p.S1 + P * s1 + (int64_t)n * ld1, 0, ld1, r, 1, 1));
+    }
+    if ((e = run(Lc, s)) != cudaSuccess) return e;
+    if ((e = qr_apply(p.S1, s1, ld1, ld1, n, 2 * n + 1, P, p.w, s)) != cudaSuccess) return e;
+    if (odd) {
+      Work w1 = p.w;
+      w1.V += P * p.w.sVU; w1.U += P * p.w.sVU; w1.W += P * p.w.sW;
+      // [C_t | y_t] sits in columns 0..n of item P (ld ld1): factor its r rows, apply to column n
+      if ((e = qr_apply(p.S1 + P * s1, s1, ld1, rb, n, n + 1, 1, w1, s)) != cudaSuccess) return e;
+    }
+    // ---- stage 2 (eliminated t = 2p, p >= 1; + the odd level's last column as item P) ----
+    // [Er_t | El_t | 0 | e_t ; R~_t | 0 | X_t | z~_t]
+    {
+      const int64_t cnt = P - 1;
+      double *S2b = p.S2 + s2;   // item 1
+      const double *S1b = p.S1 + s1;
+      Lc.add(cd(c.Er + 2 * c.sE, 2 * c.sE, n, S2b, s2, ld2, n, n, cnt));
+      Lc.add(cd(S1b, s1, ld1, S2b + n, s2, ld2, n, n, cnt, 1.0, 0, 1));
+      Lc.add(cd(c.El + 2 * c.sE, 2 * c.sE, n, S2b + (int64_t)n * ld2, s2, ld2, n, n, cnt));
+      Lc.add(cd(nullptr, 0, 1, S2b + (int64_t)n * ld2 + n, s2, ld2, n, n, cnt));
+      Lc.add(cd(nullptr, 0, 1, S2b + (int64_t)2 * n * ld2, s2, ld2, n, n, cnt));
+      Lc.add(cd(S1b + (int64_t)n * ld1, s1, ld1, S2b + (int64_t)2 * n * ld2 + n, s2, ld2, n, n, cnt));
+      Lc.add(cd(c.e + 2 * c.se, 2 * c.se, 1, S2b + (int64_t)3 * n * ld2, s2, ld2, n, 1, cnt));
+      Lc.add(cd(S1b + (int64_t)2 * n * ld1, s1, ld1, S2b + (int64_t)3 * n * ld2 + n, s2, ld2, n, 1, cnt));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+    }
+    if (odd) {   // item P: the last column, X = 0
+      const int64_t t = K - 1;
+      double *S2l = p.S2 + P * s2;
+      const double *S1l = p.S1 + P * s1;
+      Lc.add(cd(c.Er + t * c.sE, 0, n, S2l, 0, ld2, n, n, 1));
+      Lc.add(cd(S1l, 0, ld1, S2l + n, 0, ld2, n, n, 1, 1.0, 0, 1));
+      Lc.add(cd(c.El + t * c.sE, 0, n, S2l + (int64_t)n * ld2, 0, ld2, n, n, 1));
+      Lc.add(cd(nullptr, 0, 1, S2l + (int64_t)n * ld2 + n, 0, ld2, n, n, 1));
+      Lc.add(cd(nullptr, 0, 1, S2l + (int64_t)2 * n * ld2, 0, ld2, 2 * n, n, 1));
+      Lc.add(cd(c.e + t * c.se, 0, 1, S2l + (int64_t)3 * n * ld2, 0, ld2, n, 1, 1));
+      Lc.add(cd(S1l + (int64_t)n * ld1, 0, ld1, S2l + (int64_t)3 * n * ld2 + n, 0, ld2, n, 1, 1));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+    }
+    // item 0 (t = 0, no left neighbour: "nothing to do"): R = R~, R_r = X, z = z~; no coupling row
+    Lc.add(cd(p.S1, 0, ld1, p.S2, 0, ld2, n, n, 1, 1.0, 0, 1));
+    Lc.add(cd(nullptr, 0, 1, p.S2 + n, 0, ld2, n, n, 1));
+    Lc.add(cd(nullptr, 0, 1, p.S2 + (int64_t)n * ld2, 0, ld2, 2 * n, n, 1));
+    Lc.add(cd(p.S1 + (int64_t)n * ld1, 0, ld1, p.S2 + (int64_t)2 * n * ld2, 0, ld2, n, n, 1));
+    Lc.add(cd(nullptr, 0, 1, p.S2 + (int64_t)2 * n * ld2 + n, 0, ld2, n, n, 1));
+    Lc.add(cd(p.S1 + (int64_t)2 * n * ld1, 0, ld1, p.S2 + (int64_t)3 * n * ld2, 0, ld2, n, 1, 1));
+    Lc.add(cd(nullptr, 0, 1, p.S2 + (int64_t)3 * n * ld2 + n, 0, ld2, n, 1, 1));
+    if ((e = run(Lc, s)) != cudaSuccess) return e;
+    if (P - 1 + (odd ? 1 : 0) > 0)
+      if ((e = qr_apply(p.S2 + s2, s2, ld2, ld2, n, 3 * n + 1, P - 1 + (odd ? 1 : 0), p.w, s)) != cudaSuccess)
+        return e;
+    // ---- stage 3 (survivors u = 2p + 1): [D~_u; C_u (; Z_{K-1}) | y~; y_u (; z^)] ----
+    if (ld3 > 2 * r) {   // Z rows (odd level) / zero padding up to n rows
+      Lc.add(cd(nullptr, 0, 1, p.S3 + 2 * r, s3, ld3, ld3 - 2 * r, n + 1, P));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+    }
+    Lc.add(cd(p.S1 + (int64_t)n * ld1 + n, s1, ld1, p.S3, s3, ld3, r, n, P));
+    Lc.add(cd(p.S1 + (int64_t)2 * n * ld1 + n, s1, ld1, p.S3 + (int64_t)n * ld3, s3, ld3, r, 1, P));
+    Lc.add(cd(c.C + c.sC, 2 * c.sC, c.ldC, p.S3 + r, s3, ld3, r, n, P));
+    Lc.add(cd(c.y + c.sy, 2 * c.sy, 1, p.S3 + (int64_t)n * ld3 + r, s3, ld3, r, 1, P));
+    if (odd) {
+      Lc.add(cd(p.S2 + P * s2 + (int64_t)n * ld2 + n, 0, ld2, p.S3 + (P - 1) * s3 + 2 * r, 0, ld3, n, n, 1));
+      Lc.add(cd(p.S2 + P * s2 + (int64_t)3 * n * ld2 + n, 0, ld2, p.S3 + (P - 1) * s3 + (int64_t)n * ld3 + 2 * r, 0,
+                ld3, n, 1, 1));
+    }
+    if ((e = run(Lc, s)) != cudaSuccess) return e;
+    if ((e = qr_apply(p.S3, s3, ld3, ld3, n, n + 1, P, p.w, s)) != cudaSuccess) return e;
+    // ---- level L+1 entries (column p = survivor 2p + 1) ----
+    double *nx = p.ent[L + 1];
+    Lc.add(cd(p.S3, s3, ld3, nx, E, n, n, n, P, 1.0, 0, 1));                                  // C'
+    Lc.add(cd(p.S3 + (int64_t)n * ld3, s3, ld3, nx + nn, E, n, n, 1, P));                     // y'
+    Lc.add(cd(p.S2 + (int64_t)n * ld2 + n, s2, ld2, nx + nn + n, E, n, n, n, P));             // El = Z_t
+    Lc.add(cd(p.S2 + (int64_t)2 * n * ld2 + n, s2, ld2, nx + 2 * nn + n, E, n, n, n, P));     // Er = X~_t
+    Lc.add(cd(p.S2 + (int64_t)3 * n * ld2 + n, s2, ld2, nx + 3 * nn + n, E, n, n, 1, P));     // e = z^_t
+    Lc.add(cd(c.nrm + c.snrm, 2 * c.snrm, 1, nx + 3 * nn + 2 * n, E, 1, 1, 1, P));            // |column|^2
+    if ((e = run(Lc, s)) != cudaSuccess) return e;
+    // ---- records of the eliminated columns t = 2p (and K - 1) ----
+    if ((e = post(p, L, c.nrm, 2 * c.snrm, P + (odd ? 1 : 0), p.rec[L], ((int64_t)1 << L) - 1,
+                  (int64_t)2 << L, s)) != cudaSuccess)
+      return e;
+    (void)Rr;
+  }
+  return cudaSuccess;
+}
+
+// ----------------------------------------------------------- backward ---
+// Levels in reverse (P:592-600 and Alg. 2): for every eliminated
+// column t of level L with its level-(L+1) neighbours l, r:
+//   x_t = w - [T_l T_r][x_l; x_r];   G = [T_l T_r] [S_ll S_lr; S_rl S_rr]
+//   S_{t,I} = -G,   S_tt = P + G [T_l T_r]^T (symmetrised)
+cudaError_t backward(const Plan &p, bool do_state, bool do_cov, cudaStream_t s) {
+  const int n = p.n;
+  const int64_t nn = (int64_t)n * n, Rr = rrec_doubles_big(n);
+  cudaError_t e;
+  CopyList Lc;
+  const int top = (int)p.Ks.size() - 1;
+  for (int L = top; L >= 0; --L) {
+    const int64_t K = p.Ks[L];
+    const int64_t P = K / 2, cnt = P + (K & 1);   // eliminated columns t = 2q, q < cnt
+    const int64_t st = (int64_t)1 << L;         // domain distance to a neighbour
+    double *x = p.x, *S = p.S;
+    const double *rec = p.rec[L];
+    const int64_t j0 = st - 1, js = 2 * st;      // step of item q: j0 + q js
+    if (do_state) {   // xg = [x_l; x_r]
+      Lc.add(cd(nullptr, 0, 1, p.xg, 2 * n, 2 * n, 2 * n, 1, cnt));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      Lc.add(cd(x + (j0 - st + js) * n, js * n, n, p.xg + 2 * n + 0, 2 * n, 2 * n, n, 1, cnt - 1));   // q >= 1
+      Lc.add(cd(x + (j0 + st) * n, js * n, n, p.xg + n, 2 * n, 2 * n, n, 1, P));                      // q < P
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+    }
+    if (do_cov) {     // SII = [S_ll S_lr; S_rl S_rr] (2n x 2n)
+      const int64_t s4 = 4 * nn;
+      Lc.add(cd(nullptr, 0, 1, p.SII, s4, 2 * n, 2 * n, 2 * n, cnt));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      Lc.add(cd(S + (j0 - st + js) * nn, js * nn, n, p.SII + s4, s4, 2 * n, n, n, cnt - 1));                // S_ll
+      Lc.add(cd(S + (j0 + st) * nn, js * nn, n, p.SII + (int64_t)n * 2 * n + n, s4, 2 * n, n, n, P));      // S_rr
+      if (L < top && P > 1) {   // S_lr = S_{q-1,q} = X_{L+1}[q]^T, S_rl = X_{L+1}[q], 1 <= q < P
+        const double *Xu = p.X[L + 1];
+        Lc.add(cd(Xu + nn, nn, n, p.SII + s4 + (int64_t)n * 2 * n, s4, 2 * n, n, n, P - 1, 1.0, 1));
+        Lc.add(cd(Xu + nn, nn, n, p.SII + s4 + n, s4, 2 * n, n, n, P - 1));
+      }
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      Gemm g;   // G = A SII,  A = [T_l T_r] (n x 2n, ld n)
+      g.batch = cnt; g.M = n; g.N = 2 * n; g.K = 2 * n; g.A = rec; g.lda = n; g.sA = Rr;
+      g.B = p.SII; g.ldb = 2 * n; g.sB = s4; g.C = p.G; g.ldc = n; g.sC = 2 * nn;
+      if ((e = gemm(g, false, false, s)) != cudaSuccess) return e;
+      // S_tt = P + G A^T
+      Lc.add(cd(rec + 2 * nn + n, Rr, n, p.Pt, nn, n, n, n, cnt));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      g.M = n; g.N = n; g.K = 2 * n; g.A = p.G; g.lda = n; g.sA = 2 * nn; g.B = rec; g.ldb = n; g.sB = Rr;
+      g.C = p.Pt; g.ldc = n; g.sC = nn; g.beta = 1.0;
+      if ((e = gemm(g, false, true, s)) != cudaSuccess) return e;
+      if ((e = sym_store(p.Pt, nn, n, S + j0 * nn, js * nn, n, cnt, s)) != cudaSuccess) return e;
+      // cross blocks of level L: X_L[t] = S_{t,t-1} = -G[:, 0:n] (t >= 1),
+      // X_L[t+1] = S_{t+1,t} = -G[:, n:2n]^T (t + 1 < K)
+      if (L >= 1) {
+        double *Xc = p.X[L];
+        Lc.add(cd(p.G + 2 * nn, 2 * nn, n, Xc + 2 * nn, 2 * nn, n, n, n, cnt - 1, -1.0));
+        Lc.add(cd(p.G + nn, 2 * nn, n, Xc + nn, 2 * nn, n, n, n, P, -1.0, 1));
+        if ((e = run(Lc, s)) != cudaSuccess) return e;
+      }
+    }
+    if (do_state) {   // x_t = w - A xg
+      Lc.add(cd(rec + 2 * nn, Rr, n, p.xt, n, n, n, 1, cnt));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      Gemm g;
+      g.batch = cnt; g.M = n; g.N = 1; g.K = 2 * n; g.A = rec; g.lda = n; g.sA = Rr; g.B = p.xg; g.ldb = 2 * n;
+      g.sB = 2 * n; g.C = p.xt; g.ldc = n; g.sC = n; g.alpha = -1.0; g.beta = 1.0;
+      if ((e = gemm(g, false, false, s)) != cudaSuccess) return e;
+      Lc.add(cd(p.xt, n, n, x + j0 * n, js * n, n, n, 1, cnt));
+      if ((e = run(Lc, s)) != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+}  // namespace big
+}  // namespace ks

@@ -256,10 +256,14 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   auto ldY = [&](int e, int64_t c) {
     if (!L0) return lde(c, EN::y + e);
     if (CC && in.yfuse) {
+      // y_e = sum_k (M^{-1})_{ek} o_k over k < RC (M^{-1} is lower triangular:
+      // the terms k > e add exact zeros), unrolled so that the loads of o
+      // issue together instead of one dependent load per iteration
       const double *oc = in.o + c * in.so;
       double yv = 0.0;
-#pragma unroll 1
-      for (int k = 0; k <= e; ++k) yv = fma(cst[CstOff<N>::Mi + e * kSmallMaxM + k], __ldg(oc + k), yv);
+#pragma unroll
+      for (int k = 0; k < kSmallMaxM; ++k)
+        if (k < in.RC) yv = fma(cst[CstOff<N>::Mi + e * kSmallMaxM + k], __ldg(oc + k), yv);
       return yv;
     }
     return ldv<64>(in.y, c, e);

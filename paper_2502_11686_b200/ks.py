@@ -22,8 +22,8 @@ LIB_PATH = os.environ.get("KS_LIB") or os.path.join(_HERE, "libks.so")   # KS_LI
 
 KS_OK, KS_ERR_ARG, KS_ERR_ORDER, KS_ERR_CUDA, KS_ERR_NCCL, KS_ERR_NOT_SPD, KS_ERR_RANK, \
     KS_ERR_WORKSPACE = range(8)
-KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH, KS_NO_FUSED_TAIL, KS_COV_IS_CHOL, KS_KEEP_WHITENING = \
-    1, 2, 4, 8, 16, 32
+KS_HOST_INPUTS, KS_OUTPUTS_BOUND, KS_GENERIC_PATH, KS_NO_FUSED_TAIL, KS_COV_IS_CHOL, KS_KEEP_WHITENING, \
+    KS_BIG_PATH = 1, 2, 4, 8, 16, 32, 64
 FAMILIES = ("whiten", "factor", "solve", "selinv", "boundary", "backward")
 
 EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solve", "ks_selinv",
@@ -191,7 +191,7 @@ class Smoother:
                  host_inputs: bool = False, bind_outputs: bool = True, cov: bool = True,
                  shard=None, inputs=None, generic: bool = False, fused_tail: bool = True,
                  dist: Optional[Dist] = None, chol: bool = False, batch: int = 1,
-                 keep_whitening: bool = False):
+                 keep_whitening: bool = False, big: bool = False):
         self.L = lib()
         self.device = torch.device(device)
         if self.device.type == "cuda" and self.device.index is None:
@@ -229,7 +229,8 @@ class Smoother:
             pr.nstate_min = int(inputs["nstate"].min().item())
         pr.flags = (KS_HOST_INPUTS if host_inputs else 0) | (KS_OUTPUTS_BOUND if bind_outputs else 0) | \
             (KS_GENERIC_PATH if generic else 0) | (0 if fused_tail else KS_NO_FUSED_TAIL) | \
-            (KS_COV_IS_CHOL if chol else 0) | (KS_KEEP_WHITENING if keep_whitening else 0)
+            (KS_COV_IS_CHOL if chol else 0) | (KS_KEEP_WHITENING if keep_whitening else 0) | \
+            (KS_BIG_PATH if big else 0)
         pr.batch = int(batch)
         self.problem = pr
         if dist is None and shard is not None:

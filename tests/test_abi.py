@@ -67,9 +67,13 @@ def test_workspace_sizing_host_logic(ks):
     assert ws(_problem(ks, 0, 6, 6)) == 0                # bad sizes
     assert ws(_problem(ks, 10, 0, 6)) == 0
     assert ws(_problem(ks, 10, 6, 6, sF=5)) == 0         # stride smaller than a block
-    assert ws(_problem(ks, 10, 6, 6, flags=64)) == 0     # unknown flag
+    assert ws(_problem(ks, 10, 6, 6, flags=1 << 12)) == 0  # unknown flag
     assert ws(_problem(ks, 10, 6, 6, flags=ks.KS_COV_IS_CHOL)) > 0
-    assert ws(_problem(ks, 10, 200, 6)) == 0             # n > KS_MAX_N
+    assert ws(_problem(ks, 10, 600, 6)) == 0             # n > KS_MAX_N
+    big = ws(_problem(ks, 500, 500, 500, so=500))        # the paper's n = m = 500 size: the large-n path
+    assert 1e10 < big < 3e10
+    assert ws(_problem(ks, 500, 500, 600, so=600)) == 0  # stage stacks beyond the panel's shared memory
+    assert ws(_problem(ks, 100, 6, 6, so=6, flags=ks.KS_BIG_PATH)) > 0
     # multi-GPU: a ks_dist without a communicator (caller-driven exchange)
     def dist(rank, nranks, first, total):
         d = C.c_void_p()

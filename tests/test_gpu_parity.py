@@ -521,3 +521,58 @@ def test_general_with_batch_and_host_inputs():
         xb = np.where(m, xs.numpy()[b * 64:(b + 1) * 64], 0.0)
         Sb = np.where(m[:, :, None] & m[:, None, :], Ss.numpy()[b * 64:(b + 1) * 64], 0.0)
         assert rel_state_err(xb, xo) <= TOL_X and rel_cov_err(Sb, So) <= TOL_S
+
+
+# ---- the large-n path (n = m = 500) ----
+
+@pytest.mark.parametrize("n,N,mmax,const", [(2, 1, 2, False), (3, 2, 4, False), (3, 5, 1, False), (6, 8, 6, True),
+                                            (6, 17, 7, False), (9, 33, 9, False), (17, 64, 17, True),
+                                            (5, 100, 2, False), (20, 21, 25, False)])
+def test_big_path_small_n(n, N, mmax, const):
+    """The large-n path's batched kernels forced at small n (KS_BIG_PATH) --
+    every level shape, odd levels, ragged m_i -- against the oracle."""
+    rng = np.random.default_rng(31 * n + N)
+    m = n if N == 1 else (mmax if const else None)
+    p = gen.random_problem(rng, N, n, m=m, m_max=mmax, const=const)
+    p.m = np.minimum(p.m, mmax).astype(np.int32)
+    if N > 1 and mmax < n:
+        p.m[:] = mmax
+    assert_parity(p, big=True)
+
+
+@pytest.mark.parametrize("cfg,N", [("c4", 65), ("c2", 300), ("c3", 257), ("c5", 1000)])
+def test_big_path_configs(cfg, N):
+    assert_parity(gen.make(cfg, N=N), big=True)
+    x1, S1, _ = gpu_smooth(gen.make(cfg, N=N), big=True)
+    x2, S2, _ = gpu_smooth(gen.make(cfg, N=N))
+    assert rel_state_err(x1, x2) <= 1e-11 and rel_cov_err(S1, S2) <= 1e-11
+
+
+@pytest.mark.parametrize("n,N", [(72, 20), (128, 9), (200, 5)])
+def test_big_path_large_n(n, N):
+    """n beyond the CTA path's shared memory: the default path is the large-n one."""
+    assert_parity(gen.paper_problem(N, n, seed=n))
+    assert_parity(gen.random_problem(np.random.default_rng(n), N, n, m=n))
+
+
+def test_big_path_batch_and_nc():
+    parts = [gen.paper_problem(12, 80, seed=s) for s in range(3)]
+    p = gen.Problem.concat(parts)
+    s = ks().Smoother(p, batch=3)
+    s.run()
+    s.check()
+    x, S = s.states.cpu().numpy(), s.cov.cpu().numpy()
+    for b, q in enumerate(parts):
+        xo, So = oracle.smooth(q)
+        assert rel_state_err(x[b * 12:(b + 1) * 12], xo) <= TOL_X
+        assert rel_cov_err(S[b * 12:(b + 1) * 12], So) <= TOL_S
+    q = gen.paper_problem(40, 72, seed=1)
+    x, _, _ = gpu_smooth(q, cov=False)
+    assert rel_state_err(x, oracle.smooth(q, cov=False)) <= TOL_X
+
+
+@pytest.mark.slow
+def test_big_path_n500():
+    """The paper's n = m = 500 size at reduced k (the oracle is plain C,
+    about 46 n^3 flops per step)."""
+    assert_parity(gen.paper_problem(6, 500, seed=5))

@@ -11,5 +11,10 @@ bash tools/prof_c5.sh 40 2 ${TAG}_c5f 58 2 ${TAG}_c5b
 python tools/prof_run.py c4 - 1 > gpurun_out/${TAG}_plain_c4.log 2>&1 || exit 1
 ncu --set full --clock-control none --import-source on -k regex:factor_level -s 15 -c 1 -o gpurun_out/${TAG}_c4f python tools/prof_run.py c4 - 1 > gpurun_out/${TAG}_ncu_c4.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:whiten -s 2 -c 2 -o gpurun_out/${TAG}_c4w python tools/prof_run.py c4 - 1 > gpurun_out/${TAG}_ncu_c4w.log 2>&1
-for r in c4f c4w; do python tools/ncu_summary.py gpurun_out/${TAG}_$r.ncu-rep > gpurun_out/${TAG}_$r.sum.txt 2>&1; python tools/ncu_hot.py gpurun_out/${TAG}_$r.ncu-rep 30 0 > gpurun_out/${TAG}_$r.hot0.txt 2>&1; done
+for r in c4f c4w; do
+  python tools/ncu_summary.py gpurun_out/${TAG}_$r.ncu-rep > gpurun_out/${TAG}_$r.sum.txt 2>&1
+  python tools/ncu_hot.py gpurun_out/${TAG}_$r.ncu-rep 30 0 > gpurun_out/${TAG}_$r.hot0.txt 2>&1
+  ncu -i gpurun_out/${TAG}_$r.ncu-rep --page raw --csv --print-units base > gpurun_out/${TAG}_$r.raw.csv 2>&1
+  rm -f gpurun_out/${TAG}_$r.ncu-rep
+done
 ls -la gpurun_out | tail -30
