@@ -151,7 +151,7 @@ def roofline(launches, N, n, m, strides, p64_tf, cfg="c5"):
             tj = json.load(f)
         rec = tj.get(cfg, {}).get(f"{fam} L={lev}")
         if rec:
-            traffic, tsrc = rec["bytes"], f"profiles/{rec['round']}_{cfg}_{fam}_L{lev}.txt ({rec['report']})"
+            traffic, tsrc = rec["bytes"], f"profiles/traffic.json <- {rec['round']} ncu --set full ({rec['report']})"
             kname = f"{rec['kernel']} L={lev}"
     except Exception:
         pass

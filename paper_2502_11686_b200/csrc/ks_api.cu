@@ -787,7 +787,7 @@ int ks_dist_create(ks_dist **out, int rank, int nranks, const unsigned char *id,
   ks_dist *d = new (std::nothrow) ks_dist;
   if (!d) return KS_ERR_ARG;
   d->rank = rank; d->nranks = nranks; d->first = first_global_step; d->nglobal = nsteps_global;
-  if (id && nranks > 1) {
+  if (id) {   // (a 1-rank communicator is legal: nothing to exchange, the library calls still run)
     if (!g_nccl.load()) { delete d; return KS_ERR_NCCL; }
     NcclUid u;
     memcpy(u.internal, id, 128);

@@ -52,81 +52,90 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // ------------------------------------------------------------------ GEMM ---
-// Column-major operands; op(A) is M x K, op(B) is K x N.  CTA tile 64 x 64,
-// K chunks of 16 in two shared-memory stages; 8 warps as 2 (M) x 4 (N), each
-// warp 32 x 16 = 4 x 2 DMMA 8x8 tiles.  Shared tiles are k-major with a
-// leading dimension of 68 doubles: the fragment loads (row g = lane/4,
+// Column-major operands; op(A) is M x K, op(B) is K x N.  CTA tile BM x BN,
+// K chunks of BK in two shared-memory stages (cp.async), 8 warps, each warp a
+// WTM x WTN block of DMMA 8x8 tiles.  Shared tiles are k-major with leading
+// dimensions = 4 mod 16 doubles: the fragment loads (row g = lane/4,
 // k = lane%4) of a half-warp hit 16 distinct 8-byte bank pairs.
-constexpr int GBM = 64, GBN = 64, GBK = 16, GLD = 68;
-
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(256) big_gemm_kernel(Gemm g) {
-  __shared__ __align__(16) double As[2][GBK][GLD];
-  __shared__ __align__(16) double Bs[2][GBK][GLD];
+//   <64, 64, 16, 32, 16>: the general shape;
+//   <16, 256, 8, 16, 32>: W = V^T C of the compact-WY update (M = 16 rows).
+template <bool TA, bool TB, int BM, int BN, int BK, int WTM, int WTN, bool SPLITK = false>
+__global__ void __launch_bounds__(256) big_gemm_kernel(Gemm g, int kchunk) {
+  constexpr int LDA = BM + 4, LDB = BN + 4, FM = WTM / 8, FN = WTN / 8, WM = BM / WTM;
+  static_assert((BM / WTM) * (BN / WTN) == 8, "8 warps");
+  static_assert((BN * BK) % 256 == 0, "whole B loads per thread");
+  __shared__ __align__(16) double As[2][BK][LDA];
+  __shared__ __align__(16) double Bs[2][BK][LDB];
   const int64_t b = blockIdx.z;
   const double *A = g.A + b * g.sA, *B = g.B + b * g.sB;
   double *C = g.C + b * g.sC;
-  const int m0 = blockIdx.x * GBM, n0 = blockIdx.y * GBN;
+  // SPLITK (one M tile): blockIdx.x selects the K range [kb, ke); the
+  // partial products are added atomically into the zeroed C
+  const int m0 = SPLITK ? 0 : blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kb = SPLITK ? blockIdx.x * kchunk : 0;
+  const int ke = SPLITK ? min(g.K, kb + kchunk) : g.K;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, q = lane & 3;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
-  double acc[4][2][2];
+  const int wm = (warp % WM) * WTM, wn = (warp / WM) * WTN;
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   auto load = [&](int st, int k0) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < (BM * BK + 255) / 256; ++r) {
       const int idx = tid + 256 * r;
+      if (idx >= BM * BK) break;
       int m, k;
-      if (TA) { m = idx / GBK; k = idx % GBK; } else { m = idx % GBM; k = idx / GBM; }
+      if (TA) { m = idx / BK; k = idx % BK; } else { m = idx % BM; k = idx / BM; }
       const int gm = m0 + m, gk = k0 + k;
-      const bool ok = gm < g.M && gk < g.K;
+      const bool ok = gm < g.M && gk < ke;
       const double *src = TA ? A + gk + (int64_t)gm * g.lda : A + gm + (int64_t)gk * g.lda;
       cp8(&As[st][k][m], ok ? src : A, ok);
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < BN * BK / 256; ++r) {
       const int idx = tid + 256 * r;
       int nn, k;
-      if (TB) { nn = idx % GBN; k = idx / GBN; } else { nn = idx / GBK; k = idx % GBK; }
+      if (TB) { nn = idx % BN; k = idx / BN; } else { nn = idx / BK; k = idx % BK; }
       const int gn = n0 + nn, gk = k0 + k;
-      const bool ok = gn < g.N && gk < g.K;
+      const bool ok = gn < g.N && gk < ke;
       const double *src = TB ? B + gn + (int64_t)gk * g.ldb : B + gk + (int64_t)gn * g.ldb;
       cp8(&Bs[st][k][nn], ok ? src : B, ok);
     }
     cp_commit();
   };
-  const int nk = (g.K + GBK - 1) / GBK;
-  load(0, 0);
+  const int nk = (ke - kb + BK - 1) / BK;
+  if (nk <= 0) return;
+  load(0, kb);
   for (int kt = 0; kt < nk; ++kt) {
     const int st = kt & 1;
     if (kt + 1 < nk) {
-      load(st ^ 1, (kt + 1) * GBK);
+      load(st ^ 1, kb + (kt + 1) * BK);
       cp_wait1();
     } else {
       cp_wait0();
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < GBK; kk += 4) {
-      double af[4], bf[2];
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[st][kk + q][wm + 8 * i + gq];
+      for (int i = 0; i < FM; ++i) af[i] = As[st][kk + q][wm + 8 * i + gq];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[st][kk + q][wn + 8 * j + gq];
+      for (int j = 0; j < FN; ++j) bf[j] = Bs[st][kk + q][wn + 8 * j + gq];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < FN; ++j) {
       const int m = m0 + wm + 8 * i + gq;
       if (m >= g.M) continue;
 #pragma unroll
@@ -134,21 +143,46 @@ __global__ void __launch_bounds__(256) big_gemm_kernel(Gemm g) {
         const int n = n0 + wn + 8 * j + 2 * q + h;
         if (n >= g.N) continue;
         double *c = C + m + (int64_t)n * g.ldc;
-        *c = (g.beta == 0.0) ? g.alpha * acc[i][j][h] : fma(g.alpha, acc[i][j][h], g.beta * *c);
+        if (SPLITK) atomicAdd(c, g.alpha * acc[i][j][h]);
+        else *c = (g.beta == 0.0) ? g.alpha * acc[i][j][h] : fma(g.alpha, acc[i][j][h], g.beta * *c);
       }
     }
+}
+
+template <bool TA, bool TB>
+cudaError_t gemm_launch(const Gemm &g, cudaStream_t s) {
+  if (g.M <= 16) {
+    // W = V^T C of the compact-WY update: 16 rows, K = the stack's rows.
+    // Split K over CTAs (128 per CTA) when it is long: one column tile per
+    // item alone would serialise the whole reduction
+    constexpr int KC = 128;
+    const int ns = (g.K + KC - 1) / KC;
+    if (ns > 1 && g.beta == 0.0) {
+      const cudaError_t e = cudaMemset2DAsync(g.C, (size_t)g.sC * 8, 0, (size_t)g.ldc * g.N * 8, (size_t)g.batch, s);
+      if (e != cudaSuccess) return e;
+      const dim3 grid((unsigned)ns, (g.N + 255) / 256, (unsigned)g.batch);
+      big_gemm_kernel<TA, TB, 16, 256, 8, 16, 32, true><<<grid, 256, 0, s>>>(g, KC);
+    } else {
+      const dim3 grid(1, (g.N + 255) / 256, (unsigned)g.batch);
+      big_gemm_kernel<TA, TB, 16, 256, 8, 16, 32><<<grid, 256, 0, s>>>(g, 0);
+    }
+  } else {
+    const dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, (unsigned)g.batch);
+    big_gemm_kernel<TA, TB, 64, 64, 16, 32, 16><<<grid, 256, 0, s>>>(g, 0);
+  }
+  return cudaSuccess;
 }
 
 cudaError_t gemm(const Gemm &g, bool ta, bool tb, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.K <= 0 && g.beta == 1.0) return cudaSuccess;
-  const dim3 grid((g.M + GBM - 1) / GBM, (g.N + GBN - 1) / GBN, (unsigned)g.batch);
-  if (ta && tb) big_gemm_kernel<true, true><<<grid, 256, 0, s>>>(g);
-  else if (ta) big_gemm_kernel<true, false><<<grid, 256, 0, s>>>(g);
-  else if (tb) big_gemm_kernel<false, true><<<grid, 256, 0, s>>>(g);
-  else big_gemm_kernel<false, false><<<grid, 256, 0, s>>>(g);
+  cudaError_t e;
+  if (ta && tb) e = gemm_launch<true, true>(g, s);
+  else if (ta) e = gemm_launch<true, false>(g, s);
+  else if (tb) e = gemm_launch<false, true>(g, s);
+  else e = gemm_launch<false, false>(g, s);
   ++g_launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ copy ---
@@ -191,7 +225,7 @@ cudaError_t copy(const CopyList &L, int64_t batch, cudaStream_t s) {
 // R part back (zeros below the diagonal), the explicit V (rows x nb, unit
 // lower trapezoidal) and U = V T^T (the compact-WY T of dlarft, forward
 // columnwise), so that Q^T C = C - U (V^T C).  One CTA per item.
-constexpr int kPanelThreads = 256;
+constexpr int kPanelThreads = 512;
 __device__ double block_sum(double v, double *red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -201,8 +235,31 @@ __device__ double block_sum(double v, double *red) {
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < kPanelThreads / 32; ++w) s += red[w];
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
   return s;
+}
+
+// CTA-wide sums of NV per-thread values at once (one shuffle tree per value,
+// one barrier pair): out[v] valid in every thread.
+template <int NV>
+__device__ __forceinline__ void block_sums(double (&acc)[NV], double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) red[warp * NV + v] = acc[v];
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kPanelThreads / 32; ++w) t += red[w * NV + v];
+    acc[v] = t;
+  }
 }
 
 __global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
@@ -212,9 +269,10 @@ __global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
   double *V = a.V + b * a.sVU, *U = a.U + b * a.sVU;
   const int rows = a.m - a.j0, nb = a.nb, tid = threadIdx.x;
   double *P = psm;                      // [nb][rows] column-major (ld = rows)
-  double *red = P + (size_t)nb * rows;  // reductions: 8 warps x kBigNB partials
-  double *T = red + 8 * kBigNB;         // [nb][nb] column-major
+  double *red = P + (size_t)nb * rows;  // reductions: (threads / 32) x kBigNB partials
+  double *T = red + (kPanelThreads / 32) * kBigNB;   // [nb][nb] column-major
   double *tau = T + kBigNB * kBigNB;
+  double *yv = tau + kBigNB;            // V^T v_j of the current column
   for (int64_t e = tid; e < (int64_t)nb * rows; e += blockDim.x) {
     const int c = (int)(e / rows), r = (int)(e - (int64_t)c * rows);
     P[e] = S[(a.j0 + r) + (int64_t)(a.j0 + c) * a.lds];
@@ -222,51 +280,60 @@ __global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
     double *x = P + (size_t)j * rows;
-    double part = 0.0;
-    for (int r = j + 1 + tid; r < rows; r += blockDim.x) part = fma(x[r], x[r], part);
-    const double sigma = block_sum(part, red);
-    const double alpha = x[j];
+    double sg[1] = {0.0};
+    for (int r = j + 1 + tid; r < rows; r += blockDim.x) sg[0] = fma(x[r], x[r], sg[0]);
+    block_sums<1>(sg, red);
+    const double sigma = sg[0], alpha = x[j];
     double tj = 0.0, beta = alpha, scal = 0.0;
     if (sigma > 0.0) {
       beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
       tj = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    __syncthreads();
     for (int r = j + 1 + tid; r < rows; r += blockDim.x) x[r] *= scal;   // v (v_j = 1 implicit)
-    if (tid == 0) { x[j] = beta; tau[j] = tj; }
     __syncthreads();
-    // H_j applied to the panel columns c > j: w_c = v^T P[:, c], P[:, c] -= tau v w_c
-    for (int c = j + 1; c < nb; ++c) {
-      double *pc = P + (size_t)c * rows;
-      double pw = (tid == 0) ? pc[j] : 0.0;
-      for (int r = j + 1 + tid; r < rows; r += blockDim.x) pw = fma(x[r], pc[r], pw);
-      const double w = block_sum(pw, red) * tj;
-      if (tid == 0) pc[j] -= w;
-      for (int r = j + 1 + tid; r < rows; r += blockDim.x) pc[r] = fma(-w, x[r], pc[r]);
-      __syncthreads();
+    // one pass, one reduction for every other panel column c != j:
+    //   acc[c] = P[j][c] + sum_{r > j} v_r P[r][c]
+    // = v^T P[:, c] for c > j (the reflector's dots) and (V^T v_j)_c for
+    // c < j (those columns already hold v_c: the T recurrence of dlarft)
+    double acc[kBigNB];
+#pragma unroll
+    for (int c = 0; c < kBigNB; ++c) acc[c] = 0.0;
+    for (int r = j + 1 + tid; r < rows; r += blockDim.x) {
+      const double vr = x[r];
+#pragma unroll
+      for (int c = 0; c < kBigNB; ++c)
+        if (c < nb && c != j) acc[c] = fma(vr, P[r + (size_t)c * rows], acc[c]);
     }
-  }
-  // T (dlarft, forward columnwise): T[j][j] = tau_j,
-  // T[0:j, j] = -tau_j T[0:j, 0:j] (V[:, 0:j]^T v_j)
-  for (int j = 0; j < nb; ++j) {
-    for (int i = 0; i < j; ++i) {   // (V^T v_j)_i = sum_r V[r][i] V[r][j], r >= j (v_j zero above j, 1 at j)
-      const double *vi = P + (size_t)i * rows, *vj = P + (size_t)j * rows;
-      double part = (tid == 0) ? vi[j] : 0.0;
-      for (int r = j + 1 + tid; r < rows; r += blockDim.x) part = fma(vi[r], vj[r], part);
-      const double s = block_sum(part, red);
-      if (tid == 0) T[i + j * kBigNB] = s;
-      __syncthreads();
+    block_sums<kBigNB>(acc, red);
+#pragma unroll
+    for (int c = 0; c < kBigNB; ++c)
+      if (c < nb && c != j) acc[c] += P[j + (size_t)c * rows];
+    __syncthreads();   // every thread has read P[j][*] before it changes
+    // H_j applied to the columns c > j: P[:, c] -= tau v (v^T P[:, c])
+    for (int r = j + tid; r < rows; r += blockDim.x) {
+      const double vr = (r == j) ? 1.0 : x[r];
+#pragma unroll
+      for (int c = 0; c < kBigNB; ++c)
+        if (c > j && c < nb) P[r + (size_t)c * rows] = fma(-tj * acc[c], vr, P[r + (size_t)c * rows]);
+    }
+    if (tid < kBigNB) {   // V^T v_j (columns < j) to shared memory for the T recurrence
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < kBigNB; ++c)
+        if (c == tid) v = acc[c];
+      yv[tid] = v;
+    }
+    __syncthreads();
+    if (tid < j) {   // T[0:j, j] = -tau_j T[0:j, 0:j] (V^T v_j)  (dlarft, forward columnwise)
+      double sv = 0.0;
+      for (int k = tid; k < j; ++k) sv = fma(T[tid + k * kBigNB], yv[k], sv);
+      T[tid + j * kBigNB] = -tj * sv;
     }
     if (tid == 0) {
-      double y[kBigNB];
-      for (int i = 0; i < j; ++i) y[i] = T[i + j * kBigNB];
-      for (int i = 0; i < j; ++i) {
-        double s = 0.0;
-        for (int k = i; k < j; ++k) s = fma(T[i + k * kBigNB], y[k], s);
-        T[i + j * kBigNB] = -tau[j] * s;
-      }
-      T[j + j * kBigNB] = tau[j];
+      x[j] = beta;
+      tau[j] = tj;
+      T[j + j * kBigNB] = tj;
     }
     __syncthreads();
   }
@@ -284,17 +351,17 @@ __global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
 #pragma unroll
     for (int c = 0; c < kBigNB; ++c) {
       if (c >= nb) break;
-      double s = 0.0;   // (V T^T)[r][c] = sum_{k >= c} V[r][k] T[c][k]
+      double sv = 0.0;   // (V T^T)[r][c] = sum_{k >= c} V[r][k] T[c][k]
 #pragma unroll
       for (int k = 0; k < kBigNB; ++k)
-        if (k >= c && k < nb) s = fma(vr[k], T[c + k * kBigNB], s);
-      U[r + (int64_t)c * a.ldv] = s;
+        if (k >= c && k < nb) sv = fma(vr[k], T[c + k * kBigNB], sv);
+      U[r + (int64_t)c * a.ldv] = sv;
     }
   }
 }
 
 size_t panel_smem(int rows) {
-  return sizeof(double) * ((size_t)kBigNB * rows + 8 * kBigNB + kBigNB * kBigNB + kBigNB);
+  return sizeof(double) * ((size_t)kBigNB * rows + (kPanelThreads / 32) * kBigNB + kBigNB * kBigNB + 2 * kBigNB);
 }
 
 cudaError_t qr_panel(const Panel &a, int64_t batch, cudaStream_t s) {
@@ -310,6 +377,12 @@ cudaError_t qr_panel(const Panel &a, int64_t batch, cudaStream_t s) {
 // In place X = T^{-1} X for the nb x nb diagonal block T = R[j0:j0+nb, j0:j0+nb]
 // (upper: back substitution; lower: forward), X = B[j0:j0+nb, 0:k]; one
 // thread per right-hand-side column, the block staged in shared memory.
+// In place X = T^{-1} X for the nb x nb (nb <= 64) diagonal block
+// T = R[j0:j0+nb, j0:j0+nb] (upper: back substitution; lower: forward),
+// X = B[j0:j0+nb, 0:k]: one WARP per right-hand-side column (lane l holds
+// rows l and l + 32), column-oriented: x_i from its owner lane, broadcast by
+// a shuffle, then every lane updates its remaining rows; the block is staged
+// in shared memory.
 __global__ void __launch_bounds__(256) big_trsm_diag_kernel(Trsm a, int j0, int nb) {
   __shared__ double Ts[64][65];
   const int64_t b = blockIdx.y;
@@ -320,35 +393,30 @@ __global__ void __launch_bounds__(256) big_trsm_diag_kernel(Trsm a, int j0, int 
     Ts[r][c] = R[(j0 + r) + (int64_t)(j0 + c) * a.ldr];
   }
   __syncthreads();
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (col >= a.k) return;
   double *x = B + j0 + (int64_t)col * a.ldb;
-  double xv[64];
-#pragma unroll
-  for (int i = 0; i < 64; ++i) xv[i] = (i < nb) ? x[i] : 0.0;
+  double x0 = lane < nb ? x[lane] : 0.0, x1 = lane + 32 < nb ? x[lane + 32] : 0.0;
   if (a.upper) {
-#pragma unroll
-    for (int i = 63; i >= 0; --i) {
-      if (i >= nb) continue;
-      double s = xv[i];
-#pragma unroll
-      for (int k = i + 1; k < 64; ++k)
-        if (k < nb) s = fma(-Ts[i][k], xv[k], s);
-      xv[i] = s / Ts[i][i];
+    for (int i = nb - 1; i >= 0; --i) {
+      const double own = (i < 32) ? x0 : x1;
+      const double xi = __shfl_sync(0xffffffffu, own, i & 31) / Ts[i][i];
+      if (i < 32) { if (lane == i) x0 = xi; } else if (lane == i - 32) x1 = xi;
+      if (lane < i) x0 = fma(-Ts[lane][i], xi, x0);
+      if (lane + 32 < i) x1 = fma(-Ts[lane + 32][i], xi, x1);
     }
   } else {
-#pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      if (i >= nb) continue;
-      double s = xv[i];
-#pragma unroll
-      for (int k = 0; k < i; ++k) s = fma(-Ts[i][k], xv[k], s);
-      xv[i] = s / Ts[i][i];
+    for (int i = 0; i < nb; ++i) {
+      const double own = (i < 32) ? x0 : x1;
+      const double xi = __shfl_sync(0xffffffffu, own, i & 31) / Ts[i][i];
+      if (i < 32) { if (lane == i) x0 = xi; } else if (lane == i - 32) x1 = xi;
+      if (lane > i && lane < nb) x0 = fma(-Ts[lane][i], xi, x0);
+      if (lane + 32 > i && lane + 32 < nb) x1 = fma(-Ts[lane + 32][i], xi, x1);
     }
   }
-#pragma unroll
-  for (int i = 0; i < 64; ++i)
-    if (i < nb) x[i] = xv[i];
+  if (lane < nb) x[lane] = x0;
+  if (lane + 32 < nb) x[lane + 32] = x1;
 }
 
 // Blocked triangular solve X = R^{-1} B (n x n triangular, B n x k), in place.
@@ -358,7 +426,7 @@ cudaError_t trsm(const Trsm &a, int n, int64_t batch, cudaStream_t s) {
   for (int t = 0; t < nblk; ++t) {
     const int jb = a.upper ? nblk - 1 - t : t;
     const int j0 = jb * BS, nb = (n - j0 < BS) ? n - j0 : BS;
-    big_trsm_diag_kernel<<<dim3((a.k + 255) / 256, (unsigned)batch), 256, 0, s>>>(a, j0, nb);
+    big_trsm_diag_kernel<<<dim3((a.k + 7) / 8, (unsigned)batch), 256, 0, s>>>(a, j0, nb);
   ++g_launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -386,7 +454,7 @@ cudaError_t trsm(const Trsm &a, int n, int64_t batch, cudaStream_t s) {
 __global__ void __launch_bounds__(256) big_chol_kernel(double *A, int64_t sA, int ld, int d, int chol_given,
                                                         unsigned long long *status, int64_t step_off, int kind,
                                                         int64_t step_mul) {
-  __shared__ double red[8];
+  __shared__ double red[32];
   __shared__ double piv;
   double *M = A + (int64_t)blockIdx.x * sA;
   const int tid = threadIdx.x;
@@ -424,10 +492,108 @@ __global__ void __launch_bounds__(256) big_chol_kernel(double *A, int64_t sA, in
     atomicMin(status, status_word((int64_t)blockIdx.x * step_mul + step_off, kind));
 }
 
+// Blocked (left-looking) Cholesky, 64-column block columns: the block column
+// A[j0:d, j0:j0+jb] -= L[j0:d, 0:j0] L[j0:j0+jb, 0:j0]^T (big_gemm), then
+// the diagonal block factored in shared memory (big_chol_diag) and the rows
+// below solved against it (big_trsm_right: X L11^T = A21).
+__global__ void __launch_bounds__(256) big_chol_diag_kernel(double *A, int64_t sA, int ld, int j0, int jb,
+                                                             unsigned long long *status, int64_t step_off, int kind,
+                                                             int64_t step_mul) {
+  __shared__ double Ls[64][65];
+  double *M = A + (int64_t)blockIdx.x * sA;
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
+    const int c = e / jb, r = e - c * jb;
+    Ls[r][c] = M[(j0 + r) + (int64_t)(j0 + c) * ld];
+  }
+  __syncthreads();
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < jb; ++j) {
+    if (threadIdx.x == 0) {
+      double dj = Ls[j][j];
+      for (int k = 0; k < j; ++k) dj = fma(-Ls[j][k], Ls[j][k], dj);
+      if (!(dj > 0.0)) { bad = 1; dj = 1.0; }
+      Ls[j][j] = sqrt(dj);
+    }
+    __syncthreads();
+    const double il = 1.0 / Ls[j][j];
+    for (int r = j + 1 + threadIdx.x; r < jb; r += blockDim.x) {
+      double v = Ls[r][j];
+      for (int k = 0; k < j; ++k) v = fma(-Ls[r][k], Ls[j][k], v);
+      Ls[r][j] = v * il;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
+    const int c = e / jb, r = e - c * jb;
+    M[(j0 + r) + (int64_t)(j0 + c) * ld] = (r >= c) ? Ls[r][c] : 0.0;
+  }
+  if (threadIdx.x == 0 && bad && status)
+    atomicMin(status, status_word((int64_t)blockIdx.x * step_mul + step_off, kind));
+}
+__global__ void __launch_bounds__(256) big_trsm_right_kernel(double *A, int64_t sA, int ld, int j0, int jb, int d) {
+  __shared__ double Ls[64][65];
+  double *M = A + (int64_t)blockIdx.y * sA;
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
+    const int c = e / jb, r = e - c * jb;
+    Ls[r][c] = M[(j0 + r) + (int64_t)(j0 + c) * ld];
+  }
+  __syncthreads();
+  const int r = j0 + jb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= d) return;
+  double xv[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c) xv[c] = (c < jb) ? M[r + (int64_t)(j0 + c) * ld] : 0.0;
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    if (c >= jb) break;
+    double v = xv[c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) v = fma(-xv[k], Ls[c][k], v);
+    xv[c] = v / Ls[c][c];
+  }
+#pragma unroll
+  for (int c = 0; c < 64; ++c)
+    if (c < jb) M[r + (int64_t)(j0 + c) * ld] = xv[c];
+}
+__global__ void big_zero_upper_kernel(double *A, int64_t sA, int ld, int d) {
+  double *M = A + (int64_t)blockIdx.y * sA;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)d * d;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / d), r = (int)(e - (int64_t)c * d);
+    if (r < c) M[r + (int64_t)c * ld] = 0.0;
+  }
+}
+
 cudaError_t chol(double *A, int64_t sA, int ld, int d, int64_t batch, bool given, unsigned long long *status,
                  int64_t step_off, int64_t step_mul, int kind, cudaStream_t s) {
   if (batch <= 0 || d <= 0) return cudaSuccess;
-  big_chol_kernel<<<(unsigned)batch, 256, 0, s>>>(A, sA, ld, d, given ? 1 : 0, status, step_off, kind, step_mul);
+  if (given) {   // KS_COV_IS_CHOL: check the diagonal, clear the upper triangle
+    big_chol_kernel<<<(unsigned)batch, 256, 0, s>>>(A, sA, ld, d, 1, status, step_off, kind, step_mul);
+    ++g_launches;
+    return cudaGetLastError();
+  }
+  cudaError_t e;
+  for (int j0 = 0; j0 < d; j0 += 64) {
+    const int jb = (d - j0 < 64) ? d - j0 : 64;
+    if (j0 > 0) {
+      Gemm g;
+      g.batch = batch; g.M = d - j0; g.N = jb; g.K = j0; g.alpha = -1.0; g.beta = 1.0;
+      g.A = A + j0; g.lda = ld; g.sA = sA; g.B = A + j0; g.ldb = ld; g.sB = sA;
+      g.C = A + j0 + (int64_t)j0 * ld; g.ldc = ld; g.sC = sA;
+      if ((e = gemm(g, false, true, s)) != cudaSuccess) return e;
+    }
+    big_chol_diag_kernel<<<(unsigned)batch, 256, 0, s>>>(A, sA, ld, j0, jb, status, step_off, kind, step_mul);
+    ++g_launches;
+    if (d - j0 - jb > 0) {
+      big_trsm_right_kernel<<<dim3((d - j0 - jb + 255) / 256, (unsigned)batch), 256, 0, s>>>(A, sA, ld, j0, jb, d);
+      ++g_launches;
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  big_zero_upper_kernel<<<dim3((unsigned)(((int64_t)d * d + 255) / 256 < 256 ? ((int64_t)d * d + 255) / 256 : 256),
+                               (unsigned)batch), 256, 0, s>>>(A, sA, ld, d);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -436,7 +602,7 @@ cudaError_t chol(double *A, int64_t sA, int ld, int d, int64_t batch, bool given
 // Sum of squares of an rows x cols block per item -> out[b * so] (+= if acc).
 __global__ void __launch_bounds__(256) big_sumsq_kernel(const double *A, int64_t sA, int lda, int rows, int cols,
                                                          double *out, int64_t so, int acc) {
-  __shared__ double red[8];
+  __shared__ double red[32];
   const double *M = A + (int64_t)blockIdx.x * sA;
   double part = 0.0;
   for (int64_t e = threadIdx.x; e < (int64_t)rows * cols; e += blockDim.x) {

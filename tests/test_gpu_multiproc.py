@@ -87,3 +87,27 @@ def test_two_processes_gloo_staged_exchange(cfg, N):
     s1.run()
     s1.check()
     assert np.array_equal(x, s1.states.cpu().numpy()) and np.array_equal(S, s1.cov.cpu().numpy())
+
+
+def test_library_nccl_communicator_one_rank():
+    """ks_dist_unique_id / ks_dist_create / ks_dist_info / ks_dist_destroy on
+    the hardware: libnccl is dlopen'ed, a 1-rank communicator is created by
+    the library (NCCL forbids two ranks on one GPU, so this box cannot run the
+    2-rank allgather; tests above cover the exchange itself), and a context
+    over it runs unsharded."""
+    import torch
+    from paper_2502_11686_b200 import generators as gen
+    from paper_2502_11686_b200 import ks
+    uid = ks.Dist.unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128
+    d = ks.Dist(0, 1, 0, 1000, uid=uid, device="cuda:0")
+    assert d.info() == {"rank": 0, "nranks": 1, "nccl_nranks": 1}
+    p = gen.make("c2", N=1000)
+    s1 = ks.Smoother(p, dist=d)
+    s1.run()
+    s1.check()
+    s2 = ks.Smoother(p)
+    s2.run()
+    s2.check()
+    assert torch.equal(s1.states, s2.states) and torch.equal(s1.cov, s2.cov)
+    del s1, d
