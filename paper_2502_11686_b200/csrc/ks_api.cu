@@ -315,10 +315,18 @@ size_t carve(ks_ctx *c, char *base) {
     b.S1 = w.take<double>(items * s1);
     b.S2 = w.take<double>(items * s2);
     b.S3 = w.take<double>(items * s3);
-    b.w.V = w.take<double>(items * vu);
-    b.w.U = w.take<double>(items * vu);
-    b.w.W = w.take<double>(items * ww);
-    b.w.sVU = vu; b.w.sW = ww; b.w.ldv = (int)(vu / ks::big::kBigNB);
+    const int64_t rows = vu / ks::big::kBigBlk;
+    for (ks::big::Work *wk : {&b.w, &b.w2}) {   // one QR scratch per stream
+      wk->V = w.take<double>(items * vu);
+      wk->U = w.take<double>(items * vu);
+      wk->U16 = w.take<double>(items * rows * ks::big::kBigNB);
+      wk->W = w.take<double>(items * ww);
+      wk->G = w.take<double>(items * ks::big::kBigBlk * ks::big::kBigBlk);
+      wk->T = w.take<double>(items * ks::big::kBigBlk * ks::big::kBigBlk);
+      wk->tau = w.take<double>(items * ks::big::kBigBlk);
+      wk->sVU = vu; wk->sU16 = rows * ks::big::kBigNB; wk->sW = ww;
+      wk->sGT = ks::big::kBigBlk * ks::big::kBigBlk; wk->stau = ks::big::kBigBlk; wk->ldv = (int)rows;
+    }
     b.Rinv = w.take<double>(items * nn);
     b.SII = w.take<double>(items * 4 * nn);
     b.G = w.take<double>(items * 2 * nn);
@@ -875,6 +883,15 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
     b.sF = p->sF; b.sH = p->sH; b.sc = p->sc; b.so = p->so; b.sK = p->sK; b.sL = p->sL;
     b.status = c->status;
     b.x = c->xout; b.S = c->Sout;
+    // the second stream of the factor (stage 3 beside stage 2); its work is
+    // ordered with the context's stream by events, so it is captured into
+    // the same CUDA graph
+    if (cudaStreamCreateWithFlags(&b.s2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev[1], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      b.s2 = nullptr;
+    }
   }
   *out = c;
   return KS_OK;
@@ -1213,6 +1230,11 @@ const char *ks_strerror(int code) {
 
 void ks_destroy(ks_ctx *c) {
   if (!c) return;
+  if (c->big) {
+    if (c->bp.s2) cudaStreamDestroy(c->bp.s2);
+    for (cudaEvent_t e : c->bp.ev)
+      if (e) cudaEventDestroy(e);
+  }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }

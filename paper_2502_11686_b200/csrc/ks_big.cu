@@ -157,7 +157,7 @@ cudaError_t gemm_launch(const Gemm &g, cudaStream_t s) {
     // item alone would serialise the whole reduction
     constexpr int KC = 128;
     const int ns = (g.K + KC - 1) / KC;
-    if (ns > 1 && g.beta == 0.0) {
+    if (ns > 1 && g.beta == 0.0 && g.sC >= (int64_t)g.ldc * g.N) {
       const cudaError_t e = cudaMemset2DAsync(g.C, (size_t)g.sC * 8, 0, (size_t)g.ldc * g.N * 8, (size_t)g.batch, s);
       if (e != cudaSuccess) return e;
       const dim3 grid((unsigned)ns, (g.N + 255) / 256, (unsigned)g.batch);
@@ -166,6 +166,14 @@ cudaError_t gemm_launch(const Gemm &g, cudaStream_t s) {
       const dim3 grid(1, (g.N + 255) / 256, (unsigned)g.batch);
       big_gemm_kernel<TA, TB, 16, 256, 8, 16, 32><<<grid, 256, 0, s>>>(g, 0);
     }
+  } else if (g.M <= 64 && g.K >= 512 && g.beta == 0.0 && g.sC >= (int64_t)g.ldc * g.N) {
+    // V^T C / V^T V of the block reflector (64 rows, K = the stack's rows): split K
+    constexpr int KC = 256;
+    const int ns = (g.K + KC - 1) / KC;
+    const cudaError_t e = cudaMemset2DAsync(g.C, (size_t)g.sC * 8, 0, (size_t)g.ldc * g.N * 8, (size_t)g.batch, s);
+    if (e != cudaSuccess) return e;
+    const dim3 grid((unsigned)ns, (g.N + 63) / 64, (unsigned)g.batch);
+    big_gemm_kernel<TA, TB, 64, 64, 16, 32, 16, true><<<grid, 256, 0, s>>>(g, KC);
   } else {
     const dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, (unsigned)g.batch);
     big_gemm_kernel<TA, TB, 64, 64, 16, 32, 16><<<grid, 256, 0, s>>>(g, 0);
@@ -241,8 +249,10 @@ __device__ double block_sum(double v, double *red) {
 
 // CTA-wide sums of NV per-thread values at once (one shuffle tree per value,
 // one barrier pair): out[v] valid in every thread.
+// (red: (threads / 32) x NV partials, then NV totals)
 template <int NV>
 __device__ __forceinline__ void block_sums(double (&acc)[NV], double *red) {
+  constexpr int NW = kPanelThreads / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int v = 0; v < NV; ++v)
@@ -253,87 +263,132 @@ __device__ __forceinline__ void block_sums(double (&acc)[NV], double *red) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) red[warp * NV + v] = acc[v];
   __syncthreads();
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
+  if (threadIdx.x < NV) {   // one thread per value sums the warps' partials
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < kPanelThreads / 32; ++w) t += red[w * NV + v];
-    acc[v] = t;
+    for (int w = 0; w < NW; ++w) t += red[w * NV + threadIdx.x];
+    red[NW * NV + threadIdx.x] = t;
   }
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = red[NW * NV + v];
+}
+
+// CTA-wide sums of 16 per-thread values plus one more: a warp reduce-scatter
+// (16 shuffles instead of 16 x 5: each exchange step halves the values a
+// lane keeps), one partial per (warp, value) in shared memory, then one
+// thread per value sums the warps -- and, in the same step, threads < 16
+// copy row j of the panel (rowj) so that every thread reads it from the
+// copy: no thread can see the row after its owner has updated it.
+// On exit acc[v] (v < 17) and pj[v] (v < 16) are valid in every thread.
+__device__ __forceinline__ void block_sums17(double (&acc)[17], double *red, const double *rowj, int ldr, int nb,
+                                             double (&pj)[16]) {
+  constexpr int NW = kPanelThreads / 32;
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc[16] += __shfl_xor_sync(full, acc[16], o);
+#pragma unroll
+  for (int h = 8, bit = 16; h >= 1; h >>= 1, bit >>= 1) {
+    const bool up = (lane & bit) != 0;
+#pragma unroll
+    for (int v = 0; v < h; ++v) {
+      const double send = up ? acc[v] : acc[v + h];
+      const double keep = up ? acc[v + h] : acc[v];
+      acc[v] = keep + __shfl_xor_sync(full, send, bit);
+    }
+  }
+  acc[0] += __shfl_xor_sync(full, acc[0], 1);
+  const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  if ((lane & 1) == 0) red[warp * 17 + idx] = acc[0];
+  if (lane == 1) red[warp * 17 + 16] = acc[16];
+  __syncthreads();
+  if (threadIdx.x < 17) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += red[w * 17 + threadIdx.x];
+    red[NW * 17 + threadIdx.x] = t;
+    if (threadIdx.x < 16) red[NW * 17 + 17 + threadIdx.x] = threadIdx.x < nb ? rowj[(size_t)threadIdx.x * ldr] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < 17; ++v) acc[v] = red[NW * 17 + v];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) pj[v] = red[NW * 17 + 17 + v];
 }
 
 __global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
   extern __shared__ __align__(16) double psm[];
   const int64_t b = blockIdx.x;
   double *S = a.S + b * a.sS;
-  double *V = a.V + b * a.sVU, *U = a.U + b * a.sVU;
+  double *V = a.V + b * a.sV, *U = a.U + b * a.sU;
   const int rows = a.m - a.j0, nb = a.nb, tid = threadIdx.x;
   double *P = psm;                      // [nb][rows] column-major (ld = rows)
-  double *red = P + (size_t)nb * rows;  // reductions: (threads / 32) x kBigNB partials
-  double *T = red + (kPanelThreads / 32) * kBigNB;   // [nb][nb] column-major
+  double *red = P + (size_t)nb * rows;  // reductions: (threads / 32) x 17 partials, 17 totals, row j
+  double *T = red + (kPanelThreads / 32 + 2) * 17;   // [nb][nb] column-major
   double *tau = T + kBigNB * kBigNB;
-  double *yv = tau + kBigNB;            // V^T v_j of the current column
+  // the panel into shared memory (asynchronous copies: all of a thread's
+  // loads in flight at once)
   for (int64_t e = tid; e < (int64_t)nb * rows; e += blockDim.x) {
     const int c = (int)(e / rows), r = (int)(e - (int64_t)c * rows);
-    P[e] = S[(a.j0 + r) + (int64_t)(a.j0 + c) * a.lds];
+    cp8(&P[e], S + (a.j0 + r) + (int64_t)(a.j0 + c) * a.lds, true);
   }
+  cp_commit();
+  cp_wait0();
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
     double *x = P + (size_t)j * rows;
-    double sg[1] = {0.0};
-    for (int r = j + 1 + tid; r < rows; r += blockDim.x) sg[0] = fma(x[r], x[r], sg[0]);
-    block_sums<1>(sg, red);
-    const double sigma = sg[0], alpha = x[j];
+    // ONE pass and ONE reduction per column (on the unscaled x = P[:, j]):
+    //   acc[16] = sum_{r > j} x_r^2                     (the norm)
+    //   acc[c]  = sum_{r > j} x_r P[r][c], c != j      (scaled below by 1/(alpha - beta))
+    // giving v^T P[:, c] for c > j (the reflector's dots) and (V^T v_j)_c
+    // for c < j (those columns already hold v_c: dlarft's T column)
+    double acc[17], pj[16];
+#pragma unroll
+    for (int c = 0; c < 17; ++c) acc[c] = 0.0;
+    for (int r = j + 1 + tid; r < rows; r += blockDim.x) {
+      const double xr = x[r];
+      acc[16] = fma(xr, xr, acc[16]);
+#pragma unroll
+      for (int c = 0; c < kBigNB; ++c)
+        if (c < nb && c != j) acc[c] = fma(xr, P[r + (size_t)c * rows], acc[c]);
+    }
+    block_sums17(acc, red, P + j, rows, nb, pj);
+    double alpha = 0.0;   // P[j][j] (from the copy: compile-time indices, no local memory)
+#pragma unroll
+    for (int v = 0; v < 16; ++v)
+      if (v == j) alpha = pj[v];
+    const double sigma = acc[16];
     double tj = 0.0, beta = alpha, scal = 0.0;
     if (sigma > 0.0) {
       beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
       tj = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    for (int r = j + 1 + tid; r < rows; r += blockDim.x) x[r] *= scal;   // v (v_j = 1 implicit)
-    __syncthreads();
-    // one pass, one reduction for every other panel column c != j:
-    //   acc[c] = P[j][c] + sum_{r > j} v_r P[r][c]
-    // = v^T P[:, c] for c > j (the reflector's dots) and (V^T v_j)_c for
-    // c < j (those columns already hold v_c: the T recurrence of dlarft)
-    double acc[kBigNB];
+    // w_c = v^T P[:, c] = P[j][c] + scal acc[c] (v_j = 1); y_c likewise for c < j
 #pragma unroll
-    for (int c = 0; c < kBigNB; ++c) acc[c] = 0.0;
-    for (int r = j + 1 + tid; r < rows; r += blockDim.x) {
-      const double vr = x[r];
+    for (int c = 0; c < kBigNB; ++c) acc[c] = fma(scal, acc[c], pj[c]);
+    // T[0:j, j] = -tau_j T[0:j, 0:j] y  (dlarft, forward columnwise): row i of T
+    // is written and read only by thread i, so no barrier is needed for it
+    if (tid < j) {
+      double sv = 0.0;
 #pragma unroll
-      for (int c = 0; c < kBigNB; ++c)
-        if (c < nb && c != j) acc[c] = fma(vr, P[r + (size_t)c * rows], acc[c]);
+      for (int k = 0; k < kBigNB; ++k)
+        if (k >= tid && k < j) sv = fma(T[tid + k * kBigNB], acc[k], sv);
+      T[tid + j * kBigNB] = -tj * sv;
     }
-    block_sums<kBigNB>(acc, red);
-#pragma unroll
-    for (int c = 0; c < kBigNB; ++c)
-      if (c < nb && c != j) acc[c] += P[j + (size_t)c * rows];
-    __syncthreads();   // every thread has read P[j][*] before it changes
-    // H_j applied to the columns c > j: P[:, c] -= tau v (v^T P[:, c])
+    // H_j applied to the columns c > j: P[:, c] -= tau v w_c, and v stored
     for (int r = j + tid; r < rows; r += blockDim.x) {
-      const double vr = (r == j) ? 1.0 : x[r];
+      const double vr = (r == j) ? 1.0 : scal * x[r];
 #pragma unroll
       for (int c = 0; c < kBigNB; ++c)
         if (c > j && c < nb) P[r + (size_t)c * rows] = fma(-tj * acc[c], vr, P[r + (size_t)c * rows]);
+      x[r] = (r == j) ? beta : vr;
     }
-    if (tid < kBigNB) {   // V^T v_j (columns < j) to shared memory for the T recurrence
-      double v = 0.0;
-#pragma unroll
-      for (int c = 0; c < kBigNB; ++c)
-        if (c == tid) v = acc[c];
-      yv[tid] = v;
-    }
-    __syncthreads();
-    if (tid < j) {   // T[0:j, j] = -tau_j T[0:j, 0:j] (V^T v_j)  (dlarft, forward columnwise)
-      double sv = 0.0;
-      for (int k = tid; k < j; ++k) sv = fma(T[tid + k * kBigNB], yv[k], sv);
-      T[tid + j * kBigNB] = -tj * sv;
-    }
+    if (tid == j) T[j + j * kBigNB] = tj;
     if (tid == 0) {
-      x[j] = beta;
       tau[j] = tj;
-      T[j + j * kBigNB] = tj;
+      a.tau[b * a.stau + j] = tj;
     }
     __syncthreads();
   }
@@ -355,19 +410,25 @@ __global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
 #pragma unroll
       for (int k = 0; k < kBigNB; ++k)
         if (k >= c && k < nb) sv = fma(vr[k], T[c + k * kBigNB], sv);
-      U[r + (int64_t)c * a.ldv] = sv;
+      U[r + (int64_t)c * a.ldu] = sv;
     }
   }
 }
 
 size_t panel_smem(int rows) {
-  return sizeof(double) * ((size_t)kBigNB * rows + (kPanelThreads / 32) * kBigNB + kBigNB * kBigNB + 2 * kBigNB);
+  return sizeof(double) * ((size_t)kBigNB * rows + (kPanelThreads / 32 + 2) * 17 + kBigNB * kBigNB + 2 * kBigNB);
 }
 
 cudaError_t qr_panel(const Panel &a, int64_t batch, cudaStream_t s) {
   const size_t sm = panel_smem(a.m - a.j0);
   cudaError_t e = set_smem_attr((const void *)big_qr_panel_kernel, (int)panel_smem(kBigMaxRows));
   if (e != cudaSuccess) return e;
+  static bool carve = false;   // (a preference only: harmless to repeat on another device)
+  if (!carve) {
+    cudaFuncSetAttribute((const void *)big_qr_panel_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   big_qr_panel_kernel<<<(unsigned)batch, kPanelThreads, sm, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
@@ -663,36 +724,108 @@ cudaError_t sym_store(const double *A, int64_t sA, int lda, double *dst, int64_t
 }
 
 // ---------------------------------------------------- blocked Householder ---
+// T of a block reflector of nb <= 64 columns from G = V^T V and tau (dlarft,
+// forward columnwise): T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j], T[j][j] = tau_j.
+__global__ void __launch_bounds__(64) big_larft_kernel(const double *G, double *T, int64_t sGT, const double *tau,
+                                                       int64_t stau, int nb) {
+  // one array: T in the strict upper triangle, tau on the diagonal, G's
+  // strict upper triangle stored transposed in the strict lower one
+  __shared__ double Ts[64][65], taus[64];
+  const int64_t b = blockIdx.x;
+  const double *Gb = G + b * sGT;
+  const int i = threadIdx.x;
+  for (int e = i; e < nb * nb; e += blockDim.x) {
+    const int c = e / nb, r = e - c * nb;
+    if (r < c) Ts[c][r] = Gb[r + (int64_t)c * kBigBlk];   // G[r][c] -> Ts[c][r]
+  }
+  if (i < nb) taus[i] = tau[b * stau + i];
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double tj = taus[j];
+    if (i < j) {
+      double sv = 0.0;
+      for (int k = i; k < j; ++k) sv = fma(Ts[i][k], Ts[j][k], sv);   // T[i][k] G[k][j]
+      Ts[i][j] = -tj * sv;
+    }
+    if (i == j) Ts[j][j] = tj;
+    __syncthreads();
+  }
+  double *Tb = T + b * sGT;
+  for (int e = i; e < kBigBlk * kBigBlk; e += blockDim.x) {
+    const int c = e / kBigBlk, r = e - c * kBigBlk;
+    Tb[e] = (r <= c && c < nb) ? Ts[r][c] : 0.0;
+  }
+}
+
 // In place QR of the first ncols_fac columns of every item's S (m x ncols,
 // ld lds), Q^T applied to all the item's remaining columns (the stage's RHS
-// blocks): per 16-column panel, big_qr_panel then W = V^T C, C -= U W.
+// blocks).  Blocks of 64 columns: four 16-column big_qr_panel calls, each
+// followed by its update of the block's remaining columns (W = V16^T C,
+// C -= U16 W), then the block reflector I - V T V^T of all 64 (T from
+// G = V^T V, big_larft) updates the trailing columns with two big GEMMs,
+// W = V^T C and C -= (V T^T) W: one read and one read-write of the trailing
+// matrix per 64 columns instead of per 16.
 cudaError_t qr_apply(double *S, int64_t sS, int lds, int m, int ncols_fac, int ncols, int64_t batch,
                      const Work &w, cudaStream_t s) {
   const int kmax = ncols_fac < m ? ncols_fac : m;
-  for (int j0 = 0; j0 < kmax; j0 += kBigNB) {
-    const int nb = (kmax - j0 < kBigNB) ? kmax - j0 : kBigNB;
-    Panel p;
-    p.S = S; p.sS = sS; p.lds = lds; p.m = m; p.j0 = j0; p.nb = nb;
-    p.V = w.V; p.U = w.U; p.sVU = w.sVU; p.ldv = w.ldv;
-    cudaError_t e = qr_panel(p, batch, s);
-    if (e != cudaSuccess) return e;
-    const int nc = ncols - (j0 + nb), rows = m - j0;
+  cudaError_t e;
+  for (int J0 = 0; J0 < kmax; J0 += kBigBlk) {
+    const int nbB = (kmax - J0 < kBigBlk) ? kmax - J0 : kBigBlk, rowsB = m - J0;
+    // the block's V (rows m - J0, zero above each panel's diagonal)
+    if ((e = cudaMemset2DAsync(w.V, (size_t)w.sVU * 8, 0, (size_t)w.ldv * nbB * 8, (size_t)batch, s)) != cudaSuccess)
+      return e;
+    for (int sub = 0; sub < nbB; sub += kBigNB) {
+      const int j0 = J0 + sub, nb = (nbB - sub < kBigNB) ? nbB - sub : kBigNB;
+      Panel p;
+      p.S = S; p.sS = sS; p.lds = lds; p.m = m; p.j0 = j0; p.nb = nb;
+      p.V = w.V + sub + (int64_t)sub * w.ldv; p.sV = w.sVU; p.ldv = w.ldv;   // rows from j0 = row sub of the block
+      p.U = w.U16; p.sU = w.sU16; p.ldu = w.ldv;
+      p.tau = w.tau + sub; p.stau = w.stau;
+      if ((e = qr_panel(p, batch, s)) != cudaSuccess) return e;
+      const int nin = nbB - sub - nb, rows = m - j0;
+      if (nin <= 0) continue;
+      double *C = S + j0 + (int64_t)(j0 + nb) * lds;   // the block's later columns
+      Gemm g1;   // W = V16^T C
+      g1.batch = batch; g1.M = nb; g1.N = nin; g1.K = rows; g1.alpha = 1.0; g1.beta = 0.0;
+      g1.A = p.V; g1.lda = w.ldv; g1.sA = w.sVU;
+      g1.B = C; g1.ldb = lds; g1.sB = sS;
+      g1.C = w.W; g1.ldc = kBigBlk; g1.sC = w.sW;
+      if ((e = gemm(g1, true, false, s)) != cudaSuccess) return e;
+      Gemm g2;   // C -= U16 W
+      g2.batch = batch; g2.M = rows; g2.N = nin; g2.K = nb; g2.alpha = -1.0; g2.beta = 1.0;
+      g2.A = w.U16; g2.lda = w.ldv; g2.sA = w.sU16;
+      g2.B = w.W; g2.ldb = kBigBlk; g2.sB = w.sW;
+      g2.C = C; g2.ldc = lds; g2.sC = sS;
+      if ((e = gemm(g2, false, false, s)) != cudaSuccess) return e;
+    }
+    const int nc = ncols - (J0 + nbB);
     if (nc <= 0) continue;
-    double *C = S + j0 + (int64_t)(j0 + nb) * lds;
-    Gemm g1;   // W = V^T C  (nb x nc)
-    g1.batch = batch; g1.M = nb; g1.N = nc; g1.K = rows; g1.alpha = 1.0; g1.beta = 0.0;
+    // the block reflector: G = V^T V, T (dlarft), U = V T^T
+    Gemm gg;
+    gg.batch = batch; gg.M = nbB; gg.N = nbB; gg.K = rowsB; gg.A = w.V; gg.lda = w.ldv; gg.sA = w.sVU;
+    gg.B = w.V; gg.ldb = w.ldv; gg.sB = w.sVU; gg.C = w.G; gg.ldc = kBigBlk; gg.sC = w.sGT;
+    if ((e = gemm(gg, true, false, s)) != cudaSuccess) return e;
+    big_larft_kernel<<<(unsigned)batch, 64, 0, s>>>(w.G, w.T, w.sGT, w.tau, w.stau, nbB);
+    ++g_launches;
+    Gemm gu;
+    gu.batch = batch; gu.M = rowsB; gu.N = nbB; gu.K = nbB; gu.A = w.V; gu.lda = w.ldv; gu.sA = w.sVU;
+    gu.B = w.T; gu.ldb = kBigBlk; gu.sB = w.sGT; gu.C = w.U; gu.ldc = w.ldv; gu.sC = w.sVU;
+    if ((e = gemm(gu, false, true, s)) != cudaSuccess) return e;
+    double *C = S + J0 + (int64_t)(J0 + nbB) * lds;
+    Gemm g1;   // W = V^T C  (nbB x nc)
+    g1.batch = batch; g1.M = nbB; g1.N = nc; g1.K = rowsB; g1.alpha = 1.0; g1.beta = 0.0;
     g1.A = w.V; g1.lda = w.ldv; g1.sA = w.sVU;
     g1.B = C; g1.ldb = lds; g1.sB = sS;
-    g1.C = w.W; g1.ldc = kBigNB; g1.sC = w.sW;
+    g1.C = w.W; g1.ldc = kBigBlk; g1.sC = w.sW;
     if ((e = gemm(g1, true, false, s)) != cudaSuccess) return e;
     Gemm g2;   // C -= U W
-    g2.batch = batch; g2.M = rows; g2.N = nc; g2.K = nb; g2.alpha = -1.0; g2.beta = 1.0;
+    g2.batch = batch; g2.M = rowsB; g2.N = nc; g2.K = nbB; g2.alpha = -1.0; g2.beta = 1.0;
     g2.A = w.U; g2.lda = w.ldv; g2.sA = w.sVU;
-    g2.B = w.W; g2.ldb = kBigNB; g2.sB = w.sW;
+    g2.B = w.W; g2.ldb = kBigBlk; g2.sB = w.sW;
     g2.C = C; g2.ldc = lds; g2.sC = sS;
     if ((e = gemm(g2, false, false, s)) != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  return cudaGetLastError();
 }
 
 }  // namespace big
@@ -767,8 +900,8 @@ void scratch_sizes(const Plan &p, int64_t &s1, int64_t &s2, int64_t &s3, int64_t
   int64_t rows = rows1(n, r);
   if (2 * n > rows) rows = 2 * n;
   if (rows3(n, r, true) > rows) rows = rows3(n, r, true);
-  vu = rows * kBigNB;
-  w = kBigNB * (3 * n + 1);
+  vu = rows * kBigBlk;
+  w = kBigBlk * (3 * n + 1);
 }
 int64_t max_stack_rows(int n, int RC) {
   const int r = RC > n ? RC : n;
@@ -972,7 +1105,8 @@ cudaError_t factor(const Plan &p, cudaStream_t s) {
     if ((e = qr_apply(p.S1, s1, ld1, ld1, n, 2 * n + 1, P, p.w, s)) != cudaSuccess) return e;
     if (odd) {
       Work w1 = p.w;
-      w1.V += P * p.w.sVU; w1.U += P * p.w.sVU; w1.W += P * p.w.sW;
+      w1.V += P * p.w.sVU; w1.U += P * p.w.sVU; w1.U16 += P * p.w.sU16; w1.W += P * p.w.sW;
+      w1.G += P * p.w.sGT; w1.T += P * p.w.sGT; w1.tau += P * p.w.stau;
       // [C_t | y_t] sits in columns 0..n of item P (ld ld1): factor its r rows, apply to column n
       if ((e = qr_apply(p.S1 + P * s1, s1, ld1, rb, n, n + 1, 1, w1, s)) != cudaSuccess) return e;
     }
@@ -1014,13 +1148,29 @@ cudaError_t factor(const Plan &p, cudaStream_t s) {
     Lc.add(cd(p.S1 + (int64_t)2 * n * ld1, 0, ld1, p.S2 + (int64_t)3 * n * ld2, 0, ld2, n, 1, 1));
     Lc.add(cd(nullptr, 0, 1, p.S2 + (int64_t)3 * n * ld2 + n, 0, ld2, n, 1, 1));
     if ((e = run(Lc, s)) != cudaSuccess) return e;
-    if (P - 1 + (odd ? 1 : 0) > 0)
-      if ((e = qr_apply(p.S2 + s2, s2, ld2, ld2, n, 3 * n + 1, P - 1 + (odd ? 1 : 0), p.w, s)) != cudaSuccess)
-        return e;
+    // Stages 2 and 3 are independent once stage 1 is done, except
+    // that an odd level's stage 3 takes the last column's stage-2 Z rows: on
+    // even levels stage 3 runs on the second stream (its own QR scratch)
+    // concurrently with stage 2 and the records.
+    const bool conc = !odd && p.s2 != nullptr;
+    auto stage2 = [&]() -> cudaError_t {
+      if (P - 1 + (odd ? 1 : 0) > 0)
+        return qr_apply(p.S2 + s2, s2, ld2, ld2, n, 3 * n + 1, P - 1 + (odd ? 1 : 0), p.w, s);
+      return cudaSuccess;
+    };
+    if (!conc && (e = stage2()) != cudaSuccess) return e;
+    cudaStream_t s3s = s;
+    const Work *w3 = &p.w;
+    if (conc) {
+      if ((e = cudaEventRecord(p.ev[0], s)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(p.s2, p.ev[0], 0)) != cudaSuccess) return e;
+      s3s = p.s2;
+      w3 = &p.w2;
+    }
     // ---- stage 3 (survivors u = 2p + 1): [D~_u; C_u (; Z_{K-1}) | y~; y_u (; z^)] ----
     if (ld3 > 2 * r) {   // Z rows (odd level) / zero padding up to n rows
       Lc.add(cd(nullptr, 0, 1, p.S3 + 2 * r, s3, ld3, ld3 - 2 * r, n + 1, P));
-      if ((e = run(Lc, s)) != cudaSuccess) return e;
+      if ((e = run(Lc, s3s)) != cudaSuccess) return e;
     }
     Lc.add(cd(p.S1 + (int64_t)n * ld1 + n, s1, ld1, p.S3, s3, ld3, r, n, P));
     Lc.add(cd(p.S1 + (int64_t)2 * n * ld1 + n, s1, ld1, p.S3 + (int64_t)n * ld3, s3, ld3, r, 1, P));
@@ -1031,8 +1181,17 @@ cudaError_t factor(const Plan &p, cudaStream_t s) {
       Lc.add(cd(p.S2 + P * s2 + (int64_t)3 * n * ld2 + n, 0, ld2, p.S3 + (P - 1) * s3 + (int64_t)n * ld3 + 2 * r, 0,
                 ld3, n, 1, 1));
     }
-    if ((e = run(Lc, s)) != cudaSuccess) return e;
-    if ((e = qr_apply(p.S3, s3, ld3, ld3, n, n + 1, P, p.w, s)) != cudaSuccess) return e;
+    if ((e = run(Lc, s3s)) != cudaSuccess) return e;
+    if ((e = qr_apply(p.S3, s3, ld3, ld3, n, n + 1, P, *w3, s3s)) != cudaSuccess) return e;
+    if (conc) {
+      if ((e = cudaEventRecord(p.ev[1], p.s2)) != cudaSuccess) return e;
+      if ((e = stage2()) != cudaSuccess) return e;
+      // ---- records of the eliminated columns (stage 2's R rows), beside stage 3 ----
+      if ((e = post(p, L, c.nrm, 2 * c.snrm, P + (odd ? 1 : 0), p.rec[L], ((int64_t)1 << L) - 1,
+                    (int64_t)2 << L, s)) != cudaSuccess)
+        return e;
+      if ((e = cudaStreamWaitEvent(s, p.ev[1], 0)) != cudaSuccess) return e;
+    }
     // ---- level L+1 entries (column p = survivor 2p + 1) ----
     double *nx = p.ent[L + 1];
     Lc.add(cd(p.S3, s3, ld3, nx, E, n, n, n, P, 1.0, 0, 1));                                  // C'
@@ -1043,8 +1202,8 @@ cudaError_t factor(const Plan &p, cudaStream_t s) {
     Lc.add(cd(c.nrm + c.snrm, 2 * c.snrm, 1, nx + 3 * nn + 2 * n, E, 1, 1, 1, P));            // |column|^2
     if ((e = run(Lc, s)) != cudaSuccess) return e;
     // ---- records of the eliminated columns t = 2p (and K - 1) ----
-    if ((e = post(p, L, c.nrm, 2 * c.snrm, P + (odd ? 1 : 0), p.rec[L], ((int64_t)1 << L) - 1,
-                  (int64_t)2 << L, s)) != cudaSuccess)
+    if (!conc && (e = post(p, L, c.nrm, 2 * c.snrm, P + (odd ? 1 : 0), p.rec[L], ((int64_t)1 << L) - 1,
+                           (int64_t)2 << L, s)) != cudaSuccess)
       return e;
     (void)Rr;
   }

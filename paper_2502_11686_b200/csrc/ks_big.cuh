@@ -47,13 +47,18 @@ struct Panel {
   double *S;
   int64_t sS;
   int lds, m, j0, nb;
-  double *V, *U;
-  int64_t sVU;
-  int ldv;
+  double *V, *U;      // V written at V (explicit, rows x nb), U = V T^T at U
+  int64_t sV, sU;
+  int ldv, ldu;
+  double *tau;        // tau_j at tau[j] (per item stride stau)
+  int64_t stau;
 };
-struct Work {   // per-item QR scratch: V, U (rows x 16), W (16 x cols)
-  double *V, *U, *W;
-  int64_t sVU, sW;
+constexpr int kBigBlk = 64;   // block reflector width of the trailing updates (4 panels)
+// per-item QR scratch: V, U (rows x 64), U16 (rows x 16), W (64 x cols),
+// G = V^T V and T (64 x 64), tau (64)
+struct Work {
+  double *V, *U, *U16, *W, *G, *T, *tau;
+  int64_t sVU, sU16, sW, sGT, stau;
   int ldv;
 };
 cudaError_t qr_apply(double *S, int64_t sS, int lds, int m, int ncols_fac, int ncols, int64_t batch,
@@ -102,7 +107,9 @@ struct Plan {
   // stage / backward scratch
   double *S1 = nullptr, *S2 = nullptr, *S3 = nullptr, *Rinv = nullptr, *SII = nullptr, *G = nullptr,
          *Pt = nullptr, *xg = nullptr, *xt = nullptr;
-  Work w{};
+  Work w{}, w2{};           // QR scratch of the main and the second stream
+  cudaStream_t s2 = nullptr;  // second stream (stage 3 beside stage 2), null: serial
+  cudaEvent_t ev[2] = {nullptr, nullptr};
   // outputs
   double *x = nullptr, *S = nullptr;
   unsigned long long *status = nullptr;

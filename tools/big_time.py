@@ -12,12 +12,18 @@ import torch  # noqa: E402
 from paper_2502_11686_b200 import generators as gen  # noqa: E402
 from paper_2502_11686_b200 import ks, model  # noqa: E402
 
-N = int(sys.argv[1]) if len(sys.argv) > 1 else 500
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 500
-p = gen.paper_problem(N, n, seed=0)
+if len(sys.argv) > 1 and sys.argv[1].startswith("c"):   # a BASELINE config on the large-n path
+    p = gen.make(sys.argv[1])
+    N, n = p.N, p.n
+    kw = {"big": True}
+else:
+    N = int(sys.argv[1]) if len(sys.argv) > 1 else 500
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+    p = gen.paper_problem(N, n, seed=0)
+    kw = {}
 st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
-s = ks.Smoother(p, stream=st)
+s = ks.Smoother(p, stream=st, **kw)
 s.run(); s.check()
 s.set_timing(True)
 l0 = s.info()["launches"]
@@ -37,7 +43,7 @@ e1.record(st)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 3
 s.check()
-sb, sf = model.step_totals(N, n, n, {"C": 0, "E": 0})
+sb, sf = model.step_totals(N, n, p.m_max, {"C": int(p.H.shape[0] > 1), "E": int(p.F.shape[0] > 1)})
 print(json.dumps({"N": N, "n": n, "ms_per_step": ms, "steps_per_s": N / ms * 1e3, "launches": nl,
                   "phases_ms": {k: v[0] for k, v in tm.items()}, "algorithmic_flops": sf,
                   "tflops": sf / ms / 1e9, "fp64_frac": sf / ms / 1e9 / 37.0}))
