@@ -1,4 +1,4 @@
-"""Two real processes, one rank each, on the single leased GPU.
+"""Real processes, one rank each (2 and 4), on the single leased GPU.
 
 Each process owns its context over a power-of-two shard of the steps
 (ks_dist_create with no communicator) and runs its local levels; the
@@ -59,13 +59,13 @@ def _rank(rank, world, port, cfg, N, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg,N", [("c5", 1 << 14), ("c2", 1 << 12), ("c3", 1 << 11)])
-def test_two_processes_gloo_staged_exchange(cfg, N):
+@pytest.mark.parametrize("cfg,N,world", [("c5", 1 << 14, 2), ("c2", 1 << 12, 2), ("c3", 1 << 11, 2),
+                                         ("c5", 1 << 15, 4), ("c1", 1 << 10, 4)])
+def test_processes_gloo_staged_exchange(cfg, N, world):
     import oracle
     from paper_2502_11686_b200 import generators as gen
     from paper_2502_11686_b200 import ks
     from tests.dense import rel_cov_err, rel_state_err
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
