@@ -313,7 +313,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         kd = ks.Dist(rank, P, lo, N, uid=obj[0], device=dev)
         nccl = kd.info()
-        nccl["torch_nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
+        v = torch.cuda.nccl.version()
+        nccl["torch_nccl_version"] = ".".join(map(str, v)) if isinstance(v, (tuple, list)) else str(v)
         print(f"[rank {rank}] ks_dist: NCCL communicator with {nccl['nccl_nranks']} ranks", file=sys.stderr,
               flush=True)
 
