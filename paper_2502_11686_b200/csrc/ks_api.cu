@@ -319,6 +319,9 @@ size_t carve(ks_ctx *c, char *base) {
     for (ks::big::Work *wk : {&b.w, &b.w2}) {   // one QR scratch per stream
       wk->V = w.take<double>(items * vu);
       wk->U = w.take<double>(items * vu);
+      wk->V2 = w.take<double>(items * vu);       // lookahead: the alternate block's V, U
+      wk->U2 = w.take<double>(items * vu);
+      wk->Wt = w.take<double>(items * ww);
       wk->U16 = w.take<double>(items * rows * ks::big::kBigNB);
       wk->W = w.take<double>(items * ww);
       wk->G = w.take<double>(items * ks::big::kBigBlk * ks::big::kBigBlk);
@@ -892,6 +895,15 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
       cudaGetLastError();
       b.s2 = nullptr;
     }
+    // the QRs' lookahead side streams (one per QR stream), unless KS_NO_LOOKAHEAD
+    if (!std::getenv("KS_NO_LOOKAHEAD"))
+      for (ks::big::Work *wk : {&b.w, &b.w2})
+        if (cudaStreamCreateWithFlags(&wk->side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&wk->evf, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&wk->evj, cudaEventDisableTiming) != cudaSuccess) {
+          cudaGetLastError();
+          wk->side = nullptr;
+        }
   }
   *out = c;
   return KS_OK;
@@ -1234,6 +1246,11 @@ void ks_destroy(ks_ctx *c) {
     if (c->bp.s2) cudaStreamDestroy(c->bp.s2);
     for (cudaEvent_t e : c->bp.ev)
       if (e) cudaEventDestroy(e);
+    for (ks::big::Work *wk : {&c->bp.w, &c->bp.w2}) {
+      if (wk->side) cudaStreamDestroy(wk->side);
+      if (wk->evf) cudaEventDestroy(wk->evf);
+      if (wk->evj) cudaEventDestroy(wk->evj);
+    }
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   delete c;

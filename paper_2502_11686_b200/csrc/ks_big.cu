@@ -26,6 +26,7 @@
 
 #include <cstdint>
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 
 #include "ks_internal.cuh"
@@ -109,6 +110,19 @@ __global__ void __launch_bounds__(256) big_gemm_kernel(Gemm g, int kchunk) {
   const int nk = (ke - kb + BK - 1) / BK;
   if (nk <= 0) return;
   load(0, kb);
+  // beta != 0: the old C tile into registers now, so that its loads overlap
+  // the k loop instead of serialising the epilogue (K is often just 16-64)
+  double cold[FM][FN][2];
+  const bool useb = !SPLITK && g.beta != 0.0;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wm + 8 * i + gq, n = n0 + wn + 8 * j + 2 * q + h;
+        cold[i][j][h] = (useb && m < g.M && n < g.N) ? C[m + (int64_t)n * g.ldc] : 0.0;
+      }
   for (int kt = 0; kt < nk; ++kt) {
     const int st = kt & 1;
     if (kt + 1 < nk) {
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(256) big_gemm_kernel(Gemm g, int kchunk) {
         if (n >= g.N) continue;
         double *c = C + m + (int64_t)n * g.ldc;
         if (SPLITK) atomicAdd(c, g.alpha * acc[i][j][h]);
-        else *c = (g.beta == 0.0) ? g.alpha * acc[i][j][h] : fma(g.alpha, acc[i][j][h], g.beta * *c);
+        else *c = useb ? fma(g.alpha, acc[i][j][h], g.beta * cold[i][j][h]) : g.alpha * acc[i][j][h];
       }
     }
 }
@@ -415,11 +429,167 @@ __global__ void __launch_bounds__(kPanelThreads) big_qr_panel_kernel(Panel a) {
   }
 }
 
+// The panel held in REGISTERS: thread t owns rows t, t + 256, ... (MR of
+// them) of all 16 columns, so the per-column passes are register FMAs (no
+// shared-memory traffic, no address arithmetic) and only the reduction, the
+// pivot row and T go through shared memory.  Same arithmetic as above, one
+// pass and one reduction per column; columns unrolled (every register index
+// is a compile-time constant).
+constexpr int kRegPanelThreads = 256;
+__device__ __forceinline__ void block_sums17r(double (&acc)[17], double *red) {
+  constexpr int NW = kRegPanelThreads / 32;
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc[16] += __shfl_xor_sync(full, acc[16], o);
+#pragma unroll
+  for (int h = 8, bit = 16; h >= 1; h >>= 1, bit >>= 1) {
+    const bool up = (lane & bit) != 0;
+#pragma unroll
+    for (int v = 0; v < h; ++v) {
+      const double send = up ? acc[v] : acc[v + h];
+      const double keep = up ? acc[v + h] : acc[v];
+      acc[v] = keep + __shfl_xor_sync(full, send, bit);
+    }
+  }
+  acc[0] += __shfl_xor_sync(full, acc[0], 1);
+  const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  if ((lane & 1) == 0) red[warp * 17 + idx] = acc[0];
+  if (lane == 1) red[warp * 17 + 16] = acc[16];
+  __syncthreads();
+  if (threadIdx.x < 17) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += red[w * 17 + threadIdx.x];
+    red[NW * 17 + threadIdx.x] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < 17; ++v) acc[v] = red[NW * 17 + v];
+}
+
+template <int MR>
+__global__ void __launch_bounds__(kRegPanelThreads, 1) big_qr_panel_reg_kernel(Panel a) {
+  constexpr int NB = kBigNB, TH = kRegPanelThreads, NW = TH / 32;
+  __shared__ double red[(NW + 1) * 17];
+  __shared__ double rowj[2][NB];       // the pivot row, double-buffered by column parity
+  __shared__ double T[NB * NB];
+  const int64_t b = blockIdx.x;
+  double *S = a.S + b * a.sS;
+  double *V = a.V + b * a.sV, *U = a.U + b * a.sU;
+  const int rows = a.m - a.j0, nb = a.nb, tid = threadIdx.x;
+  double p[MR][NB];
+#pragma unroll
+  for (int r = 0; r < MR; ++r) {
+    const int ri = tid + TH * r;
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+      p[r][c] = (ri < rows && c < nb) ? S[(a.j0 + ri) + (int64_t)(a.j0 + c) * a.lds] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    if (j >= nb) break;
+    double acc[17];
+#pragma unroll
+    for (int c = 0; c < 17; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int ri = tid + TH * r;
+      if (ri > j && ri < rows) {
+        const double xr = p[r][j];
+        acc[16] = fma(xr, xr, acc[16]);
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c != j) acc[c] = fma(xr, p[r][c], acc[c]);
+      }
+      if (ri == j)   // the pivot row's owner publishes it (read after the reduction's barriers)
+#pragma unroll
+        for (int c = 0; c < NB; ++c) rowj[j & 1][c] = p[r][c];
+    }
+    block_sums17r(acc, red);
+    const double alpha = rowj[j & 1][j], sigma = acc[16];
+    double tj = 0.0, beta = alpha, scal = 0.0;
+    if (sigma > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, sigma)), alpha);
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    // w_c = v^T P[:, c] (c > j), (V^T v_j)_c (c < j)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = fma(scal, acc[c], rowj[j & 1][c]);
+    if (tid < j) {   // T[0:j, j] = -tau_j T[0:j, 0:j] (V^T v_j)  (dlarft); row tid of T is this thread's
+      double sv = 0.0;
+#pragma unroll
+      for (int k = 0; k < NB; ++k)
+        if (k >= tid && k < j) sv = fma(T[tid + k * NB], acc[k], sv);
+      T[tid + j * NB] = -tj * sv;
+    }
+    if (tid == j) T[j + j * NB] = tj;
+    if (tid == 0) a.tau[b * a.stau + j] = tj;
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int ri = tid + TH * r;
+      if (ri >= j && ri < rows) {
+        const double vr = (ri == j) ? 1.0 : scal * p[r][j];
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c > j) p[r][c] = fma(-tj * acc[c], vr, p[r][c]);
+        p[r][j] = (ri == j) ? beta : vr;
+      }
+    }
+  }
+  __syncthreads();   // T complete
+  // write back: R (upper part, zeros below), V (explicit), U = V T^T
+#pragma unroll
+  for (int r = 0; r < MR; ++r) {
+    const int ri = tid + TH * r;
+    if (ri >= rows) continue;
+    double vr[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      const double pv = p[r][c];
+      vr[c] = (c < nb) ? ((ri < c) ? 0.0 : (ri == c ? 1.0 : pv)) : 0.0;
+      if (c < nb) {
+        S[(a.j0 + ri) + (int64_t)(a.j0 + c) * a.lds] = (ri <= c) ? pv : 0.0;
+        V[ri + (int64_t)c * a.ldv] = vr[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      if (c >= nb) break;
+      double sv = 0.0;   // (V T^T)[ri][c] = sum_{k >= c} V[ri][k] T[c][k]
+#pragma unroll
+      for (int k = 0; k < NB; ++k)
+        if (k >= c && k < nb) sv = fma(vr[k], T[c + k * NB], sv);
+      U[ri + (int64_t)c * a.ldu] = sv;
+    }
+  }
+}
+
+template <int MR>
+cudaError_t qr_panel_reg(const Panel &a, int64_t batch, cudaStream_t s) {
+  big_qr_panel_reg_kernel<MR><<<(unsigned)batch, kRegPanelThreads, 0, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 size_t panel_smem(int rows) {
   return sizeof(double) * ((size_t)kBigNB * rows + (kPanelThreads / 32 + 2) * 17 + kBigNB * kBigNB + 2 * kBigNB);
 }
 
 cudaError_t qr_panel(const Panel &a, int64_t batch, cudaStream_t s) {
+  const int rows = a.m - a.j0, mr = (rows + kRegPanelThreads - 1) / kRegPanelThreads;
+  if (!std::getenv("KS_SMEM_PANEL")) {   // the register-resident panel (default)
+    switch (mr) {
+      case 0: case 1: return qr_panel_reg<1>(a, batch, s);
+      case 2: return qr_panel_reg<2>(a, batch, s);
+      case 3: return qr_panel_reg<3>(a, batch, s);
+      case 4: return qr_panel_reg<4>(a, batch, s);
+      case 5: return qr_panel_reg<5>(a, batch, s);
+      case 6: return qr_panel_reg<6>(a, batch, s);
+      default: break;   // taller panels: the shared-memory kernel
+    }
+  }
   const size_t sm = panel_smem(a.m - a.j0);
   cudaError_t e = set_smem_attr((const void *)big_qr_panel_kernel, (int)panel_smem(kBigMaxRows));
   if (e != cudaSuccess) return e;
@@ -726,20 +896,23 @@ cudaError_t sym_store(const double *A, int64_t sA, int lda, double *dst, int64_t
 // ---------------------------------------------------- blocked Householder ---
 // T of a block reflector of nb <= 64 columns from G = V^T V and tau (dlarft,
 // forward columnwise): T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j], T[j][j] = tau_j.
-__global__ void __launch_bounds__(64) big_larft_kernel(const double *G, double *T, int64_t sGT, const double *tau,
-                                                       int64_t stau, int nb) {
+__global__ void __launch_bounds__(256) big_larft_kernel(const double *G, double *T, int64_t sGT, const double *tau,
+                                                        int64_t stau, int nb) {
   // one array: T in the strict upper triangle, tau on the diagonal, G's
   // strict upper triangle stored transposed in the strict lower one
   __shared__ double Ts[64][65], taus[64];
   const int64_t b = blockIdx.x;
   const double *Gb = G + b * sGT;
   const int i = threadIdx.x;
+  // (256 threads stage G: 16 independent loads each, all in flight)
+#pragma unroll 4
   for (int e = i; e < nb * nb; e += blockDim.x) {
     const int c = e / nb, r = e - c * nb;
-    if (r < c) Ts[c][r] = Gb[r + (int64_t)c * kBigBlk];   // G[r][c] -> Ts[c][r]
+    if (r < c) Ts[c][r] = __ldg(Gb + r + (int64_t)c * kBigBlk);   // G[r][c] -> Ts[c][r]
   }
   if (i < nb) taus[i] = tau[b * stau + i];
   __syncthreads();
+  if (i >= 64) return;   // the recurrence: one thread per row of T
   for (int j = 0; j < nb; ++j) {
     const double tj = taus[j];
     if (i < j) {
@@ -748,10 +921,10 @@ __global__ void __launch_bounds__(64) big_larft_kernel(const double *G, double *
       Ts[i][j] = -tj * sv;
     }
     if (i == j) Ts[j][j] = tj;
-    __syncthreads();
+    asm volatile("bar.sync 1, 64;" ::: "memory");   // the 64 recurrence threads only
   }
   double *Tb = T + b * sGT;
-  for (int e = i; e < kBigBlk * kBigBlk; e += blockDim.x) {
+  for (int e = i; e < kBigBlk * kBigBlk; e += 64) {
     const int c = e / kBigBlk, r = e - c * kBigBlk;
     Tb[e] = (r <= c && c < nb) ? Ts[r][c] : 0.0;
   }
@@ -765,20 +938,29 @@ __global__ void __launch_bounds__(64) big_larft_kernel(const double *G, double *
 // G = V^T V, big_larft) updates the trailing columns with two big GEMMs,
 // W = V^T C and C -= (V T^T) W: one read and one read-write of the trailing
 // matrix per 64 columns instead of per 16.
+// Lookahead (w.side): the block reflector first updates only the NEXT
+// block's 64 columns on the calling stream, which then goes on to factor
+// that block, while the rest of the trailing update runs on the side stream
+// (own W, the block's V / U kept in the alternate buffers) -- the sequential
+// panels and the bandwidth-bound trailing GEMMs overlap.  The calling stream
+// joins the side stream before the next block's own reflector touches the
+// trailing columns.
 cudaError_t qr_apply(double *S, int64_t sS, int lds, int m, int ncols_fac, int ncols, int64_t batch,
                      const Work &w, cudaStream_t s) {
   const int kmax = ncols_fac < m ? ncols_fac : m;
   cudaError_t e;
-  for (int J0 = 0; J0 < kmax; J0 += kBigBlk) {
+  bool pending = false;   // a side-stream trailing update not yet joined
+  for (int J0 = 0, blk = 0; J0 < kmax; J0 += kBigBlk, ++blk) {
     const int nbB = (kmax - J0 < kBigBlk) ? kmax - J0 : kBigBlk, rowsB = m - J0;
+    double *V = (w.side && (blk & 1)) ? w.V2 : w.V, *U = (w.side && (blk & 1)) ? w.U2 : w.U;
     // the block's V (rows m - J0, zero above each panel's diagonal)
-    if ((e = cudaMemset2DAsync(w.V, (size_t)w.sVU * 8, 0, (size_t)w.ldv * nbB * 8, (size_t)batch, s)) != cudaSuccess)
+    if ((e = cudaMemset2DAsync(V, (size_t)w.sVU * 8, 0, (size_t)w.ldv * nbB * 8, (size_t)batch, s)) != cudaSuccess)
       return e;
     for (int sub = 0; sub < nbB; sub += kBigNB) {
       const int j0 = J0 + sub, nb = (nbB - sub < kBigNB) ? nbB - sub : kBigNB;
       Panel p;
       p.S = S; p.sS = sS; p.lds = lds; p.m = m; p.j0 = j0; p.nb = nb;
-      p.V = w.V + sub + (int64_t)sub * w.ldv; p.sV = w.sVU; p.ldv = w.ldv;   // rows from j0 = row sub of the block
+      p.V = V + sub + (int64_t)sub * w.ldv; p.sV = w.sVU; p.ldv = w.ldv;   // rows from j0 = row sub of the block
       p.U = w.U16; p.sU = w.sU16; p.ldu = w.ldv;
       p.tau = w.tau + sub; p.stau = w.stau;
       if ((e = qr_panel(p, batch, s)) != cudaSuccess) return e;
@@ -798,33 +980,56 @@ cudaError_t qr_apply(double *S, int64_t sS, int lds, int m, int ncols_fac, int n
       g2.C = C; g2.ldc = lds; g2.sC = sS;
       if ((e = gemm(g2, false, false, s)) != cudaSuccess) return e;
     }
+    // the previous block's trailing update (side stream) must be done before
+    // this block's reflector updates the trailing columns
+    if (pending) {
+      if ((e = cudaStreamWaitEvent(s, w.evj, 0)) != cudaSuccess) return e;
+      pending = false;
+    }
     const int nc = ncols - (J0 + nbB);
     if (nc <= 0) continue;
     // the block reflector: G = V^T V, T (dlarft), U = V T^T
     Gemm gg;
-    gg.batch = batch; gg.M = nbB; gg.N = nbB; gg.K = rowsB; gg.A = w.V; gg.lda = w.ldv; gg.sA = w.sVU;
-    gg.B = w.V; gg.ldb = w.ldv; gg.sB = w.sVU; gg.C = w.G; gg.ldc = kBigBlk; gg.sC = w.sGT;
+    gg.batch = batch; gg.M = nbB; gg.N = nbB; gg.K = rowsB; gg.A = V; gg.lda = w.ldv; gg.sA = w.sVU;
+    gg.B = V; gg.ldb = w.ldv; gg.sB = w.sVU; gg.C = w.G; gg.ldc = kBigBlk; gg.sC = w.sGT;
     if ((e = gemm(gg, true, false, s)) != cudaSuccess) return e;
-    big_larft_kernel<<<(unsigned)batch, 64, 0, s>>>(w.G, w.T, w.sGT, w.tau, w.stau, nbB);
+    big_larft_kernel<<<(unsigned)batch, 256, 0, s>>>(w.G, w.T, w.sGT, w.tau, w.stau, nbB);
     ++g_launches;
     Gemm gu;
-    gu.batch = batch; gu.M = rowsB; gu.N = nbB; gu.K = nbB; gu.A = w.V; gu.lda = w.ldv; gu.sA = w.sVU;
-    gu.B = w.T; gu.ldb = kBigBlk; gu.sB = w.sGT; gu.C = w.U; gu.ldc = w.ldv; gu.sC = w.sVU;
+    gu.batch = batch; gu.M = rowsB; gu.N = nbB; gu.K = nbB; gu.A = V; gu.lda = w.ldv; gu.sA = w.sVU;
+    gu.B = w.T; gu.ldb = kBigBlk; gu.sB = w.sGT; gu.C = U; gu.ldc = w.ldv; gu.sC = w.sVU;
     if ((e = gemm(gu, false, true, s)) != cudaSuccess) return e;
-    double *C = S + J0 + (int64_t)(J0 + nbB) * lds;
-    Gemm g1;   // W = V^T C  (nbB x nc)
-    g1.batch = batch; g1.M = nbB; g1.N = nc; g1.K = rowsB; g1.alpha = 1.0; g1.beta = 0.0;
-    g1.A = w.V; g1.lda = w.ldv; g1.sA = w.sVU;
-    g1.B = C; g1.ldb = lds; g1.sB = sS;
-    g1.C = w.W; g1.ldc = kBigBlk; g1.sC = w.sW;
-    if ((e = gemm(g1, true, false, s)) != cudaSuccess) return e;
-    Gemm g2;   // C -= U W
-    g2.batch = batch; g2.M = rowsB; g2.N = nc; g2.K = nbB; g2.alpha = -1.0; g2.beta = 1.0;
-    g2.A = w.U; g2.lda = w.ldv; g2.sA = w.sVU;
-    g2.B = w.W; g2.ldb = kBigBlk; g2.sB = w.sW;
-    g2.C = C; g2.ldc = lds; g2.sC = sS;
-    if ((e = gemm(g2, false, false, s)) != cudaSuccess) return e;
+    // trailing columns [c0, c0 + nc): with lookahead, the next block's
+    // columns (those it will factor) here, the rest on the side stream
+    const int c0 = J0 + nbB;
+    const bool la = w.side && J0 + nbB < kmax && nc > kBigBlk;
+    const int nnow = la ? kBigBlk : nc;
+    auto update = [&](int cb, int cn, double *W, cudaStream_t st) -> cudaError_t {
+      double *C = S + J0 + (int64_t)cb * lds;
+      Gemm g1;   // W = V^T C  (nbB x cn)
+      g1.batch = batch; g1.M = nbB; g1.N = cn; g1.K = rowsB; g1.alpha = 1.0; g1.beta = 0.0;
+      g1.A = V; g1.lda = w.ldv; g1.sA = w.sVU;
+      g1.B = C; g1.ldb = lds; g1.sB = sS;
+      g1.C = W; g1.ldc = kBigBlk; g1.sC = w.sW;
+      cudaError_t ee = gemm(g1, true, false, st);
+      if (ee != cudaSuccess) return ee;
+      Gemm g2;   // C -= U W
+      g2.batch = batch; g2.M = rowsB; g2.N = cn; g2.K = nbB; g2.alpha = -1.0; g2.beta = 1.0;
+      g2.A = U; g2.lda = w.ldv; g2.sA = w.sVU;
+      g2.B = W; g2.ldb = kBigBlk; g2.sB = w.sW;
+      g2.C = C; g2.ldc = lds; g2.sC = sS;
+      return gemm(g2, false, false, st);
+    };
+    if (la) {   // fork: the rest of the trailing update beside the next block's panels
+      if ((e = cudaEventRecord(w.evf, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(w.side, w.evf, 0)) != cudaSuccess) return e;
+      if ((e = update(c0 + nnow, nc - nnow, w.Wt, w.side)) != cudaSuccess) return e;
+      if ((e = cudaEventRecord(w.evj, w.side)) != cudaSuccess) return e;
+      pending = true;
+    }
+    if ((e = update(c0, nnow, w.W, s)) != cudaSuccess) return e;
   }
+  if (pending && (e = cudaStreamWaitEvent(s, w.evj, 0)) != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1107,6 +1312,7 @@ cudaError_t factor(const Plan &p, cudaStream_t s) {
       Work w1 = p.w;
       w1.V += P * p.w.sVU; w1.U += P * p.w.sVU; w1.U16 += P * p.w.sU16; w1.W += P * p.w.sW;
       w1.G += P * p.w.sGT; w1.T += P * p.w.sGT; w1.tau += P * p.w.stau;
+      w1.V2 += P * p.w.sVU; w1.U2 += P * p.w.sVU; w1.Wt += P * p.w.sW;
       // [C_t | y_t] sits in columns 0..n of item P (ld ld1): factor its r rows, apply to column n
       if ((e = qr_apply(p.S1 + P * s1, s1, ld1, rb, n, n + 1, 1, w1, s)) != cudaSuccess) return e;
     }

@@ -60,6 +60,12 @@ struct Work {
   double *V, *U, *U16, *W, *G, *T, *tau;
   int64_t sVU, sU16, sW, sGT, stau;
   int ldv;
+  // lookahead (qr_apply): a second V / U pair (blocks alternate) and W for
+  // the trailing update that runs on `side` while the next block's panels
+  // run on the calling stream; side == null: no lookahead
+  double *V2 = nullptr, *U2 = nullptr, *Wt = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t evf = nullptr, evj = nullptr;
 };
 cudaError_t qr_apply(double *S, int64_t sS, int lds, int m, int ncols_fac, int ncols, int64_t batch,
                      const Work &w, cudaStream_t s);
