@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="profiling runs: no e2e / cpu baseline")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--no-per-config", action="store_true", help="skip the c1-c4 per_config block")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "host"],
+                    help="N > 1: the library's NCCL allgather (default), or -- a validation mode for "
+                         "boxes with fewer GPUs than ranks -- the caller-driven exchange staged through "
+                         "host memory over gloo (ranks may share a GPU; eager, not a multi-GPU number)")
     return ap.parse_args()
 
 
@@ -285,12 +289,17 @@ def main():
     from paper_2502_11686_b200 import ks, model
     from paper_2502_11686_b200 import dist as kdist
     assert torch.cuda.is_available(), "bench needs a GPU (there is no CPU fallback)"
+    host_x = world > 1 and a.exchange == "host"
+    local = local % torch.cuda.device_count() if host_x else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     P = world
     nccl = None
     if P > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if host_x:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     p = gen.make(a.config, N=a.N)
     N = p.N
     lo, hi = kdist.shard_range(N, rank, P)
@@ -305,7 +314,9 @@ def main():
     p64 = ks.peak_fp64_tflops(stream)
 
     kd = None
-    if P > 1:
+    if host_x:   # no communicator: ks_factor stops after the local levels
+        kd = ks.Dist(rank, P, lo, N)
+    elif P > 1:
         # the library's own NCCL communicator (ks_dist_*): rank 0's unique id
         # travels over the torch process group; ks_factor then allgathers the
         # boundary columns itself, on the context's stream
@@ -323,6 +334,13 @@ def main():
     def step(s, get=None):
         s.whiten()
         s.factor()          # P > 1: local levels, NCCL boundary allgather, boundary system
+        if host_x:          # validation mode: the boundary allgather through host memory (gloo)
+            snd, rcv = s.boundary_tensors()
+            sh = snd.cpu()
+            rh = torch.empty(P * sh.numel(), dtype=torch.uint8)
+            kdist.exchange_boundary(sh, rh)
+            rcv.copy_(rh.to(dev))
+            s.factor_boundary()
         s.solve_selinv()
         if get is not None:
             s.get(*get)
@@ -352,7 +370,7 @@ def main():
     # launches, the NCCL allgather included on N > 1), or eagerly with
     # --no-graph; CUDA events on the launching stream, max over ranks
     graph = None
-    if not a.no_graph:
+    if not (a.no_graph or host_x):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             step(sm)
@@ -377,7 +395,7 @@ def main():
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / a.steps
     if P > 1:
-        ms = kdist.max_over_ranks(ms, dev)
+        ms = kdist.max_over_ranks(ms, None if host_x else dev)
     sm.check()
     value = N / (ms / 1e3)
     rl = roofline(launches, M, p.n, p.m_max, strides, p64, a.config if P == 1 and a.N is None else "")
@@ -411,7 +429,7 @@ def main():
         torch.cuda.synchronize()
         mse = e0.elapsed_time(e1) / ke
         if P > 1:
-            mse = kdist.max_over_ranks(mse, dev)
+            mse = kdist.max_over_ranks(mse, None if host_x else dev)
         e2e = {"value": N / (mse / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * P),
                "d2h_bytes_per_step": int(d2h * P), "ms_per_step": mse, "steps": ke,
                "path": "ks_create(KS_HOST_INPUTS) pinned host inputs -> whiten(H2D) .. selinv -> "
@@ -449,6 +467,9 @@ def main():
                 "timing": timing,
                 "gpu_launches": int(n_launch), "clocks": clocks,
                 "phases_ms": fam_ms, "fp64_peak_tflops": p64, "nccl": nccl,
+                "exchange": ("host-staged gloo allgather, ranks sharing %d GPU(s): a validation run of "
+                             "the multi-rank path, not a multi-GPU measurement" % torch.cuda.device_count())
+                if host_x else ("library NCCL allgather" if P > 1 else None),
                 "per_config": cfgs}
         print(json.dumps(line), flush=True)
     if P > 1:

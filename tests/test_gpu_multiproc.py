@@ -111,3 +111,24 @@ def test_library_nccl_communicator_one_rank():
     s2.check()
     assert torch.equal(s1.states, s2.states) and torch.equal(s1.cov, s2.cov)
     del s1, d
+
+
+def test_bench_multi_rank_validation_mode():
+    """bench.py's multi-rank flow (shards, Dist, barriers, max over ranks, e2e,
+    one JSON line from rank 0) with 2 ranks on the one leased GPU: the
+    host-staged exchange stands in for NCCL, which refuses two ranks per GPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--exchange", "host", "--N", str(1 << 16), "--steps", "2", "--warmup", "1",
+           "--no-per-config", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "validation" in d["exchange"]
