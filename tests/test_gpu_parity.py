@@ -247,6 +247,7 @@ def _virtual_shards(p, P, cov=True, generic=False, fused=False):
         s.check()
     x = np.concatenate([s.states.cpu().numpy() for s in parts])
     S = np.concatenate([s.cov.cpu().numpy() for s in parts]) if cov else None
+    _virtual_shards.launches = [s.info()["launches"] for s in parts]
     return x, S
 
 
@@ -576,3 +577,18 @@ def test_big_path_n500():
     """The paper's n = m = 500 size at reduced k (the oracle is plain C,
     about 46 n^3 flops per step)."""
     assert_parity(gen.paper_problem(6, 500, seed=5))
+
+
+@pytest.mark.parametrize("cfg,N,P", [("c5", 1 << 14, 4), ("c5", 1 << 16, 8), ("c2", 1 << 12, 2)])
+def test_sharded_launch_count(cfg, N, P):
+    """A sharded rank runs the single-GPU plan of its N/P steps (fused tail
+    and subtree pass included) plus three launches for the boundary system
+    (re-tiling the gathered entries, its factor tail, its backward tail)."""
+    p = gen.make(cfg, N=N)
+    _virtual_shards(p, P, fused=True)
+    q = gen.make(cfg, N=N // P)
+    s = ks().Smoother(q)
+    s.run()
+    s.check()
+    one = s.info()["launches"]
+    assert all(l == one + 3 for l in _virtual_shards.launches), (one, _virtual_shards.launches)
