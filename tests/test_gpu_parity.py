@@ -592,3 +592,38 @@ def test_sharded_launch_count(cfg, N, P):
     s.check()
     one = s.info()["launches"]
     assert all(l == one + 3 for l in _virtual_shards.launches), (one, _virtual_shards.launches)
+
+
+def test_big_path_chol_and_host_inputs():
+    """The large-n path with Cholesky-factor inputs (KS_COV_IS_CHOL) and with
+    pinned host inputs (KS_HOST_INPUTS, ks_get into host buffers)."""
+    rng = np.random.default_rng(17)
+    p = gen.random_problem(rng, 40, 70, m=70)
+    xo, So = oracle.smooth(p)
+    q = gen.random_problem(np.random.default_rng(17), 40, 70, m=70)
+    q.K = np.linalg.cholesky(q.K)
+    q.L = np.linalg.cholesky(q.L)
+    x, S, _ = gpu_smooth(q, chol=True)
+    assert rel_state_err(x, xo) <= TOL_X and rel_cov_err(S, So) <= TOL_S
+    s = ks().Smoother(p, host_inputs=True, bind_outputs=False)
+    s.run()
+    xs = torch.empty((p.N, p.n), dtype=torch.float64)
+    Ss = torch.empty((p.N, p.n, p.n), dtype=torch.float64)
+    s.get(xs, Ss)
+    s.check()
+    assert rel_state_err(xs.numpy(), xo) <= TOL_X and rel_cov_err(Ss.numpy(), So) <= TOL_S
+
+
+def test_big_path_errors():
+    """Non-SPD covariance and rank deficiency are reported on the large-n path."""
+    rng = np.random.default_rng(18)
+    p = gen.random_problem(rng, 12, 66, m=66)
+    p.K[5] = -np.eye(66)
+    s = ks().Smoother(p)
+    s.run()
+    rc, step, kind = s.sync_status()
+    assert rc == ks().KS_ERR_NOT_SPD and step == 5 and kind == 1
+    p = gen.random_problem(rng, 12, 66, m=0)
+    s = ks().Smoother(p)
+    s.run()
+    assert s.sync_status()[0] == ks().KS_ERR_RANK
