@@ -216,6 +216,13 @@ int ks_update_obs(ks_ctx *ctx, const double *o);
  * the stream.  cov requires a prior ks_selinv. */
 int ks_get(ks_ctx *ctx, double *states, double *cov);
 
+/* ks_get without the synchronisation for host destinations: the copies are
+ * only enqueued on the context's stream (pinned host buffers make them
+ * asynchronous DMA), so a caller streaming many problems can overlap the
+ * device-to-host copy of one context with the work of another; the results
+ * are valid once the stream has been synchronised. */
+int ks_get_async(ks_ctx *ctx, double *states, double *cov);
+
 /* Synchronise the stream and report the first numerical failure:
  * KS_OK, KS_ERR_NOT_SPD (bad_kind 1 = K, 2 = L), KS_ERR_RANK, or (small path,
  * n, m_max <= 8) KS_ERR_ARG with bad_kind 3 when a whitened block column's

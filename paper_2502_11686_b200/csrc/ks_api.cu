@@ -1112,7 +1112,13 @@ int ks_update_obs(ks_ctx *c, const double *o) {
   return KS_OK;
 }
 
-int ks_get(ks_ctx *c, double *states, double *cov) {
+static int get_impl(ks_ctx *c, double *states, double *cov, bool sync_host);
+
+int ks_get(ks_ctx *c, double *states, double *cov) { return get_impl(c, states, cov, true); }
+
+int ks_get_async(ks_ctx *c, double *states, double *cov) { return get_impl(c, states, cov, false); }
+
+static int get_impl(ks_ctx *c, double *states, double *cov, bool sync_host) {
   if (!c) return KS_ERR_ARG;
   if ((states && !c->solved) || (cov && !c->covd)) return KS_ERR_ORDER;
   bool host = false;
@@ -1126,7 +1132,7 @@ int ks_get(ks_ctx *c, double *states, double *cov) {
   };
   copy(states, c->xout, (size_t)c->N * c->n * 8);
   copy(cov, c->Sout, (size_t)c->N * c->n * c->n * 8);
-  if (e == cudaSuccess && host) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && host && sync_host) e = cudaStreamSynchronize(c->stream);
   return cuda_fail(e);
 }
 

@@ -31,7 +31,7 @@ EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solv
            "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info",
            "ks_peak_fp64_tflops", "ks_strerror", "ks_destroy",
            "ks_dist_unique_id", "ks_dist_create", "ks_dist_info", "ks_dist_destroy",
-           "ks_level_of_steps", "ks_update_obs")
+           "ks_level_of_steps", "ks_update_obs", "ks_get_async")
 
 
 class KsError(RuntimeError):
@@ -77,6 +77,7 @@ def lib():
                   "ks_factor_boundary"):
             getattr(L, f).argtypes = [vp]
         L.ks_get.argtypes = [vp, vp, vp]
+        L.ks_get_async.argtypes = [vp, vp, vp]
         L.ks_update_obs.argtypes = [vp, vp]
         L.ks_sync_status.argtypes = [vp, C.POINTER(i64), C.POINTER(i32)]
         L.ks_boundary_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(sz)]
@@ -302,11 +303,13 @@ class Smoother:
         self.inputs["o_update"] = t   # keep alive until the enqueued work completes
         self._call(lambda ctx: self.L.ks_update_obs(ctx, t.data_ptr()), "ks_update_obs")
 
-    def get(self, states=None, cov=None):
-        """Copy results into torch tensors (device or host)."""
+    def get(self, states=None, cov=None, sync: bool = True):
+        """Copy results into torch tensors (device or host); sync=False:
+        ks_get_async (host copies only enqueued; synchronise the stream)."""
         sp = None if states is None else states.data_ptr()
         cp = None if cov is None else cov.data_ptr()
-        _check(self.L.ks_get(self.ctx, sp, cp), "ks_get")
+        fn = self.L.ks_get if sync else self.L.ks_get_async
+        _check(fn(self.ctx, sp, cp), "ks_get" if sync else "ks_get_async")
         return states, cov
 
     def sync_status(self):

@@ -175,6 +175,12 @@ def test_host_inputs_and_get():
     xd = torch.empty((p.N, p.n), dtype=torch.float64, device="cuda")
     s.get(xd, None)
     assert np.array_equal(xd.cpu().numpy(), x1)
+    # ks_get_async: enqueued only; equal once the stream is synchronised
+    xa = torch.zeros((p.N, p.n), dtype=torch.float64).pin_memory()
+    Sa = torch.zeros((p.N, p.n, p.n), dtype=torch.float64).pin_memory()
+    s.get(xa, Sa, sync=False)
+    s.stream.synchronize()
+    assert np.array_equal(xa.numpy(), x1) and np.array_equal(Sa.numpy(), S1)
 
 
 def test_level_count():
