@@ -392,6 +392,27 @@ def main():
     torch.cuda.synchronize()
     if P > 1:
         dist.barrier()
+    # spread: the same K steps again, one event pair per step (not the headline)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    evs[0].record(stream)
+    for k in range(a.steps):
+        run()
+        evs[k + 1].record(stream)
+    torch.cuda.synchronize()
+    per = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(a.steps))
+    spread = {"min": per[0], "median": per[len(per) // 2], "max": per[-1]}
+    eager_ms = None
+    if graph is not None:   # the eager (launch-by-launch) mode beside the graph replay
+        for _ in range(2):
+            step(sm)
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(a.steps):
+            step(sm)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        eager_ms = ea.elapsed_time(eb) / a.steps
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / a.steps
     if P > 1:
@@ -499,7 +520,7 @@ def main():
                            if P > 1 else "1 GPU",
                            "l2": "working set (~11 GB at c5) >> 126 MB L2; no flush"},
                 "roofline": rl, "step_roofline": step_rl, "cpu_baseline": cpu, "e2e": e2e,
-                "timing": timing,
+                "timing": timing, "ms_per_step_spread": spread, "eager_ms_per_step": eager_ms,
                 "gpu_launches": int(n_launch), "clocks": clocks,
                 "phases_ms": fam_ms, "fp64_peak_tflops": p64, "nccl": nccl,
                 "exchange": ("host-staged gloo allgather, ranks sharing %d GPU(s): a validation run of "
