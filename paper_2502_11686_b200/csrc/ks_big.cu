@@ -593,12 +593,7 @@ cudaError_t qr_panel(const Panel &a, int64_t batch, cudaStream_t s) {
   const size_t sm = panel_smem(a.m - a.j0);
   cudaError_t e = set_smem_attr((const void *)big_qr_panel_kernel, (int)panel_smem(kBigMaxRows));
   if (e != cudaSuccess) return e;
-  static bool carve = false;   // (a preference only: harmless to repeat on another device)
-  if (!carve) {
-    cudaFuncSetAttribute((const void *)big_qr_panel_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    carve = true;
-  }
+  if ((e = set_carveout_max((const void *)big_qr_panel_kernel)) != cudaSuccess) return e;
   big_qr_panel_kernel<<<(unsigned)batch, kPanelThreads, sm, s>>>(a);
   ++g_launches;
   return cudaGetLastError();

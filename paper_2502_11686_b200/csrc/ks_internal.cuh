@@ -214,6 +214,8 @@ cudaError_t launch_boundary_ptile(const double *recv, double *out, int P, int n,
 // the attribute belongs to a device context, so a per-process flag is wrong
 // with several devices.  Thread-safe; kernels are identified by address.
 cudaError_t set_smem_attr(const void *func, int bytes);
+// cudaFuncAttributePreferredSharedMemoryCarveout = max shared, per (kernel, device)
+cudaError_t set_carveout_max(const void *func);
 // ks_update_obs: y_i = M_i^{-1} o_i (rows >= m_i zero) from the kept lower
 // factors M (stride sM doubles per step: 0 = constant), written pair-
 // interleaved tiled (small path, ptiled != 0) or row-major [N][m_max].

@@ -115,6 +115,19 @@ cudaError_t launch_update_y(const double *M, int64_t sM, const double *o, int64_
   return cudaGetLastError();
 }
 
+cudaError_t set_carveout_max(const void *func) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({func, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) done.insert({func, dev});
+  return e;
+}
+
 cudaError_t set_smem_attr(const void *func, int bytes) {
   static std::mutex mu;
   static std::set<std::pair<const void *, int>> done;
