@@ -3,6 +3,7 @@
 // per-level launch loops, the multi-GPU boundary exchange and the status word.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -19,6 +20,13 @@
 using namespace ks;
 
 namespace {
+
+// NVTX range around every ABI phase (header-only NVTX v3: free without a
+// profiler attached; nsys / ncu --nvtx show the phases of a step)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
@@ -910,6 +918,7 @@ int ks_create(ks_ctx **out, const ks_problem *p, void *workspace, size_t ws_byte
 }
 
 int ks_whiten(ks_ctx *c) {
+  NvtxRange nvtx_("ks_whiten");
   if (!c) return KS_ERR_ARG;
   cudaError_t e = cudaMemsetAsync(c->status, 0xff, 16, c->stream);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -986,6 +995,7 @@ int ks_whiten(ks_ctx *c) {
 }
 
 int ks_factor(ks_ctx *c) {
+  NvtxRange nvtx_("ks_factor");
   if (!c) return KS_ERR_ARG;
   if (c->stage < 1) return KS_ERR_ORDER;
   if (c->big) {
@@ -1020,6 +1030,7 @@ int ks_boundary_buffers(ks_ctx *c, void **send, void **recv, size_t *bytes) {
 }
 
 int ks_factor_boundary(ks_ctx *c) {
+  NvtxRange nvtx_("ks_factor_boundary");
   if (!c || !c->sharded) return KS_ERR_ARG;
   if (c->stage != 2) return KS_ERR_ORDER;
   int r = run_factor_levels(c, true);
@@ -1044,6 +1055,7 @@ static int big_backward(ks_ctx *c, bool st, bool cov) {
 }
 
 int ks_solve(ks_ctx *c) {
+  NvtxRange nvtx_("ks_solve");
   if (!c) return KS_ERR_ARG;
   if (c->stage < 3) return KS_ERR_ORDER;
   if (c->big) return big_backward(c, true, false);
@@ -1058,6 +1070,7 @@ int ks_solve(ks_ctx *c) {
 }
 
 int ks_selinv(ks_ctx *c) {
+  NvtxRange nvtx_("ks_selinv");
   if (!c || !c->Sout) return KS_ERR_ARG;
   if (c->stage < 3) return KS_ERR_ORDER;
   if (c->big) return big_backward(c, false, true);
@@ -1072,6 +1085,7 @@ int ks_selinv(ks_ctx *c) {
 }
 
 int ks_solve_selinv(ks_ctx *c) {
+  NvtxRange nvtx_("ks_solve_selinv");
   if (!c || !c->Sout) return KS_ERR_ARG;
   if (c->stage < 3) return KS_ERR_ORDER;
   if (c->big) return big_backward(c, true, true);
@@ -1086,6 +1100,7 @@ int ks_solve_selinv(ks_ctx *c) {
 }
 
 int ks_update_obs(ks_ctx *c, const double *o) {
+  NvtxRange nvtx_("ks_update_obs");
   if (!c || (!o && c->mx > 0)) return KS_ERR_ARG;
   if (c->stage < 1) return KS_ERR_ORDER;
   const bool constC = c->constC;
