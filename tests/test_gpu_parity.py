@@ -633,3 +633,30 @@ def test_big_path_errors():
     s = ks().Smoother(p)
     s.run()
     assert s.sync_status()[0] == ks().KS_ERR_RANK
+
+
+@pytest.mark.parametrize("n,N,P", [(3, 1 << 10, 4), (5, 1 << 11, 2), (7, 1 << 10, 8)])
+def test_virtual_shards_odd_n(n, N, P):
+    """Odd state dimensions on sharded ranks (the small path's non-TMA
+    backward and the AoS boundary entry of an odd n)."""
+    rng = np.random.default_rng(60 + n)
+    p = gen.random_problem(rng, N, n, m_max=min(n + 1, 8))
+    p.m = np.minimum(p.m, p.m_max).astype(np.int32)
+    x, S = _virtual_shards(p, P, fused=True)
+    xo, So = oracle.smooth(p)
+    assert rel_state_err(x, xo) <= TOL_X and rel_cov_err(S, So) <= TOL_S
+    x1, S1, _ = gpu_smooth(p)
+    assert np.array_equal(x, x1) and np.array_equal(S, S1)
+
+
+@pytest.mark.parametrize("n,N", [(12, 1500), (24, 700), (40, 301)])
+def test_cta_path_larger_N(n, N):
+    """The CTA path (n > 8) at larger N: many levels, odd levels, split last columns."""
+    rng = np.random.default_rng(70 + n)
+    p = gen.random_problem(rng, N, n, m=n)
+    # a stable evolution (random_problem's 0.9 Q + 0.2 E has spectral radius
+    # > 1 at n >= 12: over 1500 steps the states would span 1e0..1e69 and the
+    # per-step relative metric would measure the conditioning, not the method)
+    p.F = 0.97 * gen.haar_orthogonal(rng, N, n)
+    p.x, p.o = gen.simulate(rng, p.F, p.K, p.H, p.L, p.m, c=p.c)
+    assert_parity(p)
