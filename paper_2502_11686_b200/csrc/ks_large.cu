@@ -43,18 +43,10 @@ constexpr int kThreads = 256, kWarps = kThreads / 32;
   if (blockIdx.x == 1 && threadIdx.x == 0)                                                          \
     printf("[%s] %lld %lld %lld %lld %lld %lld %lld %lld\n", tag, _acc[0], _acc[1], _acc[2], _acc[3], \
            _acc[4], _acc[5], _acc[6], _acc[7]);
-__device__ long long g_panel_prof[8];
-#define KS_PP(i, t0)                                                        \
-  {                                                                         \
-    const long long _n = clock64();                                         \
-    _ppa[i] += _n - t0;                                                     \
-    t0 = _n;                                                                \
-  }
 #else
 #define KS_PROF_DECL
 #define KS_PROF(i)
 #define KS_PROF_PRINT(tag)
-#define KS_PP(i, t0)
 #endif
 constexpr int kLdw = 12;   // leading dimension of the 8 x 8 warp tiles (12 = conflict-free)
 
@@ -132,206 +124,272 @@ __device__ __forceinline__ double rcp_nr(double x) {   // one third-order Newton
   return fma(y, fma(e, e, e), y);
 }
 
-// Warp all-reduce of 8 values at once: reduce-scatter (xor 16, 8, 4), full
-// reduce of the remaining value (xor 2, 1), then broadcast of the 8 sums:
-// 17 double shuffles instead of 40.
-__device__ __forceinline__ void warp_sum8(double (&p)[8]) {
-  const int lane = threadIdx.x & 31;
-  const bool b4 = lane & 16, b2 = lane & 8, b1 = lane & 4;
-  double h[4], qd[2], o;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double send = b4 ? p[i] : p[i + 4];
-    h[i] = (b4 ? p[i + 4] : p[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const double send = b2 ? h[i] : h[i + 2];
-    qd[i] = (b2 ? h[i + 2] : h[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  {
-    const double send = b1 ? qd[0] : qd[1];
-    o = (b1 ? qd[1] : qd[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  o += __shfl_xor_sync(0xffffffffu, o, 2);
-  o += __shfl_xor_sync(0xffffffffu, o, 1);
-  // lane holds the sum of value (lane >> 2) & 7
-#pragma unroll
-  for (int v = 0; v < 8; ++v) p[v] = __shfl_sync(0xffffffffu, o, 4 * v);
-}
-
 __device__ __forceinline__ double warp_sum(double s) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   return s;
 }
 
-// Workspace of the blocked QR (shared memory).
+// Workspace of the blocked QR (shared memory).  The reflectors themselves
+// live in the factored columns below the diagonal (LAPACK geqrf storage);
+// the workspace holds per panel the compact-WY factor T, v_1 (the reflector
+// entry on the diagonal, whose place holds R_jj) and beta, double-buffered so
+// that panel k+1 is factored while panel k's reflectors are still being
+// applied (lookahead, qr_blocked).
 struct QrWs {
-  double *V;      // [ldv x 8]  the panel's reflectors (explicit, zero padded)
-  int ldv;
-  double *T;      // [kLdw x 8] compact-WY factor
-  double *G;      // [kLdw x 8] V^T V
-  double *beta;   // [8]
-  double *tile;   // [kWarps][kLdw x 8] per-warp 8x8 scratch
+  double *T[2];   // [kLdw x 8] compact-WY factor of panel k (buffer k & 1)
+  double *v1[2];  // [8]
+  double *beta[2];
+  double *G;      // [kLdw x 8] panel warp scratch (Gram matrices)
+  double *tile;   // [nw][kLdw x 8] per-warp 8x8 scratch of qr_apply
 };
+__host__ __device__ constexpr int qr_ws_doubles(int nw) { return 2 * kLdw * 8 + 32 + kLdw * 8 + nw * kLdw * 8; }
+__device__ QrWs carve_ws(double *p) {
+  QrWs w;
+  w.T[0] = p;
+  w.T[1] = p + kLdw * 8;
+  w.v1[0] = p + 2 * kLdw * 8;
+  w.v1[1] = w.v1[0] + 8;
+  w.beta[0] = w.v1[0] + 16;
+  w.beta[1] = w.v1[0] + 24;
+  w.G = p + 2 * kLdw * 8 + 32;
+  w.tile = w.G + kLdw * 8;
+  return w;
+}
 constexpr int kPanelMaxR = 5;   // rows per lane in the panel factorization (rows <= 160)
 
-// Panel factorization by warp 0: columns [k0, k0 + nb) of A, rows [k0, rows)
-// (MR rows per lane).  Householder reflector j: x = A[k0+j:, k0+j],
-// alpha = -sign(x1)|x|, v = x - alpha e1, H = I - beta v v^T,
-// beta = 1/(|x|^2 - x1 alpha) (zero column: beta = 0).  The norm and the
-// products x.a_jj of every later panel column are reduced in ONE batched
-// warp reduction (v.a_jj = x.a_jj - alpha a_jj[j]).  Writes R into the panel
-// (zeros below the diagonal), V (explicit, rows local to k0) and beta, then
-// G = V^T V (DMMA) and the compact-WY T (LAPACK larft, forward columnwise).
-template <int MR>
-__device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, QrWs &w) {
+// Entry (i, j) of the panel's reflector matrix V (rows local to the panel
+// origin P, column j < 8): v_1 on the diagonal, the stored column below it,
+// zero above and in the non-pivot columns j >= nb.
+__device__ __forceinline__ double vget(const double *P, int lda, const double *v1, int nb, int i, int j) {
+  return (j >= nb || i < j) ? 0.0 : (i == j ? v1[j] : P[i + j * lda]);
+}
+
+// Gram matrix of panel columns [0, nb) over the panel rows [r0, mrow) (rows
+// local to the panel origin P), one 8x8 DMMA tile by the calling warp, stored
+// to G (kLdw); rows and columns outside are masked to 0.
+__device__ __noinline__ void panel_gram(const double *P, int lda, int r0, int mrow, int nb, double *G) {
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;   // two independent DMMA chains
+  const bool col = g < nb;
+  int kk = r0;
+  for (; kk + 8 <= mrow; kk += 8) {
+    const double x = col ? P[(kk + q) + g * lda] : 0.0;
+    const double y = col ? P[(kk + 4 + q) + g * lda] : 0.0;
+    dmma(g0, g1, x, x);
+    dmma(g2, g3, y, y);
+  }
+  for (; kk < mrow; kk += 4) {
+    const double x = (col && kk + q < mrow) ? P[(kk + q) + g * lda] : 0.0;
+    dmma(g0, g1, x, x);
+  }
+  G[g + (2 * q) * kLdw] = g0 + g2;
+  G[g + (2 * q + 1) * kLdw] = g1 + g3;
+  __syncwarp();
+}
+
+// The panel's compact-WY factor (LAPACK larft, forward columnwise):
+// G = V^T V (DMMA, four chains) and T = U^{-1}, U = diag(1/beta) + striu(G)
+// (a zero reflector gets U_jj = 1; its V column is 0).  Lane i < 8 computes
+// row i of T right-looking: T_ii = beta_i, T_ij = -beta_j sum_{l<j} T_il G_lj,
+// each finished T_ij is folded into the pending sums at once, so the serial
+// chain per column is one multiply and one FMA (no cross-lane traffic).
+__device__ void qr_panel_t(const double *P, int lda, int mpad, int nb, const double *v1, const double *beta,
+                           double *T, double *Gs) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  {
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0, g4 = 0.0, g5 = 0.0, g6 = 0.0, g7 = 0.0;
+    dmma(g0, g1, vget(P, lda, v1, nb, q, g), vget(P, lda, v1, nb, q, g));
+    dmma(g2, g3, vget(P, lda, v1, nb, 4 + q, g), vget(P, lda, v1, nb, 4 + q, g));
+    const bool col = g < nb;
+    int kk = 8;
+    for (; kk + 16 <= mpad; kk += 16) {
+      const double x0 = col ? P[(kk + q) + g * lda] : 0.0, x1 = col ? P[(kk + 4 + q) + g * lda] : 0.0;
+      const double x2 = col ? P[(kk + 8 + q) + g * lda] : 0.0, x3 = col ? P[(kk + 12 + q) + g * lda] : 0.0;
+      dmma(g0, g1, x0, x0);
+      dmma(g2, g3, x1, x1);
+      dmma(g4, g5, x2, x2);
+      dmma(g6, g7, x3, x3);
+    }
+    if (kk < mpad) {   // mpad % 8 == 0
+      const double x0 = col ? P[(kk + q) + g * lda] : 0.0, x1 = col ? P[(kk + 4 + q) + g * lda] : 0.0;
+      dmma(g4, g5, x0, x0);
+      dmma(g6, g7, x1, x1);
+    }
+    Gs[g + (2 * q) * kLdw] = (g0 + g2) + (g4 + g6);
+    Gs[g + (2 * q + 1) * kLdw] = (g1 + g3) + (g5 + g7);
+  }
+  __syncwarp();
+  if (lane < 8) {
+    const int i = lane;
+    double bi[8], acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      bi[j] = beta[j] == 0.0 ? 1.0 : beta[j];
+      acc[j] = 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double tj = (j == i) ? bi[j] : ((j > i) ? -bi[j] * acc[j] : 0.0);
+      T[i + j * kLdw] = tj;
+#pragma unroll
+      for (int k = j + 1; k < 8; ++k) acc[k] = fma(tj, Gs[j + k * kLdw], acc[k]);
+    }
+  }
+  __syncwarp();
+}
+
+// Panel factorization by one warp: columns [k0, k0 + nb) of A, rows
+// [k0, rows) (MR rows per lane), panel origin P = A + k0 + k0 lda.
+// Householder reflector j: x = P[j:, j], alpha = -sign(x1)|x|,
+// v = x - alpha e1, H = I - beta v v^T, beta = 1/(|x|^2 - x1 alpha) (zero
+// column: beta = 0).  On exit the panel holds R on and above the diagonal
+// and v below it (v_1 and beta to the workspace buffer), and T is formed.
+//
+// |x|^2 and x . a_jj (jj > j) over rows >= j are entries of the Gram matrix
+// of the current panel columns over rows >= j, computed ONCE per panel (one
+// DMMA tile) and then DOWNDATED instead of reduced again per column:
+// reflector j is orthogonal on rows >= j, so it leaves that Gram unchanged,
+// and the Gram over rows >= j+1 is it minus the outer product of the
+// updated row j (the R row r_jj = a_jj[j] - d_jj v_1):  G' = G - r r^T.
+// Every lane holds G redundantly (bitwise identical: branches on it are
+// warp-uniform).  Accuracy guard: a downdated diagonal entry below kGramTau
+// of its value at the last exact Gram (cancellation amplifies rounding by
+// G_ref / G) triggers an exact Gram over rows >= j+1 -- rare for random or
+// well-conditioned columns, which lose a few percent per step -- so every
+// |x|^2 and dot used carries a relative error <= 8 eps / kGramTau, the
+// reflectors are orthogonal to that level, and a rank-deficient column
+// reaches the rank test with an exact norm.
+constexpr double kGramTau = 0.125;
+template <int MR>
+__device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, double *v1s, double *betas, double *T,
+                         double *Gs) {
+  const int lane = threadIdx.x & 31;
   const int mrow = rows - k0, mpad = pad8(mrow);
-#ifdef KS_LARGE_PROF
-  long long _ppa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long _pp = clock64();
-#endif
+  double *P = A + k0 + (int64_t)k0 * lda;
+  panel_gram(P, lda, 0, mrow, nb, Gs);
   double a[MR][8];
 #pragma unroll
   for (int r = 0; r < MR; ++r) {
     const int li = lane + 32 * r;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) a[r][j] = (li < mrow && j < nb) ? A[(k0 + li) + (k0 + j) * lda] : 0.0;
+    for (int j = 0; j < 8; ++j) a[r][j] = (li < mrow && j < nb) ? P[li + j * lda] : 0.0;
   }
+  double G[8][8], gref[8];   // upper triangle used
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int j = i; j < 8; ++j) G[i][j] = Gs[i + j * kLdw];
+    gref[i] = G[i][i];
+  }
+  __syncwarp();
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    // p[j] = |x|^2, p[jj] = x . a_jj (jj > j), rows li >= j
-    double p[8];
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      p[jj] = 0.0;
-      if (jj >= j) {
-#pragma unroll
-        for (int r = 0; r < MR; ++r) {
-          const int li = lane + 32 * r;
-          if (li >= j) p[jj] = fma(a[r][j], a[r][jj], p[jj]);
-        }
-      }
-    }
-    KS_PP(0, _pp)
-    warp_sum8(p);
-    KS_PP(1, _pp)
     double aj[8];   // row j of the panel (lane j, slot 0)
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) aj[jj] = (jj >= j) ? __shfl_sync(0xffffffffu, a[0][jj], j) : 0.0;
-    const double s = p[j], x1 = aj[j];
-    const bool live = (j < nb) && (s != 0.0);
+    const double s = G[j][j], x1 = aj[j];
+    const bool live = (j < nb) && (s > 0.0);
     const double nrm = live ? s * rsqrt_nr(s) : 0.0;
     const double alpha = live ? ((x1 > 0.0) ? -nrm : nrm) : x1;
     const double beta = live ? rcp_nr(s - x1 * alpha) : 0.0;
     const double v1 = live ? x1 - alpha : 0.0;
-    KS_PP(2, _pp)
     double v[MR];
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
       const int li = lane + 32 * r;
-      v[r] = !live ? 0.0 : (li > j ? a[r][j] : (li == j ? v1 : 0.0));
+      v[r] = li > j ? a[r][j] : (li == j ? v1 : 0.0);
     }
+    double rj[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj)
       if (jj > j) {
-        const double d = beta * (p[jj] - alpha * aj[jj]);
+        const double d = beta * (G[j][jj] - alpha * aj[jj]);
+        rj[jj] = fma(-d, v1, aj[jj]);
 #pragma unroll
         for (int r = 0; r < MR; ++r) a[r][jj] = fma(-d, v[r], a[r][jj]);
       }
+    if (j < nb && lane == j) a[0][j] = alpha;   // R_jj in place of v_1 (j < 8 <= 32)
+    if (lane == 0) {   // beta = 0 beyond nb: T stays finite
+      v1s[j] = v1;
+      betas[j] = beta;
+    }
+    if (j < 7) {
+      bool bad = false;
 #pragma unroll
-    for (int r = 0; r < MR; ++r) {
-      const int li = lane + 32 * r;
-      if (li < mpad) w.V[li + j * w.ldv] = (li < mrow) ? v[r] : 0.0;
-      if (j < nb) {
-        if (li == j) a[r][j] = alpha;
-        else if (li > j) a[r][j] = 0.0;
+      for (int i = 0; i < 8; ++i)
+        if (i > j) {
+#pragma unroll
+          for (int l = 0; l < 8; ++l)
+            if (l >= i) G[i][l] = fma(-rj[i], rj[l], G[i][l]);
+          bad |= (i < nb) && (G[i][i] < kGramTau * gref[i]);
+        }
+      if (bad) {   // exact Gram of the remaining columns over rows >= j + 1
+#pragma unroll
+        for (int r = 0; r < MR; ++r) {
+          const int li = lane + 32 * r;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (jj > j && li > j && li < mrow && jj < nb) P[li + jj * lda] = a[r][jj];
+        }
+        __syncwarp();
+        panel_gram(P + (j + 1) * lda, lda, j + 1, mrow, nb - (j + 1), Gs);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i > j) {
+#pragma unroll
+            for (int l = 0; l < 8; ++l)
+              if (l >= i) G[i][l] = Gs[(i - j - 1) + (l - j - 1) * kLdw];
+            gref[i] = G[i][i];
+          }
+        __syncwarp();
       }
     }
-    if (lane == 0) w.beta[j] = beta;
-    KS_PP(3, _pp)
   }
 #pragma unroll
   for (int r = 0; r < MR; ++r) {
     const int li = lane + 32 * r;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (li < mrow && j < nb) A[(k0 + li) + (k0 + j) * lda] = a[r][j];
+      if (li < mrow && j < nb) P[li + j * lda] = a[r][j];
   }
   __syncwarp();
-  KS_PP(4, _pp)
-  // G = V^T V (one 8x8 DMMA tile, K = mpad)
-  {
-    double g0 = 0.0, g1 = 0.0;
-    for (int kk = 0; kk < mpad; kk += 4) {
-      const double x = w.V[(kk + q) + g * w.ldv];
-      const double y = w.V[(kk + q) + g * w.ldv];
-      dmma(g0, g1, x, y);
-    }
-    w.G[g + (2 * q) * kLdw] = g0;
-    w.G[g + (2 * q + 1) * kLdw] = g1;
-  }
-  __syncwarp();
-  KS_PP(5, _pp)
-  // T = U^{-1}, U = diag(1/beta) + striu(V^T V) (the UT transform of the
-  // compact-WY factor; a zero reflector gets U_jj = 1, its V column is 0):
-  // lane c < 8 solves column c by back-substitution, 1/U_ii = beta_i.
-  if (lane < 8) {
-    const int c = lane;
-    double t[8], bi[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      bi[i] = w.beta[i] == 0.0 ? 1.0 : w.beta[i];
-      t[i] = 0.0;
-    }
-#pragma unroll
-    for (int i = 7; i >= 0; --i) {
-      if (i == c) t[i] = bi[i];
-      else if (i < c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = i + 1; l < 8; ++l)
-          if (l <= c) acc = fma(w.G[i + l * kLdw], t[l], acc);
-        t[i] = -bi[i] * acc;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w.T[i + c * kLdw] = t[i];
-  }
-  __syncwarp();
-  KS_PP(6, _pp)
-#ifdef KS_LARGE_PROF
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int i = 0; i < 7; ++i) g_panel_prof[i] += _ppa[i];
-#endif
+  qr_panel_t(P, lda, mpad, nb, v1s, betas, T, Gs);
 }
 
-// Q^T C for C = A[k0:k0+mpad, c0:c0+ncp] with Q = I - V T V^T:
-// W = V^T C, W = T^T W, C -= V W, one 8-column tile per warp iteration
-// (all three products of a tile in the same warp: no CTA barrier).
-__device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, const QrWs &w, int wbase = 0,
-                         int nw = kWarps) {
-  const int warp = (threadIdx.x >> 5) - wbase, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  double *sc = w.tile + warp * (kLdw * 8);
-  for (int n0 = warp * 8; n0 < ncp; n0 += nw * 8) {
-    double *C = A + k0 + (c0 + n0) * lda;
+// Q^T C for the reflectors of the panel at (k0, k0) (nb columns, buffer b)
+// and the columns [cb, ce) of A (tiles of 8 columns, tile t of the range to
+// warp wi of nwk), Q = I - V T V^T:  W = V^T C, W = T^T W, C -= V W, all
+// three products of a tile in the same warp (no barrier).  Rows [k0, k0 +
+// mpad); V read in place (vget for its diagonal 8x8 block).
+__device__ void qr_apply(double *A, int lda, int k0, int mpad, int nb, const QrWs &w, int b, int cb, int ce, int wi,
+                         int nwk, double *sc) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const double *P = A + k0 + (int64_t)k0 * lda;
+  const double *v1 = w.v1[b], *T = w.T[b];
+  // V's diagonal block as the A operand of V^T C (V[q][g], V[4+q][g]) and of
+  // V W (V[g][q], V[g][4+q]); below it the stored columns (column mask g < nb
+  // resp. q, 4+q < nb)
+  const double va0 = vget(P, lda, v1, nb, q, g), va1 = vget(P, lda, v1, nb, 4 + q, g);
+  const double vb0 = vget(P, lda, v1, nb, g, q), vb1 = vget(P, lda, v1, nb, g, 4 + q);
+  const bool cg = g < nb, cq0 = q < nb, cq1 = 4 + q < nb;
+  for (int n0 = cb + wi * 8; n0 < ce; n0 += nwk * 8) {
+    double *C = A + k0 + (int64_t)n0 * lda;
     double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;   // two independent DMMA chains
-    int kk = 0;
-    for (; kk + 8 <= mpad; kk += 8) {
-      dmma(w0, w1, w.V[(kk + q) + g * w.ldv], C[(kk + q) + g * lda]);          // V^T[g][kk+q], C[kk+q][g]
-      dmma(w2, w3, w.V[(kk + 4 + q) + g * w.ldv], C[(kk + 4 + q) + g * lda]);
+    dmma(w0, w1, va0, C[q + g * lda]);               // V^T[g][q], C[q][g]
+    dmma(w2, w3, va1, C[(4 + q) + g * lda]);
+    for (int kk = 8; kk < mpad; kk += 8) {
+      dmma(w0, w1, cg ? P[(kk + q) + g * lda] : 0.0, C[(kk + q) + g * lda]);
+      dmma(w2, w3, cg ? P[(kk + 4 + q) + g * lda] : 0.0, C[(kk + 4 + q) + g * lda]);
     }
-    if (kk < mpad) dmma(w0, w1, w.V[(kk + q) + g * w.ldv], C[(kk + q) + g * lda]);
     sc[g + (2 * q) * kLdw] = w0 + w2;
     sc[g + (2 * q + 1) * kLdw] = w1 + w3;
     __syncwarp();
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int kk = 0; kk < 8; kk += 4) {
-      const double x = w.T[(kk + q) + g * kLdw];        // T^T[g][kk+q]
-      const double y = sc[(kk + q) + g * kLdw];         // W[kk+q][g]
+      const double x = T[(kk + q) + g * kLdw];   // T^T[g][kk+q]
+      const double y = sc[(kk + q) + g * kLdw];  // W[kk+q][g]
       dmma(u0, u1, x, y);
     }
     __syncwarp();
@@ -339,12 +397,20 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, 
     sc[g + (2 * q + 1) * kLdw] = u1;
     __syncwarp();
     const double y0 = sc[q + g * kLdw], y1 = sc[(4 + q) + g * kLdw];   // W2[kk+q][g]
+    {
+      double *cp = C + g + (2 * q) * lda;
+      double c0v = cp[0], c1v = cp[lda];
+      dmma(c0v, c1v, -vb0, y0);
+      dmma(c0v, c1v, -vb1, y1);
+      cp[0] = c0v;
+      cp[lda] = c1v;
+    }
 #pragma unroll 2
-    for (int m0 = 0; m0 < mpad; m0 += 8) {
+    for (int m0 = 8; m0 < mpad; m0 += 8) {
       double *cp = C + (m0 + g) + (2 * q) * lda;
       double c0v = cp[0], c1v = cp[lda];
-      dmma(c0v, c1v, -w.V[(m0 + g) + q * w.ldv], y0);
-      dmma(c0v, c1v, -w.V[(m0 + g) + (4 + q) * w.ldv], y1);
+      dmma(c0v, c1v, cq0 ? -P[(m0 + g) + q * lda] : 0.0, y0);
+      dmma(c0v, c1v, cq1 ? -P[(m0 + g) + (4 + q) * lda] : 0.0, y1);
       cp[0] = c0v;
       cp[lda] = c1v;
     }
@@ -356,40 +422,58 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int c0, int ncp, 
 // rows x ncols column-major shared matrix A and apply Q^T to columns
 // [npiv, ncols).  A is zero-padded to pad8(rows) rows (lda >= that) and to
 // pad8(ncols) (+8 when npiv % 8 != 0) columns.  On exit the first npiv
-// columns hold R (zeros below the diagonal).  Ends with __syncthreads.
-// Warp group [wbase, wbase + nw) with its own named barrier (barid > 0), or
-// the whole CTA (barid 0).
+// columns hold R (zeros below the diagonal).  Ends with a barrier of the
+// group.  Warp group [wbase, wbase + nw) with its own named barrier
+// (barid > 0), or the whole CTA (barid 0).
+//
+// Lookahead: while warps 1..nw-1 apply panel k's reflectors to the columns
+// right of panel k+1, warp 0 applies them to panel k+1's own 8 columns and
+// factors it at once, so the serial panel chain (the QR's critical path)
+// no longer waits for the trailing update; one barrier per panel.
 __device__ __forceinline__ void group_sync(int barid, int nw) {
   if (barid == 0) __syncthreads();
   else asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(nw * 32) : "memory");
 }
+template <int MR>
+__device__ __forceinline__ void qr_panel_mr(double *A, int lda, int k0, int rows, int nb, QrWs &w, int b) {
+  qr_panel<MR>(A, lda, k0, rows, nb, w.v1[b], w.beta[b], w.T[b], w.G);
+}
 __device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w, long long *acc = nullptr,
                            int wbase = 0, int nw = kWarps, int barid = 0) {
   const int warp = (threadIdx.x >> 5) - wbase;
-#ifdef KS_LARGE_PROF
-  long long _t0 = clock64();
-#endif
+  double *sc = w.tile + warp * (kLdw * 8);
+  const int cend = pad8(ncols);
+  int kprev = -1, nbprev = 0;
   for (int k0 = 0; k0 < npiv && k0 < rows; k0 += 8) {
-    const int nb = (npiv - k0 < 8) ? npiv - k0 : 8;
+    const int nb = (npiv - k0 < 8) ? npiv - k0 : 8, b = (k0 >> 3) & 1;
     if (warp == 0) {
+      if (kprev >= 0) qr_apply(A, lda, kprev, pad8(rows - kprev), nbprev, w, b ^ 1, k0, k0 + 8, 0, 1, sc);
       const int mr = (rows - k0 + 31) >> 5;
-      if (mr <= 1) qr_panel<1>(A, lda, k0, rows, nb, w);
-      else if (mr == 2) qr_panel<2>(A, lda, k0, rows, nb, w);
-      else if (mr == 3) qr_panel<3>(A, lda, k0, rows, nb, w);
-      else if (mr == 4) qr_panel<4>(A, lda, k0, rows, nb, w);
-      else qr_panel<kPanelMaxR>(A, lda, k0, rows, nb, w);
+      if (mr <= 1) qr_panel_mr<1>(A, lda, k0, rows, nb, w, b);
+      else if (mr == 2) qr_panel_mr<2>(A, lda, k0, rows, nb, w, b);
+      else if (mr == 3) qr_panel_mr<3>(A, lda, k0, rows, nb, w, b);
+      else if (mr == 4) qr_panel_mr<4>(A, lda, k0, rows, nb, w, b);
+      else qr_panel_mr<kPanelMaxR>(A, lda, k0, rows, nb, w, b);
+    } else if (kprev >= 0 && k0 + 8 < cend) {
+      qr_apply(A, lda, kprev, pad8(rows - kprev), nbprev, w, b ^ 1, k0 + 8, cend, warp - 1, nw - 1, sc);
     }
     group_sync(barid, nw);
-#ifdef KS_LARGE_PROF
-    { const long long t1 = clock64(); if (acc) acc[0] += t1 - _t0; _t0 = t1; }
-#endif
-    const int c0 = k0 + nb;
-    if (c0 < ncols) qr_apply(A, lda, k0, pad8(rows - k0), c0, pad8(ncols - c0), w, wbase, nw);
-    group_sync(barid, nw);
-#ifdef KS_LARGE_PROF
-    { const long long t1 = clock64(); if (acc) acc[1] += t1 - _t0; _t0 = t1; }
-#endif
+    kprev = k0;
+    nbprev = nb;
   }
+  // the last panel's reflectors on everything right of it (its own non-pivot
+  // columns included), then R's lower triangle (the stored V) is cleared
+  if (kprev >= 0) {
+    const int c0 = kprev + nbprev;
+    if (c0 < ncols)
+      qr_apply(A, lda, kprev, pad8(rows - kprev), nbprev, w, (kprev >> 3) & 1, c0, c0 + pad8(ncols - c0), warp, nw, sc);
+    group_sync(barid, nw);   // the last V is read until here
+  }
+  for (int idx = threadIdx.x - wbase * 32; idx < npiv * pad8(rows); idx += nw * 32) {
+    const int j = idx / pad8(rows), i = idx - j * pad8(rows);
+    if (i > j) A[i + j * lda] = 0.0;
+  }
+  group_sync(barid, nw);
 }
 
 // X <- R^{-1} X for R (n x n upper triangular, ldr) and X (n x p, ldx), both
@@ -652,7 +736,7 @@ __device__ void ld_zs(const FactorLevelArgs &a, double *A, int lda, int r0) {
 
 // ---- shared-memory plan of the factor kernel ----
 struct FactorPlan {
-  int ld1, cols1, ld2, cols2, ld3, cols3, ldv;
+  int ld1, cols1, ld2, cols2, ld3, cols3;
   int off2, offws, total;   // doubles
   bool conc;                // stages 2 and 3 concurrently (B3 + a second workspace fit in S1's region)
 };
@@ -670,8 +754,6 @@ __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   f.cols2 = pad8(3 * n + 1) + extra;
   f.ld3 = ldpad(2 * RC + n);
   f.cols3 = pad8(n + 1) + extra;
-  const int rmax = (2 * n > 2 * RC + n) ? 2 * n : 2 * RC + n;   // >= RC + n
-  f.ldv = ldpad(rmax);
   const int s1 = f.ld1 * f.cols1;
   // post-processing reuses S1 for R^{-1}, P, a padded copy of R (3 x ldpad(n) x pad8(n))
   // and the reciprocal diagonal
@@ -679,23 +761,12 @@ __host__ __device__ inline FactorPlan factor_plan(int n, int RC) {
   const int s2 = f.ld2 * f.cols2, s3 = f.ld3 * f.cols3;
   f.off2 = ((s1 > s1p ? s1 : s1p) + 1) & ~1;
   f.offws = f.off2 + (((s2 > s3 ? s2 : s3) + 1) & ~1);
-  f.total = f.offws + f.ldv * 8 + 2 * kLdw * 8 + 8 + kWarps * kLdw * 8 + 2 * kWarps;
+  f.total = f.offws + qr_ws_doubles(kWarps) + 2 * kWarps;
   // stage 3's matrix rebuilt in S1's region (free once stage 2's matrix is
   // set up) next to a 4-warp workspace: the two QRs run on two warp groups
-  const int wsb = f.ldv * 8 + 2 * kLdw * 8 + 8 + kConcW3 * kLdw * 8;
+  const int wsb = qr_ws_doubles(kConcW3);
   f.conc = ((s3 + 1) & ~1) + wsb <= f.off2 && RC * (n + 1) <= kConcMaxPerThread * kThreads;
   return f;
-}
-
-__device__ QrWs carve_ws(double *p, int ldv) {
-  QrWs w;
-  w.V = p;
-  w.ldv = ldv;
-  w.T = w.V + ldv * 8;
-  w.G = w.T + kLdw * 8;
-  w.beta = w.G + kLdw * 8;
-  w.tile = w.beta + 8;
-  return w;
 }
 
 // Eliminate column t of the level:
@@ -715,7 +786,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   const int n = a.n, RC = a.in.RC, tid = threadIdx.x;
   const EntryView &in = a.in;
   double *S1 = sm, *P2 = sm + f.off2, *sh = sm + f.total - 2 * kWarps;
-  QrWs w = carve_ws(sm + f.offws, f.ldv);
+  QrWs w = carve_ws(sm + f.offws);
   const int ld1 = f.ld1, ld2 = f.ld2, ld3 = f.ld3;
   KS_PROF_DECL
 #ifdef KS_LARGE_PROF
@@ -810,7 +881,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
       __syncthreads();
     }
     KS_PROF(0)
-    QrWs w3 = carve_ws(S1 + ((ld3 * f.cols3 + 1) & ~1), f.ldv);
+    QrWs w3 = carve_ws(S1 + ((ld3 * f.cols3 + 1) & ~1));
     if (tid < 32 * kConcW3) qr_blocked(B3, ld3, rows3, n, n + 1, w3, qacc, 0, kConcW3, 1);
     else qr_blocked(P2, ld2, 2 * n, n, 3 * n + 1, w, qacc, kConcW3, kWarps - kConcW3, 2);
     __syncthreads();
@@ -941,11 +1012,6 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   __syncthreads();
   KS_PROF(0)
   KS_PROF_PRINT("elim: other stage1 stage3 stage2 trsm Pgemm panel apply")
-#ifdef KS_LARGE_PROF
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    printf("[panel: p+load sum8 scalar update store G T] %lld %lld %lld %lld %lld %lld %lld\n", g_panel_prof[0],
-           g_panel_prof[1], g_panel_prof[2], g_panel_prof[3], g_panel_prof[4], g_panel_prof[5], g_panel_prof[6]);
-#endif
 }
 
 __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs a) {

@@ -1,0 +1,140 @@
+// Microbenchmark (not product code): the CTA path's blocked Householder QR
+// (qr_blocked of csrc/ks_large.cu, included verbatim) on one shared-memory
+// matrix per CTA, 8 warps, one CTA per SM; cycles per QR and per phase of
+// CTA 0.  Shapes: stage 1 (96 x 97, 48 pivots) and stage 2 (96 x 145).
+// Usage: qr_bench [rows] [npiv] [ncols] [ctas]
+#include "../../paper_2502_11686_b200/csrc/ks_large.cu"
+
+namespace ks {
+namespace {
+__global__ void __launch_bounds__(kThreads) qr_bench_kernel(int rows, int npiv, int ncols, int reps,
+                                                            long long *cyc, double *out) {
+  extern __shared__ __align__(16) double sm[];
+  const int lda = ldpad(rows), cp = pad8(ncols) + 8;
+  double *A = sm;
+  QrWs w = carve_ws(sm + ((lda * cp + 1) & ~1));
+  long long tot = 0;
+  for (int rep = 0; rep < reps; ++rep) {
+    for (int i = threadIdx.x; i < lda * cp; i += blockDim.x) {
+      const int r = i % lda, c = i / lda;
+      const unsigned h = (unsigned)(r * 7919 + c * 104729 + blockIdx.x * 31 + rep * 13) * 2654435761u;
+      A[i] = (r < rows && c < ncols) ? ((double)(h >> 8) / 16777216.0 - 0.5) : 0.0;
+    }
+    __syncthreads();
+    const long long t0 = clock64();
+    qr_blocked(A, lda, rows, npiv, ncols, w);
+    const long long t1 = clock64();
+    tot += t1 - t0;
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = tot / reps;
+  if (threadIdx.x == 0) out[blockIdx.x] = A[0] + A[lda + 1];
+}
+__global__ void __launch_bounds__(kThreads) panel_bench_kernel(int rows, int reps, long long *cyc, double *out) {
+  extern __shared__ __align__(16) double sm[];
+  const int lda = ldpad(rows), cp = 16;
+  double *A = sm;
+  QrWs w = carve_ws(sm + ((lda * cp + 1) & ~1));
+  for (int i = threadIdx.x; i < lda * cp; i += blockDim.x) {
+    const int r = i % lda, c = i / lda;
+    const unsigned h = (unsigned)(r * 7919 + c * 104729 + blockIdx.x * 31) * 2654435761u;
+    A[i] = (r < rows) ? ((double)(h >> 8) / 16777216.0 - 0.5) : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    long long t0 = clock64();
+    for (int rep = 0; rep < reps; ++rep) {
+      qr_panel<3>(A, lda, 0, rows, 8, w.v1[0], w.beta[0], w.T[0], w.G);
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = (t1 - t0) / reps;
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = A[0] + A[lda + 1];
+}
+// one QR of a seeded matrix, result copied out (for the host Gram check)
+__global__ void __launch_bounds__(kThreads) qr_check_kernel(int rows, int npiv, int ncols, const double *in, double *res) {
+  extern __shared__ __align__(16) double sm[];
+  const int lda = ldpad(rows), cp = pad8(ncols) + 8;
+  double *A = sm;
+  QrWs w = carve_ws(sm + ((lda * cp + 1) & ~1));
+  for (int i = threadIdx.x; i < lda * cp; i += blockDim.x) {
+    const int r = i % lda, c = i / lda;
+    A[i] = (r < rows && c < ncols) ? in[r + c * rows] : 0.0;
+  }
+  __syncthreads();
+  qr_blocked(A, lda, rows, npiv, ncols, w);
+  for (int i = threadIdx.x; i < rows * ncols; i += blockDim.x) res[i] = A[i % rows + (i / rows) * lda];
+}
+}  // namespace
+}  // namespace ks
+
+static int check(int rows, int npiv, int ncols) {
+  const int lda = ks::ldpad(rows), cp = ks::pad8(ncols) + 8;
+  const size_t smem = 8 * (size_t)(((lda * cp + 1) & ~1) + ks::qr_ws_doubles(ks::kWarps) + 64);
+  const int ne = rows * ncols;
+  double *h = (double *)malloc(8 * ne), *r = (double *)malloc(8 * ne), *din, *dres;
+  unsigned x = 12345u + rows * 7 + ncols;
+  for (int i = 0; i < ne; ++i) { x = x * 1664525u + 1013904223u; h[i] = (double)(x >> 8) / 16777216.0 - 0.5; }
+  cudaMalloc(&din, 8 * ne); cudaMalloc(&dres, 8 * ne);
+  cudaMemcpy(din, h, 8 * ne, cudaMemcpyHostToDevice);
+  cudaFuncSetAttribute(ks::qr_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ks::qr_check_kernel<<<1, ks::kThreads, smem>>>(rows, npiv, ncols, din, dres);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(r, dres, 8 * ne, cudaMemcpyDeviceToHost);
+  double err = 0, sc = 0, low = 0;
+  for (int a = 0; a < ncols; ++a)
+    for (int b = 0; b < ncols; ++b) {
+      double g0 = 0, g1 = 0;
+      for (int i = 0; i < rows; ++i) { g0 += h[i + a * rows] * h[i + b * rows]; g1 += r[i + a * rows] * r[i + b * rows]; }
+      err = fmax(err, fabs(g0 - g1)); sc = fmax(sc, fabs(g0));
+    }
+  for (int j = 0; j < npiv && j < ncols; ++j)
+    for (int i = j + 1; i < rows; ++i) low = fmax(low, fabs(r[i + j * rows]));
+  printf("check %3d x %3d (%2d piv): gram err %.2e (rel %.2e), below-diag %.1e %s\n", rows, ncols, npiv, err, err / sc, low,
+         cudaGetErrorString(e));
+  return err / sc < 1e-13 && low == 0.0;
+}
+
+int main(int argc, char **argv) {
+  const int rows = argc > 1 ? atoi(argv[1]) : 96, npiv = argc > 2 ? atoi(argv[2]) : 48,
+            ncols = argc > 3 ? atoi(argv[3]) : 97, ctas = argc > 4 ? atoi(argv[4]) : 148;
+  const int lda = ks::ldpad(rows), cp = ks::pad8(ncols) + 8;
+  const size_t smem = 8 * (size_t)(((lda * cp + 1) & ~1) + ks::qr_ws_doubles(ks::kWarps) + 64);
+  long long *cyc;
+  double *out;
+  cudaMallocManaged(&cyc, 8);
+  cudaMalloc(&out, 8 * ctas);
+  cudaFuncSetAttribute(ks::qr_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (argc > 1 && argv[1][0] == 'c') {
+    int ok = 1;
+    const int cases[][3] = {{8, 6, 13}, {4, 6, 7}, {5, 6, 13}, {12, 6, 13}, {2, 1, 3}, {96, 48, 97}, {96, 48, 145},
+                            {144, 48, 49}, {30, 9, 20}, {17, 16, 33}, {160, 64, 129}, {3, 3, 3}, {40, 20, 41}};
+    for (auto &c : cases) ok &= check(c[0], c[1], c[2]);
+    printf(ok ? "ALL OK\n" : "FAILURES\n");
+    return !ok;
+  }
+  if (argc > 5) {
+    cudaFuncSetAttribute(ks::panel_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ks::panel_bench_kernel<<<1, ks::kThreads, smem>>>(rows, 50, cyc, out);
+    cudaDeviceSynchronize();
+    printf("panel %d x 8 (MR 3): %lld cycles\n", rows, *cyc);
+    return 0;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  ks::qr_bench_kernel<<<ctas, ks::kThreads, smem>>>(rows, npiv, ncols, 2, cyc, out);
+  cudaEventRecord(e0);
+  const int reps = 20;
+  ks::qr_bench_kernel<<<ctas, ks::kThreads, smem>>>(rows, npiv, ncols, reps, cyc, out);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaDeviceSynchronize();
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("qr %d x %d (%d pivots), %d CTAs, smem %zu B: %lld cycles/QR (CTA 0), %.2f us/QR wall, %s\n", rows, ncols,
+         npiv, ctas, smem, *cyc, 1e3 * ms / reps, cudaGetErrorString(e));
+  return 0;
+}
+// the library's per-device attribute helper (ks_api.cu), not linked here
+cudaError_t ks::set_smem_attr(const void *f, int bytes) {
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
