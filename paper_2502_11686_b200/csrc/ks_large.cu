@@ -48,6 +48,27 @@ constexpr int kThreads = 256, kWarps = kThreads / 32;
 #define KS_PROF(i)
 #define KS_PROF_PRINT(tag)
 #endif
+// Panel phase clock (-DKS_PANEL_PROF, micro-benchmarks only): cycles of the
+// panel warp's phases accumulated in g_panel_clk[0..7].
+#if defined(KS_PANEL_PROF) || defined(KS_LARGE_PROF)
+__device__ unsigned long long g_refresh[2];   // [0] exact-Gram refreshes, [1] panel columns
+#define KS_COUNT(i, v) if ((threadIdx.x & 31) == 0) atomicAdd(&g_refresh[i], (unsigned long long)(v));
+#else
+#define KS_COUNT(i, v)
+#endif
+#ifdef KS_PANEL_PROF
+__device__ long long g_panel_clk[8];
+#define KS_PCLK(i)                                                     \
+  {                                                                    \
+    const long long _n = clock64();                                    \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) g_panel_clk[i] += _n - _pc; \
+    _pc = _n;                                                          \
+  }
+#define KS_PCLK_DECL long long _pc = clock64();
+#else
+#define KS_PCLK(i)
+#define KS_PCLK_DECL
+#endif
 constexpr int kLdw = 12;   // leading dimension of the 8 x 8 warp tiles (12 = conflict-free)
 
 __host__ __device__ constexpr int pad8(int x) { return (x + 7) & ~7; }
@@ -168,24 +189,33 @@ __device__ __forceinline__ double vget(const double *P, int lda, const double *v
 // Gram matrix of panel columns [0, nb) over the panel rows [r0, mrow) (rows
 // local to the panel origin P), one 8x8 DMMA tile by the calling warp, stored
 // to G (kLdw); rows and columns outside are masked to 0.
-__device__ __noinline__ void panel_gram(const double *P, int lda, int r0, int mrow, int nb, double *G) {
+template <bool kInline>
+__device__ __forceinline__ void panel_gram_body(const double *P, int lda, int r0, int mrow, int nb, double *G) {
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;   // two independent DMMA chains
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0, g4 = 0.0, g5 = 0.0, g6 = 0.0, g7 = 0.0;   // four DMMA chains
   const bool col = g < nb;
   int kk = r0;
-  for (; kk + 8 <= mrow; kk += 8) {
-    const double x = col ? P[(kk + q) + g * lda] : 0.0;
-    const double y = col ? P[(kk + 4 + q) + g * lda] : 0.0;
-    dmma(g0, g1, x, x);
-    dmma(g2, g3, y, y);
+  for (; kk + 16 <= mrow; kk += 16) {
+    const double x0 = col ? P[(kk + q) + g * lda] : 0.0, x1 = col ? P[(kk + 4 + q) + g * lda] : 0.0;
+    const double x2 = col ? P[(kk + 8 + q) + g * lda] : 0.0, x3 = col ? P[(kk + 12 + q) + g * lda] : 0.0;
+    dmma(g0, g1, x0, x0);
+    dmma(g2, g3, x1, x1);
+    dmma(g4, g5, x2, x2);
+    dmma(g6, g7, x3, x3);
   }
-  for (; kk < mrow; kk += 4) {
-    const double x = (col && kk + q < mrow) ? P[(kk + q) + g * lda] : 0.0;
-    dmma(g0, g1, x, x);
+  for (; kk < mrow; kk += 8) {
+    const double x0 = (col && kk + q < mrow) ? P[(kk + q) + g * lda] : 0.0;
+    const double x1 = (col && kk + 4 + q < mrow) ? P[(kk + 4 + q) + g * lda] : 0.0;
+    dmma(g0, g1, x0, x0);
+    dmma(g2, g3, x1, x1);
   }
-  G[g + (2 * q) * kLdw] = g0 + g2;
-  G[g + (2 * q + 1) * kLdw] = g1 + g3;
+  G[g + (2 * q) * kLdw] = (g0 + g2) + (g4 + g6);
+  G[g + (2 * q + 1) * kLdw] = (g1 + g3) + (g5 + g7);
   __syncwarp();
+}
+// the exact recomputation of the accuracy guard (rare) out of line
+__device__ __noinline__ void panel_gram(const double *P, int lda, int r0, int mrow, int nb, double *G) {
+  panel_gram_body<false>(P, lda, r0, mrow, nb, G);
 }
 
 // The panel's compact-WY factor (LAPACK larft, forward columnwise):
@@ -222,18 +252,22 @@ __device__ void qr_panel_t(const double *P, int lda, int mpad, int nb, const dou
   __syncwarp();
   if (lane < 8) {
     const int i = lane;
-    double bi[8], acc[8];
+    double bi[8], acc[8], gv[28];   // all loads issued before the serial chain
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       bi[j] = beta[j] == 0.0 ? 1.0 : beta[j];
       acc[j] = 0.0;
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0, c = 0; j < 8; ++j)
+#pragma unroll
+      for (int k = j + 1; k < 8; ++k, ++c) gv[c] = Gs[j + k * kLdw];
+#pragma unroll
+    for (int j = 0, c = 0; j < 8; ++j) {
       const double tj = (j == i) ? bi[j] : ((j > i) ? -bi[j] * acc[j] : 0.0);
       T[i + j * kLdw] = tj;
 #pragma unroll
-      for (int k = j + 1; k < 8; ++k) acc[k] = fma(tj, Gs[j + k * kLdw], acc[k]);
+      for (int k = j + 1; k < 8; ++k, ++c) acc[k] = fma(tj, gv[c], acc[k]);
     }
   }
   __syncwarp();
@@ -262,12 +296,14 @@ __device__ void qr_panel_t(const double *P, int lda, int mpad, int nb, const dou
 // reaches the rank test with an exact norm.
 constexpr double kGramTau = 0.125;
 template <int MR>
-__device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, double *v1s, double *betas, double *T,
-                         double *Gs) {
+__device__ __noinline__ void qr_panel(double *A, int lda, int k0, int rows, int nb, double *v1s, double *betas,
+                                      double *T, double *Gs) {
   const int lane = threadIdx.x & 31;
   const int mrow = rows - k0, mpad = pad8(mrow);
   double *P = A + k0 + (int64_t)k0 * lda;
-  panel_gram(P, lda, 0, mrow, nb, Gs);
+  KS_PCLK_DECL
+  panel_gram_body<true>(P, lda, 0, mrow, nb, Gs);
+  KS_PCLK(0)
   double a[MR][8];
 #pragma unroll
   for (int r = 0; r < MR; ++r) {
@@ -283,6 +319,7 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, double *v
     gref[i] = G[i][i];
   }
   __syncwarp();
+  KS_PCLK(1)
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     double aj[8];   // row j of the panel (lane j, slot 0)
@@ -325,6 +362,7 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, double *v
           bad |= (i < nb) && (G[i][i] < kGramTau * gref[i]);
         }
       if (bad) {   // exact Gram of the remaining columns over rows >= j + 1
+        KS_COUNT(0, 1)
 #pragma unroll
         for (int r = 0; r < MR; ++r) {
           const int li = lane + 32 * r;
@@ -354,7 +392,10 @@ __device__ void qr_panel(double *A, int lda, int k0, int rows, int nb, double *v
       if (li < mrow && j < nb) P[li + j * lda] = a[r][j];
   }
   __syncwarp();
+  KS_PCLK(2)
+  KS_COUNT(1, nb)
   qr_panel_t(P, lda, mpad, nb, v1s, betas, T, Gs);
+  KS_PCLK(3)
 }
 
 // Q^T C for the reflectors of the panel at (k0, k0) (nb columns, buffer b)
@@ -438,7 +479,7 @@ template <int MR>
 __device__ __forceinline__ void qr_panel_mr(double *A, int lda, int k0, int rows, int nb, QrWs &w, int b) {
   qr_panel<MR>(A, lda, k0, rows, nb, w.v1[b], w.beta[b], w.T[b], w.G);
 }
-__device__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w, long long *acc = nullptr,
+__device__ __noinline__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w, long long *acc = nullptr,
                            int wbase = 0, int nw = kWarps, int barid = 0) {
   const int warp = (threadIdx.x >> 5) - wbase;
   double *sc = w.tile + warp * (kLdw * 8);
@@ -1012,6 +1053,10 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   __syncthreads();
   KS_PROF(0)
   KS_PROF_PRINT("elim: other stage1 stage3 stage2 trsm Pgemm panel apply")
+#ifdef KS_LARGE_PROF
+  if (blockIdx.x == 1 && threadIdx.x == 0)
+    printf("[gram refreshes %llu of %llu panel columns]\n", g_refresh[0], g_refresh[1]);
+#endif
 }
 
 __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs a) {

@@ -50,6 +50,45 @@ __global__ void __launch_bounds__(kThreads) panel_bench_kernel(int rows, int rep
   }
   if (threadIdx.x == 0) out[blockIdx.x] = A[0] + A[lda + 1];
 }
+// stages 2 and 3 concurrently as in factor_level_kernel: B2 (r2 x c2, 48
+// pivots) on warps [w3, 8), B3 (r3 x c3) on warps [0, w3)
+__global__ void __launch_bounds__(kThreads) conc_bench_kernel(int r2, int c2, int r3, int c3, int w3, int reps,
+                                                              long long *cyc, double *out) {
+  extern __shared__ __align__(16) double sm[];
+  const int ld2 = ldpad(r2), cp2 = pad8(c2) + 8, ld3 = ldpad(r3), cp3 = pad8(c3) + 8;
+  double *A2 = sm, *A3 = sm + ((ld2 * cp2 + 1) & ~1);
+  double *wsp = A3 + ((ld3 * cp3 + 1) & ~1);
+  QrWs w2 = carve_ws(wsp), w3s = carve_ws(wsp + qr_ws_doubles(kWarps));
+  long long tot = 0;
+  for (int rep = 0; rep < reps; ++rep) {
+    for (int i = threadIdx.x; i < ld2 * cp2; i += blockDim.x) {
+      const int r = i % ld2, c = i / ld2;
+      const unsigned h = (unsigned)(r * 7919 + c * 104729 + blockIdx.x * 31 + rep * 13) * 2654435761u;
+      A2[i] = (r < r2 && c < c2) ? ((double)(h >> 8) / 16777216.0 - 0.5) : 0.0;
+    }
+    for (int i = threadIdx.x; i < ld3 * cp3; i += blockDim.x) {
+      const int r = i % ld3, c = i / ld3;
+      const unsigned h = (unsigned)(r * 7919 + c * 104723 + blockIdx.x * 37 + rep * 11) * 2654435761u;
+      A3[i] = (r < r3 && c < c3) ? ((double)(h >> 8) / 16777216.0 - 0.5) : 0.0;
+    }
+    __syncthreads();
+    const long long t0 = clock64();
+    if (w3 == 0) {
+      qr_blocked(A2, ld2, r2, 48, c2, w2);
+      qr_blocked(A3, ld3, r3, 48, c3, w3s);
+    } else if ((int)(threadIdx.x >> 5) < w3) {
+      qr_blocked(A3, ld3, r3, 48, c3, w3s, nullptr, 0, w3, 1);
+    } else {
+      qr_blocked(A2, ld2, r2, 48, c2, w2, nullptr, w3, kWarps - w3, 2);
+    }
+    __syncthreads();
+    const long long t1 = clock64();
+    tot += t1 - t0;
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = tot / reps;
+  if (threadIdx.x == 0) out[blockIdx.x] = A2[0] + A3[0];
+}
+
 // one QR of a seeded matrix, result copied out (for the host Gram check)
 __global__ void __launch_bounds__(kThreads) qr_check_kernel(int rows, int npiv, int ncols, const double *in, double *res) {
   extern __shared__ __align__(16) double sm[];
@@ -112,11 +151,26 @@ int main(int argc, char **argv) {
     printf(ok ? "ALL OK\n" : "FAILURES\n");
     return !ok;
   }
+  if (argc > 1 && argv[1][0] == 'x') {   // x w3: stage 2 (96 x 145) || stage 3 (96 x 49)
+    const int w3 = atoi(argv[2]);
+    const size_t sm2 = 8 * (size_t)(((ks::ldpad(96) * (ks::pad8(145) + 8) + 1) & ~1) +
+                                    ((ks::ldpad(96) * (ks::pad8(49) + 8) + 1) & ~1) + 2 * ks::qr_ws_doubles(ks::kWarps) + 64);
+    cudaFuncSetAttribute(ks::conc_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    ks::conc_bench_kernel<<<148, ks::kThreads, sm2>>>(96, 145, 96, 49, w3, 10, cyc, out);
+    cudaError_t e = cudaDeviceSynchronize();
+    printf("conc w3=%d: %lld cycles (%s)\n", w3, *cyc, cudaGetErrorString(e));
+    return 0;
+  }
   if (argc > 5) {
     cudaFuncSetAttribute(ks::panel_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     ks::panel_bench_kernel<<<1, ks::kThreads, smem>>>(rows, 50, cyc, out);
     cudaDeviceSynchronize();
     printf("panel %d x 8 (MR 3): %lld cycles\n", rows, *cyc);
+#ifdef KS_PANEL_PROF
+    long long h[8];
+    cudaMemcpyFromSymbol(h, ks::g_panel_clk, sizeof(h));
+    printf("  gram %lld  load %lld  columns %lld  T %lld (per panel)\n", h[0] / 51, h[1] / 51, h[2] / 51, h[3] / 51);
+#endif
     return 0;
   }
   cudaEvent_t e0, e1;
