@@ -1213,6 +1213,7 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
     for (int k = tid; k < n; k += blockDim.x) e[k] = 0.0;
     return;
   }
+  KS_PROF_DECL
   const int64_t iK = (a.cntE == 1) ? 0 : i;
   const int ld = ldpad(n), p = 2 * n + 1, cp = pad8(p) + 8;
   double *Lm = sm, *X = Lm + ld * pad8(n), *sh = X + ld * cp;
@@ -1244,7 +1245,9 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
       if (r >= li) X[r + 2 * n * ld] = 0.0;
     __syncthreads();
   }
+  KS_PROF(0)
   const bool ok = a.chol ? chol_diag_ok(Lm, ld, n, sh) : cta_chol(Lm, ld, n, sh);
+  KS_PROF(1)
   if (tid == 0 && !ok) {
     const int64_t step = (a.cntE == 1) ? (a.first_global == 0 ? 1 : 0) : i;
     report(a.status, step, kBadK);
@@ -1252,12 +1255,15 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
   diag_rcp(Lm, ld, n, sh);
   __syncthreads();
   trsm_lower(Lm, ld, sh, n, X, ld, p);
+  KS_PROF(2)
   for (int k = tid; k < nn; k += blockDim.x) {
     const int r = k / n, cc = k - r * n;
     El[k] = -X[r + cc * ld];
     Er[k] = X[r + (n + cc) * ld];
   }
   for (int r = tid; r < n; r += blockDim.x) e[r] = X[r + 2 * n * ld];
+  KS_PROF(3)
+  KS_PROF_PRINT("whiten evo: loads chol trsm store")
 }
 
 // Observation blocks: L = M M^T; C = M^{-1} H, y = M^{-1} o (rows >= m_i zero).
