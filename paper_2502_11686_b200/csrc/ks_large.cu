@@ -95,8 +95,8 @@ template <bool TA, bool TB>
 __device__ void gemm(int M, int N, int K, double alpha, const double *A, int lda, const double *B, int ldb,
                      double beta, double *C, int ldc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  const int mt = M >> 3, nt = N >> 3, mp = (mt + 1) >> 1;
-  for (int tile = warp; tile < mp * nt; tile += kWarps) {
+  const int mt = M >> 3, nt = N >> 3, mp = (mt + 1) >> 1, nw = blockDim.x >> 5;
+  for (int tile = warp; tile < mp * nt; tile += nw) {
     const int m0 = (tile % mp) * 16, n0 = (tile / mp) * 8;
     const bool two = m0 + 8 < M;
     double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
@@ -158,21 +158,18 @@ __device__ __forceinline__ double warp_sum(double s) {
 // that panel k+1 is factored while panel k's reflectors are still being
 // applied (lookahead, qr_blocked).
 struct QrWs {
-  double *T[2];   // [kLdw x 8] compact-WY factor of panel k (buffer k & 1)
-  double *v1[2];  // [8]
-  double *beta[2];
+  double *base;   // T (buffer 0, 1: [kLdw x 8] each), then v1 (2 x 8), beta (2 x 8)
   double *G;      // [kLdw x 8] panel warp scratch (Gram matrices)
   double *tile;   // [nw][kLdw x 8] per-warp 8x8 scratch of qr_apply
+  // (no pointer arrays: a runtime-indexed array member would live in local memory)
+  __device__ __forceinline__ double *T(int b) const { return base + b * (kLdw * 8); }
+  __device__ __forceinline__ double *v1(int b) const { return base + 2 * kLdw * 8 + 8 * b; }
+  __device__ __forceinline__ double *beta(int b) const { return base + 2 * kLdw * 8 + 16 + 8 * b; }
 };
 __host__ __device__ constexpr int qr_ws_doubles(int nw) { return 2 * kLdw * 8 + 32 + kLdw * 8 + nw * kLdw * 8; }
-__device__ QrWs carve_ws(double *p) {
+__device__ __forceinline__ QrWs carve_ws(double *p) {
   QrWs w;
-  w.T[0] = p;
-  w.T[1] = p + kLdw * 8;
-  w.v1[0] = p + 2 * kLdw * 8;
-  w.v1[1] = w.v1[0] + 8;
-  w.beta[0] = w.v1[0] + 16;
-  w.beta[1] = w.v1[0] + 24;
+  w.base = p;
   w.G = p + 2 * kLdw * 8 + 32;
   w.tile = w.G + kLdw * 8;
   return w;
@@ -407,7 +404,7 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int nb, const QrW
                          int nwk, double *sc) {
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const double *P = A + k0 + (int64_t)k0 * lda;
-  const double *v1 = w.v1[b], *T = w.T[b];
+  const double *v1 = w.v1(b), *T = w.T(b);
   // V's diagonal block as the A operand of V^T C (V[q][g], V[4+q][g]) and of
   // V W (V[g][q], V[g][4+q]); below it the stored columns (column mask g < nb
   // resp. q, 4+q < nb)
@@ -476,10 +473,10 @@ __device__ __forceinline__ void group_sync(int barid, int nw) {
   else asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(nw * 32) : "memory");
 }
 template <int MR>
-__device__ __forceinline__ void qr_panel_mr(double *A, int lda, int k0, int rows, int nb, QrWs &w, int b) {
-  qr_panel<MR>(A, lda, k0, rows, nb, w.v1[b], w.beta[b], w.T[b], w.G);
+__device__ __forceinline__ void qr_panel_mr(double *A, int lda, int k0, int rows, int nb, const QrWs w, int b) {
+  qr_panel<MR>(A, lda, k0, rows, nb, w.v1(b), w.beta(b), w.T(b), w.G);
 }
-__device__ __noinline__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, QrWs &w, long long *acc = nullptr,
+__device__ __noinline__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, const QrWs w, long long *acc = nullptr,
                            int wbase = 0, int nw = kWarps, int barid = 0) {
   const int warp = (threadIdx.x >> 5) - wbase;
   double *sc = w.tile + warp * (kLdw * 8);
@@ -1197,10 +1194,38 @@ __global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelA
 
 // ---------------------------------------------------------------- whiten ---
 
-// Evolution blocks: K = Lam Lam^T; El = -Lam^{-1} F,
-// Er = Lam^{-1}, e = Lam^{-1} c.  One CTA per distinct block; the solve with
-// the 2n+1 right-hand sides [F | I | c] is blocked (DMMA updates).
-__global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
+// D = Li B for Li (M x M lower triangular, shared memory, ld, zero-padded to
+// pad8(M)) and B (M x N) fetched element-wise by bget(k, c) (global memory,
+// masked), each result handed to put(r, c, v): 8 x 8 output tiles over the
+// CTA's warps, DMMA with the B fragments loaded straight from global memory
+// (no staging), the k loop cut at the tile's diagonal (Li[r][k] = 0, k > r).
+template <class FB, class FO>
+__device__ void trmm_lower_g(int M, int N, const double *Li, int ld, FB bget, FO put) {
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int mt = pad8(M) >> 3, nt = pad8(N) >> 3;
+  for (int tile = warp; tile < mt * nt; tile += nw) {
+    const int m0 = (tile % mt) * 8, n0 = (tile / mt) * 8;
+    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;   // two independent DMMA chains
+    for (int k0 = 0; k0 <= m0; k0 += 8) {
+      dmma(d0, d1, Li[(m0 + g) + (k0 + q) * ld], bget(k0 + q, n0 + g));
+      dmma(e0, e1, Li[(m0 + g) + (k0 + 4 + q) * ld], bget(k0 + 4 + q, n0 + g));
+    }
+    put(m0 + g, n0 + 2 * q, d0 + e0);
+    put(m0 + g, n0 + 2 * q + 1, d1 + e1);
+  }
+}
+
+// Whitening, one step's block per CTA of kWhitenThreads:
+// the Cholesky factor in shared memory, its inverse by a blocked triangular
+// solve with the identity, then every whitened block as a triangular
+// product with the right-hand sides read straight from global memory.  Only
+// the two d x d factors live in shared memory (40 KB at d = 48: five CTAs
+// per SM instead of three 256-thread CTAs holding [F | I | c]), so several
+// serial Cholesky chains share each SM.
+constexpr int kWhitenThreads = 128;
+
+// Evolution blocks: K = Lam Lam^T; El = -Lam^{-1} F, Er = Lam^{-1}, e = Lam^{-1} c.
+__global__ void __launch_bounds__(kWhitenThreads) whiten_evo_kernel(WhitenArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int n = a.n, nn = n * n, tid = threadIdx.x;
   const int64_t i = blockIdx.x;
@@ -1215,36 +1240,26 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
   }
   KS_PROF_DECL
   const int64_t iK = (a.cntE == 1) ? 0 : i;
-  const int ld = ldpad(n), p = 2 * n + 1, cp = pad8(p) + 8;
-  double *Lm = sm, *X = Lm + ld * pad8(n), *sh = X + ld * cp;
+  const int ld = ldpad(n), np = pad8(n);
+  double *Lm = sm, *X = Lm + ld * np, *sh = X + ld * np;
   const double *K = a.K + iK * a.sK, *F = a.F + iK * a.sF;
   const double *c = a.c ? a.c + iK * a.sc : nullptr;
-  zero_smem(sm, ld * pad8(n) + ld * cp);
+  // general model: K_i's leading l_i block, F_i's first n_{i-1}
+  // columns, H_i (l_i x n_i; null: the identity's leading block)
+  const int li = a.l ? a.l[i] : (a.ns ? a.ns[i] : n), ni = a.ns ? a.ns[i] : n;
+  const int npv = (a.ns && i > 0) ? a.ns[i - 1] : n;
+  const double *Hv = a.Hev ? a.Hev + iK * a.sHev : nullptr;
+  zero_smem(sm, 2 * ld * np);
   __syncthreads();
   for (int k = tid; k < nn; k += blockDim.x) {   // asynchronous loads
     const int r = k / n, cc = k - r * n;
-    if (!a.chol || cc <= r) cp8(&Lm[r + cc * ld], K + k);   // KS_COV_IS_CHOL: lower triangle only
-    cp8(&X[r + cc * ld], F + k);
+    if (r < li && cc < li && (!a.chol || cc <= r)) cp8(&Lm[r + cc * ld], K + k);   // KS_COV_IS_CHOL: lower only
   }
   for (int r = tid; r < n; r += blockDim.x) {
-    X[r + (n + r) * ld] = 1.0;
-    X[r + 2 * n * ld] = c ? c[r] : 0.0;
+    X[r + r * ld] = 1.0;
+    if (r >= li) Lm[r + r * ld] = 1.0;   // identity beyond l_i
   }
   sync_loads();
-  if (a.Hev || a.l || a.ns) {   // general model: mask to l_i rows, H_i, n_{i-1} columns of F
-    const int li = a.l ? a.l[i] : (a.ns ? a.ns[i] : n), ni = a.ns ? a.ns[i] : n;
-    const int npv = (a.ns && i > 0) ? a.ns[i - 1] : n;
-    const double *Hv = a.Hev ? a.Hev + iK * a.sHev : nullptr;
-    for (int k = tid; k < nn; k += blockDim.x) {
-      const int r = k / n, cc = k - r * n;
-      if (r >= li || cc >= li) Lm[r + cc * ld] = (r == cc) ? 1.0 : 0.0;   // K_i: leading l_i block
-      if (r >= li || cc >= npv) X[r + cc * ld] = 0.0;
-      X[r + (n + cc) * ld] = (r < li && cc < ni) ? (Hv ? Hv[k] : (r == cc ? 1.0 : 0.0)) : 0.0;
-    }
-    for (int r = tid; r < n; r += blockDim.x)
-      if (r >= li) X[r + 2 * n * ld] = 0.0;
-    __syncthreads();
-  }
   KS_PROF(0)
   const bool ok = a.chol ? chol_diag_ok(Lm, ld, n, sh) : cta_chol(Lm, ld, n, sh);
   KS_PROF(1)
@@ -1254,20 +1269,37 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_evo_kernel(WhitenArgs a) {
   }
   diag_rcp(Lm, ld, n, sh);
   __syncthreads();
-  trsm_lower(Lm, ld, sh, n, X, ld, p);
+  trsm_lower(Lm, ld, sh, n, X, ld, n);   // X = Lam^{-1} (ends with a barrier)
   KS_PROF(2)
-  for (int k = tid; k < nn; k += blockDim.x) {
-    const int r = k / n, cc = k - r * n;
-    El[k] = -X[r + cc * ld];
-    Er[k] = X[r + (n + cc) * ld];
+  trmm_lower_g(
+      n, n, X, ld, [&](int k, int cc) { return (k < li && cc < npv) ? __ldg(F + k * n + cc) : 0.0; },
+      [&](int r, int cc, double v) {
+        if (r < n && cc < n) El[r * n + cc] = -v;
+      });
+  if (Hv) {
+    trmm_lower_g(
+        n, n, X, ld, [&](int k, int cc) { return (k < li && cc < ni) ? __ldg(Hv + k * n + cc) : 0.0; },
+        [&](int r, int cc, double v) {
+          if (r < n && cc < n) Er[r * n + cc] = v;
+        });
+  } else {
+    for (int k = tid; k < nn; k += blockDim.x) {
+      const int r = k / n, cc = k - r * n;
+      Er[k] = (cc < li && cc < ni) ? X[r + cc * ld] : 0.0;
+    }
   }
-  for (int r = tid; r < n; r += blockDim.x) e[r] = X[r + 2 * n * ld];
+  for (int r = tid; r < n; r += blockDim.x) {
+    double s = 0.0;
+    if (c)
+      for (int k = 0; k <= r && k < li; ++k) s = fma(X[r + k * ld], __ldg(c + k), s);
+    e[r] = s;
+  }
   KS_PROF(3)
   KS_PROF_PRINT("whiten evo: loads chol trsm store")
 }
 
 // Observation blocks: L = M M^T; C = M^{-1} H, y = M^{-1} o (rows >= m_i zero).
-__global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
+__global__ void __launch_bounds__(kWhitenThreads) whiten_obs_kernel(WhitenArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int n = a.n, mx = a.m_max, tid = threadIdx.x;
   const int64_t i = blockIdx.x;
@@ -1276,30 +1308,31 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
   const int rc = a.RC;
   double *C = a.C + i * (int64_t)rc * n;
   const int mx1 = mx > 0 ? mx : 1;   // (m_max = 0 with padding rows: no observation blocks)
-  const int ld = ldpad(mx1), p = n + 1, cp = pad8(p) + 8;
-  double *Lm = sm, *X = Lm + ld * pad8(mx1), *sh = X + ld * cp;
+  const int ld = ldpad(mx1), mp = pad8(mx1);
+  double *Lm = sm, *X = Lm + ld * mp, *sh = X + ld * mp;
   const double *L = a.L + i * a.sL, *H = a.H + i * a.sH, *o = a.o + i * a.so;
-  zero_smem(sm, ld * pad8(mx1) + ld * cp);
+  zero_smem(sm, 2 * ld * mp);
   __syncthreads();
   for (int k = tid; k < mi * mi; k += blockDim.x) {   // asynchronous loads
     const int r = k / mi, cc = k - r * mi;
     if (!a.chol || cc <= r) cp8(&Lm[r + cc * ld], L + r * mx + cc);   // KS_COV_IS_CHOL: lower only
   }
-  for (int k = tid; k < mi * n; k += blockDim.x) {
-    const int r = k / n, cc = k - r * n;
-    if (cc < ni) cp8(&X[r + cc * ld], H + r * n + cc);
-  }
-  for (int r = tid; r < mi; r += blockDim.x) cp8(&X[r + n * ld], o + r);
+  for (int r = tid; r < mi; r += blockDim.x) X[r + r * ld] = 1.0;
   sync_loads();
   const bool ok = a.chol ? chol_diag_ok(Lm, ld, mi, sh) : cta_chol(Lm, ld, mi, sh);
   if (tid == 0 && !ok) report(a.status, i, kBadL);
   diag_rcp(Lm, ld, mi, sh);
   __syncthreads();
-  trsm_lower(Lm, ld, sh, mi, X, ld, p);
-  for (int k = tid; k < rc * n; k += blockDim.x) {
-    const int r = k / n, cc = k - r * n;
-    // rows m_i .. m_i + n - n_i - 1: the padding rows e_k^T x_i = 0 (k >= n_i)
-    C[k] = (r < mi) ? X[r + cc * ld] : ((r - mi < n - ni && cc == ni + (r - mi)) ? 1.0 : 0.0);
+  trsm_lower(Lm, ld, sh, mi, X, ld, mi);   // X = M^{-1}
+  trmm_lower_g(
+      mi, n, X, ld, [&](int k, int cc) { return (k < mi && cc < ni) ? __ldg(H + k * n + cc) : 0.0; },
+      [&](int r, int cc, double v) {
+        if (r < mi && cc < n) C[r * n + cc] = v;
+      });
+  // rows m_i .. RC-1: the padding rows e_k^T x_i = 0 (k >= n_i), then zeros
+  for (int k = tid; k < (rc - mi) * n; k += blockDim.x) {
+    const int r = mi + k / n, cc = k % n;
+    C[r * n + cc] = (r - mi < n - ni && cc == ni + (r - mi)) ? 1.0 : 0.0;
   }
   if (a.Mall) {   // KS_KEEP_WHITENING: M_i for ks_update_obs
     for (int k = tid; k < mx * mx; k += blockDim.x) {
@@ -1308,7 +1341,12 @@ __global__ void __launch_bounds__(kThreads, 3) whiten_obs_kernel(WhitenArgs a) {
     }
   }
   if (!a.constC) {
-    for (int r = tid; r < rc; r += blockDim.x) a.y[i * rc + r] = (r < mi) ? X[r + n * ld] : 0.0;
+    for (int r = tid; r < rc; r += blockDim.x) {
+      double s = 0.0;
+      if (r < mi)
+        for (int k = 0; k <= r; ++k) s = fma(X[r + k * ld], __ldg(o + k), s);
+      a.y[i * rc + r] = s;
+    }
   } else {
     for (int k = tid; k < mi * mi; k += blockDim.x) {
       const int r = k / mi, cc = k - r * mi;
@@ -1334,9 +1372,10 @@ __global__ void whiten_y_kernel(WhitenArgs a) {
   }
 }
 
-size_t whiten_evo_smem(int n) { return 8 * ((size_t)ldpad(n) * pad8(n) + (size_t)ldpad(n) * (pad8(2 * n + 1) + 8) + pad8(n) + 8); }
+size_t whiten_evo_smem(int n) { return 8 * (2 * (size_t)ldpad(n) * pad8(n) + pad8(n) + 8); }
 size_t whiten_obs_smem(int n, int mx) {
-  return 8 * ((size_t)ldpad(mx) * pad8(mx) + (size_t)ldpad(mx) * (pad8(n + 1) + 8) + pad8(mx) + 8);
+  (void)n;
+  return 8 * (2 * (size_t)ldpad(mx) * pad8(mx) + pad8(mx) + 8);
 }
 
 }  // namespace
@@ -1371,9 +1410,9 @@ cudaError_t launch_whiten(const WhitenArgs &a, cudaStream_t s) {
   set_smem_attr((const void *)whiten_evo_kernel, 227 * 1024);
   set_smem_attr((const void *)whiten_obs_kernel, 227 * 1024);
   const int n = a.n, mx = a.m_max;
-  whiten_evo_kernel<<<(unsigned)a.cntE, kThreads, whiten_evo_smem(n), s>>>(a);
+  whiten_evo_kernel<<<(unsigned)a.cntE, kWhitenThreads, whiten_evo_smem(n), s>>>(a);
   if (a.RC > 0) {
-    whiten_obs_kernel<<<(unsigned)a.cntC, kThreads, whiten_obs_smem(n, mx > 0 ? mx : 1), s>>>(a);
+    whiten_obs_kernel<<<(unsigned)a.cntC, kWhitenThreads, whiten_obs_smem(n, mx > 0 ? mx : 1), s>>>(a);
     if (a.constC) {
       const int T = 256;
       whiten_y_kernel<<<(unsigned)((a.N + T - 1) / T), T, 8 * (size_t)mx * mx, s>>>(a);

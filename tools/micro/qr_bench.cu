@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads) panel_bench_kernel(int rows, int rep
   if (threadIdx.x < 32) {
     long long t0 = clock64();
     for (int rep = 0; rep < reps; ++rep) {
-      qr_panel<3>(A, lda, 0, rows, 8, w.v1[0], w.beta[0], w.T[0], w.G);
+      qr_panel<3>(A, lda, 0, rows, 8, w.v1(0), w.beta(0), w.T(0), w.G);
     }
     long long t1 = clock64();
     if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = (t1 - t0) / reps;
