@@ -441,55 +441,69 @@ def main():
         streams = [stream] + [torch.cuda.Stream(dev) for _ in range(nctx - 1)]
         ctxs = [ks.Smoother(local_p, device=dev, stream=st, host_inputs=True, bind_outputs=False, dist=kd)
                 for st in streams]
-        outs = [(torch.empty((M, p.n), dtype=torch.float64).pin_memory(),
-                 torch.empty((M, p.n, p.n), dtype=torch.float64).pin_memory()) for _ in range(nctx)]
         h2d = sum(t.numel() * t.element_size() for t in ctxs[0].inputs.values() if t is not None)
-        d2h = outs[0][0].numel() * 8 + outs[0][1].numel() * 8
         ke = max(2, min(a.steps, 6))
+        pk = p.n * (p.n + 1) // 2
 
-        def e2e_step(k):
-            c = ctxs[k % nctx]
-            with torch.cuda.stream(streams[k % nctx]):
-                c.whiten()
-                c.factor()
-                if host_x:
-                    snd, rcv = c.boundary_tensors()
-                    sh = snd.cpu()
-                    rh = torch.empty(P * sh.numel(), dtype=torch.uint8)
-                    kdist.exchange_boundary(sh, rh)
-                    rcv.copy_(rh.to(dev))
-                    c.factor_boundary()
-                c.solve_selinv()
-                c.get(*outs[k % nctx], sync=False)
+        def run_e2e(packed):
+            # packed: ks_get_packed (S_ii symmetric: its upper triangle by
+            # rows, n(n+1)/2 of the n^2 doubles, written straight into pinned
+            # host memory); else ks_get_async of the full n x n blocks
+            outs = [(torch.empty((M, p.n), dtype=torch.float64).pin_memory(),
+                     torch.empty((M, pk) if packed else (M, p.n, p.n), dtype=torch.float64).pin_memory())
+                    for _ in range(nctx)]
+            d2h = outs[0][0].numel() * 8 + outs[0][1].numel() * 8
 
-        for k in range(max(a.warmup, 1) * nctx):
-            e2e_step(k)
-        torch.cuda.synchronize()
-        for c in ctxs:
-            c.check()
-        if P > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for st in streams[1:]:
-            st.wait_event(e0)
-        for k in range(ke):
-            e2e_step(k)
-        ends = []
-        for st in streams:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(st)
-            ends.append(ev)
-        torch.cuda.synchronize()
-        mse = max(e0.elapsed_time(ev) for ev in ends) / ke
-        if P > 1:
-            mse = kdist.max_over_ranks(mse, None if host_x else dev)
-        e2e = {"value": N / (mse / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * P),
-               "d2h_bytes_per_step": int(d2h * P), "ms_per_step": mse, "steps": ke,
-               "path": "ks_create(KS_HOST_INPUTS) pinned host inputs -> whiten(H2D) .. solve_selinv -> "
-                       "ks_get_async(pinned host states, cov)" +
-                       (f"; {nctx} contexts on {nctx} streams take alternate steps (copies overlap the "
-                        f"other context's work)" if nctx > 1 else "")}
+            def e2e_step(k):
+                c = ctxs[k % nctx]
+                with torch.cuda.stream(streams[k % nctx]):
+                    c.whiten()
+                    c.factor()
+                    if host_x:
+                        snd, rcv = c.boundary_tensors()
+                        sh = snd.cpu()
+                        rh = torch.empty(P * sh.numel(), dtype=torch.uint8)
+                        kdist.exchange_boundary(sh, rh)
+                        rcv.copy_(rh.to(dev))
+                        c.factor_boundary()
+                    c.solve_selinv()
+                    if packed:
+                        c.get_packed(*outs[k % nctx], sync=False)
+                    else:
+                        c.get(*outs[k % nctx], sync=False)
+
+            for k in range(max(a.warmup, 1) * nctx):
+                e2e_step(k)
+            torch.cuda.synchronize()
+            for c in ctxs:
+                c.check()
+            if P > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for st in streams[1:]:
+                st.wait_event(e0)
+            for k in range(ke):
+                e2e_step(k)
+            ends = []
+            for st in streams:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(st)
+                ends.append(ev)
+            torch.cuda.synchronize()
+            mse = max(e0.elapsed_time(ev) for ev in ends) / ke
+            if P > 1:
+                mse = kdist.max_over_ranks(mse, None if host_x else dev)
+            return {"value": N / (mse / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d * P),
+                    "d2h_bytes_per_step": int(d2h * P), "ms_per_step": mse, "steps": ke,
+                    "path": "ks_create(KS_HOST_INPUTS) pinned host inputs -> whiten(H2D) .. solve_selinv -> " +
+                            ("ks_get_packed(pinned host states, covariance upper triangles n(n+1)/2 per step)"
+                             if packed else "ks_get_async(pinned host states, full n x n covariances)") +
+                            (f"; {nctx} contexts on {nctx} streams take alternate steps (copies overlap the "
+                             f"other context's work)" if nctx > 1 else "")}
+
+        e2e = run_e2e(True)
+        e2e["full_cov"] = run_e2e(False)
         del ctxs
         torch.cuda.empty_cache()
 

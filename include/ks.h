@@ -223,6 +223,20 @@ int ks_get(ks_ctx *ctx, double *states, double *cov);
  * are valid once the stream has been synchronised. */
 int ks_get_async(ks_ctx *ctx, double *states, double *cov);
 
+/* ks_get with the covariance blocks in PACKED symmetric form: S_ii is
+ * symmetric (reading R13: every path stores it exactly symmetric), so
+ * only its upper triangle is returned, row by row -- cov_packed[i * P + k],
+ * P = n (n + 1) / 2, k enumerating (r, c) with r <= c for r = 0 .. n-1 and
+ * c = r .. n-1 -- which carries the whole result in P / n^2 of the bytes
+ * (21 of 36 doubles at n = 6; the host-copy volume of an end-to-end solve).
+ * cov_packed (N * P doubles) is device memory or PAGE-LOCKED host memory
+ * (pinned / registered): a kernel on the context's stream writes it
+ * directly (host destinations over PCIe, no staging buffer).  Pageable host
+ * memory is KS_ERR_ARG.  states as in ks_get.  sync != 0 synchronises the
+ * stream when a destination is on the host (ks_get), sync == 0 only enqueues
+ * (ks_get_async).  Needs a prior ks_selinv (KS_ERR_ORDER otherwise). */
+int ks_get_packed(ks_ctx *ctx, double *states, double *cov_packed, int sync);
+
 /* Synchronise the stream and report the first numerical failure:
  * KS_OK, KS_ERR_NOT_SPD (bad_kind 1 = K, 2 = L), KS_ERR_RANK, or (small path,
  * n, m_max <= 8) KS_ERR_ARG with bad_kind 3 when a whitened block column's

@@ -1131,6 +1131,66 @@ static int get_impl(ks_ctx *c, double *states, double *cov, bool sync_host);
 
 int ks_get(ks_ctx *c, double *states, double *cov) { return get_impl(c, states, cov, true); }
 
+namespace {
+// S (N x n x n, row-major blocks) -> the upper triangles by rows (ks_get_packed)
+__global__ void pack_cov_kernel(const double *__restrict__ S, int64_t N, int n, double *__restrict__ out) {
+  const int P = n * (n + 1) / 2;
+  const int64_t total = N * P;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / P;
+    int rem = (int)(idx - i * P), r = 0;
+    while (rem >= n - r) {
+      rem -= n - r;
+      ++r;
+    }
+    out[idx] = __ldg(S + i * n * n + (int64_t)r * n + r + rem);
+  }
+}
+}  // namespace
+
+int ks_get_packed(ks_ctx *c, double *states, double *cov_packed, int sync) {
+  if (!c) return KS_ERR_ARG;
+  if ((states && !c->solved) || (cov_packed && !c->covd)) return KS_ERR_ORDER;
+  double *dst = cov_packed;
+  bool host = false;
+  if (cov_packed) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, cov_packed) != cudaSuccess) {
+      cudaGetLastError();
+      return KS_ERR_ARG;
+    }
+    if (at.type == cudaMemoryTypeHost) {   // page-locked: the kernel writes through its device alias
+      if (!at.devicePointer) return KS_ERR_ARG;
+      dst = (double *)at.devicePointer;
+      host = true;
+    } else if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) {
+      return KS_ERR_ARG;   // pageable host memory
+    }
+  }
+  int r = get_impl(c, states, nullptr, false);
+  if (r != KS_OK) return r;
+  if (cov_packed && c->N > 0) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t total = c->N * (int64_t)(c->n * (c->n + 1) / 2);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    pack_cov_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->Sout, c->N, c->n, dst);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  if (sync) {
+    bool hs = host;
+    if (states) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, states) != cudaSuccess) { cudaGetLastError(); hs = true; }
+      else if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) hs = true;
+    }
+    if (hs) return cuda_fail(cudaStreamSynchronize(c->stream));
+  }
+  return KS_OK;
+}
+
 int ks_get_async(ks_ctx *c, double *states, double *cov) { return get_impl(c, states, cov, false); }
 
 static int get_impl(ks_ctx *c, double *states, double *cov, bool sync_host) {

@@ -31,7 +31,7 @@ EXPORTS = ("ks_workspace_bytes", "ks_create", "ks_whiten", "ks_factor", "ks_solv
            "ks_set_timing", "ks_get_timing", "ks_get_launch_times", "ks_info",
            "ks_peak_fp64_tflops", "ks_strerror", "ks_destroy",
            "ks_dist_unique_id", "ks_dist_create", "ks_dist_info", "ks_dist_destroy",
-           "ks_level_of_steps", "ks_update_obs", "ks_get_async")
+           "ks_level_of_steps", "ks_update_obs", "ks_get_async", "ks_get_packed")
 
 
 class KsError(RuntimeError):
@@ -78,6 +78,7 @@ def lib():
             getattr(L, f).argtypes = [vp]
         L.ks_get.argtypes = [vp, vp, vp]
         L.ks_get_async.argtypes = [vp, vp, vp]
+        L.ks_get_packed.argtypes = [vp, vp, vp, i32]
         L.ks_update_obs.argtypes = [vp, vp]
         L.ks_sync_status.argtypes = [vp, C.POINTER(i64), C.POINTER(i32)]
         L.ks_boundary_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(sz)]
@@ -311,6 +312,14 @@ class Smoother:
         fn = self.L.ks_get if sync else self.L.ks_get_async
         _check(fn(self.ctx, sp, cp), "ks_get" if sync else "ks_get_async")
         return states, cov
+
+    def get_packed(self, states=None, cov_packed=None, sync: bool = True):
+        """ks_get_packed: covariance blocks as their upper triangles by rows
+        (N x n(n+1)/2) into a device tensor or a PINNED host tensor."""
+        sp = None if states is None else states.data_ptr()
+        cp = None if cov_packed is None else cov_packed.data_ptr()
+        _check(self.L.ks_get_packed(self.ctx, sp, cp, 1 if sync else 0), "ks_get_packed")
+        return states, cov_packed
 
     def sync_status(self):
         st, kd = C.c_int64(-1), C.c_int(0)

@@ -183,6 +183,41 @@ def test_host_inputs_and_get():
     assert np.array_equal(xa.numpy(), x1) and np.array_equal(Sa.numpy(), S1)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["c2", "c4", "c1"])
+def test_get_packed(case):
+    """ks_get_packed: the upper triangles by rows of the covariance blocks
+    equal the full blocks' (bitwise), into device memory, pinned host memory
+    (written by the kernel over PCIe) and asynchronously; pageable host
+    memory and a missing ks_selinv are rejected."""
+    p = gen.make(case, N={"c2": 1500, "c4": 45, "c1": 7}[case])
+    x1, S1, _ = gpu_smooth(p)
+    n = p.n
+    iu = np.triu_indices(n)
+    want = S1[:, iu[0], iu[1]]
+    s = ks().Smoother(p, host_inputs=True, bind_outputs=False)
+    s.run()
+    Pk = n * (n + 1) // 2
+    dev = torch.full((p.N, Pk), np.nan, dtype=torch.float64, device="cuda")
+    xd = torch.empty((p.N, n), dtype=torch.float64, device="cuda")
+    s.get_packed(xd, dev)
+    assert np.array_equal(dev.cpu().numpy(), want) and np.array_equal(xd.cpu().numpy(), x1)
+    hp = torch.full((p.N, Pk), np.nan, dtype=torch.float64).pin_memory()
+    xh = torch.empty((p.N, n), dtype=torch.float64).pin_memory()
+    s.get_packed(xh, hp)
+    assert np.array_equal(hp.numpy(), want) and np.array_equal(xh.numpy(), x1)
+    ha = torch.full((p.N, Pk), np.nan, dtype=torch.float64).pin_memory()
+    s.get_packed(None, ha, sync=False)
+    s.stream.synchronize()
+    assert np.array_equal(ha.numpy(), want)
+    with pytest.raises(ks().KsError):
+        s.get_packed(None, torch.empty((p.N, Pk), dtype=torch.float64))   # pageable
+    s2 = ks().Smoother(p)
+    s2.whiten(); s2.factor(); s2.solve()
+    with pytest.raises(ks().KsError):
+        s2.get_packed(None, dev)
+
+
 def test_level_count():
     for N in (1, 2, 3, 7, 8, 9, 1000, 4096):
         s = ks().Smoother(gen.make("c1", N=max(N, 2)) if N > 1 else gen.random_problem(
