@@ -218,6 +218,22 @@ def test_get_packed(case):
         s2.get_packed(None, dev)
 
 
+@pytest.mark.parametrize("eps", [1e-3, 1e-6])
+def test_cta_panel_gram_guard(eps):
+    """The CTA path's Gram-downdated Householder panel (DESIGN reading R28):
+    observation and evolution matrices whose odd columns nearly repeat the
+    even ones (relative difference eps) make the stacked block columns of
+    every stage-1 panel nearly pairwise dependent, so the downdated norms
+    cancel and the accuracy guard recomputes the Gram exactly (counted in
+    the profiling build; tools/micro/qr_bench.cu checks the same at the QR
+    level).  The smoothed results still match the oracle."""
+    p = gen.make("c4", N=45)
+    rng = np.random.default_rng(7)
+    for A in (p.H, p.F):
+        A[..., 1::2] = A[..., 0::2] + eps * rng.standard_normal(A[..., 0::2].shape)
+    assert_parity(p, generic=True)
+
+
 def test_level_count():
     for N in (1, 2, 3, 7, 8, 9, 1000, 4096):
         s = ks().Smoother(gen.make("c1", N=max(N, 2)) if N > 1 else gen.random_problem(
