@@ -468,6 +468,15 @@ __device__ void qr_apply(double *A, int lda, int k0, int mpad, int nb, const QrW
 // right of panel k+1, warp 0 applies them to panel k+1's own 8 columns and
 // factors it at once, so the serial panel chain (the QR's critical path)
 // no longer waits for the trailing update; one barrier per panel.
+// The blocked QR is inlined at its call sites (an out-of-line copy costs
+// caller/callee register saves through local memory, which misses the small
+// L1 left beside 222 KB of shared memory: c4 factor L0 8.23 vs 8.89 ms); the
+// panels (the bulk of the code) stay out of line, one copy per height.
+#ifdef KS_QRB_NOINLINE   // A/B
+#define KS_QRB_INLINE __device__ __noinline__
+#else
+#define KS_QRB_INLINE __device__ __forceinline__
+#endif
 __device__ __forceinline__ void group_sync(int barid, int nw) {
   if (barid == 0) __syncthreads();
   else asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(nw * 32) : "memory");
@@ -476,7 +485,7 @@ template <int MR>
 __device__ __forceinline__ void qr_panel_mr(double *A, int lda, int k0, int rows, int nb, const QrWs w, int b) {
   qr_panel<MR>(A, lda, k0, rows, nb, w.v1(b), w.beta(b), w.T(b), w.G);
 }
-__device__ __noinline__ void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, const QrWs w, long long *acc = nullptr,
+KS_QRB_INLINE void qr_blocked(double *A, int lda, int rows, int npiv, int ncols, const QrWs w, long long *acc = nullptr,
                            int wbase = 0, int nw = kWarps, int barid = 0) {
   const int warp = (threadIdx.x >> 5) - wbase;
   double *sc = w.tile + warp * (kLdw * 8);
