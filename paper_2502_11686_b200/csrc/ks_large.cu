@@ -860,7 +860,9 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     pf_l2(in.y + (t + 1) * in.sy, RC);
   }
   double pt = 0.0, pu = 0.0;
-  if (l0n && hr && t + 2 < a.K) pu = part_sumsq(in.El + (t + 2) * in.sEl, n * n);
+  // |El_{t+2}|: pulled into L2 now, summed after stage 1 (its loads then hit L2)
+  const bool el2 = l0n && hr && t + 2 < a.K;
+  if (el2) pf_l2(in.El + (t + 2) * in.sEl, (int64_t)n * n);
 
   // ---- stage 1 ----
   zero_smem(S1, ld1 * f.cols1);
@@ -882,6 +884,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   KS_PROF(3)
   qr_blocked(S1, ld1, RC + n, n, 2 * n + 1, w, qacc);
   KS_PROF(1)
+  if (el2) pu += part_sumsq(in.El + (t + 2) * in.sEl, n * n);
 
   if (f.conc && hr && hl) {
     // ---- stages 2 and 3 concurrently: independent QRs once stage 1 is done.
@@ -1021,11 +1024,10 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   if (hr && tid == 0) a.next[pnext * entry_doubles(n) + 3 * n * n + 2 * n] = nrm_u;
 
   // ---- R record: rank check, T = R^{-1}[R_l R_r], w = R^{-1} z, P = R^{-1} R^{-T} ----
-  if (tid == 0) {
-    const double thr = kRankTol * nrm_t;
-    bool bad = false;
-    for (int d = 0; d < n; ++d) bad |= !(fabs(P2[d + d * ld2]) > thr);
-    if (bad) report(a.status, (((t + 1) << (a.level - a.lbase)) - 1) + a.step0, kBadRank);
+  {   // one diagonal entry per thread, one CTA vote
+    const bool bad_d = tid < n && !(fabs(P2[tid + tid * ld2]) > kRankTol * nrm_t);
+    if (__syncthreads_or(bad_d) && tid == 0)
+      report(a.status, (((t + 1) << (a.level - a.lbase)) - 1) + a.step0, kBadRank);
   }
   const int ldr = ldpad(n), np = pad8(n);
   // R_tt copied into a zero-padded block (the blocked solves read whole 8x8
