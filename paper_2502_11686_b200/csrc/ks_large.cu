@@ -1101,20 +1101,23 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorLevelArgs 
 }
 
 // ---- backward ----
+// Shared memory of the backward kernel: T = [T_l | T_r] (T_r at column np),
+// the three blocks of S_II = [S_ll S_lr; S_lr^T S_rr] (S_lr^T is read
+// transposed, not stored), the states.  S_{t,I} overwrites S_ll / S_rr
+// column block by column block and S_tt lands in S_lr's place, so the CTA
+// needs 101 KB at n = 48: two CTAs per SM.
 struct BwdPlan {
-  int ldt, ldS, ldp, offS, offStI, offP, offx, total;
+  int ldt, np, offLL, offLR, offRR, offx, total;
 };
 __host__ __device__ inline BwdPlan bwd_plan(int n) {
   BwdPlan b;
   b.ldt = ldpad(n);
-  b.ldS = ldpad(2 * n);
-  b.ldp = ldpad(n);
-  const int ct = pad8(2 * n);
-  b.offS = b.ldt * ct;
-  b.offStI = b.offS + b.ldS * ct;
-  b.offP = b.offStI + b.ldt * ct;
-  b.offx = b.offP + b.ldp * pad8(n);
-  b.total = b.offx + 4 * pad8(n);
+  b.np = pad8(n);
+  b.offLL = b.ldt * 2 * b.np;
+  b.offLR = b.offLL + b.ldt * b.np;
+  b.offRR = b.offLR + b.ldt * b.np;
+  b.offx = b.offRR + b.ldt * b.np;
+  b.total = b.offx + 4 * b.np;
   return b;
 }
 
@@ -1122,18 +1125,19 @@ __host__ __device__ inline BwdPlan bwd_plan(int n) {
 //   x_t     = w - T_l x_l - T_r x_r
 //   S_{t,I} = -T S_II      (T = [T_l T_r], S_II = [S_ll S_lr; S_lr^T S_rr])
 //   S_tt    = P - S_{t,I} T^T, symmetrised (reading R13)
-// both products on the FP64 tensor cores.  S_lr (= S_{t-1,t+1}) is the cross
-// block stored at level L+1; S_{t-1,t} = S_tl^T and S_{t,t+1} = S_tr are
-// stored for level L-1.
-__global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelArgs a) {
+// both products on the FP64 tensor cores (P enters as the accumulator,
+// read from the R record).  S_lr (= S_{t-1,t+1}) is the cross block stored
+// at level L+1; S_{t-1,t} = S_tl^T and S_{t,t+1} = S_tr are stored for level
+// L-1.
+__global__ void __launch_bounds__(kThreads, 2) backward_level_kernel(BackwardLevelArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int n = a.n, nn = n * n, tid = threadIdx.x;
   const BwdPlan bp = bwd_plan(n);
   const int64_t b = blockIdx.x, t = 2 * b;
   if (t >= a.K) return;
   const bool hl = (t + a.t0) > 0, hr = (t + 1) < a.K;
-  double *TT = sm, *SII = sm + bp.offS, *StI = sm + bp.offStI, *Pm = sm + bp.offP, *xv = sm + bp.offx;
-  const int ldt = bp.ldt, ldS = bp.ldS, ldp = bp.ldp, np = pad8(n), n2p = pad8(2 * n);
+  const int ldt = bp.ldt, np = bp.np, mt = np >> 3;
+  double *TT = sm, *Sll = sm + bp.offLL, *Slr = sm + bp.offLR, *Srr = sm + bp.offRR, *xv = sm + bp.offx;
   const double *rec = a.rrec + b * rrec_doubles(n);
   const int64_t step = 1ll << a.shift;
   const int64_t j = ((t + 1) << a.shift) - 1, jl = j - step, jr = j + step;
@@ -1142,15 +1146,14 @@ __global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelA
   for (int idx = tid; idx < nn; idx += blockDim.x) {   // asynchronous: all blocks in flight at once
     const int r = idx / n, c = idx - r * n;
     cp8(&TT[r + c * ldt], rec + idx);
-    cp8(&TT[r + (n + c) * ldt], rec + nn + idx);
-    cp8(&Pm[r + c * ldp], rec + 2 * nn + idx);
+    cp8(&TT[r + (np + c) * ldt], rec + nn + idx);
   }
   if (a.do_state) {
     const double *xlp = hl ? (jl < 0 ? a.xhalo : a.x + jl * n) : nullptr;
     const double *xrp = hr ? a.x + jr * n : nullptr;
     for (int i = tid; i < n; i += blockDim.x) {
       xv[i] = xlp ? xlp[i] : 0.0;
-      xv[n + i] = xrp ? xrp[i] : 0.0;
+      xv[np + i] = xrp ? xrp[i] : 0.0;
     }
   }
   if (a.do_cov) {
@@ -1159,45 +1162,103 @@ __global__ void __launch_bounds__(kThreads) backward_level_kernel(BackwardLevelA
     const double *Sx = (hl && hr) ? a.Xup + b * nn : nullptr;   // slot b-1: S_{t-1,t+1}
     for (int idx = tid; idx < nn; idx += blockDim.x) {
       const int r = idx / n, c = idx - r * n;
-      if (Sl) cp8(&SII[r + c * ldS], Sl + idx);
-      if (Sr) cp8(&SII[(n + r) + (n + c) * ldS], Sr + idx);
-      if (Sx) {
-        cp8(&SII[r + (n + c) * ldS], Sx + idx);
-        cp8(&SII[(n + c) + r * ldS], Sx + idx);
-      }
+      if (Sl) cp8(&Sll[r + c * ldt], Sl + idx);
+      if (Sr) cp8(&Srr[r + c * ldt], Sr + idx);
+      if (Sx) cp8(&Slr[r + c * ldt], Sx + idx);
     }
   }
   sync_loads();
   if (a.do_state) {
     for (int i = tid; i < n; i += blockDim.x) {
       double s = rec[3 * nn + i];
-      for (int k = 0; k < 2 * n; ++k) s = fma(-TT[i + k * ldt], xv[k], s);
+      for (int k = 0; k < n; ++k) s = fma(-TT[i + k * ldt], xv[k], s);
+      for (int k = 0; k < n; ++k) s = fma(-TT[i + (np + k) * ldt], xv[np + k], s);
       a.x[j * n + i] = s;
     }
   }
   if (!a.do_cov) return;
-  gemm<false, false>(np, n2p, n2p, -1.0, TT, ldt, SII, ldS, 0.0, StI, ldt);   // S_{t,I} = -T S_II
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int nw = blockDim.x >> 5;
+  // S_{t,I} = -T S_II: output tile (row tile i, column block cb of 2 mt); the
+  // tiles of a warp stay in registers until every warp has read S_II, then
+  // overwrite S_ll (left half) / S_rr (right half) in place
+  constexpr int kMaxT = 16;   // tiles per warp (mt <= 8: n <= 64)
+  double acc0[kMaxT], acc1[kMaxT];
+  const int ntile = mt * 2 * mt;
+#pragma unroll
+  for (int u = 0; u < kMaxT; ++u) {
+    acc0[u] = 0.0;
+    acc1[u] = 0.0;
+    const int tile = warp + u * nw;
+    if (tile < ntile) {
+      const int i = tile % mt, cb = tile / mt, m0 = i * 8;
+      const bool left = cb < mt;
+      const int c0 = (left ? cb : cb - mt) * 8;
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+      for (int k0 = 0; k0 < np; k0 += 8) {   // k < np: T_l times [S_ll | S_lr]
+        const double *B = left ? Sll : Slr;
+        dmma(d0, d1, TT[(m0 + g) + (k0 + q) * ldt], B[(k0 + q) + (c0 + g) * ldt]);
+        dmma(e0, e1, TT[(m0 + g) + (k0 + 4 + q) * ldt], B[(k0 + 4 + q) + (c0 + g) * ldt]);
+      }
+      for (int k0 = 0; k0 < np; k0 += 8) {   // k >= np: T_r times [S_lr^T | S_rr]
+        const double b0 = left ? Slr[(c0 + g) + (k0 + q) * ldt] : Srr[(k0 + q) + (c0 + g) * ldt];
+        const double b1 = left ? Slr[(c0 + g) + (k0 + 4 + q) * ldt] : Srr[(k0 + 4 + q) + (c0 + g) * ldt];
+        dmma(d0, d1, TT[(m0 + g) + (np + k0 + q) * ldt], b0);
+        dmma(e0, e1, TT[(m0 + g) + (np + k0 + 4 + q) * ldt], b1);
+      }
+      acc0[u] = -(d0 + e0);
+      acc1[u] = -(d1 + e1);
+    }
+  }
   __syncthreads();
-  gemm<false, true>(np, np, n2p, -1.0, StI, ldt, TT, ldt, 1.0, Pm, ldp);     // S_tt = P - S_{t,I} T^T
+#pragma unroll
+  for (int u = 0; u < kMaxT; ++u) {
+    const int tile = warp + u * nw;
+    if (tile < ntile) {
+      const int i = tile % mt, cb = tile / mt, m0 = i * 8;
+      double *D = cb < mt ? Sll : Srr;
+      const int c0 = (cb < mt ? cb : cb - mt) * 8;
+      D[(m0 + g) + (c0 + 2 * q) * ldt] = acc0[u];
+      D[(m0 + g) + (c0 + 2 * q + 1) * ldt] = acc1[u];
+    }
+  }
+  __syncthreads();
+  // S_tt = P - S_{t,I} T^T, P the accumulator (R record, row-major), into S_lr's place
+  const double *Pg = rec + 2 * nn;
+  for (int tile = warp; tile < mt * mt; tile += nw) {
+    const int m0 = (tile % mt) * 8, n0 = (tile / mt) * 8, r = m0 + g, c = n0 + 2 * q;
+    double d0 = (r < n && c < n) ? Pg[r * n + c] : 0.0, d1 = (r < n && c + 1 < n) ? Pg[r * n + c + 1] : 0.0;
+    double e0 = 0.0, e1 = 0.0;
+    for (int k0 = 0; k0 < np; k0 += 8) {
+      dmma(d0, d1, -Sll[(m0 + g) + (k0 + q) * ldt], TT[(n0 + g) + (k0 + q) * ldt]);
+      dmma(e0, e1, -Sll[(m0 + g) + (k0 + 4 + q) * ldt], TT[(n0 + g) + (k0 + 4 + q) * ldt]);
+    }
+    for (int k0 = 0; k0 < np; k0 += 8) {
+      dmma(d0, d1, -Srr[(m0 + g) + (k0 + q) * ldt], TT[(n0 + g) + (np + k0 + q) * ldt]);
+      dmma(e0, e1, -Srr[(m0 + g) + (k0 + 4 + q) * ldt], TT[(n0 + g) + (np + k0 + 4 + q) * ldt]);
+    }
+    Slr[r + c * ldt] = d0 + e0;
+    Slr[r + (c + 1) * ldt] = d1 + e1;
+  }
   __syncthreads();
   double *So = a.S + j * nn;
   for (int idx = tid; idx < nn; idx += blockDim.x) {
     const int r = idx / n, c = idx - r * n;
-    So[idx] = 0.5 * (Pm[r + c * ldp] + Pm[c + r * ldp]);
+    So[idx] = 0.5 * (Slr[r + c * ldt] + Slr[c + r * ldt]);
   }
   if (a.Xcur) {
     if (hl) {
       double *X = a.Xcur + t * nn;                   // slot t-1: S_{t-1,t} = S_tl^T
       for (int idx = tid; idx < nn; idx += blockDim.x) {
         const int r = idx / n, c = idx - r * n;
-        X[idx] = StI[c + r * ldt];
+        X[idx] = Sll[c + r * ldt];
       }
     }
     if (hr) {
       double *X = a.Xcur + (t + 1) * nn;             // slot t: S_{t,t+1} = S_tr
       for (int idx = tid; idx < nn; idx += blockDim.x) {
         const int r = idx / n, c = idx - r * n;
-        X[idx] = StI[r + (n + c) * ldt];
+        X[idx] = Srr[r + c * ldt];
       }
     }
   }
@@ -1412,6 +1473,8 @@ cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s) {
 
 cudaError_t launch_backward_level(const BackwardLevelArgs &a, cudaStream_t s) {
   set_smem_attr((const void *)backward_level_kernel, 227 * 1024);
+  const int mt = pad8(a.n) / 8;
+  if (mt * 2 * mt > 16 * kWarps) return cudaErrorInvalidValue;   // n <= 64 (the kernel's register tiles)
   const int64_t grid = (a.K + 1) / 2;
   backward_level_kernel<<<(unsigned)grid, kThreads, backward_smem_bytes(a.n), s>>>(a);
   return cudaGetLastError();
