@@ -1129,6 +1129,7 @@ __host__ __device__ inline BwdPlan bwd_plan(int n) {
 // read from the R record).  S_lr (= S_{t-1,t+1}) is the cross block stored
 // at level L+1; S_{t-1,t} = S_tl^T and S_{t,t+1} = S_tr are stored for level
 // L-1.
+template <int kRB>
 __global__ void __launch_bounds__(kThreads, 2) backward_level_kernel(BackwardLevelArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int n = a.n, nn = n * n, tid = threadIdx.x;
@@ -1179,66 +1180,86 @@ __global__ void __launch_bounds__(kThreads, 2) backward_level_kernel(BackwardLev
   if (!a.do_cov) return;
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const int nw = blockDim.x >> 5;
-  // S_{t,I} = -T S_II: output tile (row tile i, column block cb of 2 mt); the
-  // tiles of a warp stay in registers until every warp has read S_II, then
-  // overwrite S_ll (left half) / S_rr (right half) in place
-  constexpr int kMaxT = 16;   // tiles per warp (mt <= 8: n <= 64)
-  double acc0[kMaxT], acc1[kMaxT];
-  const int ntile = mt * 2 * mt;
+  // S_{t,I} = -T S_II: work item = kRB vertically adjacent row tiles of one
+  // column block (of 2 mt), sharing each B fragment (fewer shared-memory
+  // loads per DMMA); the items of a warp stay in registers until every warp
+  // has read S_II, then overwrite S_ll (left half) / S_rr (right half)
+  constexpr int kMaxI = 4;   // items per warp: ceil(mt / kRB) * 2 mt <= kMaxI * nw (kRB = 3: n <= 48, 4: n <= 64)
+  const int rb = (mt + kRB - 1) / kRB, nitem = rb * 2 * mt;
+  double acc[kMaxI][kRB][2];
 #pragma unroll
-  for (int u = 0; u < kMaxT; ++u) {
-    acc0[u] = 0.0;
-    acc1[u] = 0.0;
-    const int tile = warp + u * nw;
-    if (tile < ntile) {
-      const int i = tile % mt, cb = tile / mt, m0 = i * 8;
+  for (int u = 0; u < kMaxI; ++u) {
+    const int item = warp + u * nw;
+#pragma unroll
+    for (int v = 0; v < kRB; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+    if (item < nitem) {
+      const int i0 = (item % rb) * kRB, cb = item / rb;
       const bool left = cb < mt;
       const int c0 = (left ? cb : cb - mt) * 8;
-      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      for (int k0 = 0; k0 < np; k0 += 8) {   // k < np: T_l times [S_ll | S_lr]
-        const double *B = left ? Sll : Slr;
-        dmma(d0, d1, TT[(m0 + g) + (k0 + q) * ldt], B[(k0 + q) + (c0 + g) * ldt]);
-        dmma(e0, e1, TT[(m0 + g) + (k0 + 4 + q) * ldt], B[(k0 + 4 + q) + (c0 + g) * ldt]);
+      const double *B = left ? Sll : Slr;
+      for (int k0 = 0; k0 < np; k0 += 4) {   // k < np: T_l times [S_ll | S_lr]
+        const double bv = B[(k0 + q) + (c0 + g) * ldt];
+#pragma unroll
+        for (int v = 0; v < kRB; ++v)
+          if (i0 + v < mt) dmma(acc[u][v][0], acc[u][v][1], TT[((i0 + v) * 8 + g) + (k0 + q) * ldt], bv);
       }
-      for (int k0 = 0; k0 < np; k0 += 8) {   // k >= np: T_r times [S_lr^T | S_rr]
-        const double b0 = left ? Slr[(c0 + g) + (k0 + q) * ldt] : Srr[(k0 + q) + (c0 + g) * ldt];
-        const double b1 = left ? Slr[(c0 + g) + (k0 + 4 + q) * ldt] : Srr[(k0 + 4 + q) + (c0 + g) * ldt];
-        dmma(d0, d1, TT[(m0 + g) + (np + k0 + q) * ldt], b0);
-        dmma(e0, e1, TT[(m0 + g) + (np + k0 + 4 + q) * ldt], b1);
+      for (int k0 = 0; k0 < np; k0 += 4) {   // k >= np: T_r times [S_lr^T | S_rr]
+        const double bv = left ? Slr[(c0 + g) + (k0 + q) * ldt] : Srr[(k0 + q) + (c0 + g) * ldt];
+#pragma unroll
+        for (int v = 0; v < kRB; ++v)
+          if (i0 + v < mt) dmma(acc[u][v][0], acc[u][v][1], TT[((i0 + v) * 8 + g) + (np + k0 + q) * ldt], bv);
       }
-      acc0[u] = -(d0 + e0);
-      acc1[u] = -(d1 + e1);
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < kMaxT; ++u) {
-    const int tile = warp + u * nw;
-    if (tile < ntile) {
-      const int i = tile % mt, cb = tile / mt, m0 = i * 8;
+  for (int u = 0; u < kMaxI; ++u) {
+    const int item = warp + u * nw;
+    if (item < nitem) {
+      const int i0 = (item % rb) * kRB, cb = item / rb;
       double *D = cb < mt ? Sll : Srr;
       const int c0 = (cb < mt ? cb : cb - mt) * 8;
-      D[(m0 + g) + (c0 + 2 * q) * ldt] = acc0[u];
-      D[(m0 + g) + (c0 + 2 * q + 1) * ldt] = acc1[u];
+#pragma unroll
+      for (int v = 0; v < kRB; ++v)
+        if (i0 + v < mt) {
+          const int m0 = (i0 + v) * 8;
+          D[(m0 + g) + (c0 + 2 * q) * ldt] = -acc[u][v][0];
+          D[(m0 + g) + (c0 + 2 * q + 1) * ldt] = -acc[u][v][1];
+        }
     }
   }
   __syncthreads();
-  // S_tt = P - S_{t,I} T^T, P the accumulator (R record, row-major), into S_lr's place
+  // S_tt = P - S_{t,I} T^T, P the accumulator (R record, row-major), into
+  // S_lr's place; items of kRB row tiles sharing the B (T^T) fragment
   const double *Pg = rec + 2 * nn;
-  for (int tile = warp; tile < mt * mt; tile += nw) {
-    const int m0 = (tile % mt) * 8, n0 = (tile / mt) * 8, r = m0 + g, c = n0 + 2 * q;
-    double d0 = (r < n && c < n) ? Pg[r * n + c] : 0.0, d1 = (r < n && c + 1 < n) ? Pg[r * n + c + 1] : 0.0;
-    double e0 = 0.0, e1 = 0.0;
-    for (int k0 = 0; k0 < np; k0 += 8) {
-      dmma(d0, d1, -Sll[(m0 + g) + (k0 + q) * ldt], TT[(n0 + g) + (k0 + q) * ldt]);
-      dmma(e0, e1, -Sll[(m0 + g) + (k0 + 4 + q) * ldt], TT[(n0 + g) + (k0 + 4 + q) * ldt]);
+  for (int item = warp; item < rb * mt; item += nw) {
+    const int i0 = (item % rb) * kRB, n0 = (item / rb) * 8, c = n0 + 2 * q;
+    double d[kRB][2];
+#pragma unroll
+    for (int v = 0; v < kRB; ++v) {
+      const int r = (i0 + v) * 8 + g;
+      d[v][0] = (i0 + v < mt && r < n && c < n) ? Pg[r * n + c] : 0.0;
+      d[v][1] = (i0 + v < mt && r < n && c + 1 < n) ? Pg[r * n + c + 1] : 0.0;
     }
-    for (int k0 = 0; k0 < np; k0 += 8) {
-      dmma(d0, d1, -Srr[(m0 + g) + (k0 + q) * ldt], TT[(n0 + g) + (np + k0 + q) * ldt]);
-      dmma(e0, e1, -Srr[(m0 + g) + (k0 + 4 + q) * ldt], TT[(n0 + g) + (np + k0 + 4 + q) * ldt]);
+    for (int k0 = 0; k0 < np; k0 += 4) {
+      const double bv = TT[(n0 + g) + (k0 + q) * ldt];
+#pragma unroll
+      for (int v = 0; v < kRB; ++v)
+        if (i0 + v < mt) dmma(d[v][0], d[v][1], -Sll[((i0 + v) * 8 + g) + (k0 + q) * ldt], bv);
     }
-    Slr[r + c * ldt] = d0 + e0;
-    Slr[r + (c + 1) * ldt] = d1 + e1;
+    for (int k0 = 0; k0 < np; k0 += 4) {
+      const double bv = TT[(n0 + g) + (np + k0 + q) * ldt];
+#pragma unroll
+      for (int v = 0; v < kRB; ++v)
+        if (i0 + v < mt) dmma(d[v][0], d[v][1], -Srr[((i0 + v) * 8 + g) + (k0 + q) * ldt], bv);
+    }
+#pragma unroll
+    for (int v = 0; v < kRB; ++v)
+      if (i0 + v < mt) {
+        const int r = (i0 + v) * 8 + g;
+        Slr[r + c * ldt] = d[v][0];
+        Slr[r + (c + 1) * ldt] = d[v][1];
+      }
   }
   __syncthreads();
   double *So = a.S + j * nn;
@@ -1472,11 +1493,17 @@ cudaError_t launch_factor_level(const FactorLevelArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_backward_level(const BackwardLevelArgs &a, cudaStream_t s) {
-  set_smem_attr((const void *)backward_level_kernel, 227 * 1024);
   const int mt = pad8(a.n) / 8;
-  if (mt * 2 * mt > 16 * kWarps) return cudaErrorInvalidValue;   // n <= 64 (the kernel's register tiles)
   const int64_t grid = (a.K + 1) / 2;
-  backward_level_kernel<<<(unsigned)grid, kThreads, backward_smem_bytes(a.n), s>>>(a);
+  if ((mt + 2) / 3 * 2 * mt <= 4 * kWarps) {   // three row tiles per work item
+    set_smem_attr((const void *)backward_level_kernel<3>, 227 * 1024);
+    backward_level_kernel<3><<<(unsigned)grid, kThreads, backward_smem_bytes(a.n), s>>>(a);
+  } else if ((mt + 3) / 4 * 2 * mt <= 4 * kWarps) {   // n <= 64
+    set_smem_attr((const void *)backward_level_kernel<4>, 227 * 1024);
+    backward_level_kernel<4><<<(unsigned)grid, kThreads, backward_smem_bytes(a.n), s>>>(a);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
