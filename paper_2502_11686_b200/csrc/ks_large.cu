@@ -865,7 +865,12 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   if (el2) pf_l2(in.El + (t + 2) * in.sEl, (int64_t)n * n);
 
   // ---- stage 1 ----
+  // Concurrent stages 2 / 3 (f.conc): stage 2's global blocks Er_t, El_t, e_t
+  // are loaded into its (still unused) matrix B2 now, as a second cp.async
+  // group that completes behind stage 1's QR.
+  const bool conc = f.conc && hr && hl;
   zero_smem(S1, ld1 * f.cols1);
+  if (conc) zero_smem(P2, ld2 * f.cols2);
   __syncthreads();
   ld_blk(S1, ld1, 0, 0, in.C + t * in.sC, n, RC, n, RC);
   ld_blk(S1, ld1, 0, 2 * n, in.y + t * in.sy, 1, RC, 1, RC);
@@ -875,7 +880,17 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     ld_blk(S1, ld1, RC, n, in.Er + u * in.sEr, n, n, n, n);
     ld_blk(S1, ld1, RC, 2 * n, in.e + u * in.se, 1, n, 1, n);
   }
-  sync_loads();
+  if (conc) {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
+    ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
+    ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");   // stage 1's group only
+    __syncthreads();
+  } else {
+    sync_loads();
+  }
   if (l0n) {   // |C_t|, |El_{t+1}| (column t), |Er_{t+1}| (column t+1), before the QR overwrites them
     pt += sumsq_blk(S1, ld1, 0, 0, RC + (hr ? n : 0), n);
     if (hr) pu += sumsq_blk(S1, ld1, RC, n, n, n);
@@ -886,7 +901,7 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
   KS_PROF(1)
   if (el2) pu += part_sumsq(in.El + (t + 2) * in.sEl, n * n);
 
-  if (f.conc && hr && hl) {
+  if (conc) {
     // ---- stages 2 and 3 concurrently: independent QRs once stage 1 is done.
     // Stage 2's matrix B2 goes to P2 as below; stage 3's B3 is rebuilt in S1's
     // region (D~ | y~ held in registers across the rebuild) with a second
@@ -894,11 +909,6 @@ __device__ void eliminate(const FactorLevelArgs &a, double *sm, const FactorPlan
     // its own panel warp and named barrier, so the two serial panel chains
     // overlap.
     const int64_t u = t + 1;
-    zero_smem(P2, ld2 * f.cols2);
-    __syncthreads();
-    ld_blk(P2, ld2, 0, 0, in.Er + t * in.sEr, n, n, n, n);
-    ld_blk(P2, ld2, 0, n, in.El + t * in.sEl, n, n, n, n);
-    ld_blk(P2, ld2, 0, 3 * n, in.e + t * in.se, 1, n, 1, n);
     cp_blk(P2, ld2, n, 0, S1, ld1, 0, 0, n, n);            // R~_t
     cp_blk(P2, ld2, n, 2 * n, S1, ld1, 0, n, n, n + 1);    // X_t, z~_t
     const int nd = RC * (n + 1);                           // D~_{t+1} (RC x n) | y~_{t+1}
