@@ -218,6 +218,9 @@ struct Rr {
 // constant level-0 blocks (El, Er, e, C with RC <= kSmallMaxM rows).
 template <int N>
 constexpr int kParkDoubles = N * (N + 2) + N * (N + 1) / 2;
+// the fused tail's split form also parks stage 1's z~_t for pass A's thread
+template <int N>
+constexpr int kParkSP = kParkDoubles<N> + N;
 template <int N>
 struct CstOff {
   static constexpr int El = 0, Er = N * N, e = 2 * N * N, C = 2 * N * N + N,
@@ -225,10 +228,17 @@ struct CstOff {
       size = 2 * N * N + N + kSmallMaxM * N + kSmallMaxM * kSmallMaxM;
 };
 
-template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false, bool ZS = false>
+// SPL (the fused tail only, SIN): the pair's work is split over three
+// threads of one slot -- role 0 stage 1 + pass B (+ T_r), role 1 stage 3,
+// role 2 pass A + post -- which meet at two CTA barriers (after stage 1's
+// parking, at the end); `active` false only joins the barriers.  Same
+// operations in the same order per result as the one-thread form (bitwise).
+template <int N, bool L0, bool CE, bool CC, bool OAOS, bool SIN = false, bool ZS = false, bool SPL = false>
 __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_t t, bool hr, bool hl,
                                                 int64_t pnext, bool zs_in, bool zs_out,
-                                                volatile int *zsync = nullptr, int zval = 0) {
+                                                volatile int *zsync = nullptr, int zval = 0, int role = 0,
+                                                int slot = 0, bool active = true) {
+  static_assert(!SPL || SIN, "the split form runs in the fused tail");
   using TR = Tri<N>;
 #ifndef KS_ROW_UNROLL
 #define KS_ROW_UNROLL 1
@@ -249,7 +259,13 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // constant level-0 blocks (stride-0 model) are staged once per CTA in
   // shared memory by the kernel prologue and read there (broadcast)
   extern __shared__ double smem_park[];
-  const double *cst = smem_park + (size_t)blockDim.x * kParkDoubles<N>;
+  const double *cst = smem_park + (SPL ? (size_t)64 * kParkSP<N> : (size_t)blockDim.x * kParkDoubles<N>);
+  // roles (SPL): r0 stage 1 + pass B, r1 stage 3, r2 pass A + post
+  const bool r0 = !SPL || (active && role == 0), r1 = !SPL || (active && role == 1),
+             r2 = !SPL || (active && role == 2);
+  auto split_bar = [&](int id) {
+    if (SPL) asm volatile("barrier.sync %0, 192;" ::"r"(id) : "memory");   // one call site each
+  };
   auto ldC = [&](int e, int64_t c) {
     return L0 ? (CC ? cst[CstOff<N>::C + e] : ldv<64>(in.C, c, e)) : lde(c, EN::C + e);
   };
@@ -308,8 +324,9 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   double z[N];
 
   // rank reference: |block column of UA|_F (reading R9)
-  double ref2, ref2u = 0.0;
-  if (!L0) {
+  double ref2 = 1.0, ref2u = 0.0;
+  if (SPL && !active) {
+  } else if (!L0) {
     const double v = lde(t, EN::nrm);
     ref2 = v * v;
     if (hr) {
@@ -335,8 +352,8 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // weights (N x (N+2)) and a copy of R~_t (packed), so that at most ~76
   // doubles are live in registers at any point (stage 1 -> stage 2 pass B ->
   // stage 3 -> pass A).
-  double *sp = smem_park + threadIdx.x;
-  const int bs = blockDim.x;
+  double *sp = smem_park + (SPL ? slot : threadIdx.x);
+  const int bs = SPL ? 64 : blockDim.x;
   auto park = [&](int e, double v) { sp[e * bs] = v; };
   auto unpark = [&](int e) { return sp[e * bs]; };
   constexpr int kLeft = 0, kRt = N * (N + 2);
@@ -395,7 +412,8 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       pfEr(i, t);
     }
   }
-  if (!L0) {
+  if (!r0) {
+  } else if (!L0) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
 #pragma unroll
@@ -420,7 +438,7 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // ---- stage 1: rows of [El_{t+1} | Er_{t+1} | e_{t+1}] into [R | X | z] ----
   // leftover rows [0 | d | y~] (rows of D~_{t+1}) are parked, with their
   // weights, for stage 3.
-  if (hr) {
+  if (r0 && hr) {
     const int64_t u = t + 1;
 #pragma unroll UR
     for (int i = 0; i < N; ++i) {
@@ -454,9 +472,16 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   // ---- stage 2, pass B: rows of [Er_t | 0] into [R~_t | X_t] -> R_tt, R_{t,t+1}, X~_t ----
   // (pass A below recomputes the same rotations -- bitwise, same inputs and
   // operations -- for [El_t | e_t]).
+  if (r0) {
 #pragma unroll
-  for (int k = 0; k < TR::size; ++k) park(kRt + k, R[k]);
-  if (!L0 && !SIN && hr) {   // stage 3's base block C_{t+1}, y_{t+1}
+    for (int k = 0; k < TR::size; ++k) park(kRt + k, R[k]);
+    if (SPL) {   // z~_t for pass A's thread
+#pragma unroll
+      for (int i = 0; i < N; ++i) park(kParkDoubles<N> + i, z[i]);
+    }
+  }
+  split_bar(1);
+  if (r0 && !L0 && !SIN && hr) {   // stage 3's base block C_{t+1}, y_{t+1}
 #pragma unroll
     for (int i = 0; i < N; ++i) {
 #pragma unroll
@@ -464,7 +489,8 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       pfv<64>(in.ent, t + 1, EN::y + i);
     }
   }
-  if (hl) {
+  if (!r0) {
+  } else if (hl) {
 #pragma unroll UR
     for (int i = 0; i < N; ++i) {
       double er[N], xr[N];
@@ -498,23 +524,25 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
     }
   }
   // T_r = R_tt^{-1} R_{t,t+1} = U^{-1} X (unit triangular: no division)
+  if (r0) {
 #pragma unroll
-  for (int i = N - 1; i >= 0; --i) {
+    for (int i = N - 1; i >= 0; --i) {
 #pragma unroll
-    for (int c = 0; c < N; ++c) {
-      double sr = X[i][c];
+      for (int c = 0; c < N; ++c) {
+        double sr = X[i][c];
 #pragma unroll
-      for (int k = i + 1; k < N; ++k) sr = fma(-R[TR::at(i, k)], X[k][c], sr);
-      X[i][c] = sr;
+        for (int k = i + 1; k < N; ++k) sr = fma(-R[TR::at(i, k)], X[k][c], sr);
+        X[i][c] = sr;
+      }
     }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) str(RR::Tr + i * N + j, X[i][j]);
   }
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-#pragma unroll
-    for (int j = 0; j < N; ++j) str(RR::Tr + i * N + j, X[i][j]);
 
   // ---- stage 3: [D~_{t+1}; C_{t+1}; Zs] -> the survivor's C'_{t+1}, y' ----
-  if (hr) {
+  if (r1 && hr) {
     const int64_t u = t + 1;
     double R3[TR::size];
     double z3[N];
@@ -577,8 +605,13 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
   }
 
   // ---- stage 2, pass A: rows of [Er_t | El_t | e_t] into [R~_t | 0 | z~_t] ----
+  if (r2) {   // (SPL) roles 0 and 1 are done
 #pragma unroll
   for (int k = 0; k < TR::size; ++k) R[k] = unpark(kRt + k);
+  if (SPL) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) z[i] = unpark(kParkDoubles<N> + i);
+  }
   double Rl[N][N];
 #pragma unroll
   for (int i = 0; i < N; ++i)
@@ -688,6 +721,8 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
       str(RR::P + TR::at(i, j), s);
     }
   }
+  }   // r2
+  split_bar(2);
 }
 
 // Resident CTAs (of 64 threads) per SM the register allocation targets.
@@ -727,6 +762,34 @@ __device__ __forceinline__ void factor_item(const SmallFactorArgs &a, int64_t p,
       small_eliminate<N, L0, CE, CC, OAOS, SIN, ZS>(a, t, true, hl, p, (triple || waits) && (K - 1 + a.t0 > 0),
                                                     false, waits ? zsync : nullptr, zval);
   }
+}
+
+// The fused tail's split form (small_eliminate SPL): slot `slot` (0..63) of
+// role `role`; three threads per pair.  Every thread makes the same calls
+// (the barriers inside): an odd level (serial form: the last pair's slot
+// eliminates the last column first) has a round 0 in which only that slot
+// works; the base case (K = 1) is slot 0's single column.
+template <int N>
+__device__ __forceinline__ void factor_item_split(const SmallFactorArgs &a, int64_t p, bool has, int role, int slot) {
+  const int64_t K = a.K;
+  if (K == 1) {
+    const bool hl = a.t0 > 0;
+    small_eliminate<N, false, false, false, false, true, false, true>(a, 0, false, hl, 0, false, hl, nullptr, 0, role,
+                                                                       slot, has);
+    return;
+  }
+  const bool odd = (K >= 3) && (K & 1);
+  if (odd) {
+    const int64_t t = K - 1;
+    const bool hl = t + a.t0 > 0;
+    small_eliminate<N, false, false, false, false, true, false, true>(a, t, false, hl, 0, false, hl, nullptr, 0, role,
+                                                                       slot, has && p == K / 2 - 1);
+  }
+  const int64_t t = 2 * p;
+  const bool hl = t + a.t0 > 0;
+  const bool triple = odd && p == K / 2 - 1;
+  small_eliminate<N, false, false, false, false, true, false, true>(
+      a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false, nullptr, 0, role, slot, has);
 }
 
 template <int N, bool L0, bool CE, bool CC, bool OAOS, bool ZS = false>
@@ -772,9 +835,10 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
 // them).  Same per-column code (small_eliminate) as the level kernels.
 // shared memory of the tail kernel with first-level width K0 (a multiple of
 // 64): park | const | buffer A (K0 columns) | buffer B (max(64, K0 / 2))
+constexpr int kTailThreads = 192;   // three threads (roles) per pair slot
 template <int N>
 __host__ __device__ constexpr size_t tail_smem_doubles(int K0) {
-  return (size_t)64 * kParkDoubles<N> + CstOff<N>::size +
+  return (size_t)64 * kParkSP<N> + CstOff<N>::size +
          (size_t)(K0 + (K0 / 2 > 64 ? K0 / 2 : 64)) * (3 * N * N + 2 * N + 1);
 }
 template <int N>
@@ -786,10 +850,10 @@ __host__ __device__ constexpr size_t tail_smem_bytes() {
   return tail_max_cols<N>() ? tail_smem_doubles<N>(tail_max_cols<N>()) * sizeof(double) : 0;
 }
 template <int N>
-__global__ void __launch_bounds__(64, 1) small_factor_tail_kernel(SmallTailArgs t) {
+__global__ void __launch_bounds__(kTailThreads, 1) small_factor_tail_kernel(SmallTailArgs t) {
   extern __shared__ double smem_park[];
   constexpr int64_t E = 3 * N * N + 2 * N + 1;
-  double *bufA = smem_park + (size_t)blockDim.x * kParkDoubles<N> + CstOff<N>::size;
+  double *bufA = smem_park + (size_t)64 * kParkSP<N> + CstOff<N>::size;
   // W == 0: one CTA runs whole levels; W > 0: CTA c owns the subtree of the W
   // columns [cW, cW + W) of the first level (W a power of two, every level
   // halving exactly), so all its levels are local (a column's
@@ -816,9 +880,9 @@ __global__ void __launch_bounds__(64, 1) small_factor_tail_kernel(SmallTailArgs 
     a.out = last ? t.out_last : TView{out, 64 * E};
     a.outAoS = last ? t.out_last_aos : 0;
     a.out_off = (t.W && !last) ? c * (kloc / 2) : 0;
-    const int64_t npairs = t.W ? kloc / 2 : (a.K >= 2 ? a.K / 2 : 1);
-    for (int64_t p = threadIdx.x; p < npairs; p += blockDim.x)
-      factor_item<N, false, false, false, false, true>(a, (t.W ? c * (kloc / 2) : 0) + p);
+    const int64_t npairs = t.W ? kloc / 2 : (a.K >= 2 ? a.K / 2 : 1);   // <= 64
+    const int slot = threadIdx.x & 63, role = threadIdx.x >> 6;
+    factor_item_split<N>(a, (t.W ? c * (kloc / 2) : 0) + slot, slot < npairs, role, slot);
     __syncthreads();
     double *tmp = in;
     in = out;
@@ -1712,7 +1776,7 @@ template <int N>
 cudaError_t factor_tail_n(const SmallTailArgs &t, cudaStream_t s) {
   const size_t smem = tail_smem_bytes<N>();
   set_smem_attr((const void *)small_factor_tail_kernel<N>, (int)smem);
-  small_factor_tail_kernel<N><<<(unsigned)(t.W ? t.K[0] / t.W : 1), 64, smem, s>>>(t);
+  small_factor_tail_kernel<N><<<(unsigned)(t.W ? t.K[0] / t.W : 1), kTailThreads, smem, s>>>(t);
   return cudaGetLastError();
 }
 template <int N>
