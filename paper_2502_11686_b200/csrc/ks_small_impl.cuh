@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "ks_internal.cuh"
@@ -218,9 +219,10 @@ struct Rr {
 // constant level-0 blocks (El, Er, e, C with RC <= kSmallMaxM rows).
 template <int N>
 constexpr int kParkDoubles = N * (N + 2) + N * (N + 1) / 2;
-// the fused tail's split form also parks stage 1's z~_t for pass A's thread
+// the split form (three threads per pair) also parks stage 1's z~_t for pass A's thread
 template <int N>
 constexpr int kParkSP = kParkDoubles<N> + N;
+constexpr int kTailThreads = 192;   // split form: three threads (roles) per pair slot
 template <int N>
 struct CstOff {
   static constexpr int El = 0, Er = N * N, e = 2 * N * N, C = 2 * N * N + N,
@@ -228,7 +230,7 @@ struct CstOff {
       size = 2 * N * N + N + kSmallMaxM * N + kSmallMaxM * kSmallMaxM;
 };
 
-// SPL (the fused tail only, SIN): the pair's work is split over three
+// SPL (the fused tail and latency-bound levels): the pair's work is split over three
 // threads of one slot -- role 0 stage 1 + pass B (+ T_r), role 1 stage 3,
 // role 2 pass A + post -- which meet at two CTA barriers (after stage 1's
 // parking, at the end); `active` false only joins the barriers.  Same
@@ -238,7 +240,6 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
                                                 int64_t pnext, bool zs_in, bool zs_out,
                                                 volatile int *zsync = nullptr, int zval = 0, int role = 0,
                                                 int slot = 0, bool active = true) {
-  static_assert(!SPL || SIN, "the split form runs in the fused tail");
   using TR = Tri<N>;
 #ifndef KS_ROW_UNROLL
 #define KS_ROW_UNROLL 1
@@ -769,12 +770,12 @@ __device__ __forceinline__ void factor_item(const SmallFactorArgs &a, int64_t p,
 // (the barriers inside): an odd level (serial form: the last pair's slot
 // eliminates the last column first) has a round 0 in which only that slot
 // works; the base case (K = 1) is slot 0's single column.
-template <int N>
+template <int N, bool SIN = true, bool OAOS = false>
 __device__ __forceinline__ void factor_item_split(const SmallFactorArgs &a, int64_t p, bool has, int role, int slot) {
   const int64_t K = a.K;
   if (K == 1) {
     const bool hl = a.t0 > 0;
-    small_eliminate<N, false, false, false, false, true, false, true>(a, 0, false, hl, 0, false, hl, nullptr, 0, role,
+    small_eliminate<N, false, false, false, OAOS, SIN, false, true>(a, 0, false, hl, 0, false, hl, nullptr, 0, role,
                                                                        slot, has);
     return;
   }
@@ -782,14 +783,25 @@ __device__ __forceinline__ void factor_item_split(const SmallFactorArgs &a, int6
   if (odd) {
     const int64_t t = K - 1;
     const bool hl = t + a.t0 > 0;
-    small_eliminate<N, false, false, false, false, true, false, true>(a, t, false, hl, 0, false, hl, nullptr, 0, role,
+    small_eliminate<N, false, false, false, OAOS, SIN, false, true>(a, t, false, hl, 0, false, hl, nullptr, 0, role,
                                                                        slot, has && p == K / 2 - 1);
   }
   const int64_t t = 2 * p;
   const bool hl = t + a.t0 > 0;
   const bool triple = odd && p == K / 2 - 1;
-  small_eliminate<N, false, false, false, false, true, false, true>(
+  small_eliminate<N, false, false, false, OAOS, SIN, false, true>(
       a, t, true, hl, p, triple && (K - 1 + a.t0 > 0), false, nullptr, 0, role, slot, has);
+}
+
+// A level >= 1 with few pairs (latency-bound: at most one 64-pair CTA per
+// SM) in the split form: 192 threads = three roles x 64 pair slots per CTA,
+// the odd level's last column in the serial form (its slot's round 0).
+template <int N, bool OAOS>
+__global__ void __launch_bounds__(kTailThreads, 1) small_factor_split_kernel(SmallFactorArgs a) {
+  const int slot = threadIdx.x & 63, role = threadIdx.x >> 6;
+  const int64_t npairs = a.K >= 2 ? a.K / 2 : 1;
+  const int64_t p = (int64_t)blockIdx.x * 64 + slot;
+  factor_item_split<N, false, OAOS>(a, p, p < npairs, role, slot);
 }
 
 template <int N, bool L0, bool CE, bool CC, bool OAOS, bool ZS = false>
@@ -835,7 +847,6 @@ __global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(
 // them).  Same per-column code (small_eliminate) as the level kernels.
 // shared memory of the tail kernel with first-level width K0 (a multiple of
 // 64): park | const | buffer A (K0 columns) | buffer B (max(64, K0 / 2))
-constexpr int kTailThreads = 192;   // three threads (roles) per pair slot
 template <int N>
 __host__ __device__ constexpr size_t tail_smem_doubles(int K0) {
   return (size_t)64 * kParkSP<N> + CstOff<N>::size +
@@ -1756,6 +1767,16 @@ cudaError_t factor_launch(const SmallFactorArgs &a, cudaStream_t s) {
 
 template <int N, bool OAOS>
 cudaError_t factor_oaos(const SmallFactorArgs &a, cudaStream_t s) {
+  const int64_t npairs = a.K >= 2 ? a.K / 2 : 1;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (a.in.ent.p != nullptr && npairs <= (int64_t)64 * sms && !std::getenv("KS_NO_SPLIT_LEVELS")) {
+    // latency-bound level (one 64-pair CTA per SM at most): three threads per pair
+    const size_t smem = ((size_t)64 * kParkSP<N> + CstOff<N>::size) * sizeof(double);
+    set_smem_attr((const void *)small_factor_split_kernel<N, OAOS>, (int)smem);
+    small_factor_split_kernel<N, OAOS><<<(unsigned)((npairs + 63) / 64), kTailThreads, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   if (a.in.ent.p != nullptr)   // level >= 1; an odd level splits its last column off (split_odd)
     return split_odd(a.K, 64) ? factor_launch<N, false, false, false, OAOS, true>(a, s)
                               : factor_launch<N, false, false, false, OAOS>(a, s);

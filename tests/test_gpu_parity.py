@@ -234,6 +234,19 @@ def test_cta_panel_gram_guard(eps):
     assert_parity(p, generic=True)
 
 
+@pytest.mark.parametrize("case", [("c2", 3001), ("c1", 1000), ("c3", 777), ("c5", 40000)])
+def test_split_levels_match_one_thread_form(case, monkeypatch):
+    """Levels with at most one 64-pair CTA per SM run three threads per pair
+    (stage 1 + pass B, stage 3, pass A + post); KS_NO_SPLIT_LEVELS forces the
+    one-thread-per-pair kernels (split odd levels included).  Bitwise equal."""
+    cfg, N = case
+    p = gen.make(cfg, N=N)
+    x1, S1, _ = gpu_smooth(p)
+    monkeypatch.setenv("KS_NO_SPLIT_LEVELS", "1")
+    x2, S2, _ = gpu_smooth(p)
+    assert np.array_equal(x1, x2) and np.array_equal(S1, S2)
+
+
 def test_level_count():
     for N in (1, 2, 3, 7, 8, 9, 1000, 4096):
         s = ks().Smoother(gen.make("c1", N=max(N, 2)) if N > 1 else gen.random_problem(
