@@ -87,3 +87,58 @@ def test_shard_keeps_coupling_row():
     c5 = gen.make("c5", N=1 << 12)
     s5 = c5.slice(*kdist.shard_range(1 << 12, 3, 4))
     assert s5.F.shape[0] == 1 and s5.N == 1 << 10            # constant model stays stride 0
+
+
+def test_shard_plan_any_N():
+    """shard_plan: the smallest power-of-two shard covering N over the ranks;
+    the real steps fill the ranks in order (padding only at the global end)."""
+    assert kdist.shard_plan(1 << 22, 8) == (1 << 19, [1 << 19] * 8)
+    assert kdist.shard_plan(1000, 1) == (1000, [1000])
+    assert kdist.shard_plan(1000, 8) == (128, [128] * 7 + [104])
+    assert kdist.shard_plan(100000, 8) == (16384, [16384] * 6 + [100000 - 6 * 16384, 0])
+    assert kdist.shard_plan(20000, 8) == (4096, [4096] * 4 + [20000 - 4 * 4096, 0, 0, 0])
+    assert kdist.shard_plan(3, 2) == (2, [2, 1])
+    for N in range(1, 70):
+        for P in (2, 3, 4, 8):
+            M, real = kdist.shard_plan(N, P)
+            assert M >= 2 and M & (M - 1) == 0 and M * P >= N and (M == 2 or (M // 2) * P < N)
+            assert sum(real) == N and all(0 <= k <= M for k in real)
+
+
+def _join(parts):
+    """The global padded problem the shards describe (rank order)."""
+    p0 = parts[0]
+
+    def cat(attr):
+        arrs = [getattr(q, attr) for q in parts]
+        if arrs[0] is None:
+            return None
+        return np.concatenate([np.broadcast_to(a, (q.N,) + a.shape[1:]) for a, q in zip(arrs, parts)])
+    return gen.Problem("joined", sum(q.N for q in parts), p0.n, p0.m_max,
+                       np.concatenate([q.m for q in parts]), cat("F"), cat("H"), cat("K"),
+                       cat("L"), cat("o"), cat("c"))
+
+
+@pytest.mark.parametrize("cfg,N,P", [("c1", 100, 8), ("c2", 150, 3), ("c3", 77, 4), ("c5", 45, 2),
+                                     ("c4", 5, 4)])
+def test_padded_shards_decoupled(cfg, N, P):
+    """Reading R29 pinned by the oracle: the decoupled steps pad_shard appends
+    leave the real steps' states and covariances those of the unpadded problem
+    (to rounding: another elimination order), and come out as u = 0, S = I."""
+    import oracle
+    p = gen.make(cfg, N=N)
+    M, real = kdist.shard_plan(N, P)
+    parts = [kdist.pad_shard(p, r, P) for r in range(P)]
+    assert all(q.N == M for q in parts) and [q.meta.get("shard_real", M) for q in parts] == real
+    for r, q in enumerate(parts):      # each shard's real steps are the global ones
+        k = real[r]
+        np.testing.assert_array_equal(q.o[:k], p.o[r * M:r * M + k])
+        np.testing.assert_array_equal(q.m[:k], p.m[r * M:r * M + k])
+    g = _join(parts)
+    xg, Sg = oracle.smooth(g)
+    xo, So = oracle.smooth(p)
+    scale_x = np.abs(xo).max(1, keepdims=True)
+    assert np.max(np.abs(xg[:N] - xo) / scale_x) <= 1e-10
+    assert np.max(np.abs(Sg[:N] - So).reshape(N, -1).max(1) / np.abs(So).reshape(N, -1).max(1)) <= 1e-10
+    assert np.array_equal(xg[N:], np.zeros_like(xg[N:]))
+    np.testing.assert_allclose(Sg[N:], np.broadcast_to(np.eye(p.n), Sg[N:].shape), rtol=0, atol=1e-15)

@@ -1,14 +1,15 @@
 """Real processes, one rank each (2 and 4), on the single leased GPU.
 
-Each process owns its context over a power-of-two shard of the steps
+Each process owns its context over a power-of-two shard of the steps (other
+N: the shard_plan / pad_shard decoupled padding, reading R29)
 (ks_dist_create with no communicator) and runs its local levels; the
 boundary exchange is the caller-driven path of include/ks.h: the rank's
 `send` entry goes device -> pinned host, a world-size-2 gloo allgather,
 host -> the rank's `recv` buffer, then ks_factor_boundary and the local
 backward levels.  The kernels of the two processes never wait on each other
 (the exchange is host-mediated), so one GPU is a faithful stand-in for two.
-The gathered shards must match the oracle and, the shards being powers of
-two, the single-GPU result bit for bit.
+The gathered shards must match the oracle and, for unpadded power-of-two
+shards, the single-GPU result bit for bit.
 """
 import os
 import socket
@@ -39,9 +40,9 @@ def _rank(rank, world, port, cfg, N, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         p = gen.make(cfg, N=N)
-        lo, hi = kdist.shard_range(N, rank, world)
-        d = ks.Dist(rank, world, lo, N)
-        s = ks.Smoother(p.slice(lo, hi), device="cuda:0", dist=d)
+        M, _ = kdist.shard_plan(N, world)     # any N: decoupled padding (R29)
+        d = ks.Dist(rank, world, rank * M, world * M)
+        s = ks.Smoother(kdist.pad_shard(p, rank, world), device="cuda:0", dist=d)
         s.whiten()
         s.factor()
         send, recv = s.boundary_tensors()
@@ -60,7 +61,8 @@ def _rank(rank, world, port, cfg, N, q):
 
 
 @pytest.mark.parametrize("cfg,N,world", [("c5", 1 << 14, 2), ("c2", 1 << 12, 2), ("c3", 1 << 11, 2),
-                                         ("c5", 1 << 15, 4), ("c1", 1 << 10, 4)])
+                                         ("c5", 1 << 15, 4), ("c1", 1 << 10, 4),
+                                         ("c2", 3000, 2), ("c1", 1000, 4)])
 def test_processes_gloo_staged_exchange(cfg, N, world):
     import oracle
     from paper_2502_11686_b200 import generators as gen
@@ -78,15 +80,16 @@ def test_processes_gloo_staged_exchange(cfg, N, world):
     for r, x, S, info in res:
         assert x is not None, f"rank {r}: {S}"
         assert info == {"rank": r, "nranks": world, "nccl_nranks": 0}
-    x = np.concatenate([r[1] for r in res])
-    S = np.concatenate([r[2] for r in res])
+    x = np.concatenate([r[1] for r in res])[:N]
+    S = np.concatenate([r[2] for r in res])[:N]
     p = gen.make(cfg, N=N)
     xo, So = oracle.smooth(p)
     assert rel_state_err(x, xo) <= 1e-9 and rel_cov_err(S, So) <= 1e-8
-    s1 = ks.Smoother(p)
-    s1.run()
-    s1.check()
-    assert np.array_equal(x, s1.states.cpu().numpy()) and np.array_equal(S, s1.cov.cpu().numpy())
+    if (N // world) & (N // world - 1) == 0 and N % world == 0:
+        s1 = ks.Smoother(p)
+        s1.run()
+        s1.check()
+        assert np.array_equal(x, s1.states.cpu().numpy()) and np.array_equal(S, s1.cov.cpu().numpy())
 
 
 def test_library_nccl_communicator_one_rank():

@@ -296,8 +296,8 @@ def _virtual_shards(p, P, cov=True, generic=False, fused=False):
     """The time-sharded multi-GPU algorithm with P ranks emulated on one GPU:
     each rank's local levels run in its own context; the allgather is a
     device copy into every rank's receive buffer (no rank waits on another)."""
-    M = p.N // P
-    parts = [ks().Smoother(p.slice(r * M, (r + 1) * M), shard=(r, P, None), generic=generic)
+    from paper_2502_11686_b200 import dist as kdist
+    parts = [ks().Smoother(kdist.pad_shard(p, r, P), shard=(r, P, None), generic=generic)
              for r in range(P)]
     for s in parts:
         s.whiten()
@@ -317,6 +317,13 @@ def _virtual_shards(p, P, cov=True, generic=False, fused=False):
         s.check()
     x = np.concatenate([s.states.cpu().numpy() for s in parts])
     S = np.concatenate([s.cov.cpu().numpy() for s in parts]) if cov else None
+    # padded shards (N not P x a power of two, reading R29): the decoupled
+    # steps come out as u = 0, S = I exactly; the real steps are the first N
+    assert np.array_equal(x[p.N:], np.zeros_like(x[p.N:]))
+    if cov:
+        assert np.abs(S[p.N:] - np.eye(p.n)).max(initial=0.0) <= 1e-15
+        S = S[:p.N]
+    x = x[:p.N]
     _virtual_shards.launches = [s.info()["launches"] for s in parts]
     return x, S
 
@@ -324,7 +331,10 @@ def _virtual_shards(p, P, cov=True, generic=False, fused=False):
 @pytest.mark.parametrize("generic", [False, True])
 @pytest.mark.parametrize("cfg,N,P", [("c5", 1 << 12, 2), ("c5", 1 << 12, 4), ("c5", 1 << 12, 8),
                                      ("c2", 1 << 11, 2), ("c3", 1 << 11, 8), ("c1", 1 << 10, 4),
-                                     ("c2", 3 * 256, 3), ("c4", 64, 2)])
+                                     ("c2", 3 * 256, 3), ("c4", 64, 2),
+                                     # any N (padded shards, reading R29)
+                                     ("c2", 1000, 3), ("c1", 1000, 8), ("c3", 777, 4),
+                                     ("c5", 5000, 8), ("c4", 100, 3)])
 def test_virtual_shards_match_oracle(cfg, N, P, generic):
     p = gen.make(cfg, N=N)
     x, S = _virtual_shards(p, P, generic=generic)
