@@ -302,9 +302,11 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     p = gen.make(a.config, N=a.N)
     N = p.N
-    lo, hi = kdist.shard_range(N, rank, P)
-    M = hi - lo
-    local_p = p.slice(lo, hi) if P > 1 else p
+    # rank r owns steps [r*M, (r+1)*M), M a power of two (N not P x a power
+    # of two: decoupled padding steps at the global end, R29)
+    M, _ = kdist.shard_plan(N, P)
+    lo = rank * M
+    local_p = kdist.pad_shard(p, rank, P) if P > 1 else p
     strides = {"C": int(local_p.H.shape[0] > 1 or local_p.L.shape[0] > 1),
                "E": int(local_p.F.shape[0] > 1 or local_p.K.shape[0] > 1 or local_p.c is not None)}
     # every library call goes to one side stream (CUDA graphs cannot capture
@@ -315,14 +317,14 @@ def main():
 
     kd = None
     if host_x:   # no communicator: ks_factor stops after the local levels
-        kd = ks.Dist(rank, P, lo, N)
+        kd = ks.Dist(rank, P, lo, P * M)
     elif P > 1:
         # the library's own NCCL communicator (ks_dist_*): rank 0's unique id
         # travels over the torch process group; ks_factor then allgathers the
         # boundary columns itself, on the context's stream
         obj = [ks.Dist.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        kd = ks.Dist(rank, P, lo, N, uid=obj[0], device=dev)
+        kd = ks.Dist(rank, P, lo, P * M, uid=obj[0], device=dev)
         nccl = kd.info()
         v = torch.cuda.nccl.version()
         nccl["torch_nccl_version"] = ".".join(map(str, v)) if isinstance(v, (tuple, list)) else str(v)
@@ -538,7 +540,8 @@ def main():
                 "config": {"workload": workload_desc(a.config, N), "N": N, "n": p.n, "m": p.m_max,
                            "parallelism": f"time-shard x{P} (NCCL allgather of the boundary columns)"
                            if P > 1 else "1 GPU",
-                           "l2": "working set (~11 GB at c5) >> 126 MB L2; no flush"},
+                           "l2": "working set (~11 GB at c5) >> 126 MB L2; no flush",
+                           **({"shard_steps": M, "padding_steps": P * M - N} if P > 1 else {})},
                 "roofline": rl, "step_roofline": step_rl, "cpu_baseline": cpu, "e2e": e2e,
                 "timing": timing, "ms_per_step_spread": spread, "eager_ms_per_step": eager_ms,
                 "gpu_launches": int(n_launch), "clocks": clocks,
