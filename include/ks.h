@@ -117,7 +117,10 @@ typedef struct ks_problem {
      * F_i l_i x n_{i-1}, K_i l_i x l_i, and state dimensions n_i <= n.
      * Arrays keep their uniform [n][n] / [m_max][n] / [n] shapes; rows >= l_i
      * and columns >= n_i (F: >= n_{i-1}) are ignored.  All NULL = the
-     * uniform model above (H_i = I, l_i = n_i = n). */
+     * uniform model above (H_i = I, l_i = n_i = n).  Multi-GPU shards: the
+     * first step of a shard on rank > 0 has no n_{i-1} (it lives on the
+     * previous rank), so the library cannot mask its F_i -- that block's
+     * columns >= n_{i-1} must be ZERO (dist.pad_shard zeroes them). */
     const double *Hev;       /* [N][n][n] evolution matrix H_i (the paper's H); NULL = I */
     int64_t sHev;            /* per-step stride in doubles, 0 = constant                 */
     const int32_t *l;        /* [N] evolution rows l_i in [1, n]; NULL = n_i             */

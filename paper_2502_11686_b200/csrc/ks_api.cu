@@ -205,8 +205,9 @@ int validate(const ks_problem *p, const ks_dist *d) {
   if (p->batch < 0 || (p->batch > 1 && global_steps(p, d) % p->batch != 0)) return KS_ERR_ARG;
   if (p->sHev < 0 || (p->sHev && p->sHev < n * n)) return KS_ERR_ARG;
   if (p->nstate && (p->nstate_min < 1 || p->nstate_min > p->n)) return KS_ERR_ARG;
-  // per-step n_i: the mask of F_i needs n_{i-1}, which a shard's first step does not have
-  if (p->nstate && d && d->nranks > 1) return KS_ERR_ARG;
+  // per-step n_i on a shard: its first step's F_i is used unmasked (n_{i-1}
+  // lives on the previous rank), so its columns >= n_{i-1} must be zero
+  // (include/ks.h; dist.pad_shard zeroes them)
   if (d && d->nranks > 1) {
     // power-of-two shards in rank order (the local levels then follow the
     // global trailing-ones rule with no halo)

@@ -35,6 +35,9 @@
 #ifndef KS_TMAP_PROMO
 #define KS_TMAP_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_64B   // L2 promotion of the backward TMA rows: 64 B (A/B: 256 B 0.605 ms, none 0.586, 64 B 0.569 at c5 backward L0)
 #endif
+#ifndef KS_F6_L0C_BLOCKS
+#define KS_F6_L0C_BLOCKS 6
+#endif
 #ifndef KS_F6_BLOCKS
 #define KS_F6_BLOCKS 4
 #endif
@@ -727,7 +730,14 @@ __device__ __forceinline__ void small_eliminate(const SmallFactorArgs &a, int64_
 }
 
 // Resident CTAs (of 64 threads) per SM the register allocation targets.
-constexpr int factor_min_blocks(int n) { return n <= 4 ? 8 : n == 5 ? 7 : n == 6 ? KS_F6_BLOCKS : 4; }
+// n = 6, level 0 with a constant (stride-0) observation model: every block but
+// o is staged in shared memory, so a register cap for 6 CTAs/SM (168
+// registers, 104 bytes of stack) pays there (c5 factor L0 0.848 -> 0.821 ms;
+// 5 CTAs: 0.828) while it slows the levels >= 1 (5 CTAs: L1 0.576 -> 0.747
+// ms, 216 bytes of spills).
+constexpr int factor_min_blocks(int n, bool l0c = false) {
+  return n <= 4 ? 8 : n == 5 ? 7 : n == 6 ? (l0c ? KS_F6_L0C_BLOCKS : KS_F6_BLOCKS) : 4;
+}
 
 // One work item of a factor level: pair p (plus, on an odd level, the last
 // column without right neighbour, handled first by the last pair's thread).
@@ -805,7 +815,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) small_factor_split_kernel(Sma
 }
 
 template <int N, bool L0, bool CE, bool CC, bool OAOS, bool ZS = false>
-__global__ void __launch_bounds__(64, factor_min_blocks(N)) small_factor_kernel(SmallFactorArgs a) {
+__global__ void __launch_bounds__(64, factor_min_blocks(N, L0 && CC)) small_factor_kernel(SmallFactorArgs a) {
   if (L0 && (CE || CC)) {   // stage the constant (stride-0) level-0 blocks once per CTA
     extern __shared__ double smem_park[];
     double *cst = smem_park + (size_t)blockDim.x * kParkDoubles<N>;

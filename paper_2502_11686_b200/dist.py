@@ -67,6 +67,13 @@ def pad_shard(p, rank: int, world: int):
     lo = rank * M
     k = real[rank]
     q = p.slice(lo, lo + k) if k else p.slice(0, 1)   # all-padding rank: shapes only
+    if q.nstate is not None and lo > 0 and k:
+        # per-step n_i: the library cannot mask the first step's F_i (n_{i-1}
+        # is on the previous rank, include/ks.h), so its ignored columns
+        # >= n_{i-1} are zeroed here (the same problem)
+        F = np.array(np.broadcast_to(q.F, (k,) + q.F.shape[1:]))
+        F[0, :, int(p.nstate[lo - 1]):] = 0.0
+        q.F = F
     if k == M:
         return q
     n, mx, pad = p.n, p.m_max, M - k

@@ -114,9 +114,10 @@ def _join(parts):
         if arrs[0] is None:
             return None
         return np.concatenate([np.broadcast_to(a, (q.N,) + a.shape[1:]) for a, q in zip(arrs, parts)])
+    vec = lambda attr: None if getattr(p0, attr) is None else np.concatenate([getattr(q, attr) for q in parts])
     return gen.Problem("joined", sum(q.N for q in parts), p0.n, p0.m_max,
                        np.concatenate([q.m for q in parts]), cat("F"), cat("H"), cat("K"),
-                       cat("L"), cat("o"), cat("c"))
+                       cat("L"), cat("o"), cat("c"), None, 0, {}, cat("Hev"), vec("l"), vec("nstate"))
 
 
 @pytest.mark.parametrize("cfg,N,P", [("c1", 100, 8), ("c2", 150, 3), ("c3", 77, 4), ("c5", 45, 2),
@@ -142,3 +143,26 @@ def test_padded_shards_decoupled(cfg, N, P):
     assert np.max(np.abs(Sg[:N] - So).reshape(N, -1).max(1) / np.abs(So).reshape(N, -1).max(1)) <= 1e-10
     assert np.array_equal(xg[N:], np.zeros_like(xg[N:]))
     np.testing.assert_allclose(Sg[N:], np.broadcast_to(np.eye(p.n), Sg[N:].shape), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("N,P", [(40, 2), (37, 4)])
+def test_padded_shards_general_model(N, P):
+    """Per-step n_i over shards: pad_shard zeroes the ignored columns
+    (>= n_{i-1}) of each shard's first F_i -- the library cannot mask them
+    there (include/ks.h) -- and the general-model oracle gives the unpadded
+    problem's results on the joined shards (padding: u = 0, S = I)."""
+    from oracle import general as og
+    rng = np.random.default_rng(5 + N)
+    p = gen.general_problem(rng, N, 4, m_max=4, nmin=1)
+    p.F[:, :, :] += 7.0 * (np.arange(4)[None, None, :] >= np.r_[4, p.nstate[:-1]][:, None, None])  # garbage
+    M, real = kdist.shard_plan(N, P)
+    parts = [kdist.pad_shard(p, r, P) for r in range(P)]
+    for r in range(1, P):
+        if real[r]:
+            assert not parts[r].F[0, :, p.nstate[r * M - 1]:].any()
+    g = _join(parts)
+    xg, Sg = og.smooth_general(g)
+    xo, So = og.smooth_general(p)
+    assert np.max(np.abs(xg[:N] - xo)) <= 1e-10 * np.abs(xo).max()
+    assert np.max(np.abs(Sg[:N] - So)) <= 1e-10 * np.abs(So).max()
+    assert not xg[N:].any()

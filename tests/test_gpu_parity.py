@@ -565,6 +565,24 @@ def test_general_model(n, nmin, mmax, N, generic):
 
 
 @pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("n,nmin,N,P", [(4, 1, 512, 4), (6, 3, 300, 2), (3, 1, 1000, 8)])
+def test_general_model_virtual_shards(n, nmin, N, P, generic):
+    """Per-step n_i and rectangular H_i on time shards (power-of-two and
+    padded): every rank's first F_i has its ignored columns zeroed by
+    dist.pad_shard (the library cannot mask them there, include/ks.h); the
+    gathered shards match the general-model oracle."""
+    from oracle import general as og
+    rng = np.random.default_rng(300 + n + N)
+    p = gen.general_problem(rng, N, n, m_max=n, nmin=nmin)
+    x, S = _virtual_shards(p, P, generic=generic)
+    xo, So = og.smooth_general(p)
+    mask_x = np.arange(p.n)[None, :] < p.nstate[:, None]
+    mask_S = mask_x[:, :, None] & mask_x[:, None, :]
+    assert rel_state_err(np.where(mask_x, x, 0.0), xo) <= TOL_X
+    assert rel_cov_err(np.where(mask_S, S, 0.0), So) <= TOL_S
+
+
+@pytest.mark.parametrize("generic", [False, True])
 def test_general_model_noise_free(generic):
     rng = np.random.default_rng(77)
     p = gen.general_problem(rng, 2000, 4, m_max=4, nmin=2, noise_free=True)
