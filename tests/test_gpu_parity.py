@@ -184,13 +184,14 @@ def test_host_inputs_and_get():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["c2", "c4", "c1"])
+@pytest.mark.parametrize("case", ["c2", "c4", "c1", "c5"])
 def test_get_packed(case):
     """ks_get_packed: the upper triangles by rows of the covariance blocks
     equal the full blocks' (bitwise), into device memory, pinned host memory
-    (written by the kernel over PCIe) and asynchronously; pageable host
-    memory and a missing ks_selinv are rejected."""
-    p = gen.make(case, N={"c2": 1500, "c4": 45, "c1": 7}[case])
+    (written by the kernel over PCIe; c5 at N = 2^20: 22 M doubles) and
+    asynchronously; pageable host memory and a missing ks_selinv are
+    rejected."""
+    p = gen.make(case, N={"c2": 1500, "c4": 45, "c1": 7, "c5": 1 << 20}[case])
     x1, S1, _ = gpu_smooth(p)
     n = p.n
     iu = np.triu_indices(n)
